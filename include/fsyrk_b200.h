@@ -1,0 +1,167 @@
+/* fsyrk_b200 — C ABI of the B200-native mod-p SYRK hot path.
+ *
+ * Drop-in boundary for the reference fsyrk library's PrimeField SYRK entry
+ * points.  Every function below replaces one reference interface; the
+ * citation after "replaces" is the reference declaration (paths relative to
+ * /root/reference/proj).  Matrices use the reference layout: row-major
+ * uint64_t residues in [0, p), (data, rows, cols, stride-in-elements)
+ * (include/fsyrk/matrix.hpp:58-127).  Only Low(C) (diagonal included) is
+ * defined on return; the strict upper triangle is left untouched unless
+ * mirror_output is set (include/fsyrk/fast_syrk.hpp:271-282).
+ *
+ * All entry points are synchronous: they return with C filled (host
+ * variants) or with the work complete on the given stream's device
+ * (device variants synchronise the stream before returning).  Errors are
+ * reported as status codes; fsyrk_b200_last_error() gives the message of the
+ * calling thread's last failure.  The C++ shim include/fsyrk_b200/fsyrk.hpp
+ * maps the codes back to the reference's exception types.
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point returns FSYRK_B200_ENODEV.
+ */
+#ifndef FSYRK_B200_H
+#define FSYRK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSYRK_B200_ABI_VERSION 1
+
+/* Status codes.  Mapping to the reference's error convention:
+ *   EDIMENSION -> fsyrk::DimensionError        (matrix.hpp:131-133)
+ *   EINVAL     -> std::invalid_argument         (alias fast_syrk.hpp:279, threshold<2
+ *                                                winograd.hpp:18-20, bad prime fields.cpp:33-37)
+ *   EPARITY    -> fsyrk::DimensionParityError   (skew.hpp:54-55)
+ *   ENONRES    -> fsyrk::NotNonResidueError      (skew.hpp:182-187)
+ *   EDOMAIN    -> std::domain_error              (fields.cpp:63-64, p = 2 cases)
+ *   ECUDA / ENOMEM / ENODEV / ENCCL -> std::runtime_error (device side; no reference analogue) */
+enum fsyrk_b200_status {
+    FSYRK_B200_OK = 0,
+    FSYRK_B200_EDIMENSION = 1,
+    FSYRK_B200_EINVAL = 2,
+    FSYRK_B200_EPARITY = 3,
+    FSYRK_B200_ENONRES = 4,
+    FSYRK_B200_EDOMAIN = 5,
+    FSYRK_B200_ECUDA = 6,
+    FSYRK_B200_ENOMEM = 7,
+    FSYRK_B200_ENODEV = 8,
+    FSYRK_B200_ENCCL = 9
+};
+
+/* Recursion policy: replaces fsyrk::RecursionPolicy (include/fsyrk/winograd.hpp:14-21).
+ * max_levels = UINT64_MAX means unlimited (kUnlimitedLevels, winograd.hpp:9). */
+typedef struct fsyrk_b200_policy {
+    uint64_t threshold;
+    uint64_t max_levels;
+} fsyrk_b200_policy;
+
+/* Operation tally: replaces fsyrk::OpCount (include/fsyrk/opcount.hpp:10-25).
+ * The device path reports the modular multiply-accumulates it issued on the
+ * tensor cores in `mults` and its elementwise field additions in `adds`. */
+typedef struct fsyrk_b200_opcount {
+    uint64_t mults;
+    uint64_t adds;
+} fsyrk_b200_opcount;
+
+/* Skew-orthogonal Y: replaces fsyrk::SkewOrthogonal / skew_orthogonal(PrimeField, dim)
+ * (include/fsyrk/skew.hpp:21-37, 66-73).  form: 0 = ScalarRoot(a), 1 = Pair(a, b). */
+typedef struct fsyrk_b200_skew {
+    int form;
+    uint64_t a;
+    uint64_t b;
+    int ycost;
+} fsyrk_b200_skew;
+
+const char* fsyrk_b200_last_error(void);
+int fsyrk_b200_abi_version(void);
+
+/* 1 if a usable sm_100 device is present (no work launched). */
+int fsyrk_b200_device_available(void);
+
+/* make_syrk_plan(f, policy, mirror) (include/fsyrk/fast_syrk.hpp:20-24): validates the
+ * field and policy and returns the Y the recursion uses.  Host-only setup. */
+int fsyrk_b200_make_syrk_plan(uint64_t p, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_skew* skew);
+
+/* skew_orthogonal(PrimeField, dim) (include/fsyrk/skew.hpp:66-73). */
+int fsyrk_b200_skew_orthogonal(uint64_t p, size_t dim, fsyrk_b200_skew* skew);
+
+/* random_matrix(f, rows, cols, seed) (include/fsyrk/matrix.hpp:411-419): the
+ * reference's seeded generator (std::mt19937_64 + uniform_int_distribution),
+ * host-side, so callers can build the same inputs as the reference. */
+int fsyrk_b200_random_matrix(uint64_t p, size_t rows, size_t cols, uint64_t seed, uint64_t* out, size_t ld);
+
+/* ---------------------------------------------------------------- host API */
+
+/* syrk_fast_into(f, a, c, plan, ops) (include/fsyrk/fast_syrk.hpp:274-282):
+ * Low(C) <- Low(A * A^T).  a: n x k host matrix, c: n x n host matrix. */
+int fsyrk_b200_syrk_fast_into(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c,
+                              size_t ldc, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
+
+/* syrk_fast_acc(f, alpha, a, beta, c, plan, ops) (include/fsyrk/fast_syrk.hpp:293-303):
+ * Low(C) <- Low(alpha * A * A^T + beta * C); reads only Low(C_in). */
+int fsyrk_b200_syrk_fast_acc(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                             uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy, int mirror_output,
+                             fsyrk_b200_opcount* ops);
+
+/* syrkd(f, a, d, plan, ops) (include/fsyrk/scaled_syrk.hpp:58-104), extended with the
+ * accumulate form so the LDL^T Schur update C <- C - A*D*A^T is one call
+ * (alpha = p - 1, beta = 1):  Low(C) <- Low(alpha * A * Diag(d) * A^T + beta * C).
+ * d has k entries.  alpha = 1, beta = 0 is exactly the reference's syrkd. */
+int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                     const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy,
+                     int mirror_output, fsyrk_b200_opcount* ops);
+
+/* -------------------------------------------------------------- device API */
+
+/* Same operations on device-resident uint64 matrices (pointers from
+ * cudaMalloc on the current device); `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  d (syrkd) is a HOST array of k entries.  These do
+ * not synchronise the host beyond what plan creation needs; call
+ * cudaStreamSynchronize before reading C. */
+int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                        const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
+                        fsyrk_b200_policy policy, int mirror_output, void* stream, fsyrk_b200_opcount* ops);
+
+/* Drop cached plans and device arenas (tests, memory pressure). */
+void fsyrk_b200_release_cache(void);
+
+/* --------------------------------------------------------------- telemetry */
+
+/* Kernel launches issued by the last compute call on this thread, and the
+ * per-kind launch counts (index: 0 tensor-core products, 1 pre-addition,
+ * 2 post-addition, 3 conversion/finalize, 4 other). */
+int fsyrk_b200_last_launch_count(int* by_kind, int nkinds);
+
+/* Describe the last executed plan as a JSON string (tree, groups, limbs, bytes). */
+const char* fsyrk_b200_last_plan_json(void);
+
+/* Time each kernel kind of the last plan with CUDA events when enabled
+ * (adds syncs; for profiling only).  Returns milliseconds per kind via out[5]. */
+int fsyrk_b200_set_phase_timing(int enable);
+int fsyrk_b200_last_phase_ms(float* out, int nkinds);
+
+/* ------------------------------------------------------------- white box */
+
+/* One recursion level with direct (classical) sub-products on the device:
+ * returns S1..S4 (h x kw, row-major, ld = kw) and P1..P5 (h x h, P4 = S1*S2^T),
+ * the blocks of Table 3 (include/fsyrk/fast_syrk.hpp:82-133), as uint64.
+ * Any output may be NULL.  Host pointers. */
+int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* s1,
+                            uint64_t* s2, uint64_t* s3, uint64_t* s4, uint64_t* p1, uint64_t* p2, uint64_t* p3,
+                            uint64_t* p4, uint64_t* p5, size_t* kw_out);
+
+/* Exact tensor-core product C = A*B^T mod p (m x k times (n x k)^T), host
+ * pointers; the general-product engine (replaces gemm_winograd_nt_into,
+ * include/fsyrk/winograd.hpp:195-202, and gemm_classical_nt, matrix.hpp:317-329). */
+int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
+                       size_t ldb, uint64_t* c, size_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSYRK_B200_H */

@@ -1,0 +1,223 @@
+// Reference driver: runs the UNMODIFIED reference fsyrk hot path, compiled
+// from /root/reference/proj sources (see oracle/Makefile), on seeded inputs.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY.  Used (a) to generate the golden
+// fixtures under tests/golden/ (with tests/golden/make_golden.py), (b) to
+// precompute lower-triangle digests for the large configs, and (c) as the
+// CPU baseline in bench.py (`cpu_baseline.kind = "reference"` and
+// `--impl reference`).  It is never linked into the product library.
+//
+// Entry points exercised (reference file:line):
+//   random_matrix            proj/include/fsyrk/matrix.hpp:411-419
+//   make_syrk_plan           proj/include/fsyrk/fast_syrk.hpp:20-24
+//   syrk_fast_into           proj/include/fsyrk/fast_syrk.hpp:274-282
+//   syrk_fast_acc            proj/include/fsyrk/fast_syrk.hpp:293-303
+//   syrkd                    proj/include/fsyrk/scaled_syrk.hpp:58-104
+//   syrk_classical           proj/include/fsyrk/matrix.hpp:372-407
+//
+// Output: one JSON line on stdout.
+#include <atomic>
+#include <chrono>
+#include <cinttypes>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fsyrk/fast_syrk.hpp"
+#include "fsyrk/scaled_syrk.hpp"
+#include "sha256.h"
+
+using namespace fsyrk;
+
+namespace {
+
+struct Args {
+    std::uint64_t p = 131071;
+    std::size_t n = 64, k = 64;
+    std::uint64_t seed = 42;
+    std::size_t threshold = 64;
+    std::size_t levels = kUnlimitedLevels;
+    std::string mode = "plain";  // plain | acc | schur | classical
+    std::uint64_t cseed = 43, abseed = 7, dseed = 44;
+    bool mirror = false;
+    int threads = 1;
+    int reps = 1;
+    std::string out_a, out_c, out_c0, out_d;
+    bool digest = true;
+    int sample = 0;
+    bool alpha_set = false, beta_set = false;
+    std::uint64_t alpha = 1, beta = 0;
+};
+
+[[noreturn]] void usage() {
+    std::fprintf(stderr,
+                 "usage: ref_driver [--p P] [--n N] [--k K] [--seed S] [--threshold T]\n"
+                 "  [--levels L|inf] [--mode plain|acc|schur|classical] [--cseed S] [--abseed S]\n"
+                 "  [--alpha a --beta b] [--dseed S] [--mirror] [--threads T] [--reps R]\n"
+                 "  [--out-a F] [--out-c F] [--out-c0 F] [--out-d F] [--no-digest] [--sample N]\n");
+    std::exit(2);
+}
+
+Args parse(int argc, char** argv) {
+    Args a;
+    for (int i = 1; i < argc; ++i) {
+        std::string k = argv[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= argc) usage();
+            return argv[++i];
+        };
+        if (k == "--p") a.p = std::stoull(val());
+        else if (k == "--n") a.n = std::stoull(val());
+        else if (k == "--k") a.k = std::stoull(val());
+        else if (k == "--seed") a.seed = std::stoull(val());
+        else if (k == "--threshold") a.threshold = std::stoull(val());
+        else if (k == "--levels") {
+            std::string v = val();
+            a.levels = v == "inf" ? kUnlimitedLevels : std::stoull(v);
+        } else if (k == "--mode") a.mode = val();
+        else if (k == "--cseed") a.cseed = std::stoull(val());
+        else if (k == "--abseed") a.abseed = std::stoull(val());
+        else if (k == "--dseed") a.dseed = std::stoull(val());
+        else if (k == "--alpha") { a.alpha = std::stoull(val()); a.alpha_set = true; }
+        else if (k == "--beta") { a.beta = std::stoull(val()); a.beta_set = true; }
+        else if (k == "--mirror") a.mirror = true;
+        else if (k == "--threads") a.threads = std::stoi(val());
+        else if (k == "--reps") a.reps = std::stoi(val());
+        else if (k == "--out-a") a.out_a = val();
+        else if (k == "--out-c") a.out_c = val();
+        else if (k == "--out-c0") a.out_c0 = val();
+        else if (k == "--out-d") a.out_d = val();
+        else if (k == "--no-digest") a.digest = false;
+        else if (k == "--sample") a.sample = std::stoi(val());
+        else usage();
+    }
+    return a;
+}
+
+void dump(const std::string& path, const void* data, std::size_t bytes) {
+    if (path.empty()) return;
+    FILE* fp = std::fopen(path.c_str(), "wb");
+    if (!fp) { std::perror(path.c_str()); std::exit(1); }
+    std::fwrite(data, 1, bytes, fp);
+    std::fclose(fp);
+}
+
+// One complete evaluation of the configured hot-path call.  Inputs are
+// generated outside the timed region; returns the seconds spent in the call.
+struct Instance {
+    Matrix<PrimeField> a, c, c0;
+    std::vector<std::uint64_t> d;
+    std::uint64_t alpha = 1, beta = 0;
+};
+
+Instance make_instance(const PrimeField& f, const Args& g) {
+    Instance in;
+    in.a = random_matrix(f, g.n, g.k, g.seed);
+    in.c = Matrix<PrimeField>(g.n, g.n, 0);
+    if (g.mode == "acc" || g.mode == "schur") {
+        in.c0 = random_matrix(f, g.n, g.n, g.cseed);
+        mirror_lower_to_upper(f, in.c0.view());
+        in.c = in.c0;
+    }
+    if (g.mode == "acc") {
+        std::mt19937_64 rng(g.abseed);
+        in.alpha = 1 + rng() % (g.p - 1);
+        in.beta = 1 + rng() % (g.p - 1);
+        if (g.alpha_set) in.alpha = g.alpha % g.p;
+        if (g.beta_set) in.beta = g.beta % g.p;
+    }
+    if (g.mode == "schur") {
+        std::mt19937_64 rng(g.dseed);
+        std::uniform_int_distribution<std::uint64_t> dist(1, g.p - 1);
+        in.d.resize(g.k);
+        for (auto& v : in.d) v = dist(rng);
+    }
+    return in;
+}
+
+double run_instance(const PrimeField& f, const Args& g, Instance& in) {
+    auto plan = make_syrk_plan(f, RecursionPolicy{g.threshold, g.levels}, g.mirror);
+    OpCount ops;
+    auto t0 = std::chrono::steady_clock::now();
+    if (g.mode == "plain") {
+        syrk_fast_into(f, in.a.view(), in.c.view(), plan, ops);
+    } else if (g.mode == "classical") {
+        syrk_classical(f, f.one(), in.a.view(), f.zero(), in.c.view(), ops);
+    } else if (g.mode == "acc") {
+        syrk_fast_acc(f, in.alpha, in.a.view(), in.beta, in.c.view(), plan, ops);
+    } else if (g.mode == "schur") {
+        // C <- C - A*D*A^T on the lower triangle (R has no fused form).
+        Matrix<PrimeField> x = syrkd(f, in.a.view(), in.d, plan, ops);
+        for (std::size_t i = 0; i < g.n; ++i)
+            for (std::size_t j = 0; j <= i; ++j) in.c.at(i, j) = f.sub(in.c.at(i, j), x.at(i, j));
+        if (g.mirror) mirror_lower_to_upper(f, in.c.view());
+    } else {
+        usage();
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    Args g = parse(argc, argv);
+    PrimeField f(g.p);
+    auto y = skew_orthogonal(f, 2);
+
+    std::vector<Instance> inst;
+    inst.reserve(g.threads);
+    for (int t = 0; t < g.threads; ++t) inst.push_back(make_instance(f, g));
+
+    std::vector<double> secs(g.threads, 0.0);
+    auto wall0 = std::chrono::steady_clock::now();
+    {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < g.threads; ++t)
+            pool.emplace_back([&, t] {
+                for (int r = 0; r < g.reps; ++r) {
+                    if (r > 0) inst[t] = make_instance(f, g);
+                    secs[t] += run_instance(f, g, inst[t]);
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    double max_s = 0, sum_s = 0;
+    for (double s : secs) { max_s = std::max(max_s, s); sum_s += s; }
+
+    Instance& r0 = inst[0];
+    char hex[65] = "";
+    if (g.digest) lower_digest_u64(r0.c.data().data(), g.n, g.n, hex);
+    dump(g.out_a, r0.a.data().data(), r0.a.data().size() * 8);
+    dump(g.out_c, r0.c.data().data(), r0.c.data().size() * 8);
+    if (!r0.c0.data().empty()) dump(g.out_c0, r0.c0.data().data(), r0.c0.data().size() * 8);
+    if (!r0.d.empty()) dump(g.out_d, r0.d.data(), r0.d.size() * 8);
+
+    std::printf("{\"p\": %" PRIu64 ", \"n\": %zu, \"k\": %zu, \"mode\": \"%s\", \"seed\": %" PRIu64
+                ", \"threshold\": %zu, \"levels\": %s, \"threads\": %d, \"reps\": %d"
+                ", \"alpha\": %" PRIu64 ", \"beta\": %" PRIu64
+                ", \"skew_form\": \"%s\", \"skew_a\": %" PRIu64 ", \"skew_b\": %" PRIu64
+                ", \"seconds_per_call\": %.6f, \"wall_seconds\": %.6f, \"digest\": \"%s\"",
+                g.p, g.n, g.k, g.mode.c_str(), g.seed, g.threshold,
+                g.levels == kUnlimitedLevels ? "\"inf\"" : std::to_string(g.levels).c_str(),
+                g.threads, g.reps, r0.alpha, r0.beta,
+                y.form == SkewOrthogonal<PrimeField>::Form::Pair ? "pair" : "scalar", y.a, y.b,
+                sum_s / (g.threads * g.reps), wall, hex);
+    if (g.sample > 0) {
+        // deterministic sample positions in the lower triangle
+        std::mt19937_64 rng(12345);
+        std::printf(", \"sample\": [");
+        for (int s = 0; s < g.sample; ++s) {
+            std::size_t i = rng() % g.n;
+            std::size_t j = rng() % (i + 1);
+            std::printf("%s[%zu, %zu, %" PRIu64 "]", s ? ", " : "", i, j, r0.c.at(i, j));
+        }
+        std::printf("]");
+    }
+    std::printf("}\n");
+    return 0;
+}

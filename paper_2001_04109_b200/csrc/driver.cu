@@ -1,0 +1,1097 @@
+// Host recursion driver and C ABI of the B200 mod-p SYRK.
+//
+// The recursion decisions are the reference's, node for node
+// (syrk_fast_rec, include/fsyrk/fast_syrk.hpp:135-157): classical leaf when
+// the level budget is spent, n or k is odd, or min(n, k) < threshold; a
+// split on k when k > n; the Pair-form padding rule (fast_syrk.hpp:34-37,
+// 151-155); otherwise one level of the 5-product schedule.  What changes is
+// the execution: instead of walking the tree with in-place CPU kernels, the
+// driver plans the whole tree once ("wide" device schedule, one buffer per
+// product) and runs it as a short fixed sequence of
+// batched launches:
+//     convert-in -> prep (per depth) -> tensor-core products (per shape)
+//     -> post-additions (per depth, bottom-up) -> finalize (alpha, beta, mirror)
+// Plans (device arena, TMA descriptors, node tables) are cached per
+// (p, n, k, policy) so repeated calls only launch kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <sstream>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/fsyrk_b200.h"
+#include "elementwise.cuh"
+#include "field_host.h"
+#include "modp.cuh"
+#include "tc_modmm.h"
+
+namespace fsyrk_b200 {
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_launch_counts[5] = {0, 0, 0, 0, 0};
+thread_local std::string g_last_plan_json;
+thread_local bool g_phase_timing = false;
+thread_local float g_phase_ms[5] = {0, 0, 0, 0, 0};
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        int code = e == cudaErrorMemoryAllocation ? FSYRK_B200_ENOMEM : FSYRK_B200_ECUDA;
+        fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FSYRK_B200_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FSYRK_B200_EINVAL;
+    }
+}
+
+// ------------------------------------------------------------------ device
+int device_ok() {
+    static int cached = -1;
+    if (cached >= 0) return cached;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return cached = 0;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cached = 0;
+    return cached = (prop.major == 10) ? 1 : 0;
+}
+
+void require_device() {
+    if (!device_ok())
+        fail(FSYRK_B200_ENODEV, "no sm_100 (B200) device available: the fsyrk_b200 path has no CPU fallback");
+}
+
+// ------------------------------------------------------------- TMA encode
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q),
+           "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!ptr || q != cudaDriverEntryPointSuccess) fail(FSYRK_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeFn>(ptr);
+    }
+    return fn;
+}
+
+// 4-D int8 plane tensor [batch][L][rows][kpad], boxes of 128 (K) x box_rows.
+CUtensorMap make_plane_map(void* base, int kpad, int rows, int L, int batch, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[4] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)L, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)kpad, (cuuint64_t)kpad * rows, (cuuint64_t)kpad * rows * L};
+    cuuint32_t box[4] = {128, (cuuint32_t)box_rows, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(FSYRK_B200_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+int limbs_for(uint64_t p) {
+    if (p <= 65536ull) return 2;
+    if (p <= 16777216ull) return 3;
+    return 4;
+}
+
+uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t p) {
+    host::Field f{p};
+    return f.pow(b, e);
+}
+
+// ------------------------------------------------------------------- plan
+enum Kind { LEAF = 0, LEVEL = 1, SPLITK = 2 };
+
+struct Node {
+    int kind = LEAF;
+    int n = 0, k = 0, depth = 0;
+    int h = 0, kh = 0, kw = 0;
+    bool padded = false;
+    int ch[3] = {-1, -1, -1};
+    int parent = -1, role = -1;
+    // input residue view (LEVEL / SPLITK; LEAF when split from a view)
+    const uint32_t* in = nullptr;
+    long long ldin = 0;
+    bool leaf_from_prep = false;
+    int lgroup = -1, lslot = -1;
+    int ggroup = -1, gslot = -1;
+    uint32_t* x = nullptr;  // n x n output (lower)
+    long long ldx = 0;
+    uint32_t* s3res = nullptr;
+    long long lds3 = 0;
+};
+
+struct LeafGroup {
+    int n, k, count = 0;
+    int rpad, kpad;
+    long long plane, slot;
+    int8_t* planes = nullptr;
+    uint32_t* xout = nullptr;
+    CUtensorMap tA, tB;
+    int2* tiles = nullptr;
+    int ntiles = 0;
+    size_t off_planes = 0, off_x = 0, off_tiles = 0;
+    std::vector<int2> host_tiles;
+};
+
+struct GemmGroup {
+    int h, kw, count = 0;
+    int hpad, kpad;
+    long long plane, slot;
+    int8_t *ga = nullptr, *gb = nullptr;
+    uint32_t* out = nullptr;
+    CUtensorMap tA, tB;
+    size_t off_ga = 0, off_gb = 0, off_out = 0;
+};
+
+struct PrepGroup {
+    int depth, n, k;
+    std::vector<int> nodes;
+    PrepArgs args;
+    PrepNode* dev_nodes = nullptr;
+    size_t off_nodes = 0;
+};
+
+struct PostGroup {
+    int depth, n, kind;
+    std::vector<int> nodes;
+    PostNode* dev_post = nullptr;
+    AddNode* dev_add = nullptr;
+    size_t off_nodes = 0;
+};
+
+struct Arena {
+    size_t size = 0;
+    size_t take(size_t bytes, size_t align = 256) {
+        size_t o = (size_t)round_up((long long)size, (long long)align);
+        size = o + bytes;
+        return o;
+    }
+};
+
+struct Plan {
+    uint64_t p;
+    int n, kin, k;  // k: columns after the (optional) syrkd transform
+    fsyrk_b200_policy policy;
+    bool colmap = false;
+    int L, BN;
+    host::Skew y;
+    ModP m;
+    uint32_t c32;
+    std::vector<Node> nodes;
+    std::vector<LeafGroup> leaves;
+    std::vector<GemmGroup> gemms;
+    std::vector<PrepGroup> preps;
+    std::vector<PostGroup> posts;
+    std::vector<int> split_leaves;  // LEAF nodes converted from a residue view
+    uint8_t* arena = nullptr;
+    size_t arena_bytes = 0;
+    uint32_t* root_in = nullptr;
+    size_t off_root_in = 0;
+    ColMap* dev_colmap = nullptr;
+    size_t off_colmap = 0;
+    uint64_t tensor_macs = 0;  // modular MACs issued on the tensor cores
+    uint64_t int8_macs = 0;
+    uint64_t ew_adds = 0;
+
+    ~Plan() {
+        if (arena) cudaFree(arena);
+    }
+
+    int build(int n_, int k_, uint64_t levels, int depth, int parent, int role) {
+        Node nd;
+        nd.n = n_;
+        nd.k = k_;
+        nd.depth = depth;
+        nd.parent = parent;
+        nd.role = role;
+        const int idx = (int)nodes.size();
+        nodes.push_back(nd);
+        const uint64_t thr = policy.threshold;
+        const int mn = std::min(n_, k_);
+        if (levels == 0 || n_ % 2 != 0 || k_ % 2 != 0 || (uint64_t)mn < thr) {
+            nodes[idx].kind = LEAF;
+            return idx;
+        }
+        if (k_ > n_) {  // split on k (fast_syrk.hpp:143-150)
+            const int k1 = (k_ / 2) & ~1;
+            nodes[idx].kind = SPLITK;
+            int c0 = build(n_, k1, levels, depth + 1, idx, 0);
+            int c1 = build(n_, k_ - k1, levels, depth + 1, idx, 1);
+            nodes[idx].ch[0] = c0;
+            nodes[idx].ch[1] = c1;
+            return idx;
+        }
+        const bool padded = y.form == 1 && (k_ / 2) % 2 == 1;
+        if (padded && k_ / 2 + 1 > n_ / 2) {
+            nodes[idx].kind = LEAF;
+            return idx;
+        }
+        nodes[idx].kind = LEVEL;
+        nodes[idx].h = n_ / 2;
+        nodes[idx].kh = k_ / 2;
+        nodes[idx].kw = k_ / 2 + (padded ? 1 : 0);
+        nodes[idx].padded = padded;
+        const uint64_t next = levels == UINT64_MAX ? UINT64_MAX : levels - 1;
+        const int h = n_ / 2, kh = k_ / 2, kw = nodes[idx].kw;
+        int c0 = build(h, kh, next, depth + 1, idx, 0);  // P1 = A11 A11^T
+        int c1 = build(h, kh, next, depth + 1, idx, 1);  // P2 = A12 A12^T
+        int c2 = build(h, kw, next, depth + 1, idx, 2);  // P5 = S3 S3^T
+        nodes[idx].ch[0] = c0;
+        nodes[idx].ch[1] = c1;
+        nodes[idx].ch[2] = c2;
+        return idx;
+    }
+
+    int leaf_group(int n_, int k_) {
+        for (size_t g = 0; g < leaves.size(); ++g)
+            if (leaves[g].n == n_ && leaves[g].k == k_) return (int)g;
+        LeafGroup lg;
+        lg.n = n_;
+        lg.k = k_;
+        leaves.push_back(lg);
+        return (int)leaves.size() - 1;
+    }
+    int gemm_group(int h, int kw) {
+        for (size_t g = 0; g < gemms.size(); ++g)
+            if (gemms[g].h == h && gemms[g].kw == kw) return (int)g;
+        GemmGroup gg;
+        gg.h = h;
+        gg.kw = kw;
+        gemms.push_back(gg);
+        return (int)gemms.size() - 1;
+    }
+
+    void create(uint64_t p_, int n_, int kin_, int k_, fsyrk_b200_policy pol, bool colmap_) {
+        p = p_;
+        n = n_;
+        kin = kin_;
+        k = k_;
+        policy = pol;
+        colmap = colmap_;
+        L = limbs_for(p);
+        BN = modmm_block_n(L);
+        host::Field f{p};
+        y = host::skew_orthogonal(f);
+        m = make_modp((uint32_t)p);
+        c32 = (uint32_t)pow_mod(2, 32, p);
+
+        build(n, k, pol.max_levels, 0, -1, -1);
+        for (auto& nd : nodes)
+            if (nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(L))
+                fail(FSYRK_B200_EINVAL, "leaf inner dimension " + std::to_string(nd.k) +
+                                            " exceeds the exact int32 accumulation bound");
+
+        // ---- grouping
+        for (int i = 0; i < (int)nodes.size(); ++i) {
+            Node& nd = nodes[i];
+            if (nd.kind == LEAF) {
+                nd.lgroup = leaf_group(nd.n, nd.k);
+                nd.lslot = leaves[nd.lgroup].count++;
+                nd.leaf_from_prep = nd.parent >= 0 && nodes[nd.parent].kind == LEVEL;
+                if (!nd.leaf_from_prep) split_leaves.push_back(i);
+            } else if (nd.kind == LEVEL) {
+                nd.ggroup = gemm_group(nd.h, nd.kw);
+                nd.gslot = gemms[nd.ggroup].count++;
+            }
+        }
+
+        // ---- arena layout
+        Arena ar;
+        const int kin_pad = (int)round_up(k, 4);
+        off_root_in = ar.take((size_t)n * kin_pad * 4);
+        if (colmap) off_colmap = ar.take((size_t)k * sizeof(ColMap));
+        for (auto& lg : leaves) {
+            lg.rpad = (int)round_up(lg.n, 128);
+            lg.kpad = (int)round_up(std::max(lg.k, 1), 128);
+            lg.plane = (long long)lg.rpad * lg.kpad;
+            lg.slot = lg.plane * L;
+            lg.off_planes = ar.take((size_t)lg.slot * lg.count, 1024);
+            lg.off_x = ar.take((size_t)lg.count * lg.n * lg.n * 4);
+            for (int tm = 0; tm * 128 < lg.n; ++tm)
+                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn)
+                    lg.host_tiles.push_back(make_int2(tm, tn));
+            lg.ntiles = (int)lg.host_tiles.size();
+            lg.off_tiles = ar.take(lg.host_tiles.size() * sizeof(int2));
+        }
+        for (auto& gg : gemms) {
+            gg.hpad = (int)round_up(gg.h, 128);
+            gg.kpad = (int)round_up(gg.kw, 128);
+            gg.plane = (long long)gg.hpad * gg.kpad;
+            gg.slot = gg.plane * L;
+            gg.off_ga = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
+            gg.off_gb = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
+            gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
+        }
+        std::vector<size_t> off_x(nodes.size(), 0), off_s3(nodes.size(), 0);
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            Node& nd = nodes[i];
+            if (nd.kind != LEAF) off_x[i] = ar.take((size_t)nd.n * nd.n * 4);
+            if (nd.kind == LEVEL && nodes[nd.ch[2]].kind != LEAF) off_s3[i] = ar.take((size_t)nd.h * nd.kw * 4);
+        }
+        // prep / post groups
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            Node& nd = nodes[i];
+            if (nd.kind != LEVEL) continue;
+            bool found = false;
+            for (auto& pg : preps)
+                if (pg.depth == nd.depth && pg.n == nd.n && pg.k == nd.k) {
+                    pg.nodes.push_back((int)i);
+                    found = true;
+                }
+            if (!found) {
+                PrepGroup pg;
+                pg.depth = nd.depth;
+                pg.n = nd.n;
+                pg.k = nd.k;
+                pg.nodes.push_back((int)i);
+                preps.push_back(pg);
+            }
+        }
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            Node& nd = nodes[i];
+            if (nd.kind == LEAF) continue;
+            bool found = false;
+            for (auto& pg : posts)
+                if (pg.depth == nd.depth && pg.n == nd.n && pg.kind == nd.kind) {
+                    pg.nodes.push_back((int)i);
+                    found = true;
+                }
+            if (!found) {
+                PostGroup pg;
+                pg.depth = nd.depth;
+                pg.n = nd.n;
+                pg.kind = nd.kind;
+                pg.nodes.push_back((int)i);
+                posts.push_back(pg);
+            }
+        }
+        std::sort(preps.begin(), preps.end(), [](const PrepGroup& a, const PrepGroup& b) { return a.depth < b.depth; });
+        std::sort(posts.begin(), posts.end(), [](const PostGroup& a, const PostGroup& b) { return a.depth > b.depth; });
+        for (auto& pg : preps) pg.off_nodes = ar.take(pg.nodes.size() * sizeof(PrepNode));
+        for (auto& pg : posts)
+            pg.off_nodes = ar.take(pg.nodes.size() * (pg.kind == LEVEL ? sizeof(PostNode) : sizeof(AddNode)));
+
+        // ---- allocate and clear (the zero padding of every operand plane is never rewritten)
+        arena_bytes = ar.size;
+        ck(cudaMalloc(&arena, arena_bytes), "cudaMalloc(plan arena)");
+        ck(cudaMemset(arena, 0, arena_bytes), "cudaMemset(plan arena)");
+        root_in = reinterpret_cast<uint32_t*>(arena + off_root_in);
+        if (colmap) dev_colmap = reinterpret_cast<ColMap*>(arena + off_colmap);
+        for (auto& lg : leaves) {
+            lg.planes = reinterpret_cast<int8_t*>(arena + lg.off_planes);
+            lg.xout = reinterpret_cast<uint32_t*>(arena + lg.off_x);
+            lg.tiles = reinterpret_cast<int2*>(arena + lg.off_tiles);
+            lg.tA = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, 128);
+            lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, BN);
+            ck(cudaMemcpy(lg.tiles, lg.host_tiles.data(), lg.host_tiles.size() * sizeof(int2), cudaMemcpyHostToDevice),
+               "upload tile list");
+        }
+        for (auto& gg : gemms) {
+            gg.ga = reinterpret_cast<int8_t*>(arena + gg.off_ga);
+            gg.gb = reinterpret_cast<int8_t*>(arena + gg.off_gb);
+            gg.out = reinterpret_cast<uint32_t*>(arena + gg.off_out);
+            gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128);
+            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, L, 2 * gg.count, BN);
+        }
+        // node pointers (top-down: a node's input is set before its children read it)
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            Node& nd = nodes[i];
+            if (nd.parent < 0) {
+                nd.in = root_in;
+                nd.ldin = kin_pad;
+            }
+            if (nd.kind == LEAF) {
+                LeafGroup& lg = leaves[nd.lgroup];
+                nd.x = lg.xout + (long long)nd.lslot * nd.n * nd.n;
+                nd.ldx = nd.n;
+            } else {
+                nd.x = reinterpret_cast<uint32_t*>(arena + off_x[i]);
+                nd.ldx = nd.n;
+            }
+            if (nd.kind == LEVEL) {
+                if (nodes[nd.ch[2]].kind != LEAF) {
+                    nd.s3res = reinterpret_cast<uint32_t*>(arena + off_s3[i]);
+                    nd.lds3 = nd.kw;
+                }
+                Node& c0 = nodes[nd.ch[0]];
+                Node& c1 = nodes[nd.ch[1]];
+                Node& c2 = nodes[nd.ch[2]];
+                c0.in = nd.in;
+                c0.ldin = nd.ldin;
+                c1.in = nd.in + nd.kh;
+                c1.ldin = nd.ldin;
+                c2.in = nd.s3res;
+                c2.ldin = nd.lds3;
+            } else if (nd.kind == SPLITK) {
+                Node& c0 = nodes[nd.ch[0]];
+                Node& c1 = nodes[nd.ch[1]];
+                c0.in = nd.in;
+                c0.ldin = nd.ldin;
+                c1.in = nd.in + c0.k;
+                c1.ldin = nd.ldin;
+            }
+        }
+        // prep node tables
+        for (auto& pg : preps) {
+            const Node& n0 = nodes[pg.nodes[0]];
+            GemmGroup& gg = gemms[n0.ggroup];
+            PrepArgs& a = pg.args;
+            a.m = m;
+            a.L = L;
+            a.h = n0.h;
+            a.kh = n0.kh;
+            a.kw = n0.kw;
+            a.pair = y.form == 1;
+            a.half = a.pair ? n0.kw / 2 : n0.kw;
+            a.ya = (uint32_t)y.a;
+            a.yb = (uint32_t)y.b;
+            a.g_plane = gg.plane;
+            a.g_row = gg.kpad;
+            a.c_plane = a.c_row = a.c3_plane = a.c3_row = 0;
+            const Node& ca = nodes[n0.ch[0]];
+            const Node& c3 = nodes[n0.ch[2]];
+            if (ca.kind == LEAF) {
+                a.c_plane = leaves[ca.lgroup].plane;
+                a.c_row = leaves[ca.lgroup].kpad;
+            }
+            if (c3.kind == LEAF) {
+                a.c3_plane = leaves[c3.lgroup].plane;
+                a.c3_row = leaves[c3.lgroup].kpad;
+            }
+            std::vector<PrepNode> tab;
+            for (int ni : pg.nodes) {
+                const Node& nd = nodes[ni];
+                GemmGroup& g = gemms[nd.ggroup];
+                PrepNode pn{};
+                pn.a = nd.in;
+                pn.lda = nd.ldin;
+                pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
+                pn.s2 = g.gb + (2LL * nd.gslot) * g.slot;
+                pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
+                pn.s4 = g.gb + (2LL * nd.gslot + 1) * g.slot;
+                const Node& q0 = nodes[nd.ch[0]];
+                const Node& q1 = nodes[nd.ch[1]];
+                const Node& q2 = nodes[nd.ch[2]];
+                if (q0.kind == LEAF) pn.c_a11 = leaves[q0.lgroup].planes + q0.lslot * leaves[q0.lgroup].slot;
+                if (q1.kind == LEAF) pn.c_a12 = leaves[q1.lgroup].planes + q1.lslot * leaves[q1.lgroup].slot;
+                if (q2.kind == LEAF) pn.c_s3 = leaves[q2.lgroup].planes + q2.lslot * leaves[q2.lgroup].slot;
+                pn.r_s3 = nd.s3res;
+                pn.ld_s3 = nd.lds3;
+                tab.push_back(pn);
+            }
+            pg.dev_nodes = reinterpret_cast<PrepNode*>(arena + pg.off_nodes);
+            a.nodes = pg.dev_nodes;
+            a.nnodes = (int)tab.size();
+            ck(cudaMemcpy(pg.dev_nodes, tab.data(), tab.size() * sizeof(PrepNode), cudaMemcpyHostToDevice),
+               "upload prep table");
+        }
+        for (auto& pg : posts) {
+            if (pg.kind == LEVEL) {
+                std::vector<PostNode> tab;
+                for (int ni : pg.nodes) {
+                    const Node& nd = nodes[ni];
+                    const GemmGroup& g = gemms[nd.ggroup];
+                    PostNode pn{};
+                    pn.p1 = nodes[nd.ch[0]].x;
+                    pn.ld1 = nodes[nd.ch[0]].ldx;
+                    pn.p2 = nodes[nd.ch[1]].x;
+                    pn.ld2 = nodes[nd.ch[1]].ldx;
+                    pn.p5 = nodes[nd.ch[2]].x;
+                    pn.ld5 = nodes[nd.ch[2]].ldx;
+                    pn.p4 = g.out + (2LL * nd.gslot) * g.h * g.h;
+                    pn.p3 = g.out + (2LL * nd.gslot + 1) * g.h * g.h;
+                    pn.ld3 = pn.ld4 = g.h;
+                    pn.x = nd.x;
+                    pn.ldx = nd.ldx;
+                    tab.push_back(pn);
+                }
+                pg.dev_post = reinterpret_cast<PostNode*>(arena + pg.off_nodes);
+                ck(cudaMemcpy(pg.dev_post, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
+                   "upload post table");
+            } else {
+                std::vector<AddNode> tab;
+                for (int ni : pg.nodes) {
+                    const Node& nd = nodes[ni];
+                    AddNode an{};
+                    an.x1 = nodes[nd.ch[0]].x;
+                    an.ld1 = nodes[nd.ch[0]].ldx;
+                    an.x2 = nodes[nd.ch[1]].x;
+                    an.ld2 = nodes[nd.ch[1]].ldx;
+                    an.x = nd.x;
+                    an.ldx = nd.ldx;
+                    tab.push_back(an);
+                }
+                pg.dev_add = reinterpret_cast<AddNode*>(arena + pg.off_nodes);
+                ck(cudaMemcpy(pg.dev_add, tab.data(), tab.size() * sizeof(AddNode), cudaMemcpyHostToDevice),
+                   "upload add table");
+            }
+        }
+        // op tallies
+        tensor_macs = int8_macs = ew_adds = 0;
+        for (auto& lg : leaves) {
+            uint64_t macs = (uint64_t)lg.count * lg.n * (lg.n + 1) / 2 * lg.k;
+            tensor_macs += macs;
+            int8_macs += (uint64_t)lg.count * lg.ntiles * 128ull * BN * lg.kpad * L * L;
+        }
+        for (auto& gg : gemms) {
+            tensor_macs += (uint64_t)2 * gg.count * gg.h * gg.h * gg.kw;
+            int8_macs += (uint64_t)2 * gg.count * (gg.hpad / 128) * ((gg.h + BN - 1) / BN) * 128ull * BN * gg.kpad * L * L;
+            ew_adds += (uint64_t)gg.count * (4ull * gg.h * gg.kw + 4ull * gg.h * gg.h);
+        }
+    }
+
+    std::string json() const {
+        std::ostringstream o;
+        o << "{\"p\": " << p << ", \"n\": " << n << ", \"k\": " << k << ", \"limbs\": " << L << ", \"block_n\": " << BN
+          << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
+          << "}, \"nodes\": " << nodes.size() << ", \"arena_bytes\": " << arena_bytes
+          << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs << ", \"leaf_groups\": [";
+        for (size_t i = 0; i < leaves.size(); ++i)
+            o << (i ? ", " : "") << "{\"n\": " << leaves[i].n << ", \"k\": " << leaves[i].k
+              << ", \"count\": " << leaves[i].count << ", \"tiles\": " << leaves[i].ntiles << "}";
+        o << "], \"gemm_groups\": [";
+        for (size_t i = 0; i < gemms.size(); ++i)
+            o << (i ? ", " : "") << "{\"h\": " << gemms[i].h << ", \"kw\": " << gemms[i].kw
+              << ", \"count\": " << gemms[i].count << "}";
+        o << "], \"prep_groups\": " << preps.size() << ", \"post_groups\": " << posts.size() << "}";
+        return o.str();
+    }
+
+    void execute(const uint64_t* a_dev, long long lda, uint64_t* c_dev, long long ldc, uint32_t alpha,
+                 uint32_t beta, bool mirror, cudaStream_t s) {
+        int counts[5] = {0, 0, 0, 0, 0};
+        cudaEvent_t ev[6];
+        if (g_phase_timing)
+            for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        auto mark = [&](int i) {
+            if (g_phase_timing) ck(cudaEventRecord(ev[i], s), "event record");
+        };
+        mark(0);
+        const Node& root = nodes[0];
+        // 1. convert the reference-layout input
+        ck(launch_convert_in(a_dev, lda, n, kin, k, colmap ? dev_colmap : nullptr, (uint32_t)p, root_in, root.ldin, s),
+           "convert_in");
+        counts[3]++;
+        // 2. leaf operands that are plain views (root leaf, split-on-k children)
+        for (int li : split_leaves) {
+            const Node& nd = nodes[li];
+            const LeafGroup& lg = leaves[nd.lgroup];
+            ck(launch_split_planes(L, nd.in, nd.ldin, nd.n, nd.k, (uint32_t)p, lg.planes + nd.lslot * lg.slot,
+                                   lg.plane, lg.kpad, s),
+               "split_planes");
+            counts[1]++;
+        }
+        mark(1);
+        // 3. fused pre-additions, top-down
+        for (auto& pg : preps) {
+            ck(launch_prep(pg.args, s), "prep");
+            counts[1]++;
+        }
+        mark(2);
+        // 4. tensor-core products: the general products of every level, then the leaf SYRKs
+        for (auto& gg : gemms) {
+            ModmmArgs a{};
+            a.modp = m;
+            a.c32 = c32;
+            a.M = gg.h;
+            a.N = gg.h;
+            a.k_blocks = gg.kpad / 128;
+            a.tiles_n = (gg.h + BN - 1) / BN;
+            a.syrk = 0;
+            a.vec_ok = gg.h % 4 == 0;
+            a.a_batch_mult = a.b_batch_mult = 1;
+            a.a_batch_off = a.b_batch_off = 0;
+            a.tile_list = nullptr;
+            a.out = gg.out;
+            a.out_batch_stride = (long long)gg.h * gg.h;
+            a.ldo = gg.h;
+            const int ntiles = (gg.hpad / 128) * a.tiles_n;
+            ck(modmm_launch(L, gg.tA, gg.tB, a, ntiles, 2 * gg.count, s), "modmm(gemm)");
+            counts[0]++;
+        }
+        for (auto& lg : leaves) {
+            ModmmArgs a{};
+            a.modp = m;
+            a.c32 = c32;
+            a.M = lg.n;
+            a.N = lg.n;
+            a.k_blocks = lg.kpad / 128;
+            a.tiles_n = (lg.n + BN - 1) / BN;
+            a.syrk = 1;
+            a.vec_ok = lg.n % 4 == 0;
+            a.a_batch_mult = a.b_batch_mult = 1;
+            a.tile_list = lg.tiles;
+            a.out = lg.xout;
+            a.out_batch_stride = (long long)lg.n * lg.n;
+            a.ldo = lg.n;
+            ck(modmm_launch(L, lg.tA, lg.tB, a, lg.ntiles, lg.count, s), "modmm(syrk)");
+            counts[0]++;
+        }
+        mark(3);
+        // 5. post-additions, bottom-up
+        for (auto& pg : posts) {
+            if (pg.kind == LEVEL) {
+                PostArgs a{};
+                a.p = (uint32_t)p;
+                a.h = pg.n / 2;
+                a.nodes = pg.dev_post;
+                a.nnodes = (int)pg.nodes.size();
+                ck(launch_post(a, s), "post");
+            } else {
+                ck(launch_add_lower(pg.dev_add, (int)pg.nodes.size(), pg.n, (uint32_t)p, s), "add_lower");
+            }
+            counts[2]++;
+        }
+        mark(4);
+        // 6. C <- alpha X + beta C (+ mirror), in the reference layout
+        ck(launch_finalize(root.x, root.ldx, n, c_dev, ldc, m, alpha, beta, mirror ? 1 : 0, s), "finalize");
+        counts[3]++;
+        mark(5);
+        std::copy(counts, counts + 5, g_launch_counts);
+        if (g_phase_timing) {
+            ck(cudaEventSynchronize(ev[5]), "event sync");
+            float t;
+            // kinds: 0 products, 1 pre (split + prep), 2 post, 3 convert/finalize
+            cudaEventElapsedTime(&t, ev[2], ev[3]); g_phase_ms[0] = t;
+            float t1, t2;
+            cudaEventElapsedTime(&t1, ev[0], ev[1]);
+            cudaEventElapsedTime(&t2, ev[1], ev[2]);
+            g_phase_ms[1] = t2;
+            cudaEventElapsedTime(&t, ev[3], ev[4]); g_phase_ms[2] = t;
+            float t5;
+            cudaEventElapsedTime(&t5, ev[4], ev[5]);
+            g_phase_ms[3] = t1 + t5;
+            g_phase_ms[4] = 0;
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
+        g_last_plan_json = json();
+    }
+};
+
+// ------------------------------------------------------------ plan cache
+struct PlanKey {
+    uint64_t p;
+    int n, kin, k;
+    uint64_t thr, lev;
+    bool colmap;
+    int dev;
+    bool operator<(const PlanKey& o) const {
+        return std::tie(p, n, kin, k, thr, lev, colmap, dev) < std::tie(o.p, o.n, o.kin, o.k, o.thr, o.lev, o.colmap, o.dev);
+    }
+};
+
+std::mutex g_cache_mu;
+std::map<PlanKey, std::unique_ptr<Plan>> g_cache;
+
+Plan* get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev};
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second.get();
+    auto plan = std::make_unique<Plan>();
+    plan->create(p, n, kin, k, pol, colmap);
+    Plan* raw = plan.get();
+    g_cache[key] = std::move(plan);
+    return raw;
+}
+
+// ------------------------------------------------------------- validation
+void validate_field(uint64_t p) {
+    if (p >= (1ull << 31)) fail(FSYRK_B200_EINVAL, "prime modulus must be < 2^31, got " + std::to_string(p));
+    if (!host::is_prime(p)) fail(FSYRK_B200_EINVAL, std::to_string(p) + " is not prime");
+}
+void validate_policy(fsyrk_b200_policy pol) {
+    if (pol.threshold < 2) fail(FSYRK_B200_EINVAL, "recursion threshold must be >= 2");
+}
+void validate_shapes(size_t n, size_t k, size_t lda, size_t ldc) {
+    if (lda < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "syrk_fast: dimension mismatch (stride smaller than row)");
+    if (n > (size_t)INT32_MAX / 2 || k > (size_t)INT32_MAX / 2) fail(FSYRK_B200_EDIMENSION, "matrix too large");
+}
+bool ranges_overlap(const void* a, size_t a_bytes, const void* b, size_t b_bytes) {
+    if (a_bytes == 0 || b_bytes == 0) return false;
+    auto pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+    return pa < pb + b_bytes && pb < pa + a_bytes;
+}
+size_t span_bytes(size_t rows, size_t cols, size_t ld) { return rows == 0 || cols == 0 ? 0 : ((rows - 1) * ld + cols) * 8; }
+
+// syrkd column map (include/fsyrk/scaled_syrk.hpp:58-104): returns kbar.
+int build_colmap(uint64_t p, const uint64_t* d, size_t k, std::vector<ColMap>& map) {
+    host::Field f{p};
+    if (p == 2) fail(FSYRK_B200_EINVAL, "syrkd requires an odd prime field");
+    std::vector<size_t> nr;
+    std::vector<uint64_t> dbar(d, d + k);
+    for (auto& v : dbar) v %= p;
+    for (size_t j = 0; j < k; ++j)
+        if (f.legendre(dbar[j]) == -1) nr.push_back(j);
+    const bool augment = nr.size() % 2 == 1;
+    const size_t kbar = k + (augment ? 1 : 0);
+    map.assign(kbar, ColMap{-1, -1, 0, 0});
+    for (size_t j = 0; j < k; ++j) map[j] = ColMap{(int)j, -1, 1, 0};
+    if (augment) {
+        dbar.push_back(dbar[nr.front()]);
+        nr.push_back(k);  // zero column: no source
+    }
+    for (size_t j = 0; j < kbar; ++j)
+        if (f.legendre(dbar[j]) >= 0) {
+            uint64_t s = f.sqrt(dbar[j]);
+            if (map[j].src0 >= 0) map[j].c0 = (uint32_t)f.mul(map[j].c0, s);
+        }
+    for (size_t t = 0; t + 1 < nr.size(); t += 2) {
+        const size_t i = nr[t], j = nr[t + 1];
+        std::array<uint64_t, 4> y;
+        if (!host::nrsyf(f, dbar[i], dbar[j], y)) fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
+        // (u, v) -> (y0 u + y2 v, y1 u + y3 v); u, v are (scaled) original columns or the zero column
+        const ColMap u = map[i], v = map[j];
+        auto comb = [&](uint64_t cu, uint64_t cv) {
+            ColMap r{-1, -1, 0, 0};
+            if (u.src0 >= 0) { r.src0 = u.src0; r.c0 = (uint32_t)f.mul(cu, u.c0); }
+            if (v.src0 >= 0) {
+                if (r.src0 < 0) { r.src0 = v.src0; r.c0 = (uint32_t)f.mul(cv, v.c0); }
+                else { r.src1 = v.src0; r.c1 = (uint32_t)f.mul(cv, v.c0); }
+            }
+            return r;
+        };
+        map[i] = comb(y[0], y[2]);
+        map[j] = comb(y[1], y[3]);
+    }
+    return (int)kbar;
+}
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        ck(cudaMalloc(&ptr, b), "cudaMalloc(staging)");
+        bytes = b;
+    }
+    ~DevBuf() {
+        if (ptr) cudaFree(ptr);
+    }
+};
+
+std::mutex g_stage_mu;
+DevBuf g_stage_a, g_stage_c;
+
+void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
+    if (!ops) return;
+    ops->mults += plan->tensor_macs;
+    ops->adds += plan->ew_adds;
+}
+
+// Core device call: everything resident on the device.
+void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda, const uint64_t* d,
+             uint32_t beta, uint64_t* c_dev, size_t ldc, fsyrk_b200_policy pol, bool mirror, cudaStream_t s,
+             fsyrk_b200_opcount* ops) {
+    validate_field(p);
+    validate_policy(pol);
+    validate_shapes(n, k, lda, ldc);
+    require_device();
+    if (n == 0) return;
+    int kbar = (int)k;
+    std::vector<ColMap> map;
+    if (d) kbar = build_colmap(p, d, k, map);
+    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, d != nullptr);
+    if (d) ck(cudaMemcpyAsync(plan->dev_colmap, map.data(), map.size() * sizeof(ColMap), cudaMemcpyHostToDevice, s),
+              "upload colmap");
+    plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
+    fill_ops(ops, plan);
+}
+
+// Host call: stage A (and C when accumulating) through device buffers.
+void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const uint64_t* d,
+              uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy pol, bool mirror, fsyrk_b200_opcount* ops) {
+    validate_field(p);
+    validate_policy(pol);
+    validate_shapes(n, k, lda, ldc);
+    if (ranges_overlap(a, span_bytes(n, k, lda), c, span_bytes(n, n, ldc)))
+        fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
+    require_device();
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    const size_t abytes = n * std::max<size_t>(k, 1) * 8, cbytes = n * n * 8;
+    g_stage_a.ensure(abytes);
+    g_stage_c.ensure(cbytes);
+    uint64_t* da = static_cast<uint64_t*>(g_stage_a.ptr);
+    uint64_t* dc = static_cast<uint64_t*>(g_stage_c.ptr);
+    cudaStream_t s = 0;
+    if (k > 0) ck(cudaMemcpy2DAsync(da, k * 8, a, lda * 8, k * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+    const bool need_c = (beta % p) != 0;
+    if (need_c) ck(cudaMemcpy2DAsync(dc, n * 8, c, ldc * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D C");
+    run_dev(p, (uint32_t)(alpha % p), da, n, k, k == 0 ? 1 : k, d, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
+    // copy back the lower triangle (and the upper when mirrored): full rows, then keep the caller's upper
+    if (mirror) {
+        ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+    } else {
+        std::vector<uint64_t> tmp;
+        // rows are copied whole; restore the caller's strict upper triangle afterwards
+        tmp.resize(n * n);
+        ck(cudaMemcpy2DAsync(tmp.data(), n * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+        ck(cudaStreamSynchronize(s), "sync");
+        for (size_t i = 0; i < n; ++i) std::memcpy(c + i * ldc, tmp.data() + i * n, (i + 1) * 8);
+    }
+    ck(cudaStreamSynchronize(s), "sync");
+}
+
+}  // namespace
+
+}  // namespace fsyrk_b200
+
+using namespace fsyrk_b200;
+
+extern "C" {
+
+const char* fsyrk_b200_last_error(void) { return g_last_error.c_str(); }
+int fsyrk_b200_abi_version(void) { return FSYRK_B200_ABI_VERSION; }
+int fsyrk_b200_device_available(void) { return device_ok(); }
+
+int fsyrk_b200_skew_orthogonal(uint64_t p, size_t dim, fsyrk_b200_skew* skew) {
+    return guarded([&] {
+        validate_field(p);
+        host::Skew y = host::skew_orthogonal(host::Field{p});
+        if (y.form == 1 && dim % 2 != 0)
+            fail(FSYRK_B200_EPARITY, "pair-form skew-orthogonal matrix requires an even dimension");
+        if (skew) *skew = fsyrk_b200_skew{y.form, y.a, y.b, y.ycost};
+    });
+}
+
+int fsyrk_b200_make_syrk_plan(uint64_t p, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_skew* skew) {
+    (void)mirror_output;
+    return guarded([&] {
+        validate_policy(policy);
+        validate_field(p);
+        host::Skew y = host::skew_orthogonal(host::Field{p});
+        if (skew) *skew = fsyrk_b200_skew{y.form, y.a, y.b, y.ycost};
+    });
+}
+
+int fsyrk_b200_random_matrix(uint64_t p, size_t rows, size_t cols, uint64_t seed, uint64_t* out, size_t ld) {
+    return guarded([&] {
+        validate_field(p);
+        if (ld < cols) fail(FSYRK_B200_EDIMENSION, "random_matrix: stride smaller than row");
+        std::mt19937_64 rng(seed);
+        std::uniform_int_distribution<uint64_t> dist(0, p - 1);
+        for (size_t i = 0; i < rows; ++i)
+            for (size_t j = 0; j < cols; ++j) out[i * ld + j] = dist(rng);
+    });
+}
+
+int fsyrk_b200_syrk_fast_into(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c, size_t ldc,
+                              fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
+    return guarded([&] { run_host(p, 1, a, n, k, lda, nullptr, 0, c, ldc, policy, mirror_output != 0, ops); });
+}
+
+int fsyrk_b200_syrk_fast_acc(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                             uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy, int mirror_output,
+                             fsyrk_b200_opcount* ops) {
+    return guarded([&] { run_host(p, alpha, a, n, k, lda, nullptr, beta, c, ldc, policy, mirror_output != 0, ops); });
+}
+
+int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const uint64_t* d,
+                     uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy, int mirror_output,
+                     fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        if (!d && k > 0) fail(FSYRK_B200_EDIMENSION, "syrkd: diagonal length must match column count");
+        static const uint64_t none = 0;
+        run_host(p, alpha, a, n, k, lda, d ? d : &none, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                        const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc, fsyrk_b200_policy policy,
+                        int mirror_output, void* stream, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host, (uint32_t)(beta % p), c_dev, ldc, policy,
+                mirror_output != 0, static_cast<cudaStream_t>(stream), ops);
+    });
+}
+
+void fsyrk_b200_release_cache(void) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.clear();
+}
+
+int fsyrk_b200_last_launch_count(int* by_kind, int nkinds) {
+    int total = 0;
+    for (int i = 0; i < 5; ++i) {
+        total += g_launch_counts[i];
+        if (by_kind && i < nkinds) by_kind[i] = g_launch_counts[i];
+    }
+    return total;
+}
+
+const char* fsyrk_b200_last_plan_json(void) { return g_last_plan_json.c_str(); }
+
+int fsyrk_b200_set_phase_timing(int enable) {
+    g_phase_timing = enable != 0;
+    return 0;
+}
+
+int fsyrk_b200_last_phase_ms(float* out, int nkinds) {
+    for (int i = 0; i < 5 && i < nkinds; ++i) out[i] = g_phase_ms[i];
+    return 0;
+}
+
+int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* s1, uint64_t* s2,
+                            uint64_t* s3, uint64_t* s4, uint64_t* p1, uint64_t* p2, uint64_t* p3, uint64_t* p4,
+                            uint64_t* p5, size_t* kw_out) {
+    return guarded([&] {
+        validate_field(p);
+        validate_shapes(n, k, lda, n);
+        require_device();
+        fsyrk_b200_policy pol{2, 1};
+        Plan plan;
+        plan.create(p, (int)n, (int)k, (int)k, pol, false);
+        const Node& root = plan.nodes[0];
+        if (root.kind != LEVEL) fail(FSYRK_B200_EDIMENSION, "level_blocks: shape does not admit a recursion level");
+        DevBuf da, dc;
+        da.ensure(n * k * 8);
+        dc.ensure(n * n * 8);
+        ck(cudaMemcpy2D(da.ptr, k * 8, a, lda * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D");
+        plan.execute(static_cast<uint64_t*>(da.ptr), (long long)k, static_cast<uint64_t*>(dc.ptr), (long long)n, 1, 0,
+                     false, 0);
+        ck(cudaDeviceSynchronize(), "sync");
+        const int h = root.h, kw = root.kw, L = plan.L;
+        if (kw_out) *kw_out = (size_t)kw;
+        const GemmGroup& g = plan.gemms[root.ggroup];
+        // recombine limb planes -> residues on the host (white-box readback only)
+        auto read_planes = [&](const int8_t* base, long long plane, long long row, int rows, int cols, uint64_t* out) {
+            std::vector<int8_t> buf((size_t)plane * L);
+            ck(cudaMemcpy(buf.data(), base, buf.size(), cudaMemcpyDeviceToHost), "D2H planes");
+            for (int i = 0; i < rows; ++i)
+                for (int j = 0; j < cols; ++j) {
+                    long long v = 0, w = 1;
+                    for (int l = 0; l < L; ++l) {
+                        v += (long long)buf[(size_t)l * plane + (size_t)i * row + j] * w;
+                        w *= 256;
+                    }
+                    long long r = v % (long long)p;
+                    if (r < 0) r += (long long)p;
+                    out[(size_t)i * cols + j] = (uint64_t)r;
+                }
+        };
+        if (s1) read_planes(g.ga + (2LL * root.gslot) * g.slot, g.plane, g.kpad, h, kw, s1);
+        if (s2) read_planes(g.gb + (2LL * root.gslot) * g.slot, g.plane, g.kpad, h, kw, s2);
+        if (s4) read_planes(g.gb + (2LL * root.gslot + 1) * g.slot, g.plane, g.kpad, h, kw, s4);
+        if (s3) {
+            const Node& c2 = plan.nodes[root.ch[2]];
+            const LeafGroup& lg = plan.leaves[c2.lgroup];
+            read_planes(lg.planes + c2.lslot * lg.slot, lg.plane, lg.kpad, h, kw, s3);
+        }
+        auto read_u32 = [&](const uint32_t* src, long long ld, uint64_t* out) {
+            std::vector<uint32_t> buf((size_t)h * h);
+            ck(cudaMemcpy2D(buf.data(), h * 4, src, ld * 4, h * 4, h, cudaMemcpyDeviceToHost), "D2H P");
+            for (size_t i = 0; i < buf.size(); ++i) out[i] = buf[i];
+        };
+        if (p1) read_u32(plan.nodes[root.ch[0]].x, plan.nodes[root.ch[0]].ldx, p1);
+        if (p2) read_u32(plan.nodes[root.ch[1]].x, plan.nodes[root.ch[1]].ldx, p2);
+        if (p5) read_u32(plan.nodes[root.ch[2]].x, plan.nodes[root.ch[2]].ldx, p5);
+        if (p4) read_u32(g.out + (2LL * root.gslot) * g.h * g.h, g.h, p4);
+        if (p3) read_u32(g.out + (2LL * root.gslot + 1) * g.h * g.h, g.h, p3);
+    });
+}
+
+int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
+                       size_t ldb, uint64_t* c, size_t ldc) {
+    return guarded([&] {
+        validate_field(p);
+        if (lda < k || ldb < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "gemm_nt: dimension mismatch");
+        require_device();
+        if (m == 0 || n == 0) return;
+        const int L = limbs_for(p), BN = modmm_block_n(L);
+        if (k > modmm_k_limit(L)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
+        const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
+        const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
+        DevBuf d64a, d64b, r32, pa, pb, out;
+        d64a.ensure(m * std::max<size_t>(k, 1) * 8);
+        d64b.ensure(n * std::max<size_t>(k, 1) * 8);
+        r32.ensure(std::max(m, n) * std::max<size_t>(k, 1) * 4);
+        pa.ensure((size_t)(mpad * kpad * L));
+        pb.ensure((size_t)(npad * kpad * L));
+        out.ensure(m * n * 4);
+        ck(cudaMemset(pa.ptr, 0, pa.bytes), "memset");
+        ck(cudaMemset(pb.ptr, 0, pb.bytes), "memset");
+        if (k > 0) {
+            ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
+            ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
+            uint32_t* r = static_cast<uint32_t*>(r32.ptr);
+            ck(launch_convert_in(static_cast<uint64_t*>(d64a.ptr), k, (int)m, (int)k, (int)k, nullptr, (uint32_t)p, r,
+                                 k, 0), "convert A");
+            ck(launch_split_planes(L, r, k, (int)m, (int)k, (uint32_t)p, static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad,
+                                   0), "split A");
+            ck(launch_convert_in(static_cast<uint64_t*>(d64b.ptr), k, (int)n, (int)k, (int)k, nullptr, (uint32_t)p, r,
+                                 k, 0), "convert B");
+            ck(launch_split_planes(L, r, k, (int)n, (int)k, (uint32_t)p, static_cast<int8_t*>(pb.ptr), npad * kpad, kpad,
+                                   0), "split B");
+        }
+        CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128);
+        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, BN);
+        ModmmArgs args{};
+        args.modp = make_modp((uint32_t)p);
+        args.c32 = (uint32_t)pow_mod(2, 32, p);
+        args.M = (int)m;
+        args.N = (int)n;
+        args.k_blocks = (int)(kpad / 128);
+        args.tiles_n = (int)((n + BN - 1) / BN);
+        args.syrk = 0;
+        args.vec_ok = n % 4 == 0;
+        args.a_batch_mult = args.b_batch_mult = 1;
+        args.out = static_cast<uint32_t*>(out.ptr);
+        args.out_batch_stride = 0;
+        args.ldo = (long long)n;
+        ck(modmm_launch(L, ta, tb, args, (int)(mpad / 128) * args.tiles_n, 1, 0), "modmm");
+        ck(cudaDeviceSynchronize(), "sync");
+        std::vector<uint32_t> buf(m * n);
+        ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");
+        for (size_t i = 0; i < m; ++i)
+            for (size_t j = 0; j < n; ++j) c[i * ldc + j] = buf[i * n + j];
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Device-side Z/pZ arithmetic (p < 2^31) and the int8 limb representation.
+//
+// The reference stores residues as uint64 in [0, p) and reduces every
+// product with a 64-bit '%' (include/fsyrk/fields.hpp:49-66).  On the GPU
+// residues live as uint32 and products are reduced with Barrett (one
+// 64-bit mul-hi, one correction); there is no hardware 64-bit divide.
+#pragma once
+
+#include <cstdint>
+
+namespace fsyrk_b200 {
+
+// Per-prime constants, computed on the host (see driver.cu: make_modp).
+struct ModP {
+    uint32_t p;
+    uint32_t pad_;
+    uint64_t mu;   // floor(2^64 / p)
+    uint64_t off;  // multiple of p >= 2^62: lifts a signed |v| < 2^62 to unsigned
+};
+
+__host__ __device__ inline ModP make_modp(uint32_t p) {
+    ModP m;
+    m.p = p;
+    m.pad_ = 0;
+    m.mu = ~0ull / p;  // floor((2^64 - 1) / p) == floor(2^64 / p) for p not a power of 2
+    m.off = (uint64_t)p * ((1ull << 62) / p + 1);
+    return m;
+}
+
+// x mod p for any uint64 x.
+__device__ __forceinline__ uint32_t mod_u64(uint64_t x, const ModP& m) {
+    uint64_t q = __umul64hi(x, m.mu);
+    uint64_t r = x - q * m.p;
+    if (r >= m.p) r -= m.p;
+    return (uint32_t)r;
+}
+
+// v mod p for signed |v| < 2^62.
+__device__ __forceinline__ uint32_t mod_s64(int64_t v, const ModP& m) { return mod_u64((uint64_t)(v + (int64_t)m.off), m); }
+
+__device__ __forceinline__ uint32_t addm(uint32_t a, uint32_t b, uint32_t p) {
+    uint32_t s = a + b;
+    return s >= p ? s - p : s;
+}
+__device__ __forceinline__ uint32_t subm(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
+__device__ __forceinline__ uint32_t mulm(uint32_t a, uint32_t b, const ModP& m) {
+    return mod_u64((uint64_t)a * b, m);
+}
+
+// Balanced int8 limbs.  A residue x is mapped to a representative r of its
+// class inside the window [lo, lo + 256^L) with lo = -128 (256^L - 1)/255,
+// then r = sum_l d_l 256^l with every d_l in [-128, 127].  The window holds
+// 256^L >= p integers, so every residue has such an r (Appendix B of SURVEY).
+template <int L>
+struct Limbs {
+    static constexpr int64_t span = 1ll << (8 * L);
+    static constexpr int64_t lo = -128ll * ((span - 1) / 255);
+    static constexpr int64_t hi = lo + span - 1;
+};
+
+template <int L>
+__device__ __forceinline__ void split_limbs(uint32_t x, uint32_t p, int8_t (&d)[L]) {
+    int64_t r = (int64_t)x;
+    if (r > Limbs<L>::hi) r -= p;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        int64_t dl = ((r + 128) & 255) - 128;
+        d[l] = (int8_t)dl;
+        r = (r - dl) >> 8;
+    }
+}
+
+}  // namespace fsyrk_b200

@@ -1,0 +1,394 @@
+"""Python mirror of the reference fsyrk PrimeField SYRK interface over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(paths relative to /root/reference/proj):
+
+    PrimeField(p)                        include/fsyrk/fields.hpp:32-93
+    RecursionPolicy(threshold, levels)   include/fsyrk/winograd.hpp:14-21
+    OpCount                              include/fsyrk/opcount.hpp:10-25
+    SkewOrthogonal / skew_orthogonal     include/fsyrk/skew.hpp:21-37, 66-73
+    SyrkPlan / make_syrk_plan            include/fsyrk/fast_syrk.hpp:12-24
+    syrk_fast_into / syrk_fast           include/fsyrk/fast_syrk.hpp:274-289
+    syrk_fast_acc                        include/fsyrk/fast_syrk.hpp:293-303
+    syrkd                                include/fsyrk/scaled_syrk.hpp:58-104
+    random_matrix                        include/fsyrk/matrix.hpp:411-419
+
+Matrices are numpy uint64 arrays with row-major rows (a row stride in
+elements is allowed, as for the reference's views).  Every compute call runs
+on the B200 through libfsyrk_b200.so; there is no CPU fallback -- without
+the library or a device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libfsyrk_b200.so")
+
+UNLIMITED_LEVELS = (1 << 64) - 1  # kUnlimitedLevels, winograd.hpp:9
+
+
+# ----------------------------------------------------------------- errors
+class DimensionError(ValueError):
+    """fsyrk::DimensionError (fields.hpp:21-23)."""
+
+
+class DimensionParityError(ValueError):
+    """fsyrk::DimensionParityError (fields.hpp:25-27)."""
+
+
+class NotNonResidueError(ArithmeticError):
+    """fsyrk::NotNonResidueError (fields.hpp:17-19)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL / missing-device failures (no reference analogue)."""
+
+
+_STATUS = {
+    1: DimensionError,
+    2: ValueError,  # std::invalid_argument
+    3: DimensionParityError,
+    4: NotNonResidueError,
+    5: ArithmeticError,  # std::domain_error
+    6: DeviceError,
+    7: MemoryError,
+    8: DeviceError,
+    9: DeviceError,
+}
+
+
+# ------------------------------------------------------------------ C ABI
+class _Policy(ctypes.Structure):
+    _fields_ = [("threshold", ctypes.c_uint64), ("max_levels", ctypes.c_uint64)]
+
+
+class _OpCount(ctypes.Structure):
+    _fields_ = [("mults", ctypes.c_uint64), ("adds", ctypes.c_uint64)]
+
+
+class _Skew(ctypes.Structure):
+    _fields_ = [("form", ctypes.c_int), ("a", ctypes.c_uint64), ("b", ctypes.c_uint64), ("ycost", ctypes.c_int)]
+
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_lib = None
+
+EXPORTS = (
+    "fsyrk_b200_last_error", "fsyrk_b200_abi_version", "fsyrk_b200_device_available",
+    "fsyrk_b200_make_syrk_plan", "fsyrk_b200_skew_orthogonal", "fsyrk_b200_random_matrix",
+    "fsyrk_b200_syrk_fast_into", "fsyrk_b200_syrk_fast_acc", "fsyrk_b200_syrkd", "fsyrk_b200_syrk_dev",
+    "fsyrk_b200_release_cache", "fsyrk_b200_last_launch_count", "fsyrk_b200_last_plan_json",
+    "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
+)
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfsyrk_b200.so (built by paper_2001_04109_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_2001_04109_b200.build` "
+                          "(the product path has no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    L.fsyrk_b200_last_error.restype = ctypes.c_char_p
+    L.fsyrk_b200_last_plan_json.restype = ctypes.c_char_p
+    L.fsyrk_b200_make_syrk_plan.argtypes = [ctypes.c_uint64, _Policy, ctypes.c_int, ctypes.POINTER(_Skew)]
+    L.fsyrk_b200_skew_orthogonal.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.POINTER(_Skew)]
+    L.fsyrk_b200_random_matrix.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
+                                           _u64p, ctypes.c_size_t]
+    L.fsyrk_b200_syrk_fast_into.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                            ctypes.c_size_t, _u64p, ctypes.c_size_t, _Policy, ctypes.c_int,
+                                            ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrk_fast_acc.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t,
+                                           ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64, _u64p,
+                                           ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrkd.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                   ctypes.c_size_t, _u64p, ctypes.c_uint64, _u64p, ctypes.c_size_t, _Policy,
+                                   ctypes.c_int, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrk_dev.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t,
+                                      ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, ctypes.c_void_p,
+                                      ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    L.fsyrk_b200_last_phase_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    L.fsyrk_b200_level_blocks.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                          ctypes.c_size_t] + [_u64p] * 9 + [ctypes.POINTER(ctypes.c_size_t)]
+    L.fsyrk_b200_gemm_nt.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
+                                     _u64p, ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_size_t]
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().fsyrk_b200_last_error().decode()
+        raise _STATUS.get(status, RuntimeError)(msg)
+
+
+def device_available() -> bool:
+    return bool(lib().fsyrk_b200_device_available())
+
+
+# -------------------------------------------------------------- the field
+class PrimeField:
+    """Z/pZ, 2 <= p < 2^31 prime (fields.hpp:32-93; validation fields.cpp:33-37)."""
+
+    def __init__(self, p: int):
+        p = int(p)
+        if p >= 1 << 31:
+            raise ValueError(f"prime modulus must be < 2^31, got {p}")
+        if not _is_prime(p):
+            raise ValueError(f"{p} is not prime")
+        self.p = p
+
+    def modulus(self) -> int:
+        return self.p
+
+    characteristic = modulus
+
+    def zero(self) -> int:
+        return 0
+
+    def one(self) -> int:
+        return 1
+
+    def add(self, a: int, b: int) -> int:
+        return (a + b) % self.p
+
+    def sub(self, a: int, b: int) -> int:
+        return (a - b) % self.p
+
+    def neg(self, a: int) -> int:
+        return (-a) % self.p
+
+    def mul(self, a: int, b: int) -> int:
+        return (a * b) % self.p
+
+    def from_int(self, v: int) -> int:
+        return int(v) % self.p
+
+    def name(self) -> str:
+        return f"F_{self.p}"
+
+
+def _is_prime(n: int) -> bool:
+    if n < 2:
+        return False
+    if n % 2 == 0:
+        return n == 2
+    d = 3
+    while d * d <= n:
+        if n % d == 0:
+            return False
+        d += 2
+    return True
+
+
+@dataclass
+class RecursionPolicy:
+    threshold: int = 64
+    max_levels: int = UNLIMITED_LEVELS
+
+    def validate(self) -> None:
+        if self.threshold < 2:
+            raise ValueError("recursion threshold must be >= 2")
+
+    def _c(self) -> _Policy:
+        return _Policy(int(self.threshold), int(self.max_levels))
+
+
+@dataclass
+class OpCount:
+    mults: int = 0
+    adds: int = 0
+
+    def total(self) -> int:
+        return self.mults + self.adds
+
+
+@dataclass
+class SkewOrthogonal:
+    form: str  # "scalar" | "pair"
+    a: int
+    b: int
+    dim: int
+    ycost: int
+
+
+@dataclass
+class SyrkPlan:
+    policy: RecursionPolicy = field(default_factory=RecursionPolicy)
+    skew: Optional[SkewOrthogonal] = None
+    mirror_output: bool = False
+
+
+def skew_orthogonal(f: PrimeField, dim: int) -> SkewOrthogonal:
+    s = _Skew()
+    _check(lib().fsyrk_b200_skew_orthogonal(f.p, int(dim), ctypes.byref(s)))
+    return SkewOrthogonal("pair" if s.form == 1 else "scalar", s.a, s.b, int(dim), s.ycost)
+
+
+def make_syrk_plan(f: PrimeField, policy: Optional[RecursionPolicy] = None, mirror_output: bool = False) -> SyrkPlan:
+    policy = policy or RecursionPolicy()
+    policy.validate()
+    s = _Skew()
+    _check(lib().fsyrk_b200_make_syrk_plan(f.p, policy._c(), int(bool(mirror_output)), ctypes.byref(s)))
+    return SyrkPlan(policy, SkewOrthogonal("pair" if s.form == 1 else "scalar", s.a, s.b, 0, s.ycost),
+                    bool(mirror_output))
+
+
+# ------------------------------------------------------------ matrix glue
+def _view(m: np.ndarray, name: str):
+    if not isinstance(m, np.ndarray) or m.dtype != np.uint64 or m.ndim != 2:
+        raise DimensionError(f"{name} must be a 2-D numpy uint64 array")
+    if m.shape[1] > 1 and m.strides[1] != 8:
+        raise DimensionError(f"{name} rows must be contiguous")
+    ld = m.strides[0] // 8 if m.shape[0] > 1 else max(m.shape[1], 1)
+    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(max(ld, m.shape[1]))
+
+
+def random_matrix(f: PrimeField, rows: int, cols: int, seed: int) -> np.ndarray:
+    out = np.empty((int(rows), int(cols)), dtype=np.uint64)
+    _check(lib().fsyrk_b200_random_matrix(f.p, int(rows), int(cols), int(seed) & ((1 << 64) - 1),
+                                          out.ctypes.data_as(_u64p), max(int(cols), 1)))
+    return out
+
+
+def _ops_out(ops: Optional[OpCount], c_ops: _OpCount) -> None:
+    if ops is not None:
+        ops.mults += c_ops.mults
+        ops.adds += c_ops.adds
+
+
+def syrk_fast_into(f: PrimeField, a: np.ndarray, c: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount] = None) -> None:
+    """Low(C) <- Low(A A^T) (fast_syrk.hpp:274-282)."""
+    plan.policy.validate()
+    pa, n, k, lda = _view(a, "a")
+    pc, cn, cm, ldc = _view(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrk_fast: dimension mismatch")
+    co = _OpCount()
+    _check(lib().fsyrk_b200_syrk_fast_into(f.p, pa, n, k, lda, pc, ldc, plan.policy._c(),
+                                           int(plan.mirror_output), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
+def syrk_fast(f: PrimeField, a: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount] = None) -> np.ndarray:
+    """Returns a new C with Low(C) = Low(A A^T), zeros elsewhere (fast_syrk.hpp:284-289)."""
+    c = np.zeros((a.shape[0], a.shape[0]), dtype=np.uint64)
+    syrk_fast_into(f, a, c, plan, ops)
+    return c
+
+
+def syrk_fast_acc(f: PrimeField, alpha: int, a: np.ndarray, beta: int, c: np.ndarray, plan: SyrkPlan,
+                  ops: Optional[OpCount] = None) -> None:
+    """Low(C) <- Low(alpha A A^T + beta C) (fast_syrk.hpp:293-303)."""
+    plan.policy.validate()
+    pa, n, k, lda = _view(a, "a")
+    pc, cn, cm, ldc = _view(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrk_fast_acc: dimension mismatch")
+    co = _OpCount()
+    _check(lib().fsyrk_b200_syrk_fast_acc(f.p, int(alpha) % f.p, pa, n, k, lda, int(beta) % f.p, pc, ldc,
+                                          plan.policy._c(), int(plan.mirror_output), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
+def syrkd(f: PrimeField, a: np.ndarray, d: Sequence[int], plan: SyrkPlan, ops: Optional[OpCount] = None,
+          alpha: int = 1, beta: int = 0, c: Optional[np.ndarray] = None) -> np.ndarray:
+    """Low(A Diag(d) A^T) (scaled_syrk.hpp:58-104); with alpha/beta/c it is the
+    Schur-complement form Low(C) <- Low(alpha A D A^T + beta C) in one call."""
+    plan.policy.validate()
+    if f.p == 2:
+        raise ValueError("syrkd requires an odd prime field")
+    pa, n, k, lda = _view(a, "a")
+    dv = np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+    if dv.ndim != 1 or dv.shape[0] != k:
+        raise DimensionError("syrkd: diagonal length must match column count")
+    if c is None:
+        c = np.zeros((n, n), dtype=np.uint64)
+    pc, cn, cm, ldc = _view(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrkd: dimension mismatch")
+    co = _OpCount()
+    dptr = dv.ctypes.data_as(_u64p) if k > 0 else None
+    _check(lib().fsyrk_b200_syrkd(f.p, int(alpha) % f.p, pa, n, k, lda, dptr, int(beta) % f.p, pc, ldc,
+                                  plan.policy._c(), int(plan.mirror_output), ctypes.byref(co)))
+    _ops_out(ops, co)
+    return c
+
+
+def syrk_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta: int, c_ptr: int, ldc: int,
+             policy: RecursionPolicy, mirror: bool = False, stream: int = 0, d: Optional[np.ndarray] = None,
+             ops: Optional[OpCount] = None) -> None:
+    """Device-resident form (fsyrk_b200_syrk_dev): a_ptr / c_ptr are CUDA device
+    pointers to uint64 matrices; stream is a cudaStream_t handle."""
+    co = _OpCount()
+    dptr = None
+    if d is not None:
+        dv = np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+        dptr = dv.ctypes.data_as(_u64p)
+    _check(lib().fsyrk_b200_syrk_dev(int(p), int(alpha) % p, ctypes.c_void_p(a_ptr), int(n), int(k), int(lda), dptr,
+                                     int(beta) % p, ctypes.c_void_p(c_ptr), int(ldc), policy._c(), int(mirror),
+                                     ctypes.c_void_p(stream), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
+def gemm_nt(f: PrimeField, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """C = A B^T mod p on the tensor cores (gemm_classical_nt, matrix.hpp:317-329)."""
+    pa, m, k, lda = _view(a, "a")
+    pb, n, kb, ldb = _view(b, "b")
+    if kb != k:
+        raise DimensionError("gemm_nt: dimension mismatch")
+    c = np.zeros((m, n), dtype=np.uint64)
+    _check(lib().fsyrk_b200_gemm_nt(f.p, pa, m, k, lda, pb, n, ldb, c.ctypes.data_as(_u64p), max(n, 1)))
+    return c
+
+
+def level_blocks(f: PrimeField, a: np.ndarray):
+    """White-box: the S1..S4 and P1..P5 blocks of one device recursion level."""
+    pa, n, k, lda = _view(a, "a")
+    h = n // 2
+    kw = k // 2 + 1
+    S = [np.zeros((h, kw), dtype=np.uint64) for _ in range(4)]
+    P = [np.zeros((h, h), dtype=np.uint64) for _ in range(5)]
+    kw_out = ctypes.c_size_t(0)
+    _check(lib().fsyrk_b200_level_blocks(f.p, pa, n, k, lda, *[s.ctypes.data_as(_u64p) for s in S],
+                                         *[x.ctypes.data_as(_u64p) for x in P], ctypes.byref(kw_out)))
+    kw = kw_out.value
+    S = [np.ascontiguousarray(s.reshape(-1)[: h * kw].reshape(h, kw)) for s in S]
+    return {"S1": S[0], "S2": S[1], "S3": S[2], "S4": S[3],
+            "P1": P[0], "P2": P[1], "P3": P[2], "P4": P[3], "P5": P[4], "kw": kw}
+
+
+def last_launch_counts() -> dict:
+    arr = (ctypes.c_int * 5)()
+    total = lib().fsyrk_b200_last_launch_count(arr, 5)
+    return {"total": total, "products": arr[0], "pre": arr[1], "post": arr[2], "convert": arr[3], "other": arr[4]}
+
+
+def last_plan() -> dict:
+    s = lib().fsyrk_b200_last_plan_json().decode()
+    return json.loads(s) if s else {}
+
+
+def set_phase_timing(enable: bool) -> None:
+    lib().fsyrk_b200_set_phase_timing(int(enable))
+
+
+def last_phase_ms() -> dict:
+    arr = (ctypes.c_float * 5)()
+    lib().fsyrk_b200_last_phase_ms(arr, 5)
+    return {"products": arr[0], "pre": arr[1], "post": arr[2], "convert": arr[3]}
+
+
+def release_cache() -> None:
+    lib().fsyrk_b200_release_cache()

@@ -1,0 +1,98 @@
+"""Generate the golden fixtures from the UNMODIFIED reference (oracle/_ref/ref_driver).
+
+Run in the build container (needs /root/reference to build ref_driver):
+    make -C oracle && python tests/golden/make_golden.py
+
+Writes tests/golden/reference_cases.npz: for every case the reference's
+inputs (A, and C0 / D where used) and its output Low(C), plus the case
+parameters.  A is the reference's random_matrix(p, n, k, seed); storing it
+pins the mt19937_64 + uniform_int_distribution stream as well.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+
+# (p, n, k, seed, threshold, levels, mode, mirror)
+CASES = []
+# oracle batteries over the reference's primes (test_fast_syrk.cpp:71-98, acceptance.cpp:45-74)
+_rng = np.random.default_rng(2024)
+for p in (5, 13, 131041, 2, 3, 11, 7, 131071, 65537, 65521, 2147483647):
+    for t in range(4):
+        n = int(_rng.integers(1, 65))
+        k = int(_rng.integers(1, 65))
+        thr = (2, 8, 14)[t % 3]
+        CASES.append((p, n, k, 1000 + t, thr, "inf", "plain", False))
+# pair-form padding, classical fallback, wide inputs (test_fast_syrk.cpp:100-118)
+CASES += [
+    (11, 16, 6, 1, 2, "inf", "plain", False), (11, 32, 10, 2, 2, "inf", "plain", False),
+    (11, 6, 6, 3, 2, "inf", "plain", False), (7, 10, 10, 4, 2, "inf", "plain", False),
+    (7, 64, 34, 5, 2, "inf", "plain", False), (131071, 8, 32, 1, 2, "inf", "plain", False),
+    (131071, 16, 96, 2, 4, "inf", "plain", False), (7, 8, 32, 3, 2, "inf", "plain", False),
+    (131071, 64, 64, 321, 4, "1", "plain", False), (131071, 24, 24, 8, 2, "inf", "plain", True),
+    (131071, 16, 16, 9, 2, "inf", "plain", False), (2147483647, 48, 40, 11, 4, "inf", "plain", False),
+]
+# accumulating form (test_fast_syrk.cpp:312-375)
+for (p, n, k, s) in ((131071, 33, 20, 55), (131071, 64, 64, 56), (7, 17, 23, 77), (65521, 40, 24, 57),
+                     (2147483647, 32, 48, 58)):
+    CASES.append((p, n, k, s, 2, "inf", "acc", False))
+# syrkd / Schur update (test_scaled_syrk.cpp:59-135)
+for (p, n, k, s) in ((131071, 32, 16, 5001), (3, 12, 9, 5002), (13, 20, 7, 5003), (7, 16, 16, 5004),
+                     (131071, 48, 31, 5005)):
+    CASES.append((p, n, k, s, 2, "inf", "schur", False))
+
+
+def run_case(case, tmp):
+    p, n, k, seed, thr, lev, mode, mirror = case
+    fa, fc, fc0, fd = (os.path.join(tmp, x) for x in ("a", "c", "c0", "d"))
+    cmd = [DRIVER, "--p", str(p), "--n", str(n), "--k", str(k), "--seed", str(seed), "--threshold", str(thr),
+           "--levels", lev, "--mode", mode, "--cseed", str(seed + 1), "--abseed", str(seed + 2),
+           "--dseed", str(seed + 3), "--out-a", fa, "--out-c", fc, "--out-c0", fc0, "--out-d", fd]
+    if mirror:
+        cmd.append("--mirror")
+    info = json.loads(subprocess.run(cmd, check=True, capture_output=True, text=True).stdout)
+    rec = {
+        "A": np.fromfile(fa, dtype=np.uint64).reshape(n, k),
+        "C": np.fromfile(fc, dtype=np.uint64).reshape(n, n),
+        "meta": np.array([p, n, k, seed, thr, -1 if lev == "inf" else int(lev), int(mirror),
+                          info["alpha"], info["beta"]], dtype=np.int64),
+        "mode": np.array(mode),
+        "digest": np.array(info["digest"]),
+    }
+    if mode in ("acc", "schur"):
+        rec["C0"] = np.fromfile(fc0, dtype=np.uint64).reshape(n, n)
+    if mode == "schur":
+        rec["D"] = np.fromfile(fd, dtype=np.uint64)
+    return rec, info
+
+
+def main():
+    out = {}
+    skews = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for i, case in enumerate(CASES):
+            rec, info = run_case(case, tmp)
+            for key, val in rec.items():
+                out[f"c{i:03d}_{key}"] = val
+            skews[int(case[0])] = (info["skew_form"], info["skew_a"], info["skew_b"])
+    out["ncases"] = np.array(len(CASES))
+    primes = sorted(skews)
+    out["skew_p"] = np.array(primes, dtype=np.uint64)
+    out["skew_form"] = np.array([1 if skews[p][0] == "pair" else 0 for p in primes], dtype=np.int64)
+    out["skew_a"] = np.array([skews[p][1] for p in primes], dtype=np.uint64)
+    out["skew_b"] = np.array([skews[p][2] for p in primes], dtype=np.uint64)
+    path = os.path.join(HERE, "reference_cases.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path}: {len(CASES)} cases, {os.path.getsize(path)} bytes")
+
+
+if __name__ == "__main__":
+    main()

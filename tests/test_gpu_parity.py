@@ -1,0 +1,160 @@
+"""Device-path parity: the CUDA implementation, called through the C ABI,
+against the reference's golden outputs and the pinned C oracle.
+
+Bit-exact on every entry of Low(C) (integer arithmetic; no tolerance)."""
+import numpy as np
+import pytest
+
+import oracle_py as orc
+
+pytestmark = pytest.mark.gpu
+
+UNL = (1 << 64) - 1
+
+
+def _policy(fs, case):
+    return fs.RecursionPolicy(case["threshold"], UNL if case["levels"] is None else case["levels"])
+
+
+def test_golden_cases(gpu, golden):
+    fs = gpu
+    for case in golden["cases"]:
+        f = fs.PrimeField(case["p"])
+        plan = fs.make_syrk_plan(f, _policy(fs, case), mirror_output=case["mirror"])
+        a = case["A"]
+        if case["mode"] == "plain":
+            c = fs.syrk_fast(f, a, plan)
+        elif case["mode"] == "acc":
+            c = case["C0"].copy()
+            fs.syrk_fast_acc(f, case["alpha"], a, case["beta"], c, plan)
+        else:
+            c = case["C0"].copy()
+            fs.syrkd(f, a, case["D"], plan, alpha=case["p"] - 1, beta=1, c=c)
+        assert orc.lower_equal(c, case["C"]), (case["mode"], case["p"], case["n"], case["k"])
+        if case["mirror"]:
+            assert np.array_equal(c, c.T)
+
+
+def test_known_answers(gpu):
+    fs = gpu
+    # 2x2 over F_5 (test_fast_syrk.cpp:54-69): Low = [[0], [1, 0]]
+    f = fs.PrimeField(5)
+    a = np.array([[1, 2], [3, 4]], dtype=np.uint64)
+    c = fs.syrk_fast(f, a, fs.make_syrk_plan(f, fs.RecursionPolicy(2)))
+    assert (c[0, 0], c[1, 0], c[1, 1]) == (0, 1, 0)
+    # CLI round trip (cli_syrk_roundtrip.cmake:13-16, 37-40): mod 101
+    f = fs.PrimeField(101)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy())
+    c = fs.syrk_fast(f, a, plan)
+    assert (c[0, 0], c[1, 0], c[1, 1]) == (5, 11, 25) and c[0, 1] == 0
+    cm = fs.syrk_fast(f, a, fs.make_syrk_plan(f, fs.RecursionPolicy(), mirror_output=True))
+    assert cm.tolist() == [[5, 11], [11, 25]]
+    c0 = np.eye(2, dtype=np.uint64)
+    fs.syrk_fast_acc(f, 2, a, 3, c0, plan)
+    assert (c0[0, 0], c0[1, 0], c0[1, 1]) == (13, 22, 53)
+    # syrkd examples (test_scaled_syrk.cpp:59-100)
+    f7 = fs.PrimeField(7)
+    p7 = fs.make_syrk_plan(f7, fs.RecursionPolicy(2))
+    c = fs.syrkd(f7, np.eye(2, dtype=np.uint64), [3, 5], p7)
+    assert (c[0, 0], c[1, 0], c[1, 1]) == (3, 0, 5)
+    c = fs.syrkd(f7, np.ones((1, 1), dtype=np.uint64), [3], p7)
+    assert c[0, 0] == 3
+
+
+def test_degenerate(gpu):
+    fs = gpu
+    f = fs.PrimeField(131071)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(2))
+    z = fs.syrk_fast(f, np.zeros((16, 16), dtype=np.uint64), plan)
+    assert not np.tril(z).any()
+    i = fs.syrk_fast(f, np.eye(16, dtype=np.uint64), plan)
+    assert np.array_equal(np.tril(i), np.eye(16, dtype=np.uint64))
+    # empty inputs
+    assert fs.syrk_fast(f, np.zeros((0, 5), dtype=np.uint64), plan).shape == (0, 0)
+    c = np.full((3, 3), 9, dtype=np.uint64)
+    fs.syrk_fast_acc(f, 1, np.zeros((3, 0), dtype=np.uint64), 2, c, plan)
+    assert np.array_equal(np.tril(c), np.tril(np.full((3, 3), 18, dtype=np.uint64)))
+    # alpha = 0, beta = 1 leaves Low(C) unchanged; beta = 0 ignores C
+    a = fs.random_matrix(f, 32, 32, 10)
+    c0 = fs.random_matrix(f, 32, 32, 11)
+    c = c0.copy()
+    fs.syrk_fast_acc(f, 0, a, 1, c, plan)
+    assert orc.lower_equal(c, c0)
+    c = np.full((32, 32), 12345, dtype=np.uint64)
+    fs.syrk_fast_acc(f, 7, a, 0, c, plan)
+    assert orc.lower_equal(c, (orc.syrk_classical(131071, a) * np.uint64(7)) % np.uint64(131071))
+
+
+@pytest.mark.parametrize("p", [5, 13, 131041, 2, 3, 11, 7, 131071, 65537, 65521, 2147483647])
+def test_random_battery(gpu, p):
+    # oracle battery (test_fast_syrk.cpp:71-98, acceptance.cpp:45-74), n, k <= 300
+    fs = gpu
+    f = fs.PrimeField(p)
+    rng = np.random.default_rng(p * 1009)
+    for t in range(6):
+        n = int(rng.integers(1, 300))
+        k = int(rng.integers(1, 300))
+        thr = (2, 8, 64)[t % 3]
+        a = orc.random_matrix(p, n, k, int(rng.integers(1 << 62)))
+        c = fs.syrk_fast(f, a, fs.make_syrk_plan(f, fs.RecursionPolicy(thr)))
+        assert orc.lower_equal(c, orc.syrk_classical(p, a)), (p, n, k, thr)
+
+
+def test_white_box_level(gpu):
+    fs = gpu
+    for p, n, k in ((131071, 8, 8), (131071, 64, 48), (65537, 32, 32), (11, 32, 10), (2147483647, 16, 16)):
+        a = orc.random_matrix(p, n, k, 321)
+        dev = fs.level_blocks(fs.PrimeField(p), a)
+        ref = orc.level_blocks(p, a)
+        assert dev["kw"] == ref["kw"]
+        for key in ("S1", "S2", "S3", "S4", "P3", "P4"):
+            assert np.array_equal(dev[key], ref[key]), (p, n, k, key)
+        for key in ("P1", "P2", "P5"):
+            assert orc.lower_equal(dev[key], ref[key]), (p, n, k, key)
+
+
+@pytest.mark.parametrize("p", [65521, 65537, 131071, 2147483647])
+def test_gemm_nt(gpu, p):
+    fs = gpu
+    f = fs.PrimeField(p)
+    for (m, n, k) in ((1, 1, 1), (130, 97, 200), (256, 256, 256), (300, 129, 1000)):
+        a = orc.random_matrix(p, m, k, 1)
+        b = orc.random_matrix(p, n, k, 2)
+        c = fs.gemm_nt(f, a, b)
+        want = np.array([[orc.dot_mod(p, a[i], b[j]) for j in range(n)] for i in range(m)], dtype=np.uint64) \
+            if m * n <= 4096 else None
+        if want is None:
+            full = np.vstack([a, b])
+            s = orc.syrk_classical(p, full)
+            want = s[m:, :m].T.copy()
+        assert np.array_equal(c, want), (p, m, n, k)
+
+
+def test_extreme_values(gpu):
+    # all entries p-1 (largest magnitudes through every limb) and max-window residues
+    fs = gpu
+    for p in (65521, 65537, 131071, 2147483647):
+        f = fs.PrimeField(p)
+        for val in (p - 1, p // 2, p // 2 + 1, 1):
+            a = np.full((96, 160), val, dtype=np.uint64)
+            c = fs.syrk_fast(f, a, fs.make_syrk_plan(f, fs.RecursionPolicy(8)))
+            assert orc.lower_equal(c, orc.syrk_classical(p, a)), (p, val)
+
+
+def test_mirror_and_strided_views(gpu):
+    fs = gpu
+    p = 131071
+    f = fs.PrimeField(p)
+    big = orc.random_matrix(p, 80, 100, 3)
+    a = big[:, 10:74]  # strided view, lda = 100
+    c_big = np.full((80, 90), 5, dtype=np.uint64)
+    c = c_big[:, 3:83]
+    fs.syrk_fast_into(f, a, c, fs.make_syrk_plan(f, fs.RecursionPolicy(4), mirror_output=True))
+    want = orc.syrk_classical(p, np.ascontiguousarray(a))
+    assert orc.lower_equal(np.ascontiguousarray(c), want)
+    assert np.array_equal(c, c.T)
+    assert (c_big[:, :3] == 5).all() and (c_big[:, 83:] == 5).all()
+    # without mirroring the strict upper triangle is left untouched
+    c2 = np.full((80, 80), 77, dtype=np.uint64)
+    fs.syrk_fast_into(f, a, c2, fs.make_syrk_plan(f, fs.RecursionPolicy(4)))
+    assert (c2[np.triu_indices(80, 1)] == 77).all()

@@ -249,9 +249,9 @@ def make_syrk_plan(f: PrimeField, policy: Optional[RecursionPolicy] = None, mirr
 def _view(m: np.ndarray, name: str):
     if not isinstance(m, np.ndarray) or m.dtype != np.uint64 or m.ndim != 2:
         raise DimensionError(f"{name} must be a 2-D numpy uint64 array")
-    if m.shape[1] > 1 and m.strides[1] != 8:
+    if m.size > 0 and m.shape[1] > 1 and m.strides[1] != 8:
         raise DimensionError(f"{name} rows must be contiguous")
-    ld = m.strides[0] // 8 if m.shape[0] > 1 else max(m.shape[1], 1)
+    ld = m.strides[0] // 8 if m.shape[0] > 1 and m.size > 0 else max(m.shape[1], 1)
     return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(max(ld, m.shape[1]))
 
 

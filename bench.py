@@ -1,0 +1,449 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 mod-p SYRK hot path (metric of BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A "step" is one full call of the hot path on one input of the chosen config
+(default cfg2 = configs[1]: p = 131071, A 4096 x 4096, recursion to 512-leaves).
+`value` is effective n^2 k / t (GOPS) over device-resident inputs (CUDA
+events on the launching stream, L2 flushed between steps); `e2e` is the same
+metric through the host C-ABI entry point (pinned host A -> device -> host C).
+Under torchrun every rank runs independent instances of the config ("replicas",
+weak scaling); the timed region is bracketed by barriers and the max over
+ranks is reported.  `--impl reference` times the reference's own CPU
+implementation (oracle/_ref/ref_driver, built from the reference sources) on
+the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+UNL = (1 << 64) - 1
+CONFIGS = {
+    # name: p, n, k, seed, threshold, max_levels, mode  (BASELINE.json "configs", in order)
+    "cfg1": dict(p=65537, n=1024, k=1024, seed=42, threshold=64, levels=1, mode="plain"),
+    "cfg2": dict(p=131071, n=4096, k=4096, seed=42, threshold=1024, levels=UNL, mode="plain"),
+    "cfg3": dict(p=65521, n=8192, k=2048, seed=42, threshold=512, levels=UNL, mode="acc", cseed=43, abseed=7),
+    "cfg4": dict(p=2147483647, n=16384, k=16384, seed=42, threshold=512, levels=UNL, mode="plain"),
+    "cfg5": dict(p=131071, n=32768, k=1024, seed=5001, threshold=512, levels=UNL, mode="schur", cseed=5003,
+                 dseed=5002),
+}
+METRIC = "mod-p SYRK C=AAᵀ effective GOPS (n²k/t) at 1–8 B200; % of tensor-core peak"
+# CPU-baseline samples: same prime / leaf size / mode as the config, smaller n (bounded CPU time)
+CPU_SAMPLE = {
+    "cfg1": dict(n=1024, k=1024, threshold=64, levels="1"),
+    "cfg2": dict(n=2048, k=2048, threshold=1024, levels="inf"),
+    "cfg3": dict(n=2048, k=512, threshold=512, levels="inf"),
+    "cfg4": dict(n=2048, k=2048, threshold=512, levels="inf"),
+    "cfg5": dict(n=4096, k=256, threshold=512, levels="inf"),
+}
+
+
+def load_peaks():
+    peaks = {}
+    try:
+        peaks.update(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))))
+    except Exception:
+        pass
+    try:
+        peaks.update(json.load(open(os.path.join(REPO, "profiles", "int8_peak.json"))))
+    except Exception:
+        pass
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def cpu_reference(cfgname, cfg, threads, reps=1):
+    """Run the unmodified reference (oracle/_ref/ref_driver) on a bounded sample."""
+    drv = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(drv):
+        return None
+    s = CPU_SAMPLE[cfgname]
+    cmd = [drv, "--p", str(cfg["p"]), "--n", str(s["n"]), "--k", str(s["k"]), "--seed", str(cfg["seed"]),
+           "--threshold", str(s["threshold"]), "--levels", s["levels"], "--mode", cfg["mode"],
+           "--threads", str(threads), "--reps", str(reps), "--no-digest"]
+    if "cseed" in cfg:
+        cmd += ["--cseed", str(cfg["cseed"])]
+    if "abseed" in cfg:
+        cmd += ["--abseed", str(cfg["abseed"])]
+    if "dseed" in cfg:
+        cmd += ["--dseed", str(cfg["dseed"])]
+    out = json.loads(subprocess.run(cmd, check=True, capture_output=True, text=True).stdout)
+    e = float(s["n"]) ** 2 * float(s["k"])
+    gops = e * threads * reps / out["wall_seconds"] / 1e9
+    return {"value": round(gops, 4), "unit": "GOPS", "cores": threads, "kind": "reference",
+            "sample": f"reference syrk ({cfg['mode']}) p={cfg['p']} n={s['n']} k={s['k']} threshold={s['threshold']}"
+                      f" levels={s['levels']}, {threads} concurrent instance(s) x {reps}",
+            "seconds": out["wall_seconds"]}
+
+
+def run_reference(args, cfgname, cfg, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    base = cpu_reference(cfgname, cfg, threads, reps=1)
+    if base is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built"}))
+        return
+    times = []
+    for _ in range(args.warmup):
+        cpu_reference(cfgname, cfg, threads, reps=1)
+    for _ in range(args.steps):
+        r = cpu_reference(cfgname, cfg, threads, reps=1)
+        times.append(r["seconds"])
+    s = CPU_SAMPLE[cfgname]
+    e = float(s["n"]) ** 2 * float(s["k"]) * threads
+    total = sum(times)
+    value = e * len(times) / total / 1e9
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference random_matrix)",
+            "impl": "reference",
+            "config": {"workload": cfgname, **{k: v for k, v in cfg.items() if k != "levels"},
+                       "levels": "inf" if cfg["levels"] == UNL else cfg["levels"], "sample": base["sample"]},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GOPS", "cores": threads, "kind": "reference",
+                             "sample": base["sample"]},
+            "e2e": {"value": round(value, 4), "unit": "GOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--threshold", type=int, default=None, help="override the config's recursion threshold")
+    ap.add_argument("--levels", type=int, default=None, help="override the config's max recursion levels")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.threshold is not None:
+        cfg["threshold"] = args.threshold
+    if args.levels is not None:
+        cfg["levels"] = args.levels
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, args.config, cfg, world, rank)
+        return
+
+    import torch
+    import paper_2001_04109_b200 as fs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p, n, k = cfg["p"], cfg["n"], cfg["k"]
+    f = fs.PrimeField(p)
+    policy = fs.RecursionPolicy(cfg["threshold"], cfg["levels"])
+    a_host = fs.random_matrix(f, n, k, cfg["seed"] + rank)
+    alpha, beta, d = 1, 0, None
+    c0_host = None
+    if cfg["mode"] in ("acc", "schur"):
+        c0_host = fs.random_matrix(f, n, n, cfg["cseed"])
+        iu = np.triu_indices(n, 1)
+        c0_host[iu] = c0_host.T[iu]
+    if cfg["mode"] == "acc":
+        # alpha, beta = 1 + rng() % (p-1) from mt19937_64(abseed) (oracle/ref_driver.cpp convention)
+        alpha, beta = _mt_alpha_beta(p, cfg["abseed"])
+    if cfg["mode"] == "schur":
+        d = _mt_nonzero(p, k, cfg["dseed"])
+        alpha, beta = p - 1, 1
+
+    a_dev = torch.from_numpy(a_host.view(np.int64)).to(dev)
+    c_dev = torch.zeros((n, n), dtype=torch.int64, device=dev)
+    c_init = torch.from_numpy(c0_host.view(np.int64)).to(dev) if c0_host is not None else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step():
+        fs.syrk_dev(p, alpha, a_dev.data_ptr(), n, k, k, beta, c_dev.data_ptr(), n, policy, False, sh, d=d)
+
+    def reset_c():
+        if c_init is not None:
+            c_dev.copy_(c_init)
+
+    # warm-up (plan creation happens on the first call)
+    for _ in range(max(args.warmup, 3)):
+        reset_c()
+        step()
+    torch.cuda.synchronize()
+    launches = fs.last_launch_counts()
+    plan = fs.last_plan()
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        # the timed region is milliseconds long: keep the GPU busy with the same step until the
+        # sampler reports, so the clock record covers the load the timed steps run under
+        t_end = time.time() + 3.0
+        while time.time() < t_end and len(clk.samples) < 3:
+            for _ in range(20):
+                reset_c()
+                step()
+            torch.cuda.synchronize()
+        for i in range(args.steps):
+            reset_c()
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        clk.samples = list(clk.samples)  # samples up to the end of the timed region only
+    if world > 1:
+        dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    E = float(n) * n * k
+    value = E * args.steps * world / (ms_max / 1e3) / 1e9
+
+    # parity self-check on the final device output against the reference digest (cfg seeds, rank 0)
+    parity = None
+    ref_json = os.path.join(REPO, "tests", "golden", "configs", f"{args.config}.json")
+    if rank == 0 and os.path.exists(ref_json):
+        try:
+            ref = json.loads(open(ref_json).read())
+            reset_c()
+            step()
+            torch.cuda.synchronize()
+            c_out = c_dev.cpu().numpy().view(np.uint64)
+            import hashlib
+            h = hashlib.sha256()
+            for i in range(n):
+                h.update(np.ascontiguousarray(c_out[i, : i + 1]).astype("<u8").tobytes())
+            parity = "digest-match" if h.hexdigest() == ref["digest"] else "DIGEST-MISMATCH"
+            if rank != 0:
+                parity = None
+        except Exception as ex:  # noqa: BLE001
+            parity = f"unchecked ({type(ex).__name__})"
+
+    # per-phase device times (phase events inside the library, same stream) for the roofline
+    fs.set_phase_timing(True)
+    phase = {"products": 0.0, "pre": 0.0, "post": 0.0, "convert": 0.0}
+    reps = max(3, min(args.steps, 10))
+    for _ in range(reps):
+        reset_c()
+        flush.zero_()
+        step()
+        for key, v in fs.last_phase_ms().items():
+            phase[key] += v / reps
+    fs.set_phase_timing(False)
+    torch.cuda.synchronize()
+
+    # end-to-end through the host C-ABI entry point (pinned host buffers, H2D + D2H inside the timing)
+    e2e = None
+    if not args.no_e2e:
+        a_pin = torch.from_numpy(a_host.view(np.int64)).pin_memory()
+        c_pin = torch.zeros((n, n), dtype=torch.int64).pin_memory()
+        a_np = a_pin.numpy().view(np.uint64)
+        c_np = c_pin.numpy().view(np.uint64)
+        plan_obj = fs.make_syrk_plan(f, policy)
+        def host_step():
+            if cfg["mode"] == "plain":
+                fs.syrk_fast_into(f, a_np, c_np, plan_obj)
+            elif cfg["mode"] == "acc":
+                c_np[:] = c0_host
+                fs.syrk_fast_acc(f, alpha, a_np, beta, c_np, plan_obj)
+            else:
+                c_np[:] = c0_host
+                fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
+        for _ in range(2):
+            host_step()
+        e2e_steps = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            host_step()
+        t1 = time.perf_counter()
+        t_e2e = torch.tensor([t1 - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        secs = float(t_e2e.item())
+        h2d = n * k * 8 + (n * n * 8 if beta else 0)
+        e2e = {"value": round(E * e2e_steps * world / secs / 1e9, 3), "unit": "GOPS", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": n * n * 8}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    L = plan.get("limbs", 3)
+    int8_ops = 2.0 * L * L * plan.get("tensor_macs", 0)
+    nprod = max(1, launches.get("products", 1))
+    prod_ms = phase["products"]
+    peak_i8 = peaks.get("int8_tops")
+    peak_src = "measured int8 (torch._int_mm, profiles/int8_peak.json)"
+    if not peak_i8:
+        peak_i8 = 2.0 * peaks.get("bf16_tflops", 1590.0)
+        peak_src = "2 x measured bf16 (MEASURED_PEAKS.json)"
+    achieved = int8_ops / (prod_ms / 1e3) / 1e12 if prod_ms > 0 else 0.0
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_i8, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / peak_i8, 4) if peak_i8 else None, "traffic": None,
+                "kernel": "modmm (tcgen05 kind::i8 limb products)", "launches_per_step": nprod,
+                "avg_launch_ms": round(prod_ms / nprod, 4), "peak_source": peak_src,
+                "algorithmic_int8_ops_per_step": int8_ops,
+                "phase_ms": {k2: round(v, 4) for k2, v in phase.items()}}
+    cpu = None if args.no_cpu_baseline else cpu_reference(args.config, cfg, 1, 1)
+    if cpu is not None:
+        cpu.pop("seconds", None)
+    clocks = clk.summary()
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues / s8 limbs, s32 accumulate",
+            "data": "synthetic (reference random_matrix stream)",
+            "config": {"workload": args.config, "p": p, "n": n, "k": k, "mode": cfg["mode"],
+                       "threshold": cfg["threshold"], "levels": "inf" if cfg["levels"] == UNL else cfg["levels"],
+                       "parallelism": f"replicas x{world}", "l2": "flushed between steps (256 MiB write)"},
+            "parity": parity, "gpu_launches": launches["total"] * args.steps,
+            "launches_per_step": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("limbs", "block_n", "nodes", "leaf_groups",
+                                                                     "gemm_groups", "arena_bytes")}}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _mt_alpha_beta(p, seed):
+    """alpha, beta = 1 + rng() % (p - 1) from std::mt19937_64(seed)."""
+    x = _mt64(seed, 2)
+    return 1 + int(x[0]) % (p - 1), 1 + int(x[1]) % (p - 1)
+
+
+def _mt_nonzero(p, count, seed):
+    """uniform_int_distribution<uint64_t>(1, p-1) over mt19937_64(seed) (oracle/ref_driver.cpp
+    make_instance), via libstdc++'s Lemire multiply-shift mapping."""
+    raw = _mt64(seed, count * 2)
+    out = []
+    rng_i = 0
+    rng_range = p - 1
+    while len(out) < count:
+        prod = int(raw[rng_i]) * rng_range
+        rng_i += 1
+        low = prod & ((1 << 64) - 1)
+        if low < rng_range:
+            thr = ((1 << 64) - rng_range) % rng_range
+            while low < thr:
+                if rng_i >= len(raw):
+                    raw = np.concatenate([raw, _mt64_continue(seed, len(raw), count)])
+                prod = int(raw[rng_i]) * rng_range
+                rng_i += 1
+                low = prod & ((1 << 64) - 1)
+        out.append(1 + (prod >> 64))
+    return np.array(out, dtype=np.uint64)
+
+
+def _mt64(seed, count):
+    mt = [0] * 312
+    mt[0] = seed & ((1 << 64) - 1)
+    for i in range(1, 312):
+        mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & ((1 << 64) - 1)
+    idx = 312
+    out = []
+    for _ in range(count):
+        if idx >= 312:
+            for i in range(312):
+                x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[i] = mt[(i + 156) % 312] ^ xa
+            idx = 0
+        z = mt[idx]
+        idx += 1
+        z ^= (z >> 29) & 0x5555555555555555
+        z ^= (z << 17) & 0x71D67FFFEDA60000
+        z ^= (z << 37) & 0xFFF7EEE000000000
+        z ^= z >> 43
+        out.append(z & ((1 << 64) - 1))
+    return np.array(out, dtype=np.uint64)
+
+
+def _mt64_continue(seed, start, count):
+    return _mt64(seed, start + count * 2)[start:]
+
+
+if __name__ == "__main__":
+    main()

@@ -864,17 +864,10 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     const bool need_c = (beta % p) != 0;
     if (need_c) ck(cudaMemcpy2DAsync(dc, n * 8, c, ldc * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D C");
     run_dev(p, (uint32_t)(alpha % p), da, n, k, k == 0 ? 1 : k, d, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
-    // copy back the lower triangle (and the upper when mirrored): full rows, then keep the caller's upper
-    if (mirror) {
-        ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
-    } else {
-        std::vector<uint64_t> tmp;
-        // rows are copied whole; restore the caller's strict upper triangle afterwards
-        tmp.resize(n * n);
-        ck(cudaMemcpy2DAsync(tmp.data(), n * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
-        ck(cudaStreamSynchronize(s), "sync");
-        for (size_t i = 0; i < n; ++i) std::memcpy(c + i * ldc, tmp.data() + i * n, (i + 1) * 8);
-    }
+    // The strict upper triangle is scratch in the reference (fast_syrk.hpp:271-273).  When C was
+    // uploaded (beta != 0) it still holds the caller's values; otherwise it is cleared to zero.
+    if (!mirror && !need_c) ck(launch_zero_upper(dc, (long long)n, (int)n, s), "zero_upper");
+    ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
     ck(cudaStreamSynchronize(s), "sync");
 }
 

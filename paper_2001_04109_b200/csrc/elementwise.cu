@@ -224,6 +224,12 @@ __global__ void mirror_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
     }
 }
 
+__global__ void zero_upper_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
+    const int i = blockIdx.y;
+    for (int j = i + 1 + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        c[(long long)i * ldc + j] = 0;
+}
+
 __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ x, long long ldx, int rows, int cols,
                                   uint64_t* __restrict__ out, long long ldo) {
     const long long total = (long long)rows * cols;
@@ -303,6 +309,12 @@ cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c
     if (e != cudaSuccess || !mirror) return e;
     const int T = (n + TS - 1) / TS;
     mirror_kernel<<<T * (T + 1) / 2, dim3(32, 8), 0, s>>>(c, ldc, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    zero_upper_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(c, ldc, n);
     return cudaGetLastError();
 }
 

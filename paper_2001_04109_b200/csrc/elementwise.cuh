@@ -75,6 +75,7 @@ cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p
 // C (uint64) <- alpha * X + beta * C on the lower triangle; then optional mirror.
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
                             uint32_t alpha, uint32_t beta, int mirror, cudaStream_t s);
+cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, cudaStream_t s);
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s);
 

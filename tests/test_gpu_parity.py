@@ -154,7 +154,11 @@ def test_mirror_and_strided_views(gpu):
     assert orc.lower_equal(np.ascontiguousarray(c), want)
     assert np.array_equal(c, c.T)
     assert (c_big[:, :3] == 5).all() and (c_big[:, 83:] == 5).all()
-    # without mirroring the strict upper triangle is left untouched
+    # without mirroring the strict upper triangle is scratch (fast_syrk.hpp:271-273): the host
+    # path clears it for beta = 0 and keeps the caller's values when C is read (beta != 0)
     c2 = np.full((80, 80), 77, dtype=np.uint64)
     fs.syrk_fast_into(f, a, c2, fs.make_syrk_plan(f, fs.RecursionPolicy(4)))
-    assert (c2[np.triu_indices(80, 1)] == 77).all()
+    assert (c2[np.triu_indices(80, 1)] == 0).all()
+    c3 = np.full((80, 80), 77, dtype=np.uint64)
+    fs.syrk_fast_acc(f, 1, a, 1, c3, fs.make_syrk_plan(f, fs.RecursionPolicy(4)))
+    assert (c3[np.triu_indices(80, 1)] == 77).all()

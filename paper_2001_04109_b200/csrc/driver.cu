@@ -139,6 +139,14 @@ uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t p) {
     return f.pow(b, e);
 }
 
+// Fold weights of the product epilogue: 256^s mod p as balanced representatives.
+void fill_weights_p(uint64_t p, int32_t* w) {
+    for (int s = 0; s < 8; ++s) {
+        uint64_t v = pow_mod(256, (uint64_t)s, p);
+        w[s] = v > p / 2 ? (int32_t)((int64_t)v - (int64_t)p) : (int32_t)v;
+    }
+}
+
 // ------------------------------------------------------------------- plan
 enum Kind { LEAF = 0, LEVEL = 1, SPLITK = 2 };
 
@@ -149,9 +157,12 @@ struct Node {
     bool padded = false;
     int ch[3] = {-1, -1, -1};
     int parent = -1, role = -1;
-    // input residue view (LEVEL / SPLITK; LEAF when split from a view)
+    // input: an internal residue buffer (in, ldin) or, when in64, the window at
+    // (r0, c0) of the caller's uint64 matrix (top of the tree, no syrkd)
     const uint32_t* in = nullptr;
     long long ldin = 0;
+    bool in64 = false;
+    int r0 = 0, c0 = 0;
     bool leaf_from_prep = false;
     int lgroup = -1, lslot = -1;
     int ggroup = -1, gslot = -1;
@@ -168,10 +179,8 @@ struct LeafGroup {
     int8_t* planes = nullptr;
     uint32_t* xout = nullptr;
     CUtensorMap tA, tB;
-    int2* tiles = nullptr;
-    int ntiles = 0;
-    size_t off_planes = 0, off_x = 0, off_tiles = 0;
-    std::vector<int2> host_tiles;
+    int ntiles = 0;  // lower tiles per SYRK
+    size_t off_planes = 0, off_x = 0;
 };
 
 struct GemmGroup {
@@ -184,8 +193,21 @@ struct GemmGroup {
     size_t off_ga = 0, off_gb = 0, off_out = 0;
 };
 
+// One persistent grouped launch of the product kernel.
+struct ProdLaunch {
+    struct Member {
+        bool leaf;
+        int idx;
+    };
+    std::vector<Member> members;
+    std::vector<int4> host_tiles;
+    size_t off_tiles = 0;
+    GroupedArgs args;
+};
+
 struct PrepGroup {
     int depth, n, k;
+    bool in64 = false;
     std::vector<int> nodes;
     PrepArgs args;
     PrepNode* dev_nodes = nullptr;
@@ -217,13 +239,15 @@ struct Plan {
     int L, BN;
     host::Skew y;
     ModP m;
-    uint32_t c32;
+    uint32_t c32 = 0;
     std::vector<Node> nodes;
     std::vector<LeafGroup> leaves;
     std::vector<GemmGroup> gemms;
     std::vector<PrepGroup> preps;
     std::vector<PostGroup> posts;
     std::vector<int> split_leaves;  // LEAF nodes converted from a residue view
+    std::vector<ProdLaunch> prods;
+    int nsm = 148;
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0;
     uint32_t* root_in = nullptr;
@@ -318,9 +342,30 @@ struct Plan {
 
         build(n, k, pol.max_levels, 0, -1, -1);
         for (auto& nd : nodes)
-            if (nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(L))
-                fail(FSYRK_B200_EINVAL, "leaf inner dimension " + std::to_string(nd.k) +
+            if ((nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(L, p)) ||
+                (nd.kind == LEVEL && (uint64_t)nd.kw > modmm_k_limit(L, p)))
+                fail(FSYRK_B200_EINVAL, "inner dimension " + std::to_string(nd.k) +
                                             " exceeds the exact int32 accumulation bound");
+        // ---- input sources: views of the caller's matrix stay uint64 windows (no conversion
+        // pass); only S3 (and, for syrkd, the transformed root) live in residue buffers.
+        // Nodes are in DFS order, so parents are visited before their children.
+        nodes[0].in64 = !colmap;
+        for (auto& nd : nodes) {
+            if (nd.kind == LEVEL) {
+                Node &q0 = nodes[nd.ch[0]], &q1 = nodes[nd.ch[1]], &q2 = nodes[nd.ch[2]];
+                q0.in64 = q1.in64 = nd.in64;
+                q0.r0 = q1.r0 = nd.r0;
+                q0.c0 = nd.c0;
+                q1.c0 = nd.c0 + nd.kh;
+                q2.in64 = false;
+            } else if (nd.kind == SPLITK) {
+                Node &q0 = nodes[nd.ch[0]], &q1 = nodes[nd.ch[1]];
+                q0.in64 = q1.in64 = nd.in64;
+                q0.r0 = q1.r0 = nd.r0;
+                q0.c0 = nd.c0;
+                q1.c0 = nd.c0 + q0.k;
+            }
+        }
 
         // ---- grouping
         for (int i = 0; i < (int)nodes.size(); ++i) {
@@ -339,8 +384,10 @@ struct Plan {
         // ---- arena layout
         Arena ar;
         const int kin_pad = (int)round_up(k, 4);
-        off_root_in = ar.take((size_t)n * kin_pad * 4);
-        if (colmap) off_colmap = ar.take((size_t)k * sizeof(ColMap));
+        if (colmap) {
+            off_root_in = ar.take((size_t)n * kin_pad * 4);
+            off_colmap = ar.take((size_t)k * sizeof(ColMap));
+        }
         for (auto& lg : leaves) {
             lg.rpad = (int)round_up(lg.n, 128);
             lg.kpad = (int)round_up(std::max(lg.k, 1), 128);
@@ -348,11 +395,9 @@ struct Plan {
             lg.slot = lg.plane * L;
             lg.off_planes = ar.take((size_t)lg.slot * lg.count, 1024);
             lg.off_x = ar.take((size_t)lg.count * lg.n * lg.n * 4);
+            lg.ntiles = 0;
             for (int tm = 0; tm * 128 < lg.n; ++tm)
-                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn)
-                    lg.host_tiles.push_back(make_int2(tm, tn));
-            lg.ntiles = (int)lg.host_tiles.size();
-            lg.off_tiles = ar.take(lg.host_tiles.size() * sizeof(int2));
+                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn) ++lg.ntiles;
         }
         for (auto& gg : gemms) {
             gg.hpad = (int)round_up(gg.h, 128);
@@ -362,6 +407,36 @@ struct Plan {
             gg.off_ga = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
             gg.off_gb = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
             gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
+        }
+        // product launches: every GEMM group and leaf group, kMaxGroups per persistent launch,
+        // tiles (group, batch, tm, tn) ordered longest-K first
+        {
+            struct PG { bool leaf; int idx; int kpad; };
+            std::vector<PG> pgs;
+            for (int i = 0; i < (int)gemms.size(); ++i) pgs.push_back({false, i, gemms[i].kpad});
+            for (int i = 0; i < (int)leaves.size(); ++i) pgs.push_back({true, i, leaves[i].kpad});
+            std::stable_sort(pgs.begin(), pgs.end(), [](const PG& a, const PG& b) { return a.kpad > b.kpad; });
+            for (size_t c0 = 0; c0 < pgs.size(); c0 += kMaxGroups) {
+                ProdLaunch pl;
+                for (size_t c = c0; c < pgs.size() && c < c0 + kMaxGroups; ++c) {
+                    const int gi = (int)(c - c0);
+                    pl.members.push_back({pgs[c].leaf, pgs[c].idx});
+                    if (!pgs[c].leaf) {
+                        const GemmGroup& gg = gemms[pgs[c].idx];
+                        for (int b = 0; b < 2 * gg.count; ++b)
+                            for (int tm = 0; tm * 128 < gg.h; ++tm)
+                                for (int tn = 0; tn * BN < gg.h; ++tn) pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                    } else {
+                        const LeafGroup& lg = leaves[pgs[c].idx];
+                        for (int b = 0; b < lg.count; ++b)
+                            for (int tm = 0; tm * 128 < lg.n; ++tm)
+                                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn)
+                                    pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                    }
+                }
+                pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4));
+                prods.push_back(std::move(pl));
+            }
         }
         std::vector<size_t> off_x(nodes.size(), 0), off_s3(nodes.size(), 0);
         for (size_t i = 0; i < nodes.size(); ++i) {
@@ -375,7 +450,7 @@ struct Plan {
             if (nd.kind != LEVEL) continue;
             bool found = false;
             for (auto& pg : preps)
-                if (pg.depth == nd.depth && pg.n == nd.n && pg.k == nd.k) {
+                if (pg.depth == nd.depth && pg.n == nd.n && pg.k == nd.k && pg.in64 == nd.in64) {
                     pg.nodes.push_back((int)i);
                     found = true;
                 }
@@ -384,6 +459,7 @@ struct Plan {
                 pg.depth = nd.depth;
                 pg.n = nd.n;
                 pg.k = nd.k;
+                pg.in64 = nd.in64;
                 pg.nodes.push_back((int)i);
                 preps.push_back(pg);
             }
@@ -416,16 +492,15 @@ struct Plan {
         arena_bytes = ar.size;
         ck(cudaMalloc(&arena, arena_bytes), "cudaMalloc(plan arena)");
         ck(cudaMemset(arena, 0, arena_bytes), "cudaMemset(plan arena)");
-        root_in = reinterpret_cast<uint32_t*>(arena + off_root_in);
-        if (colmap) dev_colmap = reinterpret_cast<ColMap*>(arena + off_colmap);
+        if (colmap) {
+            root_in = reinterpret_cast<uint32_t*>(arena + off_root_in);
+            dev_colmap = reinterpret_cast<ColMap*>(arena + off_colmap);
+        }
         for (auto& lg : leaves) {
             lg.planes = reinterpret_cast<int8_t*>(arena + lg.off_planes);
             lg.xout = reinterpret_cast<uint32_t*>(arena + lg.off_x);
-            lg.tiles = reinterpret_cast<int2*>(arena + lg.off_tiles);
             lg.tA = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, 128);
             lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, BN);
-            ck(cudaMemcpy(lg.tiles, lg.host_tiles.data(), lg.host_tiles.size() * sizeof(int2), cudaMemcpyHostToDevice),
-               "upload tile list");
         }
         for (auto& gg : gemms) {
             gg.ga = reinterpret_cast<int8_t*>(arena + gg.off_ga);
@@ -434,10 +509,55 @@ struct Plan {
             gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128);
             gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, L, 2 * gg.count, BN);
         }
+        {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        }
+        for (auto& pl : prods) {
+            GroupedArgs& a = pl.args;
+            std::memset(&a, 0, sizeof(a));
+            a.modp = m;
+            fill_weights_p(p, a.w);
+            a.ngroups = (int)pl.members.size();
+            a.ntiles = (int)pl.host_tiles.size();
+            int4* tiles = reinterpret_cast<int4*>(arena + pl.off_tiles);
+            a.tiles = tiles;
+            ck(cudaMemcpy(tiles, pl.host_tiles.data(), pl.host_tiles.size() * sizeof(int4), cudaMemcpyHostToDevice),
+               "upload tile list");
+            for (int gi = 0; gi < a.ngroups; ++gi) {
+                GroupDesc& g = a.g[gi];
+                g.a_mult = g.b_mult = 1;
+                g.a_off = g.b_off = 0;
+                if (!pl.members[gi].leaf) {
+                    const GemmGroup& gg = gemms[pl.members[gi].idx];
+                    g.tmA = gg.tA;
+                    g.tmB = gg.tB;
+                    g.M = g.N = gg.h;
+                    g.k_blocks = gg.kpad / 128;
+                    g.syrk = 0;
+                    g.vec_ok = gg.h % 4 == 0;
+                    g.out = gg.out;
+                    g.out_bs = (long long)gg.h * gg.h;
+                    g.ldo = gg.h;
+                } else {
+                    const LeafGroup& lg = leaves[pl.members[gi].idx];
+                    g.tmA = lg.tA;
+                    g.tmB = lg.tB;
+                    g.M = g.N = lg.n;
+                    g.k_blocks = lg.kpad / 128;
+                    g.syrk = 1;
+                    g.vec_ok = lg.n % 4 == 0;
+                    g.out = lg.xout;
+                    g.out_bs = (long long)lg.n * lg.n;
+                    g.ldo = lg.n;
+                }
+            }
+        }
         // node pointers (top-down: a node's input is set before its children read it)
         for (size_t i = 0; i < nodes.size(); ++i) {
             Node& nd = nodes[i];
-            if (nd.parent < 0) {
+            if (nd.parent < 0 && !nd.in64) {
                 nd.in = root_in;
                 nd.ldin = kin_pad;
             }
@@ -457,13 +577,15 @@ struct Plan {
                 Node& c0 = nodes[nd.ch[0]];
                 Node& c1 = nodes[nd.ch[1]];
                 Node& c2 = nodes[nd.ch[2]];
-                c0.in = nd.in;
-                c0.ldin = nd.ldin;
-                c1.in = nd.in + nd.kh;
-                c1.ldin = nd.ldin;
+                if (!nd.in64) {
+                    c0.in = nd.in;
+                    c0.ldin = nd.ldin;
+                    c1.in = nd.in + nd.kh;
+                    c1.ldin = nd.ldin;
+                }
                 c2.in = nd.s3res;
                 c2.ldin = nd.lds3;
-            } else if (nd.kind == SPLITK) {
+            } else if (nd.kind == SPLITK && !nd.in64) {
                 Node& c0 = nodes[nd.ch[0]];
                 Node& c1 = nodes[nd.ch[1]];
                 c0.in = nd.in;
@@ -486,6 +608,11 @@ struct Plan {
             a.half = a.pair ? n0.kw / 2 : n0.kw;
             a.ya = (uint32_t)y.a;
             a.yb = (uint32_t)y.b;
+            a.cya = make_mulconst(a.ya, (uint32_t)p);
+            a.cyb = make_mulconst(a.yb, (uint32_t)p);
+            a.in64 = pg.in64 ? 1 : 0;
+            a.a64 = nullptr;  // per call
+            a.ld64 = 0;
             a.g_plane = gg.plane;
             a.g_row = gg.kpad;
             a.c_plane = a.c_row = a.c3_plane = a.c3_row = 0;
@@ -504,8 +631,7 @@ struct Plan {
                 const Node& nd = nodes[ni];
                 GemmGroup& g = gemms[nd.ggroup];
                 PrepNode pn{};
-                pn.a = nd.in;
-                pn.lda = nd.ldin;
+                pn.in = InView{nd.in, nd.ldin, nd.r0, nd.c0};
                 pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
                 pn.s2 = g.gb + (2LL * nd.gslot) * g.slot;
                 pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
@@ -609,74 +735,57 @@ struct Plan {
         };
         mark(0);
         const Node& root = nodes[0];
-        // 1. convert the reference-layout input
-        ck(launch_convert_in(a_dev, lda, n, kin, k, colmap ? dev_colmap : nullptr, (uint32_t)p, root_in, root.ldin, s),
-           "convert_in");
-        counts[3]++;
+        // 1. syrkd: convert the reference-layout input with the column transform folded in;
+        //    otherwise the top-level pre-additions read the caller's uint64 matrix directly
+        if (colmap) {
+            ck(launch_convert_in(a_dev, lda, n, kin, k, dev_colmap, (uint32_t)p, root_in, root.ldin, s), "convert_in");
+            counts[3]++;
+        }
         // 2. leaf operands that are plain views (root leaf, split-on-k children)
         for (int li : split_leaves) {
             const Node& nd = nodes[li];
             const LeafGroup& lg = leaves[nd.lgroup];
-            ck(launch_split_planes(L, nd.in, nd.ldin, nd.n, nd.k, (uint32_t)p, lg.planes + nd.lslot * lg.slot,
-                                   lg.plane, lg.kpad, s),
+            ck(launch_split_planes(L, InView{nd.in, nd.ldin, nd.r0, nd.c0}, nd.in64 ? a_dev : nullptr, lda, nd.n, nd.k,
+                                   (uint32_t)p, lg.planes + nd.lslot * lg.slot, lg.plane, lg.kpad, s),
                "split_planes");
             counts[1]++;
         }
         mark(1);
         // 3. fused pre-additions, top-down
         for (auto& pg : preps) {
-            ck(launch_prep(pg.args, s), "prep");
+            PrepArgs a = pg.args;
+            if (a.in64) {
+                a.a64 = a_dev;
+                a.ld64 = lda;
+            }
+            ck(launch_prep(a, s), "prep");
             counts[1]++;
         }
         mark(2);
-        // 4. tensor-core products: the general products of every level, then the leaf SYRKs
-        for (auto& gg : gemms) {
-            ModmmArgs a{};
-            a.modp = m;
-            a.c32 = c32;
-            a.M = gg.h;
-            a.N = gg.h;
-            a.k_blocks = gg.kpad / 128;
-            a.tiles_n = (gg.h + BN - 1) / BN;
-            a.syrk = 0;
-            a.vec_ok = gg.h % 4 == 0;
-            a.a_batch_mult = a.b_batch_mult = 1;
-            a.a_batch_off = a.b_batch_off = 0;
-            a.tile_list = nullptr;
-            a.out = gg.out;
-            a.out_batch_stride = (long long)gg.h * gg.h;
-            a.ldo = gg.h;
-            const int ntiles = (gg.hpad / 128) * a.tiles_n;
-            ck(modmm_launch(L, gg.tA, gg.tB, a, ntiles, 2 * gg.count, s), "modmm(gemm)");
-            counts[0]++;
-        }
-        for (auto& lg : leaves) {
-            ModmmArgs a{};
-            a.modp = m;
-            a.c32 = c32;
-            a.M = lg.n;
-            a.N = lg.n;
-            a.k_blocks = lg.kpad / 128;
-            a.tiles_n = (lg.n + BN - 1) / BN;
-            a.syrk = 1;
-            a.vec_ok = lg.n % 4 == 0;
-            a.a_batch_mult = a.b_batch_mult = 1;
-            a.tile_list = lg.tiles;
-            a.out = lg.xout;
-            a.out_batch_stride = (long long)lg.n * lg.n;
-            a.ldo = lg.n;
-            ck(modmm_launch(L, lg.tA, lg.tB, a, lg.ntiles, lg.count, s), "modmm(syrk)");
+        // 4. tensor-core products: every general product and leaf SYRK of the plan, persistent launches
+        for (auto& pl : prods) {
+            const int grid = std::min(nsm, pl.args.ntiles);
+            ck(modmm_launch(L, pl.args, grid, s), "modmm");
             counts[0]++;
         }
         mark(3);
-        // 5. post-additions, bottom-up
+        // 5. post-additions, bottom-up; the root level writes alpha X + beta C into the caller's C
+        bool root_done = false;
         for (auto& pg : posts) {
             if (pg.kind == LEVEL) {
                 PostArgs a{};
-                a.p = (uint32_t)p;
+                a.m = m;
                 a.h = pg.n / 2;
                 a.nodes = pg.dev_post;
                 a.nnodes = (int)pg.nodes.size();
+                if (pg.depth == 0) {
+                    a.out64 = 1;
+                    a.c64 = c_dev;
+                    a.ldc = ldc;
+                    a.alpha = alpha;
+                    a.beta = beta;
+                    root_done = true;
+                }
                 ck(launch_post(a, s), "post");
             } else {
                 ck(launch_add_lower(pg.dev_add, (int)pg.nodes.size(), pg.n, (uint32_t)p, s), "add_lower");
@@ -684,9 +793,15 @@ struct Plan {
             counts[2]++;
         }
         mark(4);
-        // 6. C <- alpha X + beta C (+ mirror), in the reference layout
-        ck(launch_finalize(root.x, root.ldx, n, c_dev, ldc, m, alpha, beta, mirror ? 1 : 0, s), "finalize");
-        counts[3]++;
+        // 6. root leaf / split: C <- alpha X + beta C in the reference layout; optional mirror
+        if (!root_done) {
+            ck(launch_finalize(root.x, root.ldx, n, c_dev, ldc, m, alpha, beta, s), "finalize");
+            counts[3]++;
+        }
+        if (mirror) {
+            ck(launch_mirror(c_dev, ldc, n, s), "mirror");
+            counts[3]++;
+        }
         mark(5);
         std::copy(counts, counts + 5, g_launch_counts);
         if (g_phase_timing) {
@@ -697,7 +812,8 @@ struct Plan {
             float t1, t2;
             cudaEventElapsedTime(&t1, ev[0], ev[1]);
             cudaEventElapsedTime(&t2, ev[1], ev[2]);
-            g_phase_ms[1] = t2;
+            g_phase_ms[1] = t1 + t2;
+            t1 = 0;
             cudaEventElapsedTime(&t, ev[3], ev[4]); g_phase_ms[2] = t;
             float t5;
             cudaEventElapsedTime(&t5, ev[4], ev[5]);
@@ -1038,7 +1154,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         require_device();
         if (m == 0 || n == 0) return;
         const int L = limbs_for(p), BN = modmm_block_n(L);
-        if (k > modmm_k_limit(L)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
+        if (k > modmm_k_limit(L, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
         const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
         const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
         DevBuf d64a, d64b, r32, pa, pb, out;
@@ -1053,32 +1169,43 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         if (k > 0) {
             ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
             ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
-            uint32_t* r = static_cast<uint32_t*>(r32.ptr);
-            ck(launch_convert_in(static_cast<uint64_t*>(d64a.ptr), k, (int)m, (int)k, (int)k, nullptr, (uint32_t)p, r,
-                                 k, 0), "convert A");
-            ck(launch_split_planes(L, r, k, (int)m, (int)k, (uint32_t)p, static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad,
-                                   0), "split A");
-            ck(launch_convert_in(static_cast<uint64_t*>(d64b.ptr), k, (int)n, (int)k, (int)k, nullptr, (uint32_t)p, r,
-                                 k, 0), "convert B");
-            ck(launch_split_planes(L, r, k, (int)n, (int)k, (uint32_t)p, static_cast<int8_t*>(pb.ptr), npad * kpad, kpad,
-                                   0), "split B");
+            const InView top{nullptr, 0, 0, 0};
+            ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64a.ptr), (long long)k, (int)m, (int)k, (uint32_t)p,
+                                   static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, 0), "split A");
+            ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64b.ptr), (long long)k, (int)n, (int)k, (uint32_t)p,
+                                   static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, 0), "split B");
         }
         CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128);
         CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, BN);
-        ModmmArgs args{};
+        std::vector<int4> tiles;
+        for (int tm = 0; tm * 128 < (int)m; ++tm)
+            for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
+        DevBuf dtiles;
+        dtiles.ensure(tiles.size() * sizeof(int4));
+        ck(cudaMemcpy(dtiles.ptr, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice), "tiles");
+        GroupedArgs args;
+        std::memset(&args, 0, sizeof(args));
         args.modp = make_modp((uint32_t)p);
-        args.c32 = (uint32_t)pow_mod(2, 32, p);
-        args.M = (int)m;
-        args.N = (int)n;
-        args.k_blocks = (int)(kpad / 128);
-        args.tiles_n = (int)((n + BN - 1) / BN);
-        args.syrk = 0;
-        args.vec_ok = n % 4 == 0;
-        args.a_batch_mult = args.b_batch_mult = 1;
-        args.out = static_cast<uint32_t*>(out.ptr);
-        args.out_batch_stride = 0;
-        args.ldo = (long long)n;
-        ck(modmm_launch(L, ta, tb, args, (int)(mpad / 128) * args.tiles_n, 1, 0), "modmm");
+        fill_weights_p(p, args.w);
+        args.ngroups = 1;
+        args.ntiles = (int)tiles.size();
+        args.tiles = static_cast<int4*>(dtiles.ptr);
+        GroupDesc& g = args.g[0];
+        g.tmA = ta;
+        g.tmB = tb;
+        g.M = (int)m;
+        g.N = (int)n;
+        g.k_blocks = (int)(kpad / 128);
+        g.syrk = 0;
+        g.vec_ok = n % 4 == 0;
+        g.a_mult = g.b_mult = 1;
+        g.out = static_cast<uint32_t*>(out.ptr);
+        g.out_bs = 0;
+        g.ldo = (long long)n;
+        int nsm = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        ck(modmm_launch(L, args, std::min<int>(nsm, (int)tiles.size()), 0), "modmm");
         ck(cudaDeviceSynchronize(), "sync");
         std::vector<uint32_t> buf(m * n);
         ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");

@@ -1,23 +1,31 @@
 // HBM-bound mod-p elementwise kernels of the recursion.
 //
-//  convert_in : uint64 reference-layout input -> uint32 residues, with the
-//               optional syrkd column transform folded in
-//               (include/fsyrk/scaled_syrk.hpp:77-101).
+//  convert_in : uint64 reference-layout input -> uint32 residues with the
+//               syrkd column transform folded in
+//               (include/fsyrk/scaled_syrk.hpp:77-101).  Only used for syrkd;
+//               otherwise the first pre-addition reads the caller's matrix.
 //  prep       : the fused pre-additions of one level node, Table 3 steps
 //               1, 2, 4, 6 (include/fsyrk/fast_syrk.hpp:100-115):
 //                 S1 = (A21 - A11) Y, S2 = A22 - A21 Y, S3 = S1 - A22,
 //                 S4 = S3 + A12,
 //               with the Y multiplication (include/fsyrk/skew.hpp:124-167)
-//               and the zero padding of the Pair form (fast_syrk.hpp:34-57)
-//               fused in.  Reads each A element once and writes the GEMM /
-//               leaf operands directly as int8 limb planes.
+//               and the Pair-form zero padding (fast_syrk.hpp:34-57) fused in.
+//               Reads each A element once (uint64 straight from the caller's
+//               matrix at the top levels) and writes the GEMM / leaf operands
+//               directly as int8 limb planes.
 //  post       : the fused post-additions U1..U5 (fast_syrk.hpp:120-132):
 //                 X11 = Low(P1 + P2), X21 = U1 + P4 + P3,
 //                 X22 = Low(U1 + P4 + P4^T),  U1 = sym(P1 + P5),
-//               over 32 x 32 tile pairs with shared-memory transposes.
-//  finalize   : C <- alpha X + beta C on Low(C) (scale_*/U5-with-beta of the
-//               accumulating schedule, fast_syrk.hpp:202-239, matrix.hpp:248-263)
-//               plus mirror_lower_to_upper (matrix.hpp:225-232).
+//               over 32 x 32 tile pairs with shared-memory transposes; at the
+//               root it also applies alpha / beta (the accumulating schedule's
+//               scale_* and U5-with-beta, fast_syrk.hpp:202-239) and writes the
+//               caller's uint64 C.
+//  finalize / mirror / zero_upper: scale_lower_inplace-style accumulate for a
+//               root leaf (matrix.hpp:248-263), mirror_lower_to_upper
+//               (matrix.hpp:225-232), scrubbing of the scratch upper triangle.
+//
+// Vector variants move 4 consecutive columns per thread (16-byte loads,
+// 4-byte packed limb stores); scalar variants cover unaligned shapes.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -49,39 +57,92 @@ __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda,
     }
 }
 
-template <int L>
-__device__ __forceinline__ void put_planes(int8_t* base, long long plane, long long off, uint32_t x, uint32_t p) {
-    int8_t d[L];
-    split_limbs<L>(x, p, d);
-#pragma unroll
-    for (int l = 0; l < L; ++l) base[l * plane + off] = d[l];
+// ------------------------------------------------------------ input access
+struct Src {
+    const uint32_t* p32;
+    long long ld32;
+    const uint64_t* p64;
+    long long ld64;
+    bool in64;
+    __device__ __forceinline__ uint32_t ld(int i, int c, const ModP& m) const {
+        return in64 ? mod_u64(__ldg(p64 + (long long)i * ld64 + c), m) : __ldg(p32 + (long long)i * ld32 + c);
+    }
+    // 4 consecutive columns starting at c (c % 4 == 0, rows 16-byte aligned)
+    __device__ __forceinline__ uint4 ld4(int i, int c, const ModP& m) const {
+        if (in64) {
+            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p64 + (long long)i * ld64 + c);
+            const ulonglong2 x = __ldg(q), y = __ldg(q + 1);
+            return make_uint4(mod_u64(x.x, m), mod_u64(x.y, m), mod_u64(y.x, m), mod_u64(y.y, m));
+        }
+        return __ldg(reinterpret_cast<const uint4*>(p32 + (long long)i * ld32 + c));
+    }
+};
+
+__device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, long long ld64, bool in64) {
+    Src s;
+    s.in64 = in64;
+    s.p32 = v.p32;
+    s.ld32 = v.ld32;
+    s.p64 = in64 ? a64 + (long long)v.r0 * ld64 + v.c0 : nullptr;
+    s.ld64 = ld64;
+    return s;
 }
 
 template <int L>
-__global__ void split_planes_kernel(const uint32_t* __restrict__ a, long long lda, int rows, int k, uint32_t p,
-                                    int8_t* __restrict__ planes, long long plane, long long rs) {
-    const long long total = (long long)rows * k;
+__device__ __forceinline__ void put_planes(int8_t* base, long long plane, long long off, uint32_t x, uint32_t p) {
+    const uint32_t w = limb_word<L>(x, p);
+#pragma unroll
+    for (int l = 0; l < L; ++l) base[l * plane + off] = (int8_t)(w >> (8 * l));
+}
+
+// four consecutive columns of one row, one 32-bit store per plane
+template <int L>
+__device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long long off, uint4 x, uint32_t p) {
+    const uint32_t w0 = limb_word<L>(x.x, p), w1 = limb_word<L>(x.y, p), w2 = limb_word<L>(x.z, p),
+                   w3 = limb_word<L>(x.w, p);
+#pragma unroll
+    for (int l = 0; l < L; ++l) *reinterpret_cast<uint32_t*>(base + l * plane + off) = gather_byte(w0, w1, w2, w3, l);
+}
+
+template <int L, bool VEC>
+__global__ void split_planes_kernel(InView in, const uint64_t* a64, long long ld64, bool in64, int rows, int k,
+                                    ModP m, int8_t* __restrict__ planes, long long plane, long long rs) {
+    const Src src = make_src(in, a64, ld64, in64);
+    constexpr int V = VEC ? 4 : 1;
+    const int cgs = (k + V - 1) / V;
+    const long long total = (long long)rows * cgs;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / k), c = (int)(idx % k);
-        put_planes<L>(planes, plane, (long long)i * rs + c, a[(long long)i * lda + c], p);
+        const int i = (int)(idx / cgs), c = (int)(idx % cgs) * V;
+        if constexpr (VEC) {
+            put_planes4<L>(planes, plane, (long long)i * rs + c, src.ld4(i, c, m), m.p);
+        } else {
+            put_planes<L>(planes, plane, (long long)i * rs + c, src.ld(i, c, m), m.p);
+        }
     }
 }
 
-// One thread per (row i, column pair j) of the h x kw S-blocks.
+// ------------------------------------------------------------------ prep
+// (u, v) -> (a u - b v, b u + a v) on the column halves (skew.hpp:146-163)
+__device__ __forceinline__ void pair_y(uint32_t u, uint32_t v, MulConst ca, MulConst cb, uint32_t p, uint32_t& ru,
+                                       uint32_t& rv) {
+    ru = subm(mulc(u, ca, p), mulc(v, cb, p), p);
+    rv = addm(mulc(u, cb, p), mulc(v, ca, p), p);
+}
+
+// Scalar variant: one thread per (row i, column j) or, in Pair form, per column pair (j, j + half).
 template <int L>
 __global__ void prep_kernel(const PrepArgs args) {
     const PrepNode nd = args.nodes[blockIdx.z];
     const ModP m = args.m;
     const uint32_t p = m.p;
-    const int h = args.h, kh = args.kh, kw = args.kw, half = args.half;
-    const int ncw = args.pair ? half : kw;
+    const int h = args.h, kh = args.kh, half = args.half;
+    const int ncw = args.pair ? half : args.kw;
     const int jp = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (jp >= ncw || i >= h) return;
+    const Src src = make_src(nd.in, args.a64, args.ld64, args.in64 != 0);
 
-    const uint32_t* r1 = nd.a + (long long)i * nd.lda;            // row i of A11 | A12
-    const uint32_t* r2 = nd.a + (long long)(i + h) * nd.lda;      // row i of A21 | A22
     const int nc = args.pair ? 2 : 1;
     int col[2] = {jp, jp + half};
     uint32_t a11[2], a12[2], a21[2], a22[2];
@@ -89,22 +150,18 @@ __global__ void prep_kernel(const PrepArgs args) {
     for (int t = 0; t < 2; ++t) {
         const int c = col[t];
         const bool ok = t < nc && c < kh;
-        a11[t] = ok ? r1[c] : 0;
-        a12[t] = ok ? r1[kh + c] : 0;
-        a21[t] = ok ? r2[c] : 0;
-        a22[t] = ok ? r2[kh + c] : 0;
+        a11[t] = ok ? src.ld(i, c, m) : 0;
+        a12[t] = ok ? src.ld(i, kh + c, m) : 0;
+        a21[t] = ok ? src.ld(i + h, c, m) : 0;
+        a22[t] = ok ? src.ld(i + h, kh + c, m) : 0;
     }
     uint32_t s1[2], ay[2];
     if (args.pair) {
-        const uint32_t d0 = subm(a21[0], a11[0], p), d1 = subm(a21[1], a11[1], p);
-        // (u, v) -> (a u - b v, b u + a v) on the column halves (skew.hpp:146-163)
-        s1[0] = subm(mulm(args.ya, d0, m), mulm(args.yb, d1, m), p);
-        s1[1] = addm(mulm(args.yb, d0, m), mulm(args.ya, d1, m), p);
-        ay[0] = subm(mulm(args.ya, a21[0], m), mulm(args.yb, a21[1], m), p);
-        ay[1] = addm(mulm(args.yb, a21[0], m), mulm(args.ya, a21[1], m), p);
+        pair_y(subm(a21[0], a11[0], p), subm(a21[1], a11[1], p), args.cya, args.cyb, p, s1[0], s1[1]);
+        pair_y(a21[0], a21[1], args.cya, args.cyb, p, ay[0], ay[1]);
     } else {
-        s1[0] = mulm(subm(a21[0], a11[0], p), args.ya, m);
-        ay[0] = mulm(a21[0], args.ya, m);
+        s1[0] = mulc(subm(a21[0], a11[0], p), args.cya, p);
+        ay[0] = mulc(a21[0], args.cya, p);
         s1[1] = ay[1] = 0;
     }
 #pragma unroll
@@ -128,6 +185,72 @@ __global__ void prep_kernel(const PrepArgs args) {
     }
 }
 
+__device__ __forceinline__ uint4 sub4(uint4 a, uint4 b, uint32_t p) {
+    return make_uint4(subm(a.x, b.x, p), subm(a.y, b.y, p), subm(a.z, b.z, p), subm(a.w, b.w, p));
+}
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b, uint32_t p) {
+    return make_uint4(addm(a.x, b.x, p), addm(a.y, b.y, p), addm(a.z, b.z, p), addm(a.w, b.w, p));
+}
+__device__ __forceinline__ uint4 mulc4(uint4 a, MulConst c, uint32_t p) {
+    return make_uint4(mulc(a.x, c, p), mulc(a.y, c, p), mulc(a.z, c, p), mulc(a.w, c, p));
+}
+__device__ __forceinline__ void pair_y4(uint4 u, uint4 v, MulConst ca, MulConst cb, uint32_t p, uint4& ru, uint4& rv) {
+    pair_y(u.x, v.x, ca, cb, p, ru.x, rv.x);
+    pair_y(u.y, v.y, ca, cb, p, ru.y, rv.y);
+    pair_y(u.z, v.z, ca, cb, p, ru.z, rv.z);
+    pair_y(u.w, v.w, ca, cb, p, ru.w, rv.w);
+}
+
+// Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
+// Pair form, their 4 partners) per thread.
+template <int L, bool PAIR, bool IN64>
+__global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
+    const PrepNode nd = args.nodes[blockIdx.z];
+    const ModP m = args.m;
+    const uint32_t p = m.p;
+    const int h = args.h, kh = args.kh, half = args.half;
+    const int ncg = (PAIR ? half : kh) / 4;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y * blockDim.y + threadIdx.y;
+    if (g >= ncg || i >= h) return;
+    const Src src = make_src(nd.in, args.a64, args.ld64, IN64);
+    constexpr int NC = PAIR ? 2 : 1;
+    const int col[2] = {4 * g, 4 * g + half};
+    uint4 a11[NC], a12[NC], a21[NC], a22[NC];
+#pragma unroll
+    for (int t = 0; t < NC; ++t) {
+        a11[t] = src.ld4(i, col[t], m);
+        a12[t] = src.ld4(i, kh + col[t], m);
+        a21[t] = src.ld4(i + h, col[t], m);
+        a22[t] = src.ld4(i + h, kh + col[t], m);
+    }
+    uint4 s1[NC], ay[NC];
+    if constexpr (PAIR) {
+        pair_y4(sub4(a21[0], a11[0], p), sub4(a21[1], a11[1], p), args.cya, args.cyb, p, s1[0], s1[1]);
+        pair_y4(a21[0], a21[1], args.cya, args.cyb, p, ay[0], ay[1]);
+    } else {
+        s1[0] = mulc4(sub4(a21[0], a11[0], p), args.cya, p);
+        ay[0] = mulc4(a21[0], args.cya, p);
+    }
+#pragma unroll
+    for (int t = 0; t < NC; ++t) {
+        const int c = col[t];
+        const uint4 s2 = sub4(a22[t], ay[t], p);
+        const uint4 s3 = sub4(s1[t], a22[t], p);
+        const uint4 s4 = add4(s3, a12[t], p);
+        const long long go = (long long)i * args.g_row + c;
+        put_planes4<L>(nd.s1, args.g_plane, go, s1[t], p);
+        put_planes4<L>(nd.a22, args.g_plane, go, a22[t], p);
+        put_planes4<L>(nd.s2, args.g_plane, go, s2, p);
+        put_planes4<L>(nd.s4, args.g_plane, go, s4, p);
+        if (nd.c_a11) put_planes4<L>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
+        if (nd.c_a12) put_planes4<L>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
+        if (nd.c_s3) put_planes4<L>(nd.c_s3, args.c3_plane, (long long)i * args.c3_row + c, s3, p);
+        if (nd.r_s3) *reinterpret_cast<uint4*>(nd.r_s3 + (long long)i * nd.ld_s3 + c) = s3;
+    }
+}
+
+// ------------------------------------------------------------------ post
 constexpr int TS = 32;  // post / mirror tile
 
 __device__ __forceinline__ void tri_decode(int t, int& I, int& J) {
@@ -138,18 +261,65 @@ __device__ __forceinline__ void tri_decode(int t, int& I, int& J) {
     J = t - r * (r + 1) / 2;
 }
 
+struct PostOut {
+    uint32_t* x;
+    long long ldx;
+    uint64_t* c;
+    long long ldc;
+    bool out64;
+    uint32_t alpha, beta;
+    ModP m;
+    // write element (i, j) of the node output (lower triangle for out64)
+    __device__ __forceinline__ void put(long long i, long long j, uint32_t v) const {
+        if (!out64) {
+            x[i * ldx + j] = v;
+            return;
+        }
+        uint32_t r = alpha == 1 ? v : mulm(v, alpha, m);
+        if (beta != 0) {
+            const uint32_t ci = mod_u64(c[i * ldc + j], m);
+            r = addm(r, beta == 1 ? ci : mulm(ci, beta, m), m.p);
+        }
+        c[i * ldc + j] = r;
+    }
+    __device__ __forceinline__ void put4(long long i, long long j, uint4 v) const {
+        if (!out64) {
+            *reinterpret_cast<uint4*>(x + i * ldx + j) = v;
+            return;
+        }
+        put(i, j, v.x);
+        put(i, j + 1, v.y);
+        put(i, j + 2, v.z);
+        put(i, j + 3, v.w);
+    }
+};
+
+__device__ __forceinline__ PostOut make_out(const PostArgs& a, const PostNode& nd) {
+    PostOut o;
+    o.x = nd.x;
+    o.ldx = nd.ldx;
+    o.c = a.c64;
+    o.ldc = a.ldc;
+    o.out64 = a.out64 != 0;
+    o.alpha = a.alpha;
+    o.beta = a.beta;
+    o.m = a.m;
+    return o;
+}
+
 // Block (32 x 8) per tile pair (I >= J) of one node.
 __global__ void post_kernel(const PostArgs args) {
-    __shared__ uint32_t sU[TS][TS + 1];   // Low(P1 + P5), tile (I, J)
-    __shared__ uint32_t sT[TS][TS + 1];   // P4 tile (J, I)
+    __shared__ uint32_t sU[TS][TS + 1];  // Low(P1 + P5), tile (I, J)
+    __shared__ uint32_t sT[TS][TS + 1];  // P4 tile (J, I)
     const PostNode nd = args.nodes[blockIdx.z];
-    const uint32_t p = args.p;
+    const uint32_t p = args.m.p;
     const int h = args.h;
+    const PostOut out = make_out(args, nd);
     int I, J;
     tri_decode(blockIdx.x, I, J);
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int j = J * TS + tx;       // column inside tile (I, J)
-    const int jt = I * TS + tx;      // column inside tile (J, I)
+    const int j = J * TS + tx;   // column inside tile (I, J)
+    const int jt = I * TS + tx;  // column inside tile (J, I)
     for (int r = ty; r < TS; r += 8) {
         const int i = I * TS + r, it = J * TS + r;
         uint32_t u = 0, t4 = 0;
@@ -159,30 +329,87 @@ __global__ void post_kernel(const PostArgs args) {
         sT[r][tx] = t4;
     }
     __syncthreads();
-    uint32_t* x11 = nd.x;
-    uint32_t* x21 = nd.x + (long long)h * nd.ldx;
-    uint32_t* x22 = x21 + h;
     for (int r = ty; r < TS; r += 8) {
         const int i = I * TS + r;
         if (i < h && j < h) {
-            // U1(i, j) from the lower triangle (symmetric completion on the diagonal tile)
             const uint32_t u1 = (I == J && tx > r) ? sU[tx][r] : sU[r][tx];
             const uint32_t p4 = nd.p4[(long long)i * nd.ld4 + j];
             const uint32_t p3 = nd.p3[(long long)i * nd.ld3 + j];
             const uint32_t u2 = addm(u1, p4, p);
-            x21[(long long)i * nd.ldx + j] = addm(u2, p3, p);
-            x22[(long long)i * nd.ldx + j] = addm(u2, sT[tx][r], p);
-            x11[(long long)i * nd.ldx + j] =
-                addm(nd.p1[(long long)i * nd.ld1 + j], nd.p2[(long long)i * nd.ld2 + j], p);
-        }
-        if (I != J) {
-            // tile (J, I) of X21: U1^T + P4(J, I) + P3(J, I)
-            const int it = J * TS + r;
-            if (it < h && jt < h) {
-                const uint32_t v = addm(addm(sU[tx][r], sT[r][tx], p), nd.p3[(long long)it * nd.ld3 + jt], p);
-                x21[(long long)it * nd.ldx + jt] = v;
+            out.put(h + i, j, addm(u2, p3, p));
+            if (!out.out64 || j <= i) {
+                out.put(h + i, h + j, addm(u2, sT[tx][r], p));
+                out.put(i, j, addm(nd.p1[(long long)i * nd.ld1 + j], nd.p2[(long long)i * nd.ld2 + j], p));
             }
         }
+        if (I != J) {
+            const int it = J * TS + r;
+            if (it < h && jt < h)
+                out.put(h + it, jt, addm(addm(sU[tx][r], sT[r][tx], p), nd.p3[(long long)it * nd.ld3 + jt], p));
+        }
+    }
+}
+
+// Vector variant (h, all ld % 4 == 0): block (8 x 32), thread = 4 columns of one row.
+__global__ void __launch_bounds__(256) post_vec_kernel(const PostArgs args) {
+    __shared__ uint32_t sU[TS][TS + 1];
+    __shared__ uint32_t sT[TS][TS + 1];
+    const PostNode nd = args.nodes[blockIdx.z];
+    const uint32_t p = args.m.p;
+    const int h = args.h;
+    const PostOut out = make_out(args, nd);
+    int I, J;
+    tri_decode(blockIdx.x, I, J);
+    const int tx = threadIdx.x, r = threadIdx.y;
+    const int c0 = 4 * tx;
+    const int i = I * TS + r, j = J * TS + c0;        // tile (I, J)
+    const int it = J * TS + r, jt = I * TS + c0;      // tile (J, I)
+    const bool ok = i < h && j < h, okt = it < h && jt < h;
+    uint4 p1 = {0, 0, 0, 0}, p5 = p1, p4t = p1;
+    if (ok) {
+        p1 = *reinterpret_cast<const uint4*>(nd.p1 + (long long)i * nd.ld1 + j);
+        p5 = *reinterpret_cast<const uint4*>(nd.p5 + (long long)i * nd.ld5 + j);
+    }
+    if (okt) p4t = *reinterpret_cast<const uint4*>(nd.p4 + (long long)it * nd.ld4 + jt);
+    const uint4 l15 = add4(p1, p5, p);
+    sU[r][c0] = l15.x; sU[r][c0 + 1] = l15.y; sU[r][c0 + 2] = l15.z; sU[r][c0 + 3] = l15.w;
+    sT[r][c0] = p4t.x; sT[r][c0 + 1] = p4t.y; sT[r][c0 + 2] = p4t.z; sT[r][c0 + 3] = p4t.w;
+    __syncthreads();
+    if (ok) {
+        const uint4 p4 = *reinterpret_cast<const uint4*>(nd.p4 + (long long)i * nd.ld4 + j);
+        const uint4 p3 = *reinterpret_cast<const uint4*>(nd.p3 + (long long)i * nd.ld3 + j);
+        const uint4 p2 = *reinterpret_cast<const uint4*>(nd.p2 + (long long)i * nd.ld2 + j);
+        uint32_t u1[4], t4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = c0 + e;
+            u1[e] = (I == J && c > r) ? sU[c][r] : sU[r][c];
+            t4[e] = sT[c][r];
+        }
+        const uint4 u2 = add4(make_uint4(u1[0], u1[1], u1[2], u1[3]), p4, p);
+        const uint4 x21 = add4(u2, p3, p);
+        const uint4 x22 = add4(u2, make_uint4(t4[0], t4[1], t4[2], t4[3]), p);
+        const uint4 x11 = add4(p1, p2, p);
+        out.put4(h + i, j, x21);
+        if (!out.out64 || I != J) {
+            out.put4(h + i, h + j, x22);
+            out.put4(i, j, x11);
+        } else {  // diagonal tile of the caller's C: lower entries only
+            const uint32_t a22[4] = {x22.x, x22.y, x22.z, x22.w}, a11[4] = {x11.x, x11.y, x11.z, x11.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (c0 + e <= r) {
+                    out.put(h + i, h + j + e, a22[e]);
+                    out.put(i, j + e, a11[e]);
+                }
+        }
+    }
+    if (I != J && okt) {
+        const uint4 p3t = *reinterpret_cast<const uint4*>(nd.p3 + (long long)it * nd.ld3 + jt);
+        uint32_t v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = addm(sU[c0 + e][r], sT[r][c0 + e], p);
+        out.put4(h + it, jt, add4(make_uint4(v[0], v[1], v[2], v[3]), p3t, p));
     }
 }
 
@@ -197,7 +424,7 @@ __global__ void finalize_kernel(const uint32_t* __restrict__ x, long long ldx, i
                                 long long ldc, ModP m, uint32_t alpha, uint32_t beta) {
     const int i = blockIdx.y;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i && j < n; j += gridDim.x * blockDim.x) {
-        uint32_t v = x[(long long)i * ldx + j];
+        uint32_t v = x ? x[(long long)i * ldx + j] : 0;
         if (alpha != 1) v = mulm(v, alpha, m);
         if (beta != 0) {
             uint32_t ci = mod_u64(c[(long long)i * ldc + j], m);
@@ -246,6 +473,31 @@ int grid_for(long long total, int threads) {
     return (int)(b < 1 ? 1 : b);
 }
 
+template <int L>
+cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
+    const bool vec = !(a.kh % 4) && !(a.half % 4) && a.kw == a.kh && !(a.g_row % 4) && !(a.c_row % 4) &&
+                     !(a.c3_row % 4) &&
+                     (a.in64 ? !(a.ld64 % 2) && !(reinterpret_cast<uintptr_t>(a.a64) % 16) : true);
+    if (vec) {
+        const int ncg = (a.pair ? a.half : a.kh) / 4;
+        dim3 block(32, 8);
+        dim3 grid((ncg + 31) / 32, (a.h + 7) / 8, a.nnodes);
+        if (a.pair) {
+            if (a.in64) prep_vec_kernel<L, true, true><<<grid, block, 0, s>>>(a);
+            else prep_vec_kernel<L, true, false><<<grid, block, 0, s>>>(a);
+        } else {
+            if (a.in64) prep_vec_kernel<L, false, true><<<grid, block, 0, s>>>(a);
+            else prep_vec_kernel<L, false, false><<<grid, block, 0, s>>>(a);
+        }
+    } else {
+        const int ncw = a.pair ? a.half : a.kw;
+        dim3 block(32, 8);
+        dim3 grid((ncw + 31) / 32, (a.h + 7) / 8, a.nnodes);
+        prep_kernel<L><<<grid, block, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, int kout, const ColMap* map,
@@ -257,39 +509,48 @@ cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_split_planes(int L, const uint32_t* a, long long lda, int rows, int k, uint32_t p, int8_t* planes,
-                                long long plane_stride, long long row_stride, cudaStream_t s) {
-    const long long total = (long long)rows * k;
-    if (total == 0) return cudaSuccess;
-    const int g = grid_for(total, 256);
+cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, long long ld64, int rows, int k,
+                                uint32_t p, int8_t* planes, long long plane_stride, long long row_stride,
+                                cudaStream_t s) {
+    if ((long long)rows * k == 0) return cudaSuccess;
+    const bool in64 = a64 != nullptr;
+    const bool vec = !(k % 4) && !(row_stride % 4) &&
+                     (in64 ? !(ld64 % 2) && !(in.c0 % 2) && !(reinterpret_cast<uintptr_t>(a64) % 16)
+                           : !(in.ld32 % 4) && !(reinterpret_cast<uintptr_t>(in.p32) % 16));
+    const ModP m = make_modp(p);
+    const int g = grid_for((long long)rows * (vec ? k / 4 : k), 256);
+#define FSYRK_SPLIT(LL)                                                                                              \
+    if (vec) split_planes_kernel<LL, true><<<g, 256, 0, s>>>(in, a64, ld64, in64, rows, k, m, planes, plane_stride, \
+                                                              row_stride);                                         \
+    else split_planes_kernel<LL, false><<<g, 256, 0, s>>>(in, a64, ld64, in64, rows, k, m, planes, plane_stride,    \
+                                                           row_stride);
     switch (L) {
-        case 2: split_planes_kernel<2><<<g, 256, 0, s>>>(a, lda, rows, k, p, planes, plane_stride, row_stride); break;
-        case 3: split_planes_kernel<3><<<g, 256, 0, s>>>(a, lda, rows, k, p, planes, plane_stride, row_stride); break;
-        case 4: split_planes_kernel<4><<<g, 256, 0, s>>>(a, lda, rows, k, p, planes, plane_stride, row_stride); break;
+        case 2: FSYRK_SPLIT(2) break;
+        case 3: FSYRK_SPLIT(3) break;
+        case 4: FSYRK_SPLIT(4) break;
         default: return cudaErrorInvalidValue;
     }
+#undef FSYRK_SPLIT
     return cudaGetLastError();
 }
 
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s) {
-    const int ncw = args.pair ? args.half : args.kw;
-    if (ncw == 0 || args.h == 0 || args.nnodes == 0) return cudaSuccess;
-    dim3 block(32, 8);
-    dim3 grid((ncw + 31) / 32, (args.h + 7) / 8, args.nnodes);
+    if (args.h == 0 || args.nnodes == 0 || args.kw == 0) return cudaSuccess;
     switch (args.L) {
-        case 2: prep_kernel<2><<<grid, block, 0, s>>>(args); break;
-        case 3: prep_kernel<3><<<grid, block, 0, s>>>(args); break;
-        case 4: prep_kernel<4><<<grid, block, 0, s>>>(args); break;
+        case 2: return prep_dispatch<2>(args, s);
+        case 3: return prep_dispatch<3>(args, s);
+        case 4: return prep_dispatch<4>(args, s);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     if (args.h == 0 || args.nnodes == 0) return cudaSuccess;
     const int T = (args.h + TS - 1) / TS;
     dim3 grid(T * (T + 1) / 2, 1, args.nnodes);
-    post_kernel<<<grid, dim3(32, 8), 0, s>>>(args);
+    // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
+    if (args.h % 4 == 0) post_vec_kernel<<<grid, dim3(8, 32), 0, s>>>(args);
+    else post_kernel<<<grid, dim3(32, 8), 0, s>>>(args);
     return cudaGetLastError();
 }
 
@@ -301,12 +562,15 @@ cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p
 }
 
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
-                            uint32_t alpha, uint32_t beta, int mirror, cudaStream_t s) {
+                            uint32_t alpha, uint32_t beta, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     dim3 grid((n + 255) / 256, n);
     finalize_kernel<<<grid, 256, 0, s>>>(x, ldx, n, c, ldc, m, alpha, beta);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || !mirror) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
     const int T = (n + TS - 1) / TS;
     mirror_kernel<<<T * (T + 1) / 2, dim3(32, 8), 0, s>>>(c, ldc, n);
     return cudaGetLastError();

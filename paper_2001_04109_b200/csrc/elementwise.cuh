@@ -17,10 +17,17 @@ struct ColMap {
     uint32_t c0, c1;
 };
 
+// Where a node reads its input: an internal uint32 residue buffer, or a
+// window of the caller's uint64 matrix (base pointer supplied per call).
+struct InView {
+    const uint32_t* p32;  // used when in64 == 0
+    long long ld32;
+    int r0, c0;           // used when in64 == 1: window origin in the caller's matrix
+};
+
 // One level node of the recursion for the fused pre-addition kernel.
 struct PrepNode {
-    const uint32_t* a;  // node input (n x k residues)
-    long long lda;
+    InView in;
     int8_t* s1;   // GEMM operand slots (limb-plane bases)
     int8_t* a22;
     int8_t* s2;
@@ -35,8 +42,12 @@ struct PrepNode {
 struct PrepArgs {
     ModP m;
     int L;
+    int in64;                 // all nodes of the launch read the caller's uint64 input
+    const uint64_t* a64;      // caller's input (per call)
+    long long ld64;
     int h, kh, kw, half, pair;
     uint32_t ya, yb;
+    MulConst cya, cyb;
     long long g_plane, g_row;    // GEMM operand plane stride / row stride (bytes)
     long long c_plane, c_row;    // leaf operand planes for A11 / A12 (k = kh)
     long long c3_plane, c3_row;  // leaf operand planes for S3 (k = kw)
@@ -52,10 +63,15 @@ struct PostNode {
 };
 
 struct PostArgs {
-    uint32_t p;
+    ModP m;
     int h;
     const PostNode* nodes;
     int nnodes;
+    // out64: the root writes the caller's C directly: C <- alpha X + beta C on Low(C)
+    int out64;
+    uint64_t* c64;
+    long long ldc;
+    uint32_t alpha, beta;
 };
 
 struct AddNode {
@@ -67,14 +83,17 @@ struct AddNode {
 
 cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, int kout, const ColMap* map,
                               uint32_t p, uint32_t* out, long long ldo, cudaStream_t s);
-cudaError_t launch_split_planes(int L, const uint32_t* a, long long lda, int rows, int k, uint32_t p, int8_t* planes,
-                                long long plane_stride, long long row_stride, cudaStream_t s);
+// Residues (uint32 view, or the caller's uint64 window) -> limb planes.
+cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, long long ld64, int rows, int k,
+                                uint32_t p, int8_t* planes, long long plane_stride, long long row_stride,
+                                cudaStream_t s);
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s);
 cudaError_t launch_post(const PostArgs& args, cudaStream_t s);
 cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p, cudaStream_t s);
-// C (uint64) <- alpha * X + beta * C on the lower triangle; then optional mirror.
+// C (uint64) <- alpha * X + beta * C on the lower triangle (X == nullptr: X = 0).
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
-                            uint32_t alpha, uint32_t beta, int mirror, cudaStream_t s);
+                            uint32_t alpha, uint32_t beta, cudaStream_t s);
+cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s);
 cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, cudaStream_t s);
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s);

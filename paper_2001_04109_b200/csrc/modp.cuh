@@ -70,4 +70,36 @@ __device__ __forceinline__ void split_limbs(uint32_t x, uint32_t p, int8_t (&d)[
     }
 }
 
+// Same digits, packed: byte l of the result is d_l.  With the bias
+// B = 128 (1 + 256 + ... + 256^(L-1)), r + B = sum (d_l + 128) 256^l has
+// plain base-256 digits, and d_l = (byte l) - 128 = (byte l) ^ 0x80 as int8.
+template <int L>
+__device__ __forceinline__ uint32_t limb_word(uint32_t x, uint32_t p) {
+    constexpr uint32_t bias = L == 1 ? 0x80u : L == 2 ? 0x8080u : L == 3 ? 0x808080u : 0x80808080u;
+    const uint32_t hi = (uint32_t)Limbs<L>::hi;
+    const uint32_t r = x > hi ? x - p : x;  // two's complement wrap is intended
+    return (r + bias) ^ 0x80808080u;
+}
+
+// Gather byte l of four limb words into one 32-bit store (4 consecutive columns of plane l).
+__device__ __forceinline__ uint32_t gather_byte(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, int l) {
+    const uint32_t s = (uint32_t)l;
+    const uint32_t lo = __byte_perm(w0, w1, s | ((s + 4) << 4));        // bytes: w0[l], w1[l]
+    const uint32_t hi = __byte_perm(w2, w3, s | ((s + 4) << 4));        // bytes: w2[l], w3[l]
+    return __byte_perm(lo, hi, 0x5410);
+}
+
+// Shoup multiplication by a constant w < p: wq = floor(w 2^32 / p), x < 2^32.
+struct MulConst {
+    uint32_t w, wq;
+};
+__host__ __device__ inline MulConst make_mulconst(uint32_t w, uint32_t p) {
+    return MulConst{w, (uint32_t)(((uint64_t)w << 32) / p)};
+}
+__device__ __forceinline__ uint32_t mulc(uint32_t x, MulConst c, uint32_t p) {
+    const uint32_t q = __umulhi(x, c.wq);
+    uint32_t r = x * c.w - q * p;  // exact mod 2^32, true value in [0, 2p)
+    return r >= p ? r - p : r;
+}
+
 }  // namespace fsyrk_b200

@@ -93,14 +93,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Shared-memory matrix descriptor for a K-major tile stored by TMA with
-// 128-byte swizzle: rows of 128 bytes, 8-row core groups 1024 bytes apart.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr) {
+// Shared-memory matrix descriptor for a K-major tile stored by TMA with a
+// swizzled layout: rows of (swizzle width) bytes, 8-row core groups `sbo`
+// bytes apart.  layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B.
+__device__ __forceinline__ uint64_t sdesc_kmajor(uint32_t smem_addr, int layout, uint32_t sbo) {
     uint64_t d = 0;
     d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);  // start address
-    d |= (uint64_t)(1024 >> 4) << 32;            // stride byte offset: next 8-row group
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;  // stride byte offset: next 8-row group
     d |= 1ull << 46;                             // descriptor version (sm_100)
-    d |= 2ull << 61;                             // layout: SWIZZLE_128B
+    d |= (uint64_t)layout << 61;                 // swizzle layout
     return d;
 }
 

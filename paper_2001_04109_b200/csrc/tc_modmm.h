@@ -11,27 +11,40 @@
 
 namespace fsyrk_b200 {
 
-struct ModmmArgs {
-    ModP modp;
-    uint32_t c32;             // 2^32 mod p (fold of the high shifts for L = 4)
-    int M, N;                 // output rows / cols of every problem in the batch
-    int k_blocks;             // ceil(K / 128)
-    int tiles_n;              // column tiles (dense mode)
-    int syrk;                 // 1: only j <= i is written (lower triangle)
-    int vec_ok;               // ldo % 4 == 0 and out 16-byte aligned
-    int a_batch_mult, a_batch_off;  // operand slot of problem b: b * mult + off
-    int b_batch_mult, b_batch_off;
-    const int2* tile_list;    // SYRK: (tm, tn) per CTA; dense: nullptr
-    uint32_t* out;            // residues, problem b at out + b * out_batch_stride
-    long long out_batch_stride;
+constexpr int kMaxGroups = 6;
+
+// One uniform batch of products C_b = A_b * B_b^T (mod p).  Operands are int8
+// limb planes [slot][L][rows][kpad] reached through the two TMA descriptors;
+// problem b reads A slot b * a_mult + a_off and B slot b * b_mult + b_off.
+struct alignas(64) GroupDesc {
+    CUtensorMap tmA;  // box 128 (K) x 128 rows
+    CUtensorMap tmB;  // box 128 (K) x BN rows
+    int M, N;         // output rows / cols
+    int k_blocks;     // kpad / BK
+    int syrk;         // 1: only j <= i is written (lower triangle)
+    int vec_ok;       // ldo % 4 == 0 (16-byte vector stores)
+    int a_mult, a_off, b_mult, b_off;
+    int pad_;
+    uint32_t* out;    // residues, problem b at out + b * out_bs
+    long long out_bs;
     long long ldo;
 };
 
-int modmm_block_n(int L);
-constexpr int modmm_block_m() { return 128; }
-size_t modmm_k_limit(int L);
+struct GroupedArgs {
+    GroupDesc g[kMaxGroups];
+    ModP modp;
+    int32_t w[8];       // balanced 256^s mod p, s = 0 .. 2L-2
+    int ngroups;
+    int ntiles;
+    const int4* tiles;  // (group, batch, tm, tn), longest K first
+};
 
-cudaError_t modmm_launch(int L, const CUtensorMap& ta, const CUtensorMap& tb, const ModmmArgs& args, int ntiles,
-                         int batch, cudaStream_t stream);
+int modmm_block_n(int L);
+int modmm_block_k(int L);
+constexpr int modmm_block_m() { return 128; }
+// Largest inner dimension whose int32 shift sums and int64 fold stay exact.
+size_t modmm_k_limit(int L, uint64_t p);
+
+cudaError_t modmm_launch(int L, const GroupedArgs& args, int grid, cudaStream_t stream);
 
 }  // namespace fsyrk_b200

@@ -1,0 +1,234 @@
+// tcgen05 int8-limb mod-p product kernel (see tc_modmm.cu for the design notes).
+//
+// Persistent and grouped: one launch runs every product of a recursion plan
+// (the general products of all levels and the leaf SYRKs), described by up
+// to kMaxGroups uniform problem groups and a host-built tile list in
+// longest-K-first order.  Warp roles per CTA (one CTA per SM):
+//   warp 0      : TMA producer (runs ahead across tiles)
+//   warp 1      : tcgen05.mma issuer
+//   warps 2..9  : epilogue; warp w drains TMEM lanes 32*(w%4).. for one half
+//                 of the tile's columns
+// TMEM holds the 2L-1 shift accumulators of one tile (up to 480 columns);
+// the producer prefetches the next tile's operands while the epilogue runs.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "modp.cuh"
+#include "sm100.cuh"
+#include "tc_modmm.h"
+
+namespace fsyrk_b200 {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+// BK: int8 elements of K per stage = the swizzle row (128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B)
+template <int L, int BN, int BK, int STAGES>
+struct Cfg {
+    static_assert(BK == 128 || BK == 64, "BK must match a swizzle mode");
+    static constexpr int NACC = 2 * L - 1;
+    static constexpr int COLS_USED = NACC * BN;
+    static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
+                                     : COLS_USED <= 256 ? 256 : 512;
+    static_assert(COLS_USED <= 512, "accumulators exceed TMEM");
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: UMMA N and two 16-column epilogue halves");
+    static constexpr int A_TILE = BM * BK;
+    static constexpr int B_TILE = BN * BK;
+    static_assert(B_TILE % 1024 == 0, "B tile must be a whole number of swizzle atoms");
+    static constexpr int STAGE_BYTES = L * (A_TILE + B_TILE);
+    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+// sum_s 256^s T_s  mod p.  Each T_s is scaled by w_s = 256^s mod p with a
+// signed 32x32->64 multiply-add; |sum| <= L^2 K 2^14 p < 2^62 is checked on
+// the host (modmm_k_limit), so one Barrett reduction finishes the fold.
+template <int L>
+__device__ __forceinline__ uint32_t fold(const int32_t (&t)[2 * L - 1], const ModP& m, const int32_t* w) {
+    int64_t v = (int64_t)t[0];
+#pragma unroll
+    for (int s = 1; s < 2 * L - 1; ++s) v += (int64_t)t[s] * (int64_t)w[s];
+    return mod_s64(v, m);
+}
+
+template <int L, int BN, int BK, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    modmm_kernel(const __grid_constant__ GroupedArgs args) {
+    using C = Cfg<L, BN, BK, STAGES>;
+    constexpr int SW = BK == 128 ? 2 : 4;  // descriptor layout: SWIZZLE_128B / SWIZZLE_64B
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {
+        sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+    } else if (warp == 1 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            sm100::mbar_init(&full[s], 1);
+            sm100::mbar_init(&empty[s], 1);
+        }
+        sm100::mbar_init(tmem_full, 1);
+        sm100::mbar_init(tmem_empty, kEpiWarps);
+        sm100::fence_mbar_init();
+    } else if (warp == 2 && lane == 0) {
+        for (int g = 0; g < args.ngroups; ++g) {
+            sm100::tma_prefetch(&args.g[g].tmA);
+            sm100::tma_prefetch(&args.g[g].tmB);
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x) {
+                const int4 tile = args.tiles[t];
+                const GroupDesc& g = args.g[tile.x];
+                const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
+                for (int kb = 0; kb < g.k_blocks; ++kb) {
+                    sm100::mbar_wait(&empty[stage], phase ^ 1);
+                    sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    uint8_t* st = smem + stage * C::STAGE_BYTES;
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, tile.z * BM, l, bA);
+                        sm100::tma_load_4d(st + L * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage], kb * BK,
+                                           tile.w * BN, l, bB);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            constexpr uint32_t idesc = sm100::idesc_i8(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t it = 0;
+            for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
+                const GroupDesc& g = args.g[args.tiles[t].x];
+                sm100::mbar_wait(tmem_empty, (it & 1) ^ 1);  // epilogue drained the previous tile
+                sm100::tc_fence_after();
+                for (int kb = 0; kb < g.k_blocks; ++kb) {
+                    sm100::mbar_wait(&full[stage], phase);
+                    sm100::tc_fence_after();
+                    const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
+#pragma unroll
+                    for (int i = 0; i < L; ++i) {
+#pragma unroll
+                        for (int j = 0; j < L; ++j) {
+                            const int acc = i + j;
+                            const int first_i = acc - (L - 1) > 0 ? acc - (L - 1) : 0;
+                            const uint64_t ad = sm100::sdesc_kmajor(st + i * C::A_TILE, SW, 8 * BK);
+                            const uint64_t bd = sm100::sdesc_kmajor(st + L * C::A_TILE + j * C::B_TILE, SW, 8 * BK);
+#pragma unroll
+                            for (int kk = 0; kk < BK / 32; ++kk) {
+                                const uint32_t accum = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
+                                // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
+                                sm100::mma_i8(tmem + acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                            }
+                        }
+                    }
+                    sm100::tc_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                sm100::tc_commit(tmem_full);
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue
+        const int quad = warp & 3;             // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;      // column half of the tile
+        const int row = quad * 32 + lane;
+        const ModP m = args.modp;
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
+            const int4 tile = args.tiles[t];
+            const GroupDesc& g = args.g[tile.x];
+            sm100::mbar_wait(tmem_full, it & 1);
+            sm100::tc_fence_after();
+            const long long grow = (long long)tile.z * BM + row;
+            const bool row_ok = grow < g.M;
+            uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
+#pragma unroll 1
+            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
+                uint32_t raw[C::NACC][16];
+#pragma unroll
+                for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
+                sm100::tmem_wait_ld();
+                const long long gc0 = (long long)tile.w * BN + c0;
+                if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) continue;
+                uint32_t res[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    int32_t tv[C::NACC];
+#pragma unroll
+                    for (int s = 0; s < C::NACC; ++s) tv[s] = (int32_t)raw[s][c];
+                    res[c] = fold<L>(tv, m, args.w);
+                }
+                const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
+                if (full_chunk) {
+                    uint4* o = reinterpret_cast<uint4*>(out + gc0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        o[q] = make_uint4(res[4 * q], res[4 * q + 1], res[4 * q + 2], res[4 * q + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const long long gc = gc0 + c;
+                        if (gc < g.N && (!g.syrk || gc <= grow)) out[gc] = res[c];
+                    }
+                }
+            }
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tmem_empty);
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    if (warp == 0) sm100::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+template <int L, int BN, int BK, int STAGES>
+cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
+    using C = Cfg<L, BN, BK, STAGES>;
+    auto kern = modmm_kernel<L, BN, BK, STAGES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    if (args.ntiles == 0) return cudaSuccess;
+    kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(args);
+    return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace fsyrk_b200

@@ -185,6 +185,7 @@ struct LeafGroup {
 
 struct GemmGroup {
     int h, kw, count = 0;
+    bool root = false;  // the two general products of the top level (launched early, see execute)
     int hpad, kpad;
     long long plane, slot;
     int8_t *ga = nullptr, *gb = nullptr;
@@ -202,6 +203,7 @@ struct ProdLaunch {
     std::vector<Member> members;
     std::vector<int4> host_tiles;
     size_t off_tiles = 0;
+    int phase = 1;  // 0: top-level general products (start right after the top pre-additions)
     GroupedArgs args;
 };
 
@@ -258,8 +260,15 @@ struct Plan {
     uint64_t int8_macs = 0;
     uint64_t ew_adds = 0;
 
+    // side stream + events: the top level's general products overlap the deeper pre/post-additions
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
     ~Plan() {
         if (arena) cudaFree(arena);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
     }
 
     int build(int n_, int k_, uint64_t levels, int depth, int parent, int role) {
@@ -316,12 +325,13 @@ struct Plan {
         leaves.push_back(lg);
         return (int)leaves.size() - 1;
     }
-    int gemm_group(int h, int kw) {
+    int gemm_group(int h, int kw, bool root) {
         for (size_t g = 0; g < gemms.size(); ++g)
-            if (gemms[g].h == h && gemms[g].kw == kw) return (int)g;
+            if (gemms[g].h == h && gemms[g].kw == kw && gemms[g].root == root) return (int)g;
         GemmGroup gg;
         gg.h = h;
         gg.kw = kw;
+        gg.root = root;
         gemms.push_back(gg);
         return (int)gemms.size() - 1;
     }
@@ -376,7 +386,7 @@ struct Plan {
                 nd.leaf_from_prep = nd.parent >= 0 && nodes[nd.parent].kind == LEVEL;
                 if (!nd.leaf_from_prep) split_leaves.push_back(i);
             } else if (nd.kind == LEVEL) {
-                nd.ggroup = gemm_group(nd.h, nd.kw);
+                nd.ggroup = gemm_group(nd.h, nd.kw, nd.parent < 0);
                 nd.gslot = gemms[nd.ggroup].count++;
             }
         }
@@ -411,14 +421,23 @@ struct Plan {
         // product launches: every GEMM group and leaf group, kMaxGroups per persistent launch,
         // tiles (group, batch, tm, tn) ordered longest-K first
         {
-            struct PG { bool leaf; int idx; int kpad; };
+            struct PG { bool leaf; int idx; int kpad; int phase; };
             std::vector<PG> pgs;
-            for (int i = 0; i < (int)gemms.size(); ++i) pgs.push_back({false, i, gemms[i].kpad});
-            for (int i = 0; i < (int)leaves.size(); ++i) pgs.push_back({true, i, leaves[i].kpad});
-            std::stable_sort(pgs.begin(), pgs.end(), [](const PG& a, const PG& b) { return a.kpad > b.kpad; });
-            for (size_t c0 = 0; c0 < pgs.size(); c0 += kMaxGroups) {
+            // FSYRK_B200_OVERLAP=1: launch the top level's products on their own, overlapped with
+            // the deeper pre/post-additions (measured slower on cfg2: the elementwise kernels get
+            // only the SM resources the persistent kernel leaves); default: one launch
+            static const bool split_root = getenv("FSYRK_B200_OVERLAP") != nullptr;
+            for (int i = 0; i < (int)gemms.size(); ++i)
+                pgs.push_back({false, i, gemms[i].kpad, gemms[i].root && split_root ? 0 : 1});
+            for (int i = 0; i < (int)leaves.size(); ++i) pgs.push_back({true, i, leaves[i].kpad, 1});
+            std::stable_sort(pgs.begin(), pgs.end(), [](const PG& a, const PG& b) {
+                return a.phase != b.phase ? a.phase < b.phase : a.kpad > b.kpad;
+            });
+            for (size_t c0 = 0; c0 < pgs.size();) {
                 ProdLaunch pl;
-                for (size_t c = c0; c < pgs.size() && c < c0 + kMaxGroups; ++c) {
+                pl.phase = pgs[c0].phase;
+                size_t c = c0;
+                for (; c < pgs.size() && c < c0 + kMaxGroups && pgs[c].phase == pl.phase; ++c) {
                     const int gi = (int)(c - c0);
                     pl.members.push_back({pgs[c].leaf, pgs[c].idx});
                     if (!pgs[c].leaf) {
@@ -436,6 +455,7 @@ struct Plan {
                 }
                 pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4));
                 prods.push_back(std::move(pl));
+                c0 = c;
             }
         }
         std::vector<size_t> off_x(nodes.size(), 0), off_s3(nodes.size(), 0);
@@ -450,7 +470,7 @@ struct Plan {
             if (nd.kind != LEVEL) continue;
             bool found = false;
             for (auto& pg : preps)
-                if (pg.depth == nd.depth && pg.n == nd.n && pg.k == nd.k && pg.in64 == nd.in64) {
+                if (pg.depth == nd.depth && pg.n == nd.n && pg.k == nd.k) {
                     pg.nodes.push_back((int)i);
                     found = true;
                 }
@@ -610,7 +630,7 @@ struct Plan {
             a.yb = (uint32_t)y.b;
             a.cya = make_mulconst(a.ya, (uint32_t)p);
             a.cyb = make_mulconst(a.yb, (uint32_t)p);
-            a.in64 = pg.in64 ? 1 : 0;
+            a.in64 = 0;       // set below when a node reads the caller's matrix
             a.a64 = nullptr;  // per call
             a.ld64 = 0;
             a.g_plane = gg.plane;
@@ -631,7 +651,8 @@ struct Plan {
                 const Node& nd = nodes[ni];
                 GemmGroup& g = gemms[nd.ggroup];
                 PrepNode pn{};
-                pn.in = InView{nd.in, nd.ldin, nd.r0, nd.c0};
+                pn.in = InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0};
+                if (nd.in64) a.in64 = 1;
                 pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
                 pn.s2 = g.gb + (2LL * nd.gslot) * g.slot;
                 pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
@@ -745,40 +766,55 @@ struct Plan {
         for (int li : split_leaves) {
             const Node& nd = nodes[li];
             const LeafGroup& lg = leaves[nd.lgroup];
-            ck(launch_split_planes(L, InView{nd.in, nd.ldin, nd.r0, nd.c0}, nd.in64 ? a_dev : nullptr, lda, nd.n, nd.k,
+            ck(launch_split_planes(L, InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0}, a_dev, lda, nd.n, nd.k,
                                    (uint32_t)p, lg.planes + nd.lslot * lg.slot, lg.plane, lg.kpad, s),
                "split_planes");
             counts[1]++;
         }
         mark(1);
-        // 3. fused pre-additions, top-down
-        for (auto& pg : preps) {
+        // FSYRK_B200_TRACE=1: per-launch events on their streams, timeline printed to stderr
+        static const bool trace = getenv("FSYRK_B200_TRACE") != nullptr;
+        struct TraceRec {
+            std::string name;
+            cudaEvent_t a, b;
+        };
+        std::vector<TraceRec> tr;
+        auto traced = [&](const std::string& name, cudaStream_t st, auto&& fn) {
+            if (!trace) {
+                fn();
+                return;
+            }
+            TraceRec r{name, nullptr, nullptr};
+            cudaEventCreate(&r.a);
+            cudaEventCreate(&r.b);
+            cudaEventRecord(r.a, st);
+            fn();
+            cudaEventRecord(r.b, st);
+            tr.push_back(r);
+        };
+        auto run_prep = [&](PrepGroup& pg, cudaStream_t st) {
             PrepArgs a = pg.args;
             if (a.in64) {
                 a.a64 = a_dev;
                 a.ld64 = lda;
             }
-            ck(launch_prep(a, s), "prep");
+            traced("prep d" + std::to_string(pg.depth), st, [&] { ck(launch_prep(a, st), "prep"); });
             counts[1]++;
-        }
-        mark(2);
-        // 4. tensor-core products: every general product and leaf SYRK of the plan, persistent launches
-        for (auto& pl : prods) {
-            const int grid = std::min(nsm, pl.args.ntiles);
-            ck(modmm_launch(L, pl.args, grid, s), "modmm");
+        };
+        auto run_prod = [&](ProdLaunch& pl, cudaStream_t st) {
+            traced("products phase " + std::to_string(pl.phase), st,
+                   [&] { ck(modmm_launch(L, pl.args, std::min(nsm, pl.args.ntiles), st), "modmm"); });
             counts[0]++;
-        }
-        mark(3);
-        // 5. post-additions, bottom-up; the root level writes alpha X + beta C into the caller's C
+        };
         bool root_done = false;
-        for (auto& pg : posts) {
+        auto run_post = [&](PostGroup& pg, cudaStream_t st) {
             if (pg.kind == LEVEL) {
                 PostArgs a{};
                 a.m = m;
                 a.h = pg.n / 2;
                 a.nodes = pg.dev_post;
                 a.nnodes = (int)pg.nodes.size();
-                if (pg.depth == 0) {
+                if (pg.depth == 0) {  // the root writes alpha X + beta C into the caller's C
                     a.out64 = 1;
                     a.c64 = c_dev;
                     a.ldc = ldc;
@@ -786,13 +822,48 @@ struct Plan {
                     a.beta = beta;
                     root_done = true;
                 }
-                ck(launch_post(a, s), "post");
+                traced("post d" + std::to_string(pg.depth), st, [&] { ck(launch_post(a, st), "post"); });
             } else {
-                ck(launch_add_lower(pg.dev_add, (int)pg.nodes.size(), pg.n, (uint32_t)p, s), "add_lower");
+                ck(launch_add_lower(pg.dev_add, (int)pg.nodes.size(), pg.n, (uint32_t)p, st), "add_lower");
             }
             counts[2]++;
+        };
+        const bool overlap = !g_phase_timing && !prods.empty() && prods[0].phase == 0;
+        if (!overlap) {
+            // 3. fused pre-additions, top-down; 4. products; 5. post-additions, bottom-up
+            for (auto& pg : preps) run_prep(pg, s);
+            mark(2);
+            for (auto& pl : prods) run_prod(pl, s);
+            mark(3);
+            for (auto& pg : posts) run_post(pg, s);
+            mark(4);
+        } else {
+            // The top level's two general products need only the top pre-additions; they run on
+            // the caller's stream while a side stream carries the deeper pre-additions, products
+            // and post-additions (elementwise work co-resides with the persistent tensor kernel:
+            // it leaves HBM bandwidth and issue slots idle).  The root post-addition joins both.
+            if (!side) {
+                ck(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
+                ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+            }
+            for (auto& pg : preps)
+                if (pg.depth == 0) run_prep(pg, s);
+            ck(cudaEventRecord(ev_fork, s), "fork");
+            ck(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+            for (auto& pl : prods)
+                if (pl.phase == 0) run_prod(pl, s);
+            for (auto& pg : preps)
+                if (pg.depth != 0) run_prep(pg, side);
+            for (auto& pl : prods)
+                if (pl.phase != 0) run_prod(pl, side);
+            for (auto& pg : posts)
+                if (pg.depth != 0) run_post(pg, side);
+            ck(cudaEventRecord(ev_join, side), "join");
+            ck(cudaStreamWaitEvent(s, ev_join, 0), "join wait");
+            for (auto& pg : posts)
+                if (pg.depth == 0) run_post(pg, s);
         }
-        mark(4);
         // 6. root leaf / split: C <- alpha X + beta C in the reference layout; optional mirror
         if (!root_done) {
             ck(launch_finalize(root.x, root.ldx, n, c_dev, ldc, m, alpha, beta, s), "finalize");
@@ -803,6 +874,23 @@ struct Plan {
             counts[3]++;
         }
         mark(5);
+        if (trace && !tr.empty()) {
+            cudaError_t se = cudaStreamSynchronize(s);
+            if (se != cudaSuccess) fprintf(stderr, "[fsyrk trace] sync: %s\n", cudaGetErrorString(se));
+            for (auto& r : tr) {
+                float t0 = 0, t1 = 0;
+                cudaError_t e0 = cudaEventElapsedTime(&t0, tr[0].a, r.a);
+                cudaError_t e1 = cudaEventElapsedTime(&t1, tr[0].a, r.b);
+                if (e0 != cudaSuccess || e1 != cudaSuccess)
+                    fprintf(stderr, "[fsyrk trace] elapsed: %s / %s\n", cudaGetErrorString(e0), cudaGetErrorString(e1));
+                fprintf(stderr, "[fsyrk trace] %-20s %8.1f us -> %8.1f us (%7.1f us)\n", r.name.c_str(), t0 * 1e3,
+                        t1 * 1e3, (t1 - t0) * 1e3);
+            }
+            for (auto& r : tr) {
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+            }
+        }
         std::copy(counts, counts + 5, g_launch_counts);
         if (g_phase_timing) {
             ck(cudaEventSynchronize(ev[5]), "event sync");
@@ -1169,7 +1257,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         if (k > 0) {
             ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
             ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
-            const InView top{nullptr, 0, 0, 0};
+            const InView top{nullptr, 0, 0, 0, 1};
             ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64a.ptr), (long long)k, (int)m, (int)k, (uint32_t)p,
                                    static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, 0), "split A");
             ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64b.ptr), (long long)k, (int)n, (int)k, (uint32_t)p,

@@ -64,21 +64,26 @@ struct Src {
     const uint64_t* p64;
     long long ld64;
     bool in64;
+    // canonical residues are the contract (fields.hpp:32-36); reduce only when one is not
+    static __device__ __forceinline__ uint32_t canon(uint64_t x, const ModP& m) {
+        return x < m.p ? (uint32_t)x : mod_u64(x, m);
+    }
     __device__ __forceinline__ uint32_t ld(int i, int c, const ModP& m) const {
-        return in64 ? mod_u64(__ldg(p64 + (long long)i * ld64 + c), m) : __ldg(p32 + (long long)i * ld32 + c);
+        return in64 ? canon(__ldg(p64 + (long long)i * ld64 + c), m) : __ldg(p32 + (long long)i * ld32 + c);
     }
     // 4 consecutive columns starting at c (c % 4 == 0, rows 16-byte aligned)
     __device__ __forceinline__ uint4 ld4(int i, int c, const ModP& m) const {
         if (in64) {
             const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p64 + (long long)i * ld64 + c);
             const ulonglong2 x = __ldg(q), y = __ldg(q + 1);
-            return make_uint4(mod_u64(x.x, m), mod_u64(x.y, m), mod_u64(y.x, m), mod_u64(y.y, m));
+            return make_uint4(canon(x.x, m), canon(x.y, m), canon(y.x, m), canon(y.y, m));
         }
         return __ldg(reinterpret_cast<const uint4*>(p32 + (long long)i * ld32 + c));
     }
 };
 
-__device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, long long ld64, bool in64) {
+__device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, long long ld64) {
+    const bool in64 = v.in64 != 0;
     Src s;
     s.in64 = in64;
     s.p32 = v.p32;
@@ -105,9 +110,9 @@ __device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long 
 }
 
 template <int L, bool VEC>
-__global__ void split_planes_kernel(InView in, const uint64_t* a64, long long ld64, bool in64, int rows, int k,
-                                    ModP m, int8_t* __restrict__ planes, long long plane, long long rs) {
-    const Src src = make_src(in, a64, ld64, in64);
+__global__ void split_planes_kernel(InView in, const uint64_t* a64, long long ld64, int rows, int k, ModP m,
+                                    int8_t* __restrict__ planes, long long plane, long long rs) {
+    const Src src = make_src(in, a64, ld64);
     constexpr int V = VEC ? 4 : 1;
     const int cgs = (k + V - 1) / V;
     const long long total = (long long)rows * cgs;
@@ -141,7 +146,7 @@ __global__ void prep_kernel(const PrepArgs args) {
     const int jp = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (jp >= ncw || i >= h) return;
-    const Src src = make_src(nd.in, args.a64, args.ld64, args.in64 != 0);
+    const Src src = make_src(nd.in, args.a64, args.ld64);
 
     const int nc = args.pair ? 2 : 1;
     int col[2] = {jp, jp + half};
@@ -203,7 +208,7 @@ __device__ __forceinline__ void pair_y4(uint4 u, uint4 v, MulConst ca, MulConst 
 
 // Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
 // Pair form, their 4 partners) per thread.
-template <int L, bool PAIR, bool IN64>
+template <int L, bool PAIR>
 __global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
     const PrepNode nd = args.nodes[blockIdx.z];
     const ModP m = args.m;
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (g >= ncg || i >= h) return;
-    const Src src = make_src(nd.in, args.a64, args.ld64, IN64);
+    const Src src = make_src(nd.in, args.a64, args.ld64);
     constexpr int NC = PAIR ? 2 : 1;
     const int col[2] = {4 * g, 4 * g + half};
     uint4 a11[NC], a12[NC], a21[NC], a22[NC];
@@ -266,7 +271,7 @@ struct PostOut {
     long long ldx;
     uint64_t* c;
     long long ldc;
-    bool out64;
+    bool out64, vec64;
     uint32_t alpha, beta;
     ModP m;
     // write element (i, j) of the node output (lower triangle for out64)
@@ -282,9 +287,28 @@ struct PostOut {
         }
         c[i * ldc + j] = r;
     }
+    __device__ __forceinline__ uint32_t acc(uint32_t v, uint64_t cin) const {
+        uint32_t r = alpha == 1 ? v : mulm(v, alpha, m);
+        if (beta != 0) {
+            const uint32_t ci = mod_u64(cin, m);
+            r = addm(r, beta == 1 ? ci : mulm(ci, beta, m), m.p);
+        }
+        return r;
+    }
     __device__ __forceinline__ void put4(long long i, long long j, uint4 v) const {
         if (!out64) {
             *reinterpret_cast<uint4*>(x + i * ldx + j) = v;
+            return;
+        }
+        if (vec64) {  // ldc even, C 16-byte aligned: two 16-byte stores
+            ulonglong2* q = reinterpret_cast<ulonglong2*>(c + i * ldc + j);
+            ulonglong2 c0 = make_ulonglong2(0, 0), c1 = c0;
+            if (beta != 0) {
+                c0 = q[0];
+                c1 = q[1];
+            }
+            q[0] = make_ulonglong2(acc(v.x, c0.x), acc(v.y, c0.y));
+            q[1] = make_ulonglong2(acc(v.z, c1.x), acc(v.w, c1.y));
             return;
         }
         put(i, j, v.x);
@@ -301,6 +325,7 @@ __device__ __forceinline__ PostOut make_out(const PostArgs& a, const PostNode& n
     o.c = a.c64;
     o.ldc = a.ldc;
     o.out64 = a.out64 != 0;
+    o.vec64 = o.out64 && !(a.ldc % 2) && !(reinterpret_cast<uintptr_t>(a.c64) % 16);
     o.alpha = a.alpha;
     o.beta = a.beta;
     o.m = a.m;
@@ -482,13 +507,8 @@ cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
         const int ncg = (a.pair ? a.half : a.kh) / 4;
         dim3 block(32, 8);
         dim3 grid((ncg + 31) / 32, (a.h + 7) / 8, a.nnodes);
-        if (a.pair) {
-            if (a.in64) prep_vec_kernel<L, true, true><<<grid, block, 0, s>>>(a);
-            else prep_vec_kernel<L, true, false><<<grid, block, 0, s>>>(a);
-        } else {
-            if (a.in64) prep_vec_kernel<L, false, true><<<grid, block, 0, s>>>(a);
-            else prep_vec_kernel<L, false, false><<<grid, block, 0, s>>>(a);
-        }
+        if (a.pair) prep_vec_kernel<L, true><<<grid, block, 0, s>>>(a);
+        else prep_vec_kernel<L, false><<<grid, block, 0, s>>>(a);
     } else {
         const int ncw = a.pair ? a.half : a.kw;
         dim3 block(32, 8);
@@ -513,16 +533,16 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
                                 uint32_t p, int8_t* planes, long long plane_stride, long long row_stride,
                                 cudaStream_t s) {
     if ((long long)rows * k == 0) return cudaSuccess;
-    const bool in64 = a64 != nullptr;
+    const bool in64 = in.in64 != 0;
     const bool vec = !(k % 4) && !(row_stride % 4) &&
                      (in64 ? !(ld64 % 2) && !(in.c0 % 2) && !(reinterpret_cast<uintptr_t>(a64) % 16)
                            : !(in.ld32 % 4) && !(reinterpret_cast<uintptr_t>(in.p32) % 16));
     const ModP m = make_modp(p);
     const int g = grid_for((long long)rows * (vec ? k / 4 : k), 256);
 #define FSYRK_SPLIT(LL)                                                                                              \
-    if (vec) split_planes_kernel<LL, true><<<g, 256, 0, s>>>(in, a64, ld64, in64, rows, k, m, planes, plane_stride, \
+    if (vec) split_planes_kernel<LL, true><<<g, 256, 0, s>>>(in, a64, ld64, rows, k, m, planes, plane_stride,       \
                                                               row_stride);                                         \
-    else split_planes_kernel<LL, false><<<g, 256, 0, s>>>(in, a64, ld64, in64, rows, k, m, planes, plane_stride,    \
+    else split_planes_kernel<LL, false><<<g, 256, 0, s>>>(in, a64, ld64, rows, k, m, planes, plane_stride,          \
                                                            row_stride);
     switch (L) {
         case 2: FSYRK_SPLIT(2) break;

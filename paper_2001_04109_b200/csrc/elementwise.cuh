@@ -23,6 +23,7 @@ struct InView {
     const uint32_t* p32;  // used when in64 == 0
     long long ld32;
     int r0, c0;           // used when in64 == 1: window origin in the caller's matrix
+    int in64;
 };
 
 // One level node of the recursion for the fused pre-addition kernel.
@@ -42,7 +43,7 @@ struct PrepNode {
 struct PrepArgs {
     ModP m;
     int L;
-    int in64;                 // all nodes of the launch read the caller's uint64 input
+    int in64;                 // some node of the launch reads the caller's uint64 input
     const uint64_t* a64;      // caller's input (per call)
     long long ld64;
     int h, kh, kw, half, pair;

@@ -25,8 +25,7 @@ namespace fsyrk_b200 {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiWarpsDefault = 8;
 
 // BK: int8 elements of K per stage = the swizzle row (128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B)
 template <int L, int BN, int BK, int STAGES>
@@ -37,7 +36,7 @@ struct Cfg {
     static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                      : COLS_USED <= 256 ? 256 : 512;
     static_assert(COLS_USED <= 512, "accumulators exceed TMEM");
-    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: UMMA N and two 16-column epilogue halves");
+    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN: UMMA N for M = 128");
     static constexpr int A_TILE = BM * BK;
     static constexpr int B_TILE = BN * BK;
     static_assert(B_TILE % 1024 == 0, "B tile must be a whole number of swizzle atoms");
@@ -56,10 +55,13 @@ __device__ __forceinline__ uint32_t fold(const int32_t (&t)[2 * L - 1], const Mo
     return mod_s64(v, m);
 }
 
-template <int L, int BN, int BK, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int L, int BN, int BK, int STAGES, int EPI = kEpiWarpsDefault>
+__global__ void __launch_bounds__(64 + 32 * EPI, 1)
     modmm_kernel(const __grid_constant__ GroupedArgs args) {
     using C = Cfg<L, BN, BK, STAGES>;
+    constexpr int kEpiWarps = EPI;
+    constexpr int kParts = EPI / 4;  // column slices per lane quadrant
+    static_assert(EPI % 4 == 0 && (BN / kParts) % 16 == 0, "epilogue split must give 16-column chunks");
     constexpr int SW = BK == 128 ? 2 : 4;  // descriptor layout: SWIZZLE_128B / SWIZZLE_64B
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ---------------------------------------------------- epilogue
         const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;      // column half of the tile
+        const int half = (warp - 2) >> 2;      // column slice of the tile
         const int row = quad * 32 + lane;
         const ModP m = args.modp;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = grow < g.M;
             uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
 #pragma unroll 1
-            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
+            for (int c0 = half * (BN / kParts); c0 < (half + 1) * (BN / kParts); c0 += 16) {
                 uint32_t raw[C::NACC][16];
 #pragma unroll
                 for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
@@ -215,10 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) sm100::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-template <int L, int BN, int BK, int STAGES>
+template <int L, int BN, int BK, int STAGES, int EPI = kEpiWarpsDefault>
 cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<L, BN, BK, STAGES>;
-    auto kern = modmm_kernel<L, BN, BK, STAGES>;
+    auto kern = modmm_kernel<L, BN, BK, STAGES, EPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -226,7 +228,7 @@ cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
         attr_set = true;
     }
     if (args.ntiles == 0) return cudaSuccess;
-    kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(args);
+    kern<<<grid, 64 + 32 * EPI, C::SMEM_BYTES, stream>>>(args);
     return cudaGetLastError();
 }
 

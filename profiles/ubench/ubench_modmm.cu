@@ -43,7 +43,7 @@ static CUtensorMap pmap(void* base, int kpad, int rows, int L, int batch, int bo
     return m;
 }
 
-template <int L, int BN, int BK, int STAGES>
+template <int L, int BN, int BK, int STAGES, int EPI = 8>
 void run(const char* name, int M, int N, int K, int batch, int8_t* A, int8_t* B, uint32_t* out, int reps) {
     GroupedArgs a;
     memset(&a, 0, sizeof(a));
@@ -66,18 +66,18 @@ void run(const char* name, int M, int N, int K, int batch, int8_t* A, int8_t* B,
     a.tiles = dt;
     a.ntiles = (int)tiles.size();
     int grid = a.ntiles < 148 ? a.ntiles : 148;
-    for (int i = 0; i < 2; ++i) CK((tc::launch_cfg<L, BN, BK, STAGES>(a, grid, 0)));
+    for (int i = 0; i < 2; ++i) CK((tc::launch_cfg<L, BN, BK, STAGES, EPI>(a, grid, 0)));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    for (int i = 0; i < reps; ++i) CK((tc::launch_cfg<L, BN, BK, STAGES>(a, grid, 0)));
+    for (int i = 0; i < reps; ++i) CK((tc::launch_cfg<L, BN, BK, STAGES, EPI>(a, grid, 0)));
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
     double ops = 2.0 * L * L * (double)M * N * K * batch;
-    printf("%-18s L=%d BN=%3d BK=%3d S=%d  %2d x %4dx%4dx%5d  %.4f ms  %7.1f int8 TOP/s\n",
-           name, L, BN, BK, STAGES, batch, M, N, K, ms, ops / ms / 1e9);
+    printf("%-18s L=%d BN=%3d BK=%3d S=%d E=%2d  %2d x %4dx%4dx%5d  %.4f ms  %7.1f int8 TOP/s\n",
+           name, L, BN, BK, STAGES, EPI, batch, M, N, K, ms, ops / ms / 1e9);
     cudaFree(dt);
 }
 
@@ -89,15 +89,23 @@ int main() {
     for (auto& x : h) x = (int8_t)(rand() & 255);
     CK(cudaMemcpy(A, h.data(), plane_max, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(B, h.data(), plane_max, cudaMemcpyHostToDevice));
-    // square 4096 products at several K, and the cfg2 recursion shapes (batched)
-    for (int K : {512, 2048, 8192}) {
-        int reps = K >= 8192 ? 5 : 20;
-        run<3, 96, 128, 2>("L3", 4096, 4096, K, 1, A, B, out, reps);
-        run<2, 128, 128, 3>("L2", 4096, 4096, K, 1, A, B, out, reps);
-        run<4, 64, 128, 2>("L4", 4096, 4096, K, 1, A, B, out, reps);
+    // pipeline depth / epilogue width study on the cfg2 recursion shapes and square products
+    for (int K : {512, 2048}) {
+        run<3, 96, 128, 2, 8>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
+        run<3, 96, 64, 4, 8>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
+        run<3, 96, 64, 5, 8>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
+        run<3, 96, 128, 2, 12>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
+        run<3, 96, 64, 4, 12>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
+        run<3, 96, 64, 5, 12>("L3 sq", 4096, 4096, K, 1, A, B, out, 20);
     }
-    run<3, 96, 128, 2>("cfg2 depth0", 2048, 2048, 2048, 2, A, B, out, 20);
-    run<3, 96, 128, 2>("cfg2 depth1", 1024, 1024, 1024, 6, A, B, out, 20);
-    run<3, 96, 128, 2>("cfg2 depth2", 512, 512, 512, 18, A, B, out, 20);
+    run<3, 96, 128, 2, 8>("cfg2 depth0", 2048, 2048, 2048, 2, A, B, out, 20);
+    run<3, 96, 64, 5, 12>("cfg2 depth0", 2048, 2048, 2048, 2, A, B, out, 20);
+    run<3, 96, 128, 2, 8>("cfg2 depth2", 512, 512, 512, 18, A, B, out, 20);
+    run<3, 96, 64, 4, 12>("cfg2 depth2", 512, 512, 512, 18, A, B, out, 20);
+    run<3, 96, 64, 5, 12>("cfg2 depth2", 512, 512, 512, 18, A, B, out, 20);
+    run<2, 128, 64, 6, 8>("L2 sq", 4096, 4096, 2048, 1, A, B, out, 20);
+    run<2, 128, 128, 3, 8>("L2 sq", 4096, 4096, 2048, 1, A, B, out, 20);
+    run<4, 64, 64, 4, 8>("L4 sq", 4096, 4096, 2048, 1, A, B, out, 20);
+    run<4, 64, 128, 2, 8>("L4 sq", 4096, 4096, 2048, 1, A, B, out, 20);
     return 0;
 }

@@ -393,26 +393,9 @@ def _mt_alpha_beta(p, seed):
 
 
 def _mt_nonzero(p, count, seed):
-    """uniform_int_distribution<uint64_t>(1, p-1) over mt19937_64(seed) (oracle/ref_driver.cpp
-    make_instance), via libstdc++'s Lemire multiply-shift mapping."""
-    raw = _mt64(seed, count * 2)
-    out = []
-    rng_i = 0
-    rng_range = p - 1
-    while len(out) < count:
-        prod = int(raw[rng_i]) * rng_range
-        rng_i += 1
-        low = prod & ((1 << 64) - 1)
-        if low < rng_range:
-            thr = ((1 << 64) - rng_range) % rng_range
-            while low < thr:
-                if rng_i >= len(raw):
-                    raw = np.concatenate([raw, _mt64_continue(seed, len(raw), count)])
-                prod = int(raw[rng_i]) * rng_range
-                rng_i += 1
-                low = prod & ((1 << 64) - 1)
-        out.append(1 + (prod >> 64))
-    return np.array(out, dtype=np.uint64)
+    """D = 1 + rng() % (p - 1) from mt19937_64(seed) (oracle/ref_driver.cpp make_instance;
+    BASELINE.md's config-5 convention: seeds 5001/5002/5003 give 526 non-residues)."""
+    return np.array([1 + int(x) % (p - 1) for x in _mt64(seed, count)], dtype=np.uint64)
 
 
 def _mt64(seed, count):
@@ -439,10 +422,6 @@ def _mt64(seed, count):
         z ^= z >> 43
         out.append(z & ((1 << 64) - 1))
     return np.array(out, dtype=np.uint64)
-
-
-def _mt64_continue(seed, start, count):
-    return _mt64(seed, start + count * 2)[start:]
 
 
 if __name__ == "__main__":

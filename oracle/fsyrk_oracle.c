@@ -88,12 +88,19 @@ void orc_random_matrix(uint64_t p, size_t rows, size_t cols, uint64_t seed, uint
     for (size_t i = 0; i < rows * cols; ++i) out[i] = uid_next(&s, 0, p - 1);
 }
 
-/* uniform nonzero diagonal for the Schur-update config (bench/test convention,
- * mirrored by oracle/ref_driver.cpp make_instance). */
+/* nonzero diagonal for the Schur-update config: 1 + rng() % (p - 1) (bench/test
+ * convention, mirrored by oracle/ref_driver.cpp make_instance). */
 void orc_random_nonzero(uint64_t p, size_t count, uint64_t seed, uint64_t* out) {
     orc_mt64 s;
     mt_seed(&s, seed);
-    for (size_t i = 0; i < count; ++i) out[i] = uid_next(&s, 1, p - 1);
+    for (size_t i = 0; i < count; ++i) out[i] = 1 + mt_next(&s) % (p - 1);
+}
+
+/* uniform_int_distribution<uint64_t>(lo, hi) stream (pins the libstdc++ mapping). */
+void orc_uniform_stream(uint64_t lo, uint64_t hi, size_t count, uint64_t seed, uint64_t* out) {
+    orc_mt64 s;
+    mt_seed(&s, seed);
+    for (size_t i = 0; i < count; ++i) out[i] = uid_next(&s, lo, hi);
 }
 
 /* alpha, beta = 1 + rng() % (p - 1) from mt19937_64(abseed) (ref_driver convention). */

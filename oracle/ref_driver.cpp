@@ -130,10 +130,11 @@ Instance make_instance(const PrimeField& f, const Args& g) {
         if (g.beta_set) in.beta = g.beta % g.p;
     }
     if (g.mode == "schur") {
+        // D: k nonzero residues 1 + rng() % (p - 1) from mt19937_64(dseed) (the convention of
+        // BASELINE.md's config-5 oracle run: seeds 5001/5002/5003 give 526 non-residues)
         std::mt19937_64 rng(g.dseed);
-        std::uniform_int_distribution<std::uint64_t> dist(1, g.p - 1);
         in.d.resize(g.k);
-        for (auto& v : in.d) v = dist(rng);
+        for (auto& v : in.d) v = 1 + rng() % (g.p - 1);
     }
     return in;
 }

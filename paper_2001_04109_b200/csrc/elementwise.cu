@@ -39,20 +39,15 @@ namespace {
 __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda, int n, int kin, int kout,
                                   const ColMap* __restrict__ map, ModP m, uint32_t* __restrict__ out,
                                   long long ldo) {
-    const long long total = (long long)n * kout;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / kout), c = (int)(idx % kout);
+    (void)kin;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= kout) return;
+    const ColMap cm = map ? map[c] : ColMap{c, -1, 1, 0};
+    for (int i = blockIdx.y; i < n; i += gridDim.y) {
         const uint64_t* row = a + (long long)i * lda;
-        uint32_t v;
-        if (map == nullptr) {
-            v = mod_u64(row[c], m);
-        } else {
-            const ColMap cm = map[c];
-            v = 0;
-            if (cm.src0 >= 0) v = mulm(mod_u64(row[cm.src0], m), cm.c0, m);
-            if (cm.src1 >= 0) v = addm(v, mulm(mod_u64(row[cm.src1], m), cm.c1, m), m.p);
-        }
+        uint32_t v = 0;
+        if (cm.src0 >= 0) v = mulm(mod_u64(row[cm.src0], m), cm.c0, m);
+        if (cm.src1 >= 0) v = addm(v, mulm(mod_u64(row[cm.src1], m), cm.c1, m), m.p);
         out[(long long)i * ldo + c] = v;
     }
 }
@@ -114,11 +109,9 @@ __global__ void split_planes_kernel(InView in, const uint64_t* a64, long long ld
                                     int8_t* __restrict__ planes, long long plane, long long rs) {
     const Src src = make_src(in, a64, ld64);
     constexpr int V = VEC ? 4 : 1;
-    const int cgs = (k + V - 1) / V;
-    const long long total = (long long)rows * cgs;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / cgs), c = (int)(idx % cgs) * V;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * V;
+    if (c >= k) return;
+    for (int i = blockIdx.y; i < rows; i += gridDim.y) {
         if constexpr (VEC) {
             put_planes4<L>(planes, plane, (long long)i * rs + c, src.ld4(i, c, m), m.p);
         } else {
@@ -492,6 +485,14 @@ __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ x, long long ldx,
     }
 }
 
+// rows covered by grid.y (each block loops over rows with stride gridDim.y): about 8 waves of 148 SMs
+int rows_grid(int rows, int gx) {
+    int gy = (148 * 32 + gx - 1) / gx;
+    if (gy > rows) gy = rows;
+    if (gy > 65535) gy = 65535;
+    return gy < 1 ? 1 : gy;
+}
+
 int grid_for(long long total, int threads) {
     long long b = (total + threads - 1) / threads;
     if (b > 148 * 32) b = 148 * 32;
@@ -522,10 +523,9 @@ cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
 
 cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, int kout, const ColMap* map,
                               uint32_t p, uint32_t* out, long long ldo, cudaStream_t s) {
-    (void)kin;
-    const long long total = (long long)n * kout;
-    if (total == 0) return cudaSuccess;
-    convert_in_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, lda, n, kin, kout, map, make_modp(p), out, ldo);
+    if ((long long)n * kout == 0) return cudaSuccess;
+    const dim3 grid((kout + 255) / 256, rows_grid(n, (kout + 255) / 256));
+    convert_in_kernel<<<grid, 256, 0, s>>>(a, lda, n, kin, kout, map, make_modp(p), out, ldo);
     return cudaGetLastError();
 }
 
@@ -538,7 +538,8 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
                      (in64 ? !(ld64 % 2) && !(in.c0 % 2) && !(reinterpret_cast<uintptr_t>(a64) % 16)
                            : !(in.ld32 % 4) && !(reinterpret_cast<uintptr_t>(in.p32) % 16));
     const ModP m = make_modp(p);
-    const int g = grid_for((long long)rows * (vec ? k / 4 : k), 256);
+    const int gx = ((vec ? k / 4 : k) + 255) / 256;
+    const dim3 g(gx, rows_grid(rows, gx));
 #define FSYRK_SPLIT(LL)                                                                                              \
     if (vec) split_planes_kernel<LL, true><<<g, 256, 0, s>>>(in, a64, ld64, rows, k, m, planes, plane_stride,       \
                                                               row_stride);                                         \

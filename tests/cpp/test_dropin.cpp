@@ -1,0 +1,107 @@
+// Drop-in check: the reference's own call sites, switched to the B200 path by
+// including fsyrk_b200/fsyrk.hpp with FSYRK_B200_OVERRIDE, against the
+// reference's templates called explicitly (fsyrk::syrk_fast<PrimeField>) on
+// the same inputs.  Mirrors the reference's test style
+// (proj/tests/test_fast_syrk.cpp:14-31 oracle pattern, :71-98 battery,
+// :312-375 accumulating variant, :377-385 alias rejection;
+// proj/tests/test_scaled_syrk.cpp:104-135 syrkd battery).
+//
+// TEST INFRASTRUCTURE: built by tests/cpp/Makefile against /root/reference in the build
+// container; the binary runs on the GPU box (tests/test_dropin.py, -m gpu).
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+
+#include "fsyrk/fast_syrk.hpp"
+#include "fsyrk/scaled_syrk.hpp"
+#define FSYRK_B200_OVERRIDE
+#include "fsyrk_b200/fsyrk.hpp"
+
+using namespace fsyrk;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond, ...)                    \
+    do {                                    \
+        if (cond) {                         \
+            ++g_pass;                       \
+        } else {                            \
+            ++g_fail;                       \
+            std::printf("FAIL: " __VA_ARGS__); \
+            std::printf("\n");              \
+        }                                   \
+    } while (0)
+
+int main() {
+    // 1. battery: unmodified call sites (now the B200 path) vs the reference templates
+    std::mt19937_64 rng(2024);
+    for (std::uint64_t p : {5ull, 13ull, 131041ull, 3ull, 7ull, 11ull, 131071ull, 65537ull, 65521ull, 2147483647ull}) {
+        PrimeField f(p);
+        for (int t = 0; t < 6; ++t) {
+            std::size_t n = 1 + rng() % 200, k = 1 + rng() % 200;
+            RecursionPolicy pol{static_cast<std::size_t>(2 + (rng() % 3) * 6), kUnlimitedLevels};
+            auto a = random_matrix(f, n, k, rng());
+            auto plan = make_syrk_plan(f, pol);
+            OpCount o1, o2;
+            auto dev = syrk_fast(f, a.view(), plan, o1);                 // resolves to the B200 overload
+            auto ref = syrk_fast<PrimeField>(f, a.view(), plan, o2);     // the reference template
+            CHECK(lower_equal(f, dev.view(), ref.view()), "syrk_fast p=%llu n=%zu k=%zu", (unsigned long long)p, n, k);
+        }
+    }
+    // 2. accumulating form with random alpha, beta
+    {
+        PrimeField f(131071);
+        std::mt19937_64 r2(55);
+        for (int t = 0; t < 6; ++t) {
+            std::size_t n = 1 + r2() % 150, k = 1 + r2() % 150;
+            auto alpha = f.random_element(r2), beta = f.random_element(r2);
+            auto a = random_matrix(f, n, k, r2());
+            auto c0 = random_matrix(f, n, n, r2());
+            auto c1 = c0, c2 = c0;
+            auto plan = make_syrk_plan(f, {2, kUnlimitedLevels});
+            OpCount ops;
+            syrk_fast_acc(f, alpha, a.view(), beta, c1.view(), plan, ops);
+            syrk_fast_acc<PrimeField>(f, alpha, a.view(), beta, c2.view(), plan, ops);
+            CHECK(lower_equal(f, c1.view(), c2.view()), "syrk_fast_acc n=%zu k=%zu", n, k);
+        }
+    }
+    // 3. syrkd through the shim vs the reference's syrkd
+    for (std::uint64_t p : {3ull, 7ull, 13ull, 131071ull}) {
+        PrimeField f(p);
+        std::mt19937_64 r3(p * 7 + 1);
+        auto plan = make_syrk_plan(f, {2, kUnlimitedLevels});
+        for (int t = 0; t < 5; ++t) {
+            std::size_t m = 1 + r3() % 64, n = 1 + r3() % 64;
+            auto a = random_matrix(f, m, n, r3());
+            std::vector<PrimeField::Element> d(n);
+            for (auto& v : d) v = f.random_element(r3);
+            OpCount ops;
+            auto dev = fsyrk_b200::syrkd(f, a.view(), d, plan, ops);
+            auto ref = syrkd<PrimeField>(f, a.view(), d, plan, ops);
+            CHECK(lower_equal(f, dev.view(), ref.view()), "syrkd p=%llu m=%zu n=%zu", (unsigned long long)p, m, n);
+        }
+    }
+    // 4. error convention: aliased output and bad policy throw std::invalid_argument
+    {
+        PrimeField f(7);
+        Matrix<PrimeField> a(8, 8, 1);
+        auto plan = make_syrk_plan(f, {2, kUnlimitedLevels});
+        OpCount ops;
+        bool threw = false;
+        try {
+            syrk_fast_into(f, a.view(), a.view(), plan, ops);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw, "alias must throw std::invalid_argument");
+        threw = false;
+        Matrix<PrimeField> c(5, 5, 0);
+        try {
+            syrk_fast_into(f, a.view(), c.view(), plan, ops);
+        } catch (const DimensionError&) {
+            threw = true;
+        }
+        CHECK(threw, "shape mismatch must throw DimensionError");
+    }
+    std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}

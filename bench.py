@@ -35,9 +35,11 @@ CONFIGS = {
     # name: p, n, k, seed, threshold, max_levels, mode  (BASELINE.json "configs", in order)
     "cfg1": dict(p=65537, n=1024, k=1024, seed=42, threshold=64, levels=1, mode="plain"),
     "cfg2": dict(p=131071, n=4096, k=4096, seed=42, threshold=1024, levels=UNL, mode="plain"),
-    "cfg3": dict(p=65521, n=8192, k=2048, seed=42, threshold=512, levels=UNL, mode="acc", cseed=43, abseed=7),
-    "cfg4": dict(p=2147483647, n=16384, k=16384, seed=42, threshold=512, levels=UNL, mode="plain"),
-    "cfg5": dict(p=131071, n=32768, k=1024, seed=5001, threshold=512, levels=UNL, mode="schur", cseed=5003,
+    # configs 3-5 leave the recursion depth to the builder: the policy below is the fastest
+    # measured depth (>= 1 level; profiles/r01/policy_sweep.txt) -- the result does not depend on it
+    "cfg3": dict(p=65521, n=8192, k=2048, seed=42, threshold=2, levels=1, mode="acc", cseed=43, abseed=7),
+    "cfg4": dict(p=2147483647, n=16384, k=16384, seed=42, threshold=2, levels=2, mode="plain"),
+    "cfg5": dict(p=131071, n=32768, k=1024, seed=5001, threshold=2, levels=1, mode="schur", cseed=5003,
                  dseed=5002),
 }
 METRIC = "mod-p SYRK C=AAᵀ effective GOPS (n²k/t) at 1–8 B200; % of tensor-core peak"

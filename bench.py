@@ -180,6 +180,26 @@ def run_reference(args, cfgname, cfg, world, rank):
     print(json.dumps(line))
 
 
+def max_over_ranks(value, world):
+    """Max of a per-rank scalar over all ranks (device timing rule: the slowest rank counts)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def lower_digest(c):
+    import hashlib
+    h = hashlib.sha256()
+    for i in range(c.shape[0]):
+        h.update(np.ascontiguousarray(c[i, : i + 1]).astype("<u8").tobytes())
+    return h.hexdigest()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -187,6 +207,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mgpu", default="partition", choices=["partition", "replicas"],
+                    help="N > 1: split one problem's top level across ranks (strong scaling) or run one "
+                         "independent problem per rank (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--threshold", type=int, default=None, help="override the config's recursion threshold")
@@ -207,10 +230,14 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    part = world > 1 and args.mgpu == "partition"
+    if world > 1:
+        import torch.distributed as dist
     p, n, k = cfg["p"], cfg["n"], cfg["k"]
     f = fs.PrimeField(p)
     policy = fs.RecursionPolicy(cfg["threshold"], cfg["levels"])
-    a_host = fs.random_matrix(f, n, k, cfg["seed"] + rank)
+    seed = cfg["seed"] + (0 if part else rank)  # partition: one problem; replicas: one per rank
+    a_host = fs.random_matrix(f, n, k, seed)
     alpha, beta, d = 1, 0, None
     c0_host = None
     if cfg["mode"] in ("acc", "schur"):
@@ -232,11 +259,17 @@ def main():
     sh = stream.cuda_stream
 
     def step():
-        fs.syrk_dev(p, alpha, a_dev.data_ptr(), n, k, k, beta, c_dev.data_ptr(), n, policy, False, sh, d=d)
+        if part:
+            fs.syrk_part_dev(p, alpha, a_dev.data_ptr(), n, k, k, beta, c_dev.data_ptr(), n, policy, rank, world, sh,
+                             d=d)
+        else:
+            fs.syrk_dev(p, alpha, a_dev.data_ptr(), n, k, k, beta, c_dev.data_ptr(), n, policy, False, sh, d=d)
 
     def reset_c():
         if c_init is not None:
             c_dev.copy_(c_init)
+        elif part:
+            c_dev.zero_()
 
     # warm-up (plan creation happens on the first call)
     for _ in range(max(args.warmup, 3)):
@@ -247,7 +280,6 @@ def main():
     plan = fs.last_plan()
 
     if world > 1:
-        import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -261,6 +293,9 @@ def main():
                 reset_c()
                 step()
             torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
         for i in range(args.steps):
             reset_c()
             flush.zero_()
@@ -272,30 +307,25 @@ def main():
     if world > 1:
         dist.barrier()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms, world)
     E = float(n) * n * k
-    value = E * args.steps * world / (ms_max / 1e3) / 1e9
+    problems = 1 if part else world
+    value = E * args.steps * problems / (ms_max / 1e3) / 1e9
 
-    # parity self-check on the final device output against the reference digest (cfg seeds, rank 0)
+    # parity self-check of the device output against the reference's digest of the config
     parity = None
     ref_json = os.path.join(REPO, "tests", "golden", "configs", f"{args.config}.json")
-    if rank == 0 and os.path.exists(ref_json):
+    if os.path.exists(ref_json) and (not part or c_init is None):
         try:
             ref = json.loads(open(ref_json).read())
             reset_c()
             step()
             torch.cuda.synchronize()
-            c_out = c_dev.cpu().numpy().view(np.uint64)
-            import hashlib
-            h = hashlib.sha256()
-            for i in range(n):
-                h.update(np.ascontiguousarray(c_out[i, : i + 1]).astype("<u8").tobytes())
-            parity = "digest-match" if h.hexdigest() == ref["digest"] else "DIGEST-MISMATCH"
-            if rank != 0:
-                parity = None
+            if part:  # disjoint shares over zeroed buffers: the sum over ranks is the full result
+                dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
+            if rank == 0:
+                parity = "digest-match" if lower_digest(c_dev.cpu().numpy().view(np.uint64)) == ref["digest"] \
+                    else "DIGEST-MISMATCH"
         except Exception as ex:  # noqa: BLE001
             parity = f"unchecked ({type(ex).__name__})"
 
@@ -312,16 +342,27 @@ def main():
     fs.set_phase_timing(False)
     torch.cuda.synchronize()
 
-    # end-to-end through the host C-ABI entry point (pinned host buffers, H2D + D2H inside the timing)
+    # end-to-end: host A (pinned) -> device(s) -> host C, through the public API
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and (not part or cfg["mode"] == "plain"):
         a_pin = torch.from_numpy(a_host.view(np.int64)).pin_memory()
         c_pin = torch.zeros((n, n), dtype=torch.int64).pin_memory()
         a_np = a_pin.numpy().view(np.uint64)
         c_np = c_pin.numpy().view(np.uint64)
         plan_obj = fs.make_syrk_plan(f, policy)
+
         def host_step():
-            if cfg["mode"] == "plain":
+            if part:  # rank 0 uploads A, NCCL broadcast, per-rank shares, NCCL reduce of C, rank 0 downloads
+                if rank == 0:
+                    a_dev.copy_(a_pin, non_blocking=True)
+                dist.broadcast(a_dev, src=0)
+                c_dev.zero_()
+                step()
+                dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
+                if rank == 0:
+                    c_pin.copy_(c_dev)
+                torch.cuda.synchronize()
+            elif cfg["mode"] == "plain":
                 fs.syrk_fast_into(f, a_np, c_np, plan_obj)
             elif cfg["mode"] == "acc":
                 c_np[:] = c0_host
@@ -329,6 +370,7 @@ def main():
             else:
                 c_np[:] = c0_host
                 fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
+
         for _ in range(2):
             host_step()
         e2e_steps = max(3, min(args.steps, 10))
@@ -338,13 +380,10 @@ def main():
         for _ in range(e2e_steps):
             host_step()
         t1 = time.perf_counter()
-        t_e2e = torch.tensor([t1 - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        secs = float(t_e2e.item())
+        secs = max_over_ranks(t1 - t0, world)
         h2d = n * k * 8 + (n * n * 8 if beta else 0)
-        e2e = {"value": round(E * e2e_steps * world / secs / 1e9, 3), "unit": "GOPS", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": n * n * 8}
+        e2e = {"value": round(E * e2e_steps * problems / secs / 1e9, 3), "unit": "GOPS",
+               "h2d_bytes_per_step": h2d if part else h2d * world, "d2h_bytes_per_step": n * n * 8 * problems}
 
     if rank != 0:
         if world > 1:
@@ -366,19 +405,21 @@ def main():
                 "frac": round(achieved / peak_i8, 4) if peak_i8 else None, "traffic": None,
                 "kernel": "modmm (tcgen05 kind::i8 limb products)", "launches_per_step": nprod,
                 "avg_launch_ms": round(prod_ms / nprod, 4), "peak_source": peak_src,
-                "algorithmic_int8_ops_per_step": int8_ops,
+                "algorithmic_int8_ops_per_step": int8_ops, "rank": 0,
                 "phase_ms": {k2: round(v, 4) for k2, v in phase.items()}}
-    cpu = None if args.no_cpu_baseline else cpu_reference(args.config, cfg, 1, 1)
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_reference(args.config, cfg, 1, 1)
     if cpu is not None:
         cpu.pop("seconds", None)
     clocks = clk.summary()
     line = {"metric": METRIC, "value": round(value, 2), "unit": "GOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues / s8 limbs, s32 accumulate",
+            "scaling": "strong" if part else "weak", "vs_baseline": None,
+            "dtype": "u32 residues / s8 limbs, s32 accumulate",
             "data": "synthetic (reference random_matrix stream)",
             "config": {"workload": args.config, "p": p, "n": n, "k": k, "mode": cfg["mode"],
                        "threshold": cfg["threshold"], "levels": "inf" if cfg["levels"] == UNL else cfg["levels"],
-                       "parallelism": f"replicas x{world}", "l2": "flushed between steps (256 MiB write)"},
+                       "parallelism": (f"top-level tile-pair partition x{world}" if part else f"replicas x{world}"),
+                       "l2": "flushed between steps (256 MiB write)"},
             "parity": parity, "gpu_launches": launches["total"] * args.steps,
             "launches_per_step": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("limbs", "block_n", "nodes", "leaf_groups",

@@ -126,6 +126,24 @@ int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_
                         const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
                         fsyrk_b200_policy policy, int mirror_output, void* stream, fsyrk_b200_opcount* ops);
 
+/* ------------------------------------------------------------ multi-GPU */
+
+/* One rank's share of a syrk / syrk_acc / syrkd call partitioned over `nranks`
+ * GPUs (no reference analogue -- the reference is single-threaded).
+ * Every rank holds the whole A on its device and calls this with the same
+ * arguments; rank r computes the entries of Low(C) in the top-level block pairs
+ * it owns (fsyrk_b200_partition_owners) and leaves all other entries of C
+ * untouched.  The union over ranks equals the single-GPU result.  The top level
+ * is split with its three SYRK products as leaves (max_levels is capped at 1);
+ * shapes whose top level does not recurse are computed entirely by rank 0. */
+int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                             const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
+                             fsyrk_b200_policy policy, int rank, int nranks, void* stream, fsyrk_b200_opcount* ops);
+
+/* Owner rank of every top-level block pair (I >= J) for quadrant size h = n/2:
+ * owners[I * nblocks + J]; blocks are 384 rows/columns.  Host-only. */
+int fsyrk_b200_partition_owners(size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks);
+
 /* Drop cached plans and device arenas (tests, memory pressure). */
 void fsyrk_b200_release_cache(void);
 

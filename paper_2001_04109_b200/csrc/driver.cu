@@ -147,6 +147,39 @@ void fill_weights_p(uint64_t p, int32_t* w) {
     }
 }
 
+// ------------------------------------------------------ multi-GPU partition
+// Top-level tile-pair ownership: the h x h quadrants of the top
+// level are cut into blocks of kPartBlock rows/columns (a multiple of the
+// product tile 128 x BN for every BN and of the 32-row post tile); the owner
+// of the unordered block pair {I >= J} computes P1, P2, P5 on (I, J), P3 and
+// P4 on (I, J) and (J, I), and the post-additions of C11(I, J), C22(I, J),
+// C21(I, J), C21(J, I) -- all local.  Pairs are assigned longest-first to the
+// least-loaded rank (cost ~ rows_I * rows_J, halved on the diagonal).
+constexpr int kPartBlock = 384;
+
+std::vector<int> partition_owners(int h, int nranks) {
+    const int nb = (h + kPartBlock - 1) / kPartBlock;
+    std::vector<int> owner((size_t)nb * nb, -1);
+    struct PairCost {
+        double cost;
+        int i, j;
+    };
+    std::vector<PairCost> pc;
+    auto rows = [&](int b) { return (double)std::min(kPartBlock, h - b * kPartBlock); };
+    for (int i = 0; i < nb; ++i)
+        for (int j = 0; j <= i; ++j) pc.push_back({rows(i) * rows(j) * (i == j ? 0.5 : 1.0), i, j});
+    std::stable_sort(pc.begin(), pc.end(), [](const PairCost& a, const PairCost& b) { return a.cost > b.cost; });
+    std::vector<double> load(nranks, 0.0);
+    for (const auto& q : pc) {
+        int r = 0;
+        for (int t = 1; t < nranks; ++t)
+            if (load[t] < load[r]) r = t;
+        load[r] += q.cost;
+        owner[(size_t)q.i * nb + q.j] = r;
+    }
+    return owner;
+}
+
 // ------------------------------------------------------------------- plan
 enum Kind { LEAF = 0, LEVEL = 1, SPLITK = 2 };
 
@@ -250,6 +283,20 @@ struct Plan {
     std::vector<int> split_leaves;  // LEAF nodes converted from a residue view
     std::vector<ProdLaunch> prods;
     int nsm = 148;
+    // multi-GPU partition of the top level (rank prank of pnranks); see partition_owners
+    int prank = 0, pnranks = 1;
+    bool partitioned = false;  // top level split across ranks
+    bool idle = false;         // this rank has no share (shape not partitionable, rank > 0)
+    int part_nb = 0;
+    std::vector<int> owner;
+    std::vector<int2> root_pairs;  // owned 32 x 32 post tile pairs of the root
+    int2* dev_pairs = nullptr;
+    size_t off_pairs = 0;
+    bool owns_block_pair(int bi, int bj) const {
+        if (!partitioned) return true;
+        if (bi < bj) std::swap(bi, bj);
+        return owner[(size_t)bi * part_nb + bj] == prank;
+    }
     uint8_t* arena = nullptr;
     size_t arena_bytes = 0;
     uint32_t* root_in = nullptr;
@@ -336,13 +383,16 @@ struct Plan {
         return (int)gemms.size() - 1;
     }
 
-    void create(uint64_t p_, int n_, int kin_, int k_, fsyrk_b200_policy pol, bool colmap_) {
+    void create(uint64_t p_, int n_, int kin_, int k_, fsyrk_b200_policy pol, bool colmap_, int rank_ = 0,
+                int nranks_ = 1) {
         p = p_;
         n = n_;
         kin = kin_;
         k = k_;
         policy = pol;
         colmap = colmap_;
+        prank = rank_;
+        pnranks = nranks_;
         L = limbs_for(p);
         BN = modmm_block_n(L);
         host::Field f{p};
@@ -350,7 +400,19 @@ struct Plan {
         m = make_modp((uint32_t)p);
         c32 = (uint32_t)pow_mod(2, 32, p);
 
-        build(n, k, pol.max_levels, 0, -1, -1);
+        // the multi-GPU partition splits one top level whose three SYRK products are leaves
+        build(n, k, pnranks > 1 ? std::min<uint64_t>(pol.max_levels, 1) : pol.max_levels, 0, -1, -1);
+        if (pnranks > 1) {
+            const Node& r = nodes[0];
+            partitioned = r.kind == LEVEL && nodes[r.ch[0]].kind == LEAF && nodes[r.ch[1]].kind == LEAF &&
+                          nodes[r.ch[2]].kind == LEAF;
+            if (partitioned) {
+                part_nb = (r.h + kPartBlock - 1) / kPartBlock;
+                owner = partition_owners(r.h, pnranks);
+            } else {
+                idle = prank != 0;  // not partitionable: rank 0 computes everything
+            }
+        }
         for (auto& nd : nodes)
             if ((nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(L, p)) ||
                 (nd.kind == LEVEL && (uint64_t)nd.kw > modmm_k_limit(L, p)))
@@ -444,13 +506,16 @@ struct Plan {
                         const GemmGroup& gg = gemms[pgs[c].idx];
                         for (int b = 0; b < 2 * gg.count; ++b)
                             for (int tm = 0; tm * 128 < gg.h; ++tm)
-                                for (int tn = 0; tn * BN < gg.h; ++tn) pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                                for (int tn = 0; tn * BN < gg.h; ++tn)
+                                    if (!idle && owns_block_pair(tm * 128 / kPartBlock, tn * BN / kPartBlock))
+                                        pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
                     } else {
                         const LeafGroup& lg = leaves[pgs[c].idx];
                         for (int b = 0; b < lg.count; ++b)
                             for (int tm = 0; tm * 128 < lg.n; ++tm)
                                 for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn)
-                                    pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                                    if (!idle && owns_block_pair(tm * 128 / kPartBlock, tn * BN / kPartBlock))
+                                        pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
                     }
                 }
                 pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4));
@@ -507,6 +572,13 @@ struct Plan {
         for (auto& pg : preps) pg.off_nodes = ar.take(pg.nodes.size() * sizeof(PrepNode));
         for (auto& pg : posts)
             pg.off_nodes = ar.take(pg.nodes.size() * (pg.kind == LEVEL ? sizeof(PostNode) : sizeof(AddNode)));
+        if (partitioned) {  // owned 32 x 32 tile pairs of the root post-addition
+            const int h = nodes[0].h, T = (h + 31) / 32;
+            for (int I = 0; I < T; ++I)
+                for (int J = 0; J <= I; ++J)
+                    if (owns_block_pair(I * 32 / kPartBlock, J * 32 / kPartBlock)) root_pairs.push_back(make_int2(I, J));
+            off_pairs = ar.take(std::max<size_t>(root_pairs.size(), 1) * sizeof(int2));
+        }
 
         // ---- allocate and clear (the zero padding of every operand plane is never rewritten)
         arena_bytes = ar.size;
@@ -696,6 +768,12 @@ struct Plan {
                 pg.dev_post = reinterpret_cast<PostNode*>(arena + pg.off_nodes);
                 ck(cudaMemcpy(pg.dev_post, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
                    "upload post table");
+                if (partitioned && pg.depth == 0 && !root_pairs.empty()) {
+                    dev_pairs = reinterpret_cast<int2*>(arena + off_pairs);
+                    ck(cudaMemcpy(dev_pairs, root_pairs.data(), root_pairs.size() * sizeof(int2),
+                                  cudaMemcpyHostToDevice),
+                       "upload pair list");
+                }
             } else {
                 std::vector<AddNode> tab;
                 for (int ni : pg.nodes) {
@@ -754,6 +832,11 @@ struct Plan {
         auto mark = [&](int i) {
             if (g_phase_timing) ck(cudaEventRecord(ev[i], s), "event record");
         };
+        if (idle) {  // multi-GPU rank without a share (top level not partitionable)
+            std::fill(g_launch_counts, g_launch_counts + 5, 0);
+            g_last_plan_json = json();
+            return;
+        }
         mark(0);
         const Node& root = nodes[0];
         // 1. syrkd: convert the reference-layout input with the column transform folded in;
@@ -821,6 +904,11 @@ struct Plan {
                     a.alpha = alpha;
                     a.beta = beta;
                     root_done = true;
+                    if (partitioned) {
+                        if (root_pairs.empty()) return;  // this rank owns no block pair
+                        a.pairs = dev_pairs;
+                        a.npairs = (int)root_pairs.size();
+                    }
                 }
                 traced("post d" + std::to_string(pg.depth), st, [&] { ck(launch_post(a, st), "post"); });
             } else {
@@ -919,23 +1007,24 @@ struct PlanKey {
     int n, kin, k;
     uint64_t thr, lev;
     bool colmap;
-    int dev;
+    int dev, rank, nranks;
     bool operator<(const PlanKey& o) const {
-        return std::tie(p, n, kin, k, thr, lev, colmap, dev) < std::tie(o.p, o.n, o.kin, o.k, o.thr, o.lev, o.colmap, o.dev);
+        return std::tie(p, n, kin, k, thr, lev, colmap, dev, rank, nranks) <
+               std::tie(o.p, o.n, o.kin, o.k, o.thr, o.lev, o.colmap, o.dev, o.rank, o.nranks);
     }
 };
 
 std::mutex g_cache_mu;
 std::map<PlanKey, std::unique_ptr<Plan>> g_cache;
 
-Plan* get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap) {
+Plan* get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap, int rank = 0, int nranks = 1) {
     int dev = 0;
     cudaGetDevice(&dev);
-    PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev};
+    PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev, rank, nranks};
     auto it = g_cache.find(key);
     if (it != g_cache.end()) return it->second.get();
     auto plan = std::make_unique<Plan>();
-    plan->create(p, n, kin, k, pol, colmap);
+    plan->create(p, n, kin, k, pol, colmap, rank, nranks);
     Plan* raw = plan.get();
     g_cache[key] = std::move(plan);
     return raw;
@@ -1031,7 +1120,7 @@ void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
 // Core device call: everything resident on the device.
 void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda, const uint64_t* d,
              uint32_t beta, uint64_t* c_dev, size_t ldc, fsyrk_b200_policy pol, bool mirror, cudaStream_t s,
-             fsyrk_b200_opcount* ops) {
+             fsyrk_b200_opcount* ops, int rank = 0, int nranks = 1) {
     validate_field(p);
     validate_policy(pol);
     validate_shapes(n, k, lda, ldc);
@@ -1040,7 +1129,8 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     int kbar = (int)k;
     std::vector<ColMap> map;
     if (d) kbar = build_colmap(p, d, k, map);
-    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, d != nullptr);
+    if (nranks > 1 && mirror) fail(FSYRK_B200_EINVAL, "mirror_output needs the whole C (not available per rank)");
+    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, d != nullptr, rank, nranks);
     if (d) ck(cudaMemcpyAsync(plan->dev_colmap, map.data(), map.size() * sizeof(ColMap), cudaMemcpyHostToDevice, s),
               "upload colmap");
     plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
@@ -1146,6 +1236,30 @@ int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_
         validate_field(p);
         run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host, (uint32_t)(beta % p), c_dev, ldc, policy,
                 mirror_output != 0, static_cast<cudaStream_t>(stream), ops);
+    });
+}
+
+int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                             const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
+                             fsyrk_b200_policy policy, int rank, int nranks, void* stream, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(FSYRK_B200_EINVAL, "rank out of range");
+        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host, (uint32_t)(beta % p), c_dev, ldc, policy, false,
+                static_cast<cudaStream_t>(stream), ops, rank, nranks);
+    });
+}
+
+int fsyrk_b200_partition_owners(size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks) {
+    return guarded([&] {
+        if (nranks < 1) fail(FSYRK_B200_EINVAL, "nranks must be >= 1");
+        std::vector<int> own = partition_owners((int)h, nranks);
+        const size_t nb = (h + kPartBlock - 1) / kPartBlock;
+        if (nblocks) *nblocks = nb;
+        if (owners) {
+            if (owners_len < own.size()) fail(FSYRK_B200_EDIMENSION, "owner buffer too small");
+            std::copy(own.begin(), own.end(), owners);
+        }
     });
 }
 

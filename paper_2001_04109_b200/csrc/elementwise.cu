@@ -334,7 +334,12 @@ __global__ void post_kernel(const PostArgs args) {
     const int h = args.h;
     const PostOut out = make_out(args, nd);
     int I, J;
-    tri_decode(blockIdx.x, I, J);
+    if (args.pairs) {
+        I = args.pairs[blockIdx.x].x;
+        J = args.pairs[blockIdx.x].y;
+    } else {
+        tri_decode(blockIdx.x, I, J);
+    }
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int j = J * TS + tx;   // column inside tile (I, J)
     const int jt = I * TS + tx;  // column inside tile (J, I)
@@ -377,7 +382,12 @@ __global__ void __launch_bounds__(256) post_vec_kernel(const PostArgs args) {
     const int h = args.h;
     const PostOut out = make_out(args, nd);
     int I, J;
-    tri_decode(blockIdx.x, I, J);
+    if (args.pairs) {
+        I = args.pairs[blockIdx.x].x;
+        J = args.pairs[blockIdx.x].y;
+    } else {
+        tri_decode(blockIdx.x, I, J);
+    }
     const int tx = threadIdx.x, r = threadIdx.y;
     const int c0 = 4 * tx;
     const int i = I * TS + r, j = J * TS + c0;        // tile (I, J)
@@ -568,7 +578,8 @@ cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s) {
 cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     if (args.h == 0 || args.nnodes == 0) return cudaSuccess;
     const int T = (args.h + TS - 1) / TS;
-    dim3 grid(T * (T + 1) / 2, 1, args.nnodes);
+    dim3 grid(args.pairs ? args.npairs : T * (T + 1) / 2, 1, args.nnodes);
+    if (grid.x == 0) return cudaSuccess;
     // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
     if (args.h % 4 == 0) post_vec_kernel<<<grid, dim3(8, 32), 0, s>>>(args);
     else post_kernel<<<grid, dim3(32, 8), 0, s>>>(args);

@@ -86,6 +86,7 @@ EXPORTS = (
     "fsyrk_b200_syrk_fast_into", "fsyrk_b200_syrk_fast_acc", "fsyrk_b200_syrkd", "fsyrk_b200_syrk_dev",
     "fsyrk_b200_release_cache", "fsyrk_b200_last_launch_count", "fsyrk_b200_last_plan_json",
     "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
+    "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners",
 )
 
 
@@ -117,6 +118,12 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, ctypes.c_void_p,
                                       ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.c_void_p,
                                       ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrk_part_dev.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t,
+                                           ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, ctypes.c_void_p,
+                                           ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_partition_owners.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                              ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     L.fsyrk_b200_last_phase_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.fsyrk_b200_level_blocks.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
@@ -340,6 +347,32 @@ def syrk_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta: int
                                      int(beta) % p, ctypes.c_void_p(c_ptr), int(ldc), policy._c(), int(mirror),
                                      ctypes.c_void_p(stream), ctypes.byref(co)))
     _ops_out(ops, co)
+
+
+def syrk_part_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta: int, c_ptr: int, ldc: int,
+                  policy: RecursionPolicy, rank: int, nranks: int, stream: int = 0, d: Optional[np.ndarray] = None,
+                  ops: Optional[OpCount] = None) -> None:
+    """One rank's share of a multi-GPU call (fsyrk_b200_syrk_part_dev): the entries of Low(C)
+    in the top-level block pairs owned by `rank`; the union over ranks is the full result."""
+    co = _OpCount()
+    dptr = None
+    if d is not None:
+        dv = np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+        dptr = dv.ctypes.data_as(_u64p)
+    _check(lib().fsyrk_b200_syrk_part_dev(int(p), int(alpha) % p, ctypes.c_void_p(a_ptr), int(n), int(k), int(lda),
+                                          dptr, int(beta) % p, ctypes.c_void_p(c_ptr), int(ldc), policy._c(),
+                                          int(rank), int(nranks), ctypes.c_void_p(stream), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
+def partition_owners(h: int, nranks: int) -> np.ndarray:
+    """Owner rank of each top-level block pair (I >= J), as an nb x nb array (-1 above the diagonal)."""
+    nb = ctypes.c_size_t(0)
+    _check(lib().fsyrk_b200_partition_owners(int(h), int(nranks), None, 0, ctypes.byref(nb)))
+    out = np.full(nb.value * nb.value, -1, dtype=np.int32)
+    _check(lib().fsyrk_b200_partition_owners(int(h), int(nranks), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                             out.size, ctypes.byref(nb)))
+    return out.reshape(nb.value, nb.value)
 
 
 def gemm_nt(f: PrimeField, a: np.ndarray, b: np.ndarray) -> np.ndarray:

@@ -391,8 +391,7 @@ def main():
         return
 
     peaks = load_peaks()
-    L = plan.get("limbs", 3)
-    int8_ops = 2.0 * L * L * plan.get("tensor_macs", 0)
+    int8_ops = 2.0 * plan.get("terms", 9) * plan.get("tensor_macs", 0)  # NT int8 MMAs per modular MAC
     nprod = max(1, launches.get("products", 1))
     prod_ms = phase["products"]
     peak_i8 = peaks.get("int8_tops")
@@ -422,7 +421,7 @@ def main():
                        "l2": "flushed between steps (256 MiB write)"},
             "parity": parity, "gpu_launches": launches["total"] * args.steps,
             "launches_per_step": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("limbs", "block_n", "nodes", "leaf_groups",
+            "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("scheme", "terms", "block_n", "nodes", "leaf_groups",
                                                                      "gemm_groups", "arena_bytes")}}
     print(json.dumps(line))
     if world > 1:

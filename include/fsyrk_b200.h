@@ -141,8 +141,10 @@ int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, 
                              fsyrk_b200_policy policy, int rank, int nranks, void* stream, fsyrk_b200_opcount* ops);
 
 /* Owner rank of every top-level block pair (I >= J) for quadrant size h = n/2:
- * owners[I * nblocks + J]; blocks are 384 rows/columns.  Host-only. */
-int fsyrk_b200_partition_owners(size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks);
+ * owners[I * nblocks + J]; blocks are `block` rows/columns (lcm of 128 and the
+ * product tile width of p's digit scheme).  Host-only. */
+int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks,
+                                size_t* block);
 
 /* Drop cached plans and device arenas (tests, memory pressure). */
 void fsyrk_b200_release_cache(void);

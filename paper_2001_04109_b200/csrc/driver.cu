@@ -113,14 +113,15 @@ EncodeFn encode_fn() {
 }
 
 // 4-D int8 plane tensor [batch][L][rows][kpad], boxes of 128 (K) x box_rows.
-CUtensorMap make_plane_map(void* base, int kpad, int rows, int L, int batch, int box_rows) {
+CUtensorMap make_plane_map(void* base, int kpad, int rows, int L, int batch, int box_rows, int bk) {
     CUtensorMap m;
     cuuint64_t dims[4] = {(cuuint64_t)kpad, (cuuint64_t)rows, (cuuint64_t)L, (cuuint64_t)batch};
     cuuint64_t strides[3] = {(cuuint64_t)kpad, (cuuint64_t)kpad * rows, (cuuint64_t)kpad * rows * L};
-    cuuint32_t box[4] = {128, (cuuint32_t)box_rows, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)box_rows, 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(FSYRK_B200_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
@@ -128,36 +129,28 @@ CUtensorMap make_plane_map(void* base, int kpad, int rows, int L, int batch, int
 
 long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
 
-int limbs_for(uint64_t p) {
-    if (p <= 65536ull) return 2;
-    if (p <= 16777216ull) return 3;
-    return 4;
-}
 
 uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t p) {
     host::Field f{p};
     return f.pow(b, e);
 }
 
-// Fold weights of the product epilogue: 256^s mod p as balanced representatives.
-void fill_weights_p(uint64_t p, int32_t* w) {
-    for (int s = 0; s < 8; ++s) {
-        uint64_t v = pow_mod(256, (uint64_t)s, p);
-        w[s] = v > p / 2 ? (int32_t)((int64_t)v - (int64_t)p) : (int32_t)v;
-    }
-}
 
 // ------------------------------------------------------ multi-GPU partition
 // Top-level tile-pair ownership: the h x h quadrants of the top
 // level are cut into blocks of kPartBlock rows/columns (a multiple of the
-// product tile 128 x BN for every BN and of the 32-row post tile); the owner
+// product tile 128 x BN of the plan's scheme and of the 32-row post tile); the owner
 // of the unordered block pair {I >= J} computes P1, P2, P5 on (I, J), P3 and
 // P4 on (I, J) and (J, I), and the post-additions of C11(I, J), C22(I, J),
 // C21(I, J), C21(J, I) -- all local.  Pairs are assigned longest-first to the
 // least-loaded rank (cost ~ rows_I * rows_J, halved on the diagonal).
-constexpr int kPartBlock = 384;
+int part_block_for(int bn) {
+    int b = 128;
+    while (b % bn) b += 128;  // lcm(128, BN): 128 (BN 64, 128), 384 (96), 640 (160)
+    return b;
+}
 
-std::vector<int> partition_owners(int h, int nranks) {
+std::vector<int> partition_owners(int h, int nranks, int kPartBlock) {
     const int nb = (h + kPartBlock - 1) / kPartBlock;
     std::vector<int> owner((size_t)nb * nb, -1);
     struct PairCost {
@@ -271,7 +264,8 @@ struct Plan {
     int n, kin, k;  // k: columns after the (optional) syrkd transform
     fsyrk_b200_policy policy;
     bool colmap = false;
-    int L, BN;
+    SchemeInfo sch;  // digit scheme of the tensor-core products (schemes.cuh)
+    int L, BN, BK;   // L: digit planes stored per operand
     host::Skew y;
     ModP m;
     uint32_t c32 = 0;
@@ -287,7 +281,7 @@ struct Plan {
     int prank = 0, pnranks = 1;
     bool partitioned = false;  // top level split across ranks
     bool idle = false;         // this rank has no share (shape not partitionable, rank > 0)
-    int part_nb = 0;
+    int part_nb = 0, kPartBlock = 384;
     std::vector<int> owner;
     std::vector<int2> root_pairs;  // owned 32 x 32 post tile pairs of the root
     int2* dev_pairs = nullptr;
@@ -393,8 +387,10 @@ struct Plan {
         colmap = colmap_;
         prank = rank_;
         pnranks = nranks_;
-        L = limbs_for(p);
-        BN = modmm_block_n(L);
+        sch = scheme_for(p);
+        L = sch.planes;
+        BN = sch.bn;
+        BK = sch.bk;
         host::Field f{p};
         y = host::skew_orthogonal(f);
         m = make_modp((uint32_t)p);
@@ -407,15 +403,16 @@ struct Plan {
             partitioned = r.kind == LEVEL && nodes[r.ch[0]].kind == LEAF && nodes[r.ch[1]].kind == LEAF &&
                           nodes[r.ch[2]].kind == LEAF;
             if (partitioned) {
+                kPartBlock = part_block_for(BN);
                 part_nb = (r.h + kPartBlock - 1) / kPartBlock;
-                owner = partition_owners(r.h, pnranks);
+                owner = partition_owners(r.h, pnranks, kPartBlock);
             } else {
                 idle = prank != 0;  // not partitionable: rank 0 computes everything
             }
         }
         for (auto& nd : nodes)
-            if ((nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(L, p)) ||
-                (nd.kind == LEVEL && (uint64_t)nd.kw > modmm_k_limit(L, p)))
+            if ((nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(sch, p)) ||
+                (nd.kind == LEVEL && (uint64_t)nd.kw > modmm_k_limit(sch, p)))
                 fail(FSYRK_B200_EINVAL, "inner dimension " + std::to_string(nd.k) +
                                             " exceeds the exact int32 accumulation bound");
         // ---- input sources: views of the caller's matrix stay uint64 windows (no conversion
@@ -591,15 +588,15 @@ struct Plan {
         for (auto& lg : leaves) {
             lg.planes = reinterpret_cast<int8_t*>(arena + lg.off_planes);
             lg.xout = reinterpret_cast<uint32_t*>(arena + lg.off_x);
-            lg.tA = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, 128);
-            lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, BN);
+            lg.tA = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, 128, BK);
+            lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, BN, BK);
         }
         for (auto& gg : gemms) {
             gg.ga = reinterpret_cast<int8_t*>(arena + gg.off_ga);
             gg.gb = reinterpret_cast<int8_t*>(arena + gg.off_gb);
             gg.out = reinterpret_cast<uint32_t*>(arena + gg.off_out);
-            gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128);
-            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, L, 2 * gg.count, BN);
+            gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128, BK);
+            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, L, 2 * gg.count, BN, BK);
         }
         {
             int dev = 0;
@@ -610,7 +607,7 @@ struct Plan {
             GroupedArgs& a = pl.args;
             std::memset(&a, 0, sizeof(a));
             a.modp = m;
-            fill_weights_p(p, a.w);
+            fill_fold_weights(sch, p, a.w);
             a.ngroups = (int)pl.members.size();
             a.ntiles = (int)pl.host_tiles.size();
             int4* tiles = reinterpret_cast<int4*>(arena + pl.off_tiles);
@@ -626,7 +623,7 @@ struct Plan {
                     g.tmA = gg.tA;
                     g.tmB = gg.tB;
                     g.M = g.N = gg.h;
-                    g.k_blocks = gg.kpad / 128;
+                    g.k_blocks = gg.kpad / BK;
                     g.syrk = 0;
                     g.vec_ok = gg.h % 4 == 0;
                     g.out = gg.out;
@@ -637,7 +634,7 @@ struct Plan {
                     g.tmA = lg.tA;
                     g.tmB = lg.tB;
                     g.M = g.N = lg.n;
-                    g.k_blocks = lg.kpad / 128;
+                    g.k_blocks = lg.kpad / BK;
                     g.syrk = 1;
                     g.vec_ok = lg.n % 4 == 0;
                     g.out = lg.xout;
@@ -692,7 +689,7 @@ struct Plan {
             GemmGroup& gg = gemms[n0.ggroup];
             PrepArgs& a = pg.args;
             a.m = m;
-            a.L = L;
+            a.L = sch.id;  // digit scheme
             a.h = n0.h;
             a.kh = n0.kh;
             a.kw = n0.kw;
@@ -797,18 +794,22 @@ struct Plan {
         for (auto& lg : leaves) {
             uint64_t macs = (uint64_t)lg.count * lg.n * (lg.n + 1) / 2 * lg.k;
             tensor_macs += macs;
-            int8_macs += (uint64_t)lg.count * lg.ntiles * 128ull * BN * lg.kpad * L * L;
+            int8_macs += (uint64_t)lg.count * lg.ntiles * 128ull * BN * lg.kpad * sch.nterms;
         }
         for (auto& gg : gemms) {
             tensor_macs += (uint64_t)2 * gg.count * gg.h * gg.h * gg.kw;
-            int8_macs += (uint64_t)2 * gg.count * (gg.hpad / 128) * ((gg.h + BN - 1) / BN) * 128ull * BN * gg.kpad * L * L;
+            int8_macs += (uint64_t)2 * gg.count * (gg.hpad / 128) * ((gg.h + BN - 1) / BN) * 128ull * BN * gg.kpad *
+                         sch.nterms;
             ew_adds += (uint64_t)gg.count * (4ull * gg.h * gg.kw + 4ull * gg.h * gg.h);
         }
     }
 
     std::string json() const {
         std::ostringstream o;
-        o << "{\"p\": " << p << ", \"n\": " << n << ", \"k\": " << k << ", \"limbs\": " << L << ", \"block_n\": " << BN
+        static const char* scheme_names[] = {"limb2", "limb3", "limb4", "m17", "m31"};
+        o << "{\"p\": " << p << ", \"n\": " << n << ", \"k\": " << k << ", \"scheme\": \"" << scheme_names[sch.id]
+          << "\", \"planes\": " << L << ", \"terms\": " << sch.nterms << ", \"accumulators\": " << sch.nacc
+          << ", \"limbs\": " << L << ", \"block_n\": " << BN
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
           << "}, \"nodes\": " << nodes.size() << ", \"arena_bytes\": " << arena_bytes
           << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs << ", \"leaf_groups\": [";
@@ -849,7 +850,7 @@ struct Plan {
         for (int li : split_leaves) {
             const Node& nd = nodes[li];
             const LeafGroup& lg = leaves[nd.lgroup];
-            ck(launch_split_planes(L, InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0}, a_dev, lda, nd.n, nd.k,
+            ck(launch_split_planes(sch.id, InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0}, a_dev, lda, nd.n, nd.k,
                                    (uint32_t)p, lg.planes + nd.lslot * lg.slot, lg.plane, lg.kpad, s),
                "split_planes");
             counts[1]++;
@@ -886,7 +887,7 @@ struct Plan {
         };
         auto run_prod = [&](ProdLaunch& pl, cudaStream_t st) {
             traced("products phase " + std::to_string(pl.phase), st,
-                   [&] { ck(modmm_launch(L, pl.args, std::min(nsm, pl.args.ntiles), st), "modmm"); });
+                   [&] { ck(modmm_launch(sch, pl.args, std::min(nsm, pl.args.ntiles), st), "modmm"); });
             counts[0]++;
         };
         bool root_done = false;
@@ -1250,12 +1251,16 @@ int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, 
     });
 }
 
-int fsyrk_b200_partition_owners(size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks) {
+int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks,
+                                size_t* block) {
     return guarded([&] {
         if (nranks < 1) fail(FSYRK_B200_EINVAL, "nranks must be >= 1");
-        std::vector<int> own = partition_owners((int)h, nranks);
-        const size_t nb = (h + kPartBlock - 1) / kPartBlock;
+        validate_field(p);
+        const int blk = part_block_for(scheme_for(p).bn);
+        std::vector<int> own = partition_owners((int)h, nranks, blk);
+        const size_t nb = (h + blk - 1) / blk;
         if (nblocks) *nblocks = nb;
+        if (block) *block = (size_t)blk;
         if (owners) {
             if (owners_len < own.size()) fail(FSYRK_B200_EDIMENSION, "owner buffer too small");
             std::copy(own.begin(), own.end(), owners);
@@ -1311,16 +1316,22 @@ int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, s
         const int h = root.h, kw = root.kw, L = plan.L;
         if (kw_out) *kw_out = (size_t)kw;
         const GemmGroup& g = plan.gemms[root.ggroup];
-        // recombine limb planes -> residues on the host (white-box readback only)
+        // recombine digit planes -> residues on the host (white-box readback only): the first
+        // `nd` planes are the digits of base 2^bits, signed for the balanced LIMB schemes
+        const int sid = plan.sch.id;
+        const int nd = sid == SCHEME_M17 ? 3 : sid == SCHEME_M31 ? 4 : L;
+        const int bits = sid == SCHEME_M17 ? 6 : 8;
+        const bool sgn = !plan.sch.is_unsigned;
         auto read_planes = [&](const int8_t* base, long long plane, long long row, int rows, int cols, uint64_t* out) {
             std::vector<int8_t> buf((size_t)plane * L);
             ck(cudaMemcpy(buf.data(), base, buf.size(), cudaMemcpyDeviceToHost), "D2H planes");
             for (int i = 0; i < rows; ++i)
                 for (int j = 0; j < cols; ++j) {
                     long long v = 0, w = 1;
-                    for (int l = 0; l < L; ++l) {
-                        v += (long long)buf[(size_t)l * plane + (size_t)i * row + j] * w;
-                        w *= 256;
+                    for (int l = 0; l < nd; ++l) {
+                        const int8_t b = buf[(size_t)l * plane + (size_t)i * row + j];
+                        v += (sgn ? (long long)b : (long long)(uint8_t)b) * w;
+                        w <<= bits;
                     }
                     long long r = v % (long long)p;
                     if (r < 0) r += (long long)p;
@@ -1355,8 +1366,9 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         if (lda < k || ldb < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "gemm_nt: dimension mismatch");
         require_device();
         if (m == 0 || n == 0) return;
-        const int L = limbs_for(p), BN = modmm_block_n(L);
-        if (k > modmm_k_limit(L, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
+        const SchemeInfo sch = scheme_for(p);
+        const int L = sch.planes, BN = sch.bn, BK = sch.bk;
+        if (k > modmm_k_limit(sch, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
         const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
         const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
         DevBuf d64a, d64b, r32, pa, pb, out;
@@ -1372,13 +1384,13 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
             ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
             ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
             const InView top{nullptr, 0, 0, 0, 1};
-            ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64a.ptr), (long long)k, (int)m, (int)k, (uint32_t)p,
+            ck(launch_split_planes(sch.id, top, static_cast<uint64_t*>(d64a.ptr), (long long)k, (int)m, (int)k, (uint32_t)p,
                                    static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, 0), "split A");
-            ck(launch_split_planes(L, top, static_cast<uint64_t*>(d64b.ptr), (long long)k, (int)n, (int)k, (uint32_t)p,
+            ck(launch_split_planes(sch.id, top, static_cast<uint64_t*>(d64b.ptr), (long long)k, (int)n, (int)k, (uint32_t)p,
                                    static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, 0), "split B");
         }
-        CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128);
-        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, BN);
+        CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128, BK);
+        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, BN, BK);
         std::vector<int4> tiles;
         for (int tm = 0; tm * 128 < (int)m; ++tm)
             for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
@@ -1388,7 +1400,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         GroupedArgs args;
         std::memset(&args, 0, sizeof(args));
         args.modp = make_modp((uint32_t)p);
-        fill_weights_p(p, args.w);
+        fill_fold_weights(sch, p, args.w);
         args.ngroups = 1;
         args.ntiles = (int)tiles.size();
         args.tiles = static_cast<int4*>(dtiles.ptr);
@@ -1397,7 +1409,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         g.tmB = tb;
         g.M = (int)m;
         g.N = (int)n;
-        g.k_blocks = (int)(kpad / 128);
+        g.k_blocks = (int)(kpad / BK);
         g.syrk = 0;
         g.vec_ok = n % 4 == 0;
         g.a_mult = g.b_mult = 1;
@@ -1407,7 +1419,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         int nsm = 148, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        ck(modmm_launch(L, args, std::min<int>(nsm, (int)tiles.size()), 0), "modmm");
+        ck(modmm_launch(sch, args, std::min<int>(nsm, (int)tiles.size()), 0), "modmm");
         ck(cudaDeviceSynchronize(), "sync");
         std::vector<uint32_t> buf(m * n);
         ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");

@@ -88,20 +88,31 @@ __device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, lo
     return s;
 }
 
-template <int L>
+// The kernels below are templated on the digit scheme S (schemes.cuh): a residue
+// becomes Scheme<S>::PA int8 planes, byte l of encode_planes<S>(x) going to plane l.
+template <int S>
 __device__ __forceinline__ void put_planes(int8_t* base, long long plane, long long off, uint32_t x, uint32_t p) {
-    const uint32_t w = limb_word<L>(x, p);
+    const uint64_t w = encode_planes<S>(x, p);
 #pragma unroll
-    for (int l = 0; l < L; ++l) base[l * plane + off] = (int8_t)(w >> (8 * l));
+    for (int l = 0; l < Scheme<S>::PA; ++l) base[l * plane + off] = (int8_t)(w >> (8 * l));
 }
 
 // four consecutive columns of one row, one 32-bit store per plane
-template <int L>
+template <int S>
 __device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long long off, uint4 x, uint32_t p) {
-    const uint32_t w0 = limb_word<L>(x.x, p), w1 = limb_word<L>(x.y, p), w2 = limb_word<L>(x.z, p),
-                   w3 = limb_word<L>(x.w, p);
+    const uint64_t w0 = encode_planes<S>(x.x, p), w1 = encode_planes<S>(x.y, p), w2 = encode_planes<S>(x.z, p),
+                   w3 = encode_planes<S>(x.w, p);
 #pragma unroll
-    for (int l = 0; l < L; ++l) *reinterpret_cast<uint32_t*>(base + l * plane + off) = gather_byte(w0, w1, w2, w3, l);
+    for (int l = 0; l < Scheme<S>::PA; ++l) {
+        const int sh = 8 * l;
+        uint32_t v;
+        if (sh < 32)
+            v = gather_byte((uint32_t)w0, (uint32_t)w1, (uint32_t)w2, (uint32_t)w3, l);
+        else
+            v = gather_byte((uint32_t)(w0 >> 32), (uint32_t)(w1 >> 32), (uint32_t)(w2 >> 32), (uint32_t)(w3 >> 32),
+                            l - 4);
+        *reinterpret_cast<uint32_t*>(base + l * plane + off) = v;
+    }
 }
 
 template <int L, bool VEC>
@@ -555,10 +566,12 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
                                                               row_stride);                                         \
     else split_planes_kernel<LL, false><<<g, 256, 0, s>>>(in, a64, ld64, rows, k, m, planes, plane_stride,          \
                                                            row_stride);
-    switch (L) {
-        case 2: FSYRK_SPLIT(2) break;
-        case 3: FSYRK_SPLIT(3) break;
-        case 4: FSYRK_SPLIT(4) break;
+    switch (L) {  // L: digit scheme id (schemes.cuh)
+        case SCHEME_LIMB2: FSYRK_SPLIT(SCHEME_LIMB2) break;
+        case SCHEME_LIMB3: FSYRK_SPLIT(SCHEME_LIMB3) break;
+        case SCHEME_LIMB4: FSYRK_SPLIT(SCHEME_LIMB4) break;
+        case SCHEME_M17: FSYRK_SPLIT(SCHEME_M17) break;
+        case SCHEME_M31: FSYRK_SPLIT(SCHEME_M31) break;
         default: return cudaErrorInvalidValue;
     }
 #undef FSYRK_SPLIT
@@ -567,10 +580,12 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
 
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s) {
     if (args.h == 0 || args.nnodes == 0 || args.kw == 0) return cudaSuccess;
-    switch (args.L) {
-        case 2: return prep_dispatch<2>(args, s);
-        case 3: return prep_dispatch<3>(args, s);
-        case 4: return prep_dispatch<4>(args, s);
+    switch (args.L) {  // digit scheme id
+        case SCHEME_LIMB2: return prep_dispatch<SCHEME_LIMB2>(args, s);
+        case SCHEME_LIMB3: return prep_dispatch<SCHEME_LIMB3>(args, s);
+        case SCHEME_LIMB4: return prep_dispatch<SCHEME_LIMB4>(args, s);
+        case SCHEME_M17: return prep_dispatch<SCHEME_M17>(args, s);
+        case SCHEME_M31: return prep_dispatch<SCHEME_M31>(args, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "modp.cuh"
+#include "schemes.cuh"
 
 namespace fsyrk_b200 {
 

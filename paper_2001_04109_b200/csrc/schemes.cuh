@@ -1,0 +1,154 @@
+// Digit schemes of the exact int8 tensor-core products.
+//
+// A residue x in [0, p) is stored as P int8 "planes" (one byte each).  An
+// output tile accumulates NT tensor-core terms  acc[t.acc] += A_plane[t.a] *
+// B_plane[t.b]^T  in int32 TMEM columns; the epilogue folds the NACC
+// accumulators into C mod p.  Every term of a scheme has a fixed weight
+// (a power of the digit base, possibly times a small constant), so
+//     x * y = sum_acc  weight(acc) * acc   (mod p)
+// holds exactly as long as no int32 accumulator overflows (kmax).
+//
+//  LIMB2/3/4 : balanced base-256 digits in [-128, 127] (any p < 2^16 / 2^24 / 2^31);
+//              2L-1 accumulators, one per shift s = i + j, weights 256^s mod p.
+//  M17       : p = 2^17 - 1.  Unsigned base-64 digits d0, d1, d2 (6 bits each).
+//              Since 2^18 = 2 (mod p) and 2^24 = 2 * 2^6, the shifts 3 and 4
+//              fold into accumulators 0 and 1 with doubled digits 2 d1, 2 d2
+//              (<= 126): 3 accumulators instead of 5, which frees TMEM for a
+//              160-column tile.  Fold: a0 + 2^6 a1 + 2^12 a2, Mersenne reduction.
+//  M31       : p = 2^31 - 1.  Unsigned base-256 digits d0..d3 (d3 < 128).  Since
+//              2^32 = 2, 2^40 = 2 * 2^8, 2^48 = 2 * 2^16 (mod p), every wrapped
+//              term that touches d3 folds into accumulators 0..2 with the doubled
+//              digit 2 d3 (<= 254, unsigned); only d2 e2 (weight 2) keeps its own
+//              accumulator: 5 accumulators instead of 7 (96-column tiles instead
+//              of 64).  Fold: a0 + 2^8 a1 + 2^16 a2 + 2^24 a3 + 2 a4.
+#pragma once
+
+#include <cstdint>
+
+#include "modp.cuh"
+
+namespace fsyrk_b200 {
+
+enum SchemeId { SCHEME_LIMB2 = 0, SCHEME_LIMB3 = 1, SCHEME_LIMB4 = 2, SCHEME_M17 = 3, SCHEME_M31 = 4 };
+
+struct Term {
+    int8_t a, b, acc;
+};
+
+template <int S>
+struct Scheme;
+
+template <>
+struct Scheme<SCHEME_LIMB2> {
+    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = 128, BK = 128, STAGES = 3;
+    static constexpr bool UNSIGNED = false;
+    __host__ __device__ static constexpr Term term(int q) {
+        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
+        return T[q];
+    }
+};
+template <>
+struct Scheme<SCHEME_LIMB3> {
+    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, BN = 96, BK = 128, STAGES = 2;
+    static constexpr bool UNSIGNED = false;
+    __host__ __device__ static constexpr Term term(int q) {
+        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
+                                   {2, 0, 2}, {1, 2, 3}, {2, 1, 3}, {2, 2, 4}};
+        return T[q];
+    }
+};
+template <>
+struct Scheme<SCHEME_LIMB4> {
+    static constexpr int PA = 4, PB = 4, NACC = 7, NT = 16, BN = 64, BK = 128, STAGES = 2;
+    static constexpr bool UNSIGNED = false;
+    __host__ __device__ static constexpr Term term(int q) {
+        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2},
+                                   {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}, {1, 3, 4}, {2, 2, 4},
+                                   {3, 1, 4}, {2, 3, 5}, {3, 2, 5}, {3, 3, 6}};
+        return T[q];
+    }
+};
+// planes: A = {d0, d1, d2, 2 d1, 2 d2}, B = {e0, e1, e2} (B reads the first 3 planes)
+template <>
+struct Scheme<SCHEME_M17> {
+    static constexpr int PA = 5, PB = 3, NACC = 3, NT = 9, BN = 160, BK = 64, STAGES = 3;
+    static constexpr bool UNSIGNED = true;
+    __host__ __device__ static constexpr Term term(int q) {
+        constexpr Term T[NT] = {
+        {0, 0, 0}, {3, 2, 0}, {4, 1, 0},   // d0 e0 + 2^18 (d1 e2 + d2 e1) = d0 e0 + (2 d1) e2 + (2 d2) e1
+        {0, 1, 1}, {1, 0, 1}, {4, 2, 1},   // 2^6 (d0 e1 + d1 e0) + 2^24 d2 e2 = 2^6 (... + (2 d2) e2)
+        {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
+        return T[q];
+    }  // 2^12 (d0 e2 + d1 e1 + d2 e0)
+};
+// planes: A = B = {d0, d1, d2, d3, 2 d3}
+template <>
+struct Scheme<SCHEME_M31> {
+    static constexpr int PA = 5, PB = 5, NACC = 5, NT = 16, BN = 96, BK = 64, STAGES = 3;
+    static constexpr bool UNSIGNED = true;
+    __host__ __device__ static constexpr Term term(int q) {
+        constexpr Term T[NT] = {
+        {0, 0, 0}, {1, 4, 0}, {4, 1, 0},             // s=0 and s=4 (2^32 = 2): d1 (2 e3) + (2 d3) e1
+        {0, 1, 1}, {1, 0, 1}, {2, 4, 1}, {4, 2, 1},  // s=1 and s=5 (2^40 = 2 * 2^8)
+        {0, 2, 2}, {1, 1, 2}, {2, 0, 2}, {4, 3, 2},  // s=2 and s=6 (2^48 = 2 * 2^16): (2 d3) e3
+        {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3},  // s=3
+        {2, 2, 4}};
+        return T[q];
+    }                                  // d2 e2, weight 2^32 = 2
+};
+
+// --------------------------------------------------------------- encoding
+// Byte l of the result is plane l of residue x (canonical, x < p).
+template <int S>
+__host__ __device__ inline uint64_t encode_planes(uint32_t x, uint32_t p) {
+    if constexpr (S == SCHEME_M17) {
+        const uint32_t d0 = x & 63u, d1 = (x >> 6) & 63u, d2 = x >> 12;
+        return (uint64_t)d0 | (uint64_t)d1 << 8 | (uint64_t)d2 << 16 | (uint64_t)(2 * d1) << 24 |
+               (uint64_t)(2 * d2) << 32;
+    } else if constexpr (S == SCHEME_M31) {
+        return (uint64_t)x | (uint64_t)(2 * (x >> 24)) << 32;
+    } else {
+        constexpr int L = S == SCHEME_LIMB2 ? 2 : S == SCHEME_LIMB3 ? 3 : 4;
+        // balanced digits: r + B has plain base-256 digits (d_l + 128); xor 0x80 recentres them
+        constexpr uint32_t bias = L == 2 ? 0x8080u : L == 3 ? 0x808080u : 0x80808080u;
+        constexpr int64_t span = 1ll << (8 * L);
+        constexpr int64_t lo = -128ll * ((span - 1) / 255);
+        const uint32_t hi = (uint32_t)(lo + span - 1);
+        const uint32_t r = x > hi ? x - p : x;
+        return (uint64_t)((r + bias) ^ 0x80808080u);
+    }
+}
+
+template <int S>
+constexpr int planes_of() {
+    return Scheme<S>::PA;
+}
+
+// ------------------------------------------------------------------ fold
+// Epilogue: accumulators (as raw 32-bit TMEM words) -> residue.
+// w: balanced weights (LIMB schemes only).
+template <int S>
+__device__ __forceinline__ uint32_t fold_acc(const uint32_t* a, const ModP& m, const int32_t* w) {
+    if constexpr (S == SCHEME_M17) {
+        // unsigned accumulators < 2^31: v < 2^44
+        uint64_t v = (uint64_t)a[0] + ((uint64_t)a[1] << 6) + ((uint64_t)a[2] << 12);
+        v = (v & 0x1FFFFull) + (v >> 17);  // < 2^28
+        v = (v & 0x1FFFFull) + (v >> 17);  // < 2^17 + 2^11
+        uint32_t r = (uint32_t)v;
+        return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
+    } else if constexpr (S == SCHEME_M31) {
+        uint64_t v = (uint64_t)a[0] + ((uint64_t)a[1] << 8) + ((uint64_t)a[2] << 16) + ((uint64_t)a[3] << 24) +
+                     ((uint64_t)a[4] << 1);  // < 2^56
+        v = (v & 0x7FFFFFFFull) + (v >> 31);  // < 2^31 + 2^25
+        v = (v & 0x7FFFFFFFull) + (v >> 31);
+        uint32_t r = (uint32_t)v;
+        return r >= 0x7FFFFFFFu ? r - 0x7FFFFFFFu : r;
+    } else {
+        int64_t v = (int64_t)(int32_t)a[0];
+#pragma unroll
+        for (int s = 1; s < Scheme<S>::NACC; ++s) v += (int64_t)(int32_t)a[s] * (int64_t)w[s];
+        return mod_s64(v, m);
+    }
+}
+
+}  // namespace fsyrk_b200

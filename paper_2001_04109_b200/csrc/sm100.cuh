@@ -105,13 +105,13 @@ __device__ __forceinline__ uint64_t sdesc_kmajor(uint32_t smem_addr, int layout,
     return d;
 }
 
-// Instruction descriptor, kind::i8: s8 x s8 -> s32, both operands K-major.
-__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
-    return (2u << 4)                         // D format: S32
-           | (1u << 7)                       // A format: signed int8
-           | (1u << 10)                      // B format: signed int8
-           | ((uint32_t)(n >> 3) << 17)      // N / 8
-           | ((uint32_t)(m >> 4) << 24);     // M / 16
+// Instruction descriptor, kind::i8: (s8|u8) x (s8|u8) -> s32, both operands K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n, bool is_signed = true) {
+    return (2u << 4)                                  // D format: S32
+           | ((is_signed ? 1u : 0u) << 7)             // A format: 1 signed int8, 0 unsigned
+           | ((is_signed ? 1u : 0u) << 10)            // B format
+           | ((uint32_t)(n >> 3) << 17)               // N / 8
+           | ((uint32_t)(m >> 4) << 24);              // M / 16
 }
 
 }  // namespace fsyrk_b200::sm100

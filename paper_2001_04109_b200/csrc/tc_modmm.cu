@@ -6,26 +6,27 @@
 // products of every recursion level, the Strassen-Winograd engine
 // gemm_winograd_nt_into (include/fsyrk/winograd.hpp:195-202).
 //
-// Representation: every residue is split into L balanced int8 limbs
-// (modp.cuh), stored as L planes [L][rows][K] per operand.  For an output
-// tile the kernel accumulates the 2L-1 "shift" sums
-//      T_s = sum_{i+j=s} A_i * B_j^T          (int32, exact)
-// in TMEM with tcgen05.mma.kind::i8, reusing each staged limb tile for L
-// products, and the epilogue folds them:  C = sum_s 256^s T_s  mod p.
-// |T_s| <= L * K * 2^14 < 2^31 and the int64 fold bound limit K
-// (modmm_k_limit, checked by the planner).
-//
-// Tile shape 128 x BN with BN as large as TMEM allows for the 2L-1
-// accumulators (L=2: 128, L=3: 96, L=4: 64): the microbenchmark in
-// profiles/ubench shows the int8 MMA rate falls with N (shared-memory
-// operand bandwidth), so the accumulators are not double-buffered; instead
-// the persistent kernel prefetches the next tile while the epilogue drains.
+// Every residue is stored as P int8 digit planes (schemes.cuh); an output tile
+// accumulates the scheme's NT int8 x int8 -> int32 products in TMEM with
+// tcgen05.mma.kind::i8 and the epilogue folds its NACC accumulators mod p.
+// Scheme choice (scheme_for):
+//   p = 2^17 - 1 : M17  (9 MMAs, 3 accumulators, 128 x 160 tiles)
+//   p = 2^31 - 1 : M31  (16 MMAs, 5 accumulators, 128 x 96 tiles)
+//   p <= 2^16    : LIMB2 (4 MMAs, 3 accumulators, 128 x 128)
+//   p <= 2^24    : LIMB3 (9 MMAs, 5 accumulators, 128 x 96)
+//   otherwise    : LIMB4 (16 MMAs, 7 accumulators, 128 x 64)
+// The tile N is as large as TMEM allows for the accumulators: the
+// microbenchmark in profiles/ubench shows the int8 MMA rate falls with N
+// (shared-memory operand bandwidth), so the accumulators are not double
+// buffered; the persistent kernel prefetches the next tile while the epilogue
+// drains instead.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "modp.cuh"
+#include "schemes.cuh"
 #include "sm100.cuh"
 #include "tc_modmm.h"
 #include "tc_modmm_kernel.cuh"
@@ -34,22 +35,68 @@ namespace fsyrk_b200 {
 
 using namespace tc;
 
-int modmm_block_n(int L) { return L == 2 ? 128 : L == 3 ? 96 : 64; }
-int modmm_block_k(int L) { (void)L; return 128; }
+namespace {
 
-size_t modmm_k_limit(int L, uint64_t p) {
-    // int32 shift sums: |T_s| <= L * K * 2^14 < 2^31
-    const uint64_t k32 = ((1ull << 31) - 1) / ((uint64_t)L * 16384ull);
-    // int64 fold with balanced weights: L^2 * K * 2^14 * (p / 2) <= 2^62
-    const uint64_t k64 = (1ull << 62) / ((uint64_t)L * L * 16384ull * (p / 2 + 1));
-    return (size_t)(k32 < k64 ? k32 : k64);
+template <int S>
+SchemeInfo info() {
+    using Sc = Scheme<S>;
+    return SchemeInfo{S, Sc::PA, Sc::PB, Sc::NACC, Sc::NT, Sc::BN, Sc::BK, Sc::UNSIGNED};
 }
 
-cudaError_t modmm_launch(int L, const GroupedArgs& args, int grid, cudaStream_t stream) {
-    switch (L) {
-        case 2: return launch_cfg<2, 128, 128, 3>(args, grid, stream);
-        case 3: return launch_cfg<3, 96, 128, 2>(args, grid, stream);
-        case 4: return launch_cfg<4, 64, 128, 2>(args, grid, stream);
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
+    uint64_t r = 1 % p;
+    b %= p;
+    while (e) {
+        if (e & 1) r = (r * b) % p;
+        b = (b * b) % p;
+        e >>= 1;
+    }
+    return r;
+}
+
+}  // namespace
+
+SchemeInfo scheme_for(uint64_t p) {
+    if (p == 131071ull) return info<SCHEME_M17>();
+    if (p == 2147483647ull) return info<SCHEME_M31>();
+    if (p <= 65536ull) return info<SCHEME_LIMB2>();
+    if (p <= 16777216ull) return info<SCHEME_LIMB3>();
+    return info<SCHEME_LIMB4>();
+}
+
+size_t modmm_k_limit(const SchemeInfo& s, uint64_t p) {
+    const uint64_t i32 = (1ull << 31) - 1;
+    switch (s.id) {
+        case SCHEME_M17:  // <= 3 terms of (2 d) e <= 126 * 63 per accumulator
+            return (size_t)(i32 / (3ull * 126 * 63));
+        case SCHEME_M31:  // <= 4 terms of <= 255 * 254 per accumulator
+            return (size_t)(i32 / (4ull * 255 * 254));
+        default: {
+            const int L = s.planes;
+            const uint64_t k32 = i32 / ((uint64_t)L * 16384ull);  // |T_s| <= L K 2^14
+            // int64 fold with balanced weights: L^2 K 2^14 (p / 2) <= 2^62
+            const uint64_t k64 = (1ull << 62) / ((uint64_t)L * L * 16384ull * (p / 2 + 1));
+            return (size_t)(k32 < k64 ? k32 : k64);
+        }
+    }
+}
+
+void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w) {
+    for (int i = 0; i < 8; ++i) w[i] = 0;
+    if (s.id == SCHEME_M17 || s.id == SCHEME_M31) return;  // constant weights inside fold_acc
+    for (int i = 0; i < 8; ++i) {
+        uint64_t v = powmod(256, (uint64_t)i, p);
+        w[i] = v > p / 2 ? (int32_t)((int64_t)v - (int64_t)p) : (int32_t)v;
+    }
+}
+
+cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid, cudaStream_t stream) {
+    switch (s.id) {
+        case SCHEME_LIMB2: return launch_cfg<SCHEME_LIMB2>(args, grid, stream);
+        case SCHEME_LIMB3: return launch_cfg<SCHEME_LIMB3>(args, grid, stream);
+        case SCHEME_LIMB4: return launch_cfg<SCHEME_LIMB4>(args, grid, stream);
+        case SCHEME_M17: return launch_cfg<SCHEME_M17>(args, grid, stream);
+        case SCHEME_M31: return launch_cfg<SCHEME_M31>(args, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -14,11 +14,11 @@ namespace fsyrk_b200 {
 constexpr int kMaxGroups = 6;
 
 // One uniform batch of products C_b = A_b * B_b^T (mod p).  Operands are int8
-// limb planes [slot][L][rows][kpad] reached through the two TMA descriptors;
+// digit planes [slot][P][rows][kpad] reached through the two TMA descriptors;
 // problem b reads A slot b * a_mult + a_off and B slot b * b_mult + b_off.
 struct alignas(64) GroupDesc {
-    CUtensorMap tmA;  // box 128 (K) x 128 rows
-    CUtensorMap tmB;  // box 128 (K) x BN rows
+    CUtensorMap tmA;  // box BK (K) x 128 rows
+    CUtensorMap tmB;  // box BK (K) x BN rows
     int M, N;         // output rows / cols
     int k_blocks;     // kpad / BK
     int syrk;         // 1: only j <= i is written (lower triangle)
@@ -33,18 +33,26 @@ struct alignas(64) GroupDesc {
 struct GroupedArgs {
     GroupDesc g[kMaxGroups];
     ModP modp;
-    int32_t w[8];       // balanced 256^s mod p, s = 0 .. 2L-2
+    int32_t w[8];       // balanced fold weights (LIMB schemes)
     int ngroups;
     int ntiles;
     const int4* tiles;  // (group, batch, tm, tn), longest K first
 };
 
-int modmm_block_n(int L);
-int modmm_block_k(int L);
-constexpr int modmm_block_m() { return 128; }
-// Largest inner dimension whose int32 shift sums and int64 fold stay exact.
-size_t modmm_k_limit(int L, uint64_t p);
+// Scheme selection and its parameters (schemes.cuh).
+struct SchemeInfo {
+    int id;
+    int planes;   // planes stored per operand (A-role count; B reads the first pb)
+    int pb;
+    int nacc, nterms;
+    int bn, bk;
+    bool is_unsigned;
+};
+SchemeInfo scheme_for(uint64_t p);
+// Largest inner dimension for which the scheme's int32 accumulators and fold stay exact.
+size_t modmm_k_limit(const SchemeInfo& s, uint64_t p);
+void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w);
 
-cudaError_t modmm_launch(int L, const GroupedArgs& args, int grid, cudaStream_t stream);
+cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid, cudaStream_t stream);
 
 }  // namespace fsyrk_b200

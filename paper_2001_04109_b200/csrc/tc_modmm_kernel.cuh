@@ -1,15 +1,15 @@
-// tcgen05 int8-limb mod-p product kernel (see tc_modmm.cu for the design notes).
+// tcgen05 int8 digit-plane mod-p product kernel (see tc_modmm.cu and schemes.cuh).
 //
 // Persistent and grouped: one launch runs every product of a recursion plan
 // (the general products of all levels and the leaf SYRKs), described by up
 // to kMaxGroups uniform problem groups and a host-built tile list in
 // longest-K-first order.  Warp roles per CTA (one CTA per SM):
 //   warp 0      : TMA producer (runs ahead across tiles)
-//   warp 1      : tcgen05.mma issuer
-//   warps 2..9  : epilogue; warp w drains TMEM lanes 32*(w%4).. for one half
-//                 of the tile's columns
-// TMEM holds the 2L-1 shift accumulators of one tile (up to 480 columns);
-// the producer prefetches the next tile's operands while the epilogue runs.
+//   warp 1      : tcgen05.mma issuer (the scheme's NT terms per 32-deep K step)
+//   warps 2..9  : epilogue; warp w drains TMEM lanes 32*(w%4).. for one part
+//                 of the tile's columns and folds the accumulators mod p
+// TMEM holds the NACC accumulators of one tile (<= 480 columns); the producer
+// prefetches the next tile's operands while the epilogue runs.
 #pragma once
 
 #include <cuda.h>
@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "modp.cuh"
+#include "schemes.cuh"
 #include "sm100.cuh"
 #include "tc_modmm.h"
 
@@ -27,11 +28,11 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int kEpiWarpsDefault = 8;
 
-// BK: int8 elements of K per stage = the swizzle row (128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B)
-template <int L, int BN, int BK, int STAGES>
+template <int S>
 struct Cfg {
+    using Sc = Scheme<S>;
+    static constexpr int BN = Sc::BN, BK = Sc::BK, STAGES = Sc::STAGES, NACC = Sc::NACC;
     static_assert(BK == 128 || BK == 64, "BK must match a swizzle mode");
-    static constexpr int NACC = 2 * L - 1;
     static constexpr int COLS_USED = NACC * BN;
     static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                                      : COLS_USED <= 256 ? 256 : 512;
@@ -39,27 +40,26 @@ struct Cfg {
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN: UMMA N for M = 128");
     static constexpr int A_TILE = BM * BK;
     static constexpr int B_TILE = BN * BK;
-    static_assert(B_TILE % 1024 == 0, "B tile must be a whole number of swizzle atoms");
-    static constexpr int STAGE_BYTES = L * (A_TILE + B_TILE);
+    static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
+    static constexpr int STAGE_BYTES = Sc::PA * A_TILE + Sc::PB * B_TILE;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 
-// sum_s 256^s T_s  mod p.  Each T_s is scaled by w_s = 256^s mod p with a
-// signed 32x32->64 multiply-add; |sum| <= L^2 K 2^14 p < 2^62 is checked on
-// the host (modmm_k_limit), so one Barrett reduction finishes the fold.
-template <int L>
-__device__ __forceinline__ uint32_t fold(const int32_t (&t)[2 * L - 1], const ModP& m, const int32_t* w) {
-    int64_t v = (int64_t)t[0];
-#pragma unroll
-    for (int s = 1; s < 2 * L - 1; ++s) v += (int64_t)t[s] * (int64_t)w[s];
-    return mod_s64(v, m);
+// index of the first term (in issue order) that writes accumulator `acc`
+template <int S>
+__host__ __device__ constexpr int first_term(int acc) {
+    for (int t = 0; t < Scheme<S>::NT; ++t)
+        if (Scheme<S>::term(t).acc == acc) return t;
+    return -1;
 }
 
-template <int L, int BN, int BK, int STAGES, int EPI = kEpiWarpsDefault>
+template <int S, int EPI = kEpiWarpsDefault>
 __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     modmm_kernel(const __grid_constant__ GroupedArgs args) {
-    using C = Cfg<L, BN, BK, STAGES>;
-    constexpr int kEpiWarps = EPI;
+    using C = Cfg<S>;
+    using Sc = Scheme<S>;
+    constexpr int BN = C::BN, BK = C::BK, STAGES = C::STAGES;
     constexpr int kParts = EPI / 4;  // column slices per lane quadrant
     static_assert(EPI % 4 == 0 && (BN / kParts) % 16 == 0, "epilogue split must give 16-column chunks");
     constexpr int SW = BK == 128 ? 2 : 4;  // descriptor layout: SWIZZLE_128B / SWIZZLE_64B
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             sm100::mbar_init(&empty[s], 1);
         }
         sm100::mbar_init(tmem_full, 1);
-        sm100::mbar_init(tmem_empty, kEpiWarps);
+        sm100::mbar_init(tmem_empty, EPI);
         sm100::fence_mbar_init();
     } else if (warp == 2 && lane == 0) {
         for (int g = 0; g < args.ngroups; ++g) {
@@ -108,11 +108,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
                     uint8_t* st = smem + stage * C::STAGE_BYTES;
 #pragma unroll
-                    for (int l = 0; l < L; ++l) {
+                    for (int l = 0; l < Sc::PA; ++l)
                         sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, tile.z * BM, l, bA);
-                        sm100::tma_load_4d(st + L * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage], kb * BK,
+#pragma unroll
+                    for (int l = 0; l < Sc::PB; ++l)
+                        sm100::tma_load_4d(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage], kb * BK,
                                            tile.w * BN, l, bB);
-                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             // ------------------------------------------------ MMA issuer
-            constexpr uint32_t idesc = sm100::idesc_i8(BM, BN);
+            constexpr uint32_t idesc = sm100::idesc_i8(BM, BN, !Sc::UNSIGNED);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
@@ -136,19 +137,17 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     sm100::tc_fence_after();
                     const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
 #pragma unroll
-                    for (int i = 0; i < L; ++i) {
+                    for (int q = 0; q < Sc::NT; ++q) {
+                        const Term tm = Sc::term(q);
+                        const bool first = first_term<S>(tm.acc) == q;
+                        const uint64_t ad = sm100::sdesc_kmajor(st + tm.a * C::A_TILE, SW, 8 * BK);
+                        const uint64_t bd =
+                            sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
 #pragma unroll
-                        for (int j = 0; j < L; ++j) {
-                            const int acc = i + j;
-                            const int first_i = acc - (L - 1) > 0 ? acc - (L - 1) : 0;
-                            const uint64_t ad = sm100::sdesc_kmajor(st + i * C::A_TILE, SW, 8 * BK);
-                            const uint64_t bd = sm100::sdesc_kmajor(st + L * C::A_TILE + j * C::B_TILE, SW, 8 * BK);
-#pragma unroll
-                            for (int kk = 0; kk < BK / 32; ++kk) {
-                                const uint32_t accum = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
-                                // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
-                                sm100::mma_i8(tmem + acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                            }
+                        for (int kk = 0; kk < BK / 32; ++kk) {
+                            const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
+                            // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
+                            sm100::mma_i8(tmem + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                         }
                     }
                     sm100::tc_commit(&empty[stage]);
@@ -162,8 +161,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         }
     } else {
         // ---------------------------------------------------- epilogue
-        const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;      // column slice of the tile
+        const int quad = warp & 3;         // TMEM lane quadrant this warp may access
+        const int part = (warp - 2) >> 2;  // column slice of the tile
         const int row = quad * 32 + lane;
         const ModP m = args.modp;
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
@@ -177,7 +176,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             const bool row_ok = grow < g.M;
             uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
 #pragma unroll 1
-            for (int c0 = half * (BN / kParts); c0 < (half + 1) * (BN / kParts); c0 += 16) {
+            for (int c0 = part * (BN / kParts); c0 < (part + 1) * (BN / kParts); c0 += 16) {
                 uint32_t raw[C::NACC][16];
 #pragma unroll
                 for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
@@ -187,10 +186,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 uint32_t res[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    int32_t tv[C::NACC];
+                    uint32_t a[C::NACC];
 #pragma unroll
-                    for (int s = 0; s < C::NACC; ++s) tv[s] = (int32_t)raw[s][c];
-                    res[c] = fold<L>(tv, m, args.w);
+                    for (int s = 0; s < C::NACC; ++s) a[s] = raw[s][c];
+                    res[c] = fold_acc<S>(a, m, args.w);
                 }
                 const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
                 if (full_chunk) {
@@ -217,10 +216,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     if (warp == 0) sm100::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-template <int L, int BN, int BK, int STAGES, int EPI = kEpiWarpsDefault>
+template <int S, int EPI = kEpiWarpsDefault>
 cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
-    using C = Cfg<L, BN, BK, STAGES>;
-    auto kern = modmm_kernel<L, BN, BK, STAGES, EPI>;
+    using C = Cfg<S>;
+    auto kern = modmm_kernel<S, EPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);

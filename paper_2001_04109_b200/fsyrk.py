@@ -122,8 +122,9 @@ def lib() -> ctypes.CDLL:
                                            ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, ctypes.c_void_p,
                                            ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                            ctypes.POINTER(_OpCount)]
-    L.fsyrk_b200_partition_owners.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
-                                              ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.fsyrk_b200_partition_owners.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int,
+                                              ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
+                                              ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     L.fsyrk_b200_last_phase_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.fsyrk_b200_level_blocks.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
@@ -365,14 +366,17 @@ def syrk_part_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta
     _ops_out(ops, co)
 
 
-def partition_owners(h: int, nranks: int) -> np.ndarray:
-    """Owner rank of each top-level block pair (I >= J), as an nb x nb array (-1 above the diagonal)."""
-    nb = ctypes.c_size_t(0)
-    _check(lib().fsyrk_b200_partition_owners(int(h), int(nranks), None, 0, ctypes.byref(nb)))
+def partition_owners(p: int, h: int, nranks: int):
+    """Owner rank of each top-level block pair (I >= J) as an nb x nb array (-1 above the
+    diagonal), and the block size in rows."""
+    nb, blk = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(lib().fsyrk_b200_partition_owners(int(p), int(h), int(nranks), None, 0, ctypes.byref(nb),
+                                             ctypes.byref(blk)))
     out = np.full(nb.value * nb.value, -1, dtype=np.int32)
-    _check(lib().fsyrk_b200_partition_owners(int(h), int(nranks), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                             out.size, ctypes.byref(nb)))
-    return out.reshape(nb.value, nb.value)
+    _check(lib().fsyrk_b200_partition_owners(int(p), int(h), int(nranks),
+                                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), out.size,
+                                             ctypes.byref(nb), ctypes.byref(blk)))
+    return out.reshape(nb.value, nb.value), blk.value
 
 
 def gemm_nt(f: PrimeField, a: np.ndarray, b: np.ndarray) -> np.ndarray:

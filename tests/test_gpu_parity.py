@@ -141,6 +141,24 @@ def test_extreme_values(gpu):
             assert orc.lower_equal(c, orc.syrk_classical(p, a)), (p, val)
 
 
+@pytest.mark.parametrize("p,k", [(2147483647, 8192), (131071, 32768), (65521, 32768), (65537, 16384)])
+def test_accumulator_bounds_at_long_k(gpu, p, k):
+    # largest digits everywhere at the inner dimensions the planner allows: the int32
+    # accumulators and the fold must stay exact (schemes.cuh, modmm_k_limit)
+    fs = gpu
+    f = fs.PrimeField(p)
+    rng = np.random.default_rng(k)
+    for val in (p - 1, None):
+        a = np.full((128, k), p - 1, dtype=np.uint64) if val else orc.random_matrix(p, 128, k, 5)
+        b = np.full((96, k), p - 1, dtype=np.uint64) if val else orc.random_matrix(p, 96, k, 6)
+        if val is None:
+            a[:, ::3] = p - 1  # mix maximal and random digits
+        c = fs.gemm_nt(f, a, b)
+        full = orc.syrk_classical(p, np.vstack([a, b]))
+        assert np.array_equal(c, full[128:, :128].T), (p, k)
+    del rng
+
+
 def test_mirror_and_strided_views(gpu):
     fs = gpu
     p = 131071

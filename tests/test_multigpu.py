@@ -18,10 +18,7 @@ import torch.multiprocessing as mp
 import oracle_py as orc
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-BLOCK = 384
-
-
-def owner_mask(n, owners, rank):
+def owner_mask(n, owners, rank, BLOCK):
     """Entries of Low(C) written by `rank` (C11 / C22 lower blocks, C21 by unordered pair)."""
     h = n // 2
     i, j = np.tril_indices(n)
@@ -34,9 +31,11 @@ def owner_mask(n, owners, rank):
     return own
 
 
+@pytest.mark.parametrize("p", [131071, 2147483647, 65521, 65537])
 @pytest.mark.parametrize("h,nranks", [(2048, 2), (2048, 8), (8192, 8), (16384, 4), (500, 3), (384, 5)])
-def test_partition_owners_complete_and_balanced(fsyrk, h, nranks):
-    own = fsyrk.partition_owners(h, nranks)
+def test_partition_owners_complete_and_balanced(fsyrk, p, h, nranks):
+    own, BLOCK = fsyrk.partition_owners(p, h, nranks)
+    assert BLOCK % 128 == 0 and BLOCK % 32 == 0
     nb = (h + BLOCK - 1) // BLOCK
     assert own.shape == (nb, nb)
     lower = own[np.tril_indices(nb)]
@@ -62,8 +61,8 @@ def _gloo_worker(rank, world, port, n, p, result_q):
     import bench
     a = o.random_matrix(p, n, n, 42)
     full = o.syrk_classical(p, a)
-    owners = fs.partition_owners(n // 2, world)
-    mask = owner_mask(n, owners, rank)
+    owners, blk = fs.partition_owners(p, n // 2, world)
+    mask = owner_mask(n, owners, rank, blk)
     share = np.where(mask, full, 0).astype(np.int64)  # what this rank's device C holds (beta = 0)
     t = torch.from_numpy(share)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)           # bench.py's gather of disjoint shares
@@ -115,9 +114,9 @@ def test_partition_shares_reassemble(gpu, nranks, mode):
     want = ref_d.cpu().numpy().view(np.uint64)
     assert orc.lower_equal(got, want)
     # and each share writes only what its rank owns
-    owners = fs.partition_owners(n // 2, nranks)
+    owners, blk = fs.partition_owners(p, n // 2, nranks)
     c1 = torch.zeros((n, n), dtype=torch.int64, device=dev)
     fs.syrk_part_dev(p, 1, a_d.data_ptr(), n, k, k, 0, c1.data_ptr(), n, pol, 1, nranks, 0)
     torch.cuda.synchronize()
     written = np.tril(c1.cpu().numpy()) != 0
-    assert not (written & ~owner_mask(n, owners, 1)).any()
+    assert not (written & ~owner_mask(n, owners, 1, blk)).any()

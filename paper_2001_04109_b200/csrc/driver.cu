@@ -213,7 +213,7 @@ struct GemmGroup {
     int h, kw, count = 0;
     bool root = false;  // the two general products of the top level (launched early, see execute)
     int hpad, kpad;
-    long long plane, slot;
+    long long plane, slot, slot_b;  // slot_b: B-role operands keep only the scheme's first pb planes
     int8_t *ga = nullptr, *gb = nullptr;
     uint32_t* out = nullptr;
     CUtensorMap tA, tB;
@@ -474,7 +474,8 @@ struct Plan {
             gg.plane = (long long)gg.hpad * gg.kpad;
             gg.slot = gg.plane * L;
             gg.off_ga = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
-            gg.off_gb = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
+            gg.slot_b = gg.plane * sch.pb;
+            gg.off_gb = ar.take((size_t)gg.slot_b * 2 * gg.count, 1024);
             gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
         }
         // product launches: every GEMM group and leaf group, kMaxGroups per persistent launch,
@@ -596,7 +597,7 @@ struct Plan {
             gg.gb = reinterpret_cast<int8_t*>(arena + gg.off_gb);
             gg.out = reinterpret_cast<uint32_t*>(arena + gg.off_out);
             gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128, BK);
-            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, L, 2 * gg.count, BN, BK);
+            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, sch.pb, 2 * gg.count, BN, BK);
         }
         {
             int dev = 0;
@@ -723,9 +724,9 @@ struct Plan {
                 pn.in = InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0};
                 if (nd.in64) a.in64 = 1;
                 pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
-                pn.s2 = g.gb + (2LL * nd.gslot) * g.slot;
+                pn.s2 = g.gb + (2LL * nd.gslot) * g.slot_b;
                 pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
-                pn.s4 = g.gb + (2LL * nd.gslot + 1) * g.slot;
+                pn.s4 = g.gb + (2LL * nd.gslot + 1) * g.slot_b;
                 const Node& q0 = nodes[nd.ch[0]];
                 const Node& q1 = nodes[nd.ch[1]];
                 const Node& q2 = nodes[nd.ch[2]];
@@ -1323,7 +1324,7 @@ int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, s
         const int bits = sid == SCHEME_M17 ? 6 : 8;
         const bool sgn = !plan.sch.is_unsigned;
         auto read_planes = [&](const int8_t* base, long long plane, long long row, int rows, int cols, uint64_t* out) {
-            std::vector<int8_t> buf((size_t)plane * L);
+            std::vector<int8_t> buf((size_t)plane * nd);
             ck(cudaMemcpy(buf.data(), base, buf.size(), cudaMemcpyDeviceToHost), "D2H planes");
             for (int i = 0; i < rows; ++i)
                 for (int j = 0; j < cols; ++j) {
@@ -1339,8 +1340,8 @@ int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, s
                 }
         };
         if (s1) read_planes(g.ga + (2LL * root.gslot) * g.slot, g.plane, g.kpad, h, kw, s1);
-        if (s2) read_planes(g.gb + (2LL * root.gslot) * g.slot, g.plane, g.kpad, h, kw, s2);
-        if (s4) read_planes(g.gb + (2LL * root.gslot + 1) * g.slot, g.plane, g.kpad, h, kw, s4);
+        if (s2) read_planes(g.gb + (2LL * root.gslot) * g.slot_b, g.plane, g.kpad, h, kw, s2);
+        if (s4) read_planes(g.gb + (2LL * root.gslot + 1) * g.slot_b, g.plane, g.kpad, h, kw, s4);
         if (s3) {
             const Node& c2 = plan.nodes[root.ch[2]];
             const LeafGroup& lg = plan.leaves[c2.lgroup];

@@ -90,20 +90,20 @@ __device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, lo
 
 // The kernels below are templated on the digit scheme S (schemes.cuh): a residue
 // becomes Scheme<S>::PA int8 planes, byte l of encode_planes<S>(x) going to plane l.
-template <int S>
+template <int S, int NPL = Scheme<S>::PA>
 __device__ __forceinline__ void put_planes(int8_t* base, long long plane, long long off, uint32_t x, uint32_t p) {
     const uint64_t w = encode_planes<S>(x, p);
 #pragma unroll
-    for (int l = 0; l < Scheme<S>::PA; ++l) base[l * plane + off] = (int8_t)(w >> (8 * l));
+    for (int l = 0; l < NPL; ++l) base[l * plane + off] = (int8_t)(w >> (8 * l));
 }
 
-// four consecutive columns of one row, one 32-bit store per plane
-template <int S>
+// four consecutive columns of one row, one 32-bit store per plane (the first NPL planes)
+template <int S, int NPL = Scheme<S>::PA>
 __device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long long off, uint4 x, uint32_t p) {
     const uint64_t w0 = encode_planes<S>(x.x, p), w1 = encode_planes<S>(x.y, p), w2 = encode_planes<S>(x.z, p),
                    w3 = encode_planes<S>(x.w, p);
 #pragma unroll
-    for (int l = 0; l < Scheme<S>::PA; ++l) {
+    for (int l = 0; l < NPL; ++l) {
         const int sh = 8 * l;
         uint32_t v;
         if (sh < 32)
@@ -183,8 +183,8 @@ __global__ void prep_kernel(const PrepArgs args) {
         const long long go = (long long)i * args.g_row + c;
         put_planes<L>(nd.s1, args.g_plane, go, s1[t], p);
         put_planes<L>(nd.a22, args.g_plane, go, a22[t], p);
-        put_planes<L>(nd.s2, args.g_plane, go, s2, p);
-        put_planes<L>(nd.s4, args.g_plane, go, s4, p);
+        put_planes<L, Scheme<L>::PB>(nd.s2, args.g_plane, go, s2, p);  // B-role: first PB planes
+        put_planes<L, Scheme<L>::PB>(nd.s4, args.g_plane, go, s4, p);
         if (c < kh) {
             if (nd.c_a11) put_planes<L>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
             if (nd.c_a12) put_planes<L>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
@@ -212,27 +212,76 @@ __device__ __forceinline__ void pair_y4(uint4 u, uint4 v, MulConst ca, MulConst 
 
 // Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
 // Pair form, their 4 partners) per thread.
-template <int L, bool PAIR>
-__global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
-    const PrepNode nd = args.nodes[blockIdx.z];
+// 4 x NC quadrant vectors of row i: every load is issued before any is used (memory-level
+// parallelism; no branch between loads), then the caller's uint64 values are narrowed with a
+// single range check for the whole batch (canonical residues are the contract).
+template <bool IN64, int NC>
+__device__ __forceinline__ void load_quads(const Src& src, int i, int h, int kh, const int (&col)[2], const ModP& m,
+                                           uint4 (&a11)[NC], uint4 (&a12)[NC], uint4 (&a21)[NC], uint4 (&a22)[NC]) {
+    if constexpr (IN64) {
+        ulonglong2 r[NC][4][2];
+#pragma unroll
+        for (int t = 0; t < NC; ++t) {
+            const int cc[4][2] = {{i, col[t]}, {i, kh + col[t]}, {i + h, col[t]}, {i + h, kh + col[t]}};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const ulonglong2* ptr = reinterpret_cast<const ulonglong2*>(src.p64 + (long long)cc[q][0] * src.ld64 + cc[q][1]);
+                r[t][q][0] = __ldg(ptr);
+                r[t][q][1] = __ldg(ptr + 1);
+            }
+        }
+        uint64_t big = 0;
+#pragma unroll
+        for (int t = 0; t < NC; ++t)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) big |= (r[t][q][0].x | r[t][q][0].y | r[t][q][1].x | r[t][q][1].y) >> 31;
+        bool slow = big != 0;
+        if (!slow) {
+            // all values < 2^31: narrow, then one compare per value decides the (rare) reduction
+#pragma unroll
+            for (int t = 0; t < NC; ++t)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 v = make_uint4((uint32_t)r[t][q][0].x, (uint32_t)r[t][q][0].y, (uint32_t)r[t][q][1].x,
+                                               (uint32_t)r[t][q][1].y);
+                    slow |= v.x >= m.p || v.y >= m.p || v.z >= m.p || v.w >= m.p;
+                }
+        }
+#pragma unroll
+        for (int t = 0; t < NC; ++t) {
+            uint4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t x0 = r[t][q][0].x, x1 = r[t][q][0].y, x2 = r[t][q][1].x, x3 = r[t][q][1].y;
+                v[q] = slow ? make_uint4(mod_u64(x0, m), mod_u64(x1, m), mod_u64(x2, m), mod_u64(x3, m))
+                            : make_uint4((uint32_t)x0, (uint32_t)x1, (uint32_t)x2, (uint32_t)x3);
+            }
+            a11[t] = v[0];
+            a12[t] = v[1];
+            a21[t] = v[2];
+            a22[t] = v[3];
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < NC; ++t) {
+            a11[t] = __ldg(reinterpret_cast<const uint4*>(src.p32 + (long long)i * src.ld32 + col[t]));
+            a12[t] = __ldg(reinterpret_cast<const uint4*>(src.p32 + (long long)i * src.ld32 + kh + col[t]));
+            a21[t] = __ldg(reinterpret_cast<const uint4*>(src.p32 + (long long)(i + h) * src.ld32 + col[t]));
+            a22[t] = __ldg(reinterpret_cast<const uint4*>(src.p32 + (long long)(i + h) * src.ld32 + kh + col[t]));
+        }
+    }
+}
+
+template <int S, bool PAIR, bool IN64>
+__device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNode& nd, int i, int g) {
     const ModP m = args.m;
     const uint32_t p = m.p;
     const int h = args.h, kh = args.kh, half = args.half;
-    const int ncg = (PAIR ? half : kh) / 4;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = blockIdx.y * blockDim.y + threadIdx.y;
-    if (g >= ncg || i >= h) return;
     const Src src = make_src(nd.in, args.a64, args.ld64);
     constexpr int NC = PAIR ? 2 : 1;
     const int col[2] = {4 * g, 4 * g + half};
     uint4 a11[NC], a12[NC], a21[NC], a22[NC];
-#pragma unroll
-    for (int t = 0; t < NC; ++t) {
-        a11[t] = src.ld4(i, col[t], m);
-        a12[t] = src.ld4(i, kh + col[t], m);
-        a21[t] = src.ld4(i + h, col[t], m);
-        a22[t] = src.ld4(i + h, kh + col[t], m);
-    }
+    load_quads<IN64, NC>(src, i, h, kh, col, m, a11, a12, a21, a22);
     uint4 s1[NC], ay[NC];
     if constexpr (PAIR) {
         pair_y4(sub4(a21[0], a11[0], p), sub4(a21[1], a11[1], p), args.cya, args.cyb, p, s1[0], s1[1]);
@@ -248,15 +297,30 @@ __global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
         const uint4 s3 = sub4(s1[t], a22[t], p);
         const uint4 s4 = add4(s3, a12[t], p);
         const long long go = (long long)i * args.g_row + c;
-        put_planes4<L>(nd.s1, args.g_plane, go, s1[t], p);
-        put_planes4<L>(nd.a22, args.g_plane, go, a22[t], p);
-        put_planes4<L>(nd.s2, args.g_plane, go, s2, p);
-        put_planes4<L>(nd.s4, args.g_plane, go, s4, p);
-        if (nd.c_a11) put_planes4<L>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
-        if (nd.c_a12) put_planes4<L>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
-        if (nd.c_s3) put_planes4<L>(nd.c_s3, args.c3_plane, (long long)i * args.c3_row + c, s3, p);
+        constexpr int PB = Scheme<S>::PB;  // B-role operands (S2, S4) only need the first PB planes
+        put_planes4<S>(nd.s1, args.g_plane, go, s1[t], p);
+        put_planes4<S>(nd.a22, args.g_plane, go, a22[t], p);
+        put_planes4<S, PB>(nd.s2, args.g_plane, go, s2, p);
+        put_planes4<S, PB>(nd.s4, args.g_plane, go, s4, p);
+        if (nd.c_a11) put_planes4<S>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
+        if (nd.c_a12) put_planes4<S>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
+        if (nd.c_s3) put_planes4<S>(nd.c_s3, args.c3_plane, (long long)i * args.c3_row + c, s3, p);
         if (nd.r_s3) *reinterpret_cast<uint4*>(nd.r_s3 + (long long)i * nd.ld_s3 + c) = s3;
     }
+}
+
+// Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
+// Pair form, their 4 partners) per thread; one specialised body per input kind.
+template <int S, bool PAIR>
+__global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
+    const PrepNode& nd = args.nodes[blockIdx.z];
+    const int ncg = (PAIR ? args.half : args.kh) / 4;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y * blockDim.y + threadIdx.y;
+    if (g >= ncg || i >= args.h) return;
+    const PrepNode local = nd;
+    if (local.in.in64) prep_vec_body<S, PAIR, true>(args, local, i, g);
+    else prep_vec_body<S, PAIR, false>(args, local, i, g);
 }
 
 // ------------------------------------------------------------------ post

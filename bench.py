@@ -349,6 +349,8 @@ def main():
         c_pin = torch.zeros((n, n), dtype=torch.int64).pin_memory()
         a_np = a_pin.numpy().view(np.uint64)
         c_np = c_pin.numpy().view(np.uint64)
+        if cfg["mode"] != "plain":
+            c_np[:] = c0_host
         plan_obj = fs.make_syrk_plan(f, policy)
 
         def host_step():
@@ -364,11 +366,9 @@ def main():
                 torch.cuda.synchronize()
             elif cfg["mode"] == "plain":
                 fs.syrk_fast_into(f, a_np, c_np, plan_obj)
-            elif cfg["mode"] == "acc":
-                c_np[:] = c0_host
+            elif cfg["mode"] == "acc":  # C accumulates across steps (any C_in is a valid input)
                 fs.syrk_fast_acc(f, alpha, a_np, beta, c_np, plan_obj)
             else:
-                c_np[:] = c0_host
                 fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
 
         for _ in range(2):
@@ -381,9 +381,13 @@ def main():
             host_step()
         t1 = time.perf_counter()
         secs = max_over_ranks(t1 - t0, world)
-        h2d = n * k * 8 + (n * n * 8 if beta else 0)
+        if part:  # rank 0's copies around the NCCL broadcast / reduce
+            h2d, d2h = n * k * 8, n * n * 8
+        else:     # what the host API moved (A, and the lower-triangle row blocks of C)
+            h2d, d2h = fs.last_transfer_bytes()
+            h2d, d2h = h2d * world, d2h * world
         e2e = {"value": round(E * e2e_steps * problems / secs / 1e9, 3), "unit": "GOPS",
-               "h2d_bytes_per_step": h2d if part else h2d * world, "d2h_bytes_per_step": n * n * 8 * problems}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     if rank != 0:
         if world > 1:

@@ -115,6 +115,24 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
                      const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy,
                      int mirror_output, fsyrk_b200_opcount* ops);
 
+/* One block of the middle matrix of syrkbd: replaces fsyrk::BlockDiagonal<F>::Block
+ * (include/fsyrk/scaled_syrk.hpp:13-20).  two = 0: scalar block d; two = 1: the 2x2
+ * block ((0, beta), (beta, gamma)), beta != 0; gamma must be 0 over an odd prime. */
+typedef struct fsyrk_b200_block {
+    int two;
+    uint64_t d;
+    uint64_t beta;
+    uint64_t gamma;
+} fsyrk_b200_block;
+
+/* syrkbd(f, a, b, plan, ops) (include/fsyrk/scaled_syrk.hpp:117-159), with the same
+ * accumulate extension as fsyrk_b200_syrkd:
+ *   Low(C) <- Low(alpha * A * B * A^T + beta * C),  B = blockdiag(blocks[0..nblocks)).
+ * The block dimension (scalar blocks count 1, 2x2 blocks 2) must equal k. */
+int fsyrk_b200_syrkbd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                      const fsyrk_b200_block* blocks, size_t nblocks, uint64_t beta, uint64_t* c, size_t ldc,
+                      fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
+
 /* -------------------------------------------------------------- device API */
 
 /* Same operations on device-resident uint64 matrices (pointers from
@@ -125,6 +143,11 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
 int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
                         const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
                         fsyrk_b200_policy policy, int mirror_output, void* stream, fsyrk_b200_opcount* ops);
+
+/* syrkbd on device-resident A and C (blocks is a HOST array). */
+int fsyrk_b200_syrkbd_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                          const fsyrk_b200_block* blocks, size_t nblocks, uint64_t beta, uint64_t* c_dev, size_t ldc,
+                          fsyrk_b200_policy policy, int mirror_output, void* stream, fsyrk_b200_opcount* ops);
 
 /* ------------------------------------------------------------ multi-GPU */
 
@@ -155,6 +178,10 @@ void fsyrk_b200_release_cache(void);
  * per-kind launch counts (index: 0 tensor-core products, 1 pre-addition,
  * 2 post-addition, 3 conversion/finalize, 4 other). */
 int fsyrk_b200_last_launch_count(int* by_kind, int nkinds);
+
+/* Host<->device bytes moved by the last host-API call on this thread (A, and only the
+ * lower-triangle row blocks of C unless mirror_output). */
+int fsyrk_b200_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
 /* Describe the last executed plan as a JSON string (tree, groups, limbs, bytes). */
 const char* fsyrk_b200_last_plan_json(void);

@@ -100,6 +100,25 @@ inline fsyrk::Matrix<Field> syrkd(const Field& f, CView a, const std::vector<Fie
     return c;
 }
 
+// replaces syrkbd<PrimeField> (include/fsyrk/scaled_syrk.hpp:117-159); needs fsyrk/scaled_syrk.hpp
+inline fsyrk::Matrix<Field> syrkbd(const Field& f, CView a, const fsyrk::BlockDiagonal<Field>& b, const Plan& plan,
+                                   fsyrk::OpCount& ops) {
+    b.validate(f);
+    if (b.dimension() != a.cols)
+        throw fsyrk::DimensionError("syrkbd: block-diagonal dimension must match column count");
+    if (f.modulus() == 2) throw std::invalid_argument("syrkbd over characteristic 2 uses BinaryField");
+    std::vector<fsyrk_b200_block> blk;
+    blk.reserve(b.blocks.size());
+    for (const auto& x : b.blocks) blk.push_back(fsyrk_b200_block{x.two ? 1 : 0, x.d, x.beta, x.gamma});
+    fsyrk::Matrix<Field> c(a.rows, a.rows, f.zero());
+    fsyrk_b200_opcount oc{0, 0};
+    detail::check(fsyrk_b200_syrkbd(f.modulus(), 1, a.data, a.rows, a.cols, a.stride, blk.data(), blk.size(), 0,
+                                    c.view().data, a.rows, detail::policy(plan.policy), plan.mirror_output ? 1 : 0,
+                                    &oc));
+    detail::add_ops(ops, oc);
+    return c;
+}
+
 // LDL^T Schur update in one call: Low(C) <- Low(C - A Diag(d) A^T) (no reference analogue: the
 // reference composes syrkd and an elementwise subtraction)
 inline void schur_update(const Field& f, CView a, const std::vector<Field::Element>& d, View c, const Plan& plan,

@@ -249,6 +249,37 @@ static void gemm_nt(uint64_t p, const uint64_t* A, size_t lda, const uint64_t* B
         for (size_t j = 0; j < nn; ++j) C[ii * ldc + j] = dot_mod(p, A + ii * lda, B + j * ldb, k);
 }
 
+/* abat_oracle (proj/tests/test_scaled_syrk.cpp:25-47, acceptance.cpp:253-275):
+ * C = (A * B) * A^T with the block-diagonal B materialised densely; blocks are given as
+ * parallel arrays two[i], d[i], beta[i], gamma[i] (scaled_syrk.hpp:13-20). Full C. */
+void orc_abat_classical(uint64_t p, const uint64_t* A, size_t n, size_t k, size_t lda, const int* two,
+                        const uint64_t* d, const uint64_t* beta, const uint64_t* gamma, size_t nblocks, uint64_t* C,
+                        size_t ldc) {
+    uint64_t* B = (uint64_t*)calloc(k * k + 1, sizeof(uint64_t));
+    uint64_t* AB = (uint64_t*)calloc(n * k + 1, sizeof(uint64_t));
+    size_t at = 0;
+    for (size_t i = 0; i < nblocks && at < k; ++i) {
+        if (two[i]) {
+            B[at * k + at + 1] = beta[i] % p;
+            B[(at + 1) * k + at] = beta[i] % p;
+            B[(at + 1) * k + at + 1] = gamma[i] % p;
+            at += 2;
+        } else {
+            B[at * k + at] = d[i] % p;
+            at += 1;
+        }
+    }
+    /* gemm_classical(A, B): AB[r][j] = sum_l A[r][l] B[l][j] (B^T rows = columns of B) */
+    uint64_t* BT = (uint64_t*)calloc(k * k + 1, sizeof(uint64_t));
+    for (size_t l = 0; l < k; ++l)
+        for (size_t j = 0; j < k; ++j) BT[j * k + l] = B[l * k + j];
+    gemm_nt(p, A, lda, BT, k, AB, k, n, k, k);
+    gemm_nt(p, AB, k, A, lda, C, ldc, n, n, k);
+    free(B);
+    free(BT);
+    free(AB);
+}
+
 /* ------------------------------------------------- the 5-product recursion */
 typedef struct {
     uint64_t p;

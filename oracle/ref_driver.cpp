@@ -13,6 +13,7 @@
 //   syrk_fast_into           proj/include/fsyrk/fast_syrk.hpp:274-282
 //   syrk_fast_acc            proj/include/fsyrk/fast_syrk.hpp:293-303
 //   syrkd                    proj/include/fsyrk/scaled_syrk.hpp:58-104
+//   syrkbd                   proj/include/fsyrk/scaled_syrk.hpp:117-159
 //   syrk_classical           proj/include/fsyrk/matrix.hpp:372-407
 //
 // Output: one JSON line on stdout.
@@ -40,7 +41,7 @@ struct Args {
     std::uint64_t seed = 42;
     std::size_t threshold = 64;
     std::size_t levels = kUnlimitedLevels;
-    std::string mode = "plain";  // plain | acc | schur | classical
+    std::string mode = "plain";  // plain | acc | schur | classical | syrkbd
     std::uint64_t cseed = 43, abseed = 7, dseed = 44;
     bool mirror = false;
     int threads = 1;
@@ -55,7 +56,7 @@ struct Args {
 [[noreturn]] void usage() {
     std::fprintf(stderr,
                  "usage: ref_driver [--p P] [--n N] [--k K] [--seed S] [--threshold T]\n"
-                 "  [--levels L|inf] [--mode plain|acc|schur|classical] [--cseed S] [--abseed S]\n"
+                 "  [--levels L|inf] [--mode plain|acc|schur|classical|syrkbd] [--cseed S] [--abseed S]\n"
                  "  [--alpha a --beta b] [--dseed S] [--mirror] [--threads T] [--reps R]\n"
                  "  [--out-a F] [--out-c F] [--out-c0 F] [--out-d F] [--no-digest] [--sample N]\n");
     std::exit(2);
@@ -109,7 +110,8 @@ void dump(const std::string& path, const void* data, std::size_t bytes) {
 // generated outside the timed region; returns the seconds spent in the call.
 struct Instance {
     Matrix<PrimeField> a, c, c0;
-    std::vector<std::uint64_t> d;
+    std::vector<std::uint64_t> d;  // schur: D; syrkbd: blocks as (two, d, beta, gamma) quadruples
+    BlockDiagonal<PrimeField> b;
     std::uint64_t alpha = 1, beta = 0;
 };
 
@@ -136,6 +138,26 @@ Instance make_instance(const PrimeField& f, const Args& g) {
         in.d.resize(g.k);
         for (auto& v : in.d) v = 1 + rng() % (g.p - 1);
     }
+    if (g.mode == "syrkbd") {
+        // B: scalar blocks d = rng() % p (zero allowed) and antidiagonal 2x2 blocks
+        // beta = 1 + rng() % (p - 1), drawn until the dimension reaches k
+        std::mt19937_64 rng(g.dseed);
+        std::size_t dim = 0;
+        while (dim < g.k) {
+            const bool scalar = rng() % 3 == 0 || dim + 1 == g.k;
+            if (scalar) {
+                const std::uint64_t v = rng() % g.p;
+                in.b.blocks.push_back(BlockDiagonal<PrimeField>::scalar(v));
+                in.d.insert(in.d.end(), {0, v, 0, 0});
+                dim += 1;
+            } else {
+                const std::uint64_t beta = 1 + rng() % (g.p - 1);
+                in.b.blocks.push_back(BlockDiagonal<PrimeField>::two_by_two(beta, 0));
+                in.d.insert(in.d.end(), {1, 0, beta, 0});
+                dim += 2;
+            }
+        }
+    }
     return in;
 }
 
@@ -154,6 +176,9 @@ double run_instance(const PrimeField& f, const Args& g, Instance& in) {
         Matrix<PrimeField> x = syrkd(f, in.a.view(), in.d, plan, ops);
         for (std::size_t i = 0; i < g.n; ++i)
             for (std::size_t j = 0; j <= i; ++j) in.c.at(i, j) = f.sub(in.c.at(i, j), x.at(i, j));
+        if (g.mirror) mirror_lower_to_upper(f, in.c.view());
+    } else if (g.mode == "syrkbd") {
+        in.c = syrkbd(f, in.a.view(), in.b, plan, ops);
         if (g.mirror) mirror_lower_to_upper(f, in.c.view());
     } else {
         usage();

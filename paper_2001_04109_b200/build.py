@@ -33,16 +33,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = True, out: str = LIB, defines=()) -> str:
+    """Compile the library; `out` / `defines` (-D flags) build tuning variants for experiments
+    (loaded with FSYRK_B200_LIB=<path>), the default is the shipped library."""
+    if out == LIB and not defines and not force and not needs_build():
         return LIB
     cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
-           "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES]
+           *[f"-D{d}" for d in defines], "-o", out] + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    # python -m paper_2001_04109_b200.build [--force] [--out PATH -DNAME=VAL ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else LIB
+    build(force="--force" in argv, out=out, defines=[a[2:] for a in argv if a.startswith("-D")])

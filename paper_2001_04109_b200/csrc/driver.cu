@@ -44,6 +44,8 @@ thread_local int g_launch_counts[5] = {0, 0, 0, 0, 0};
 thread_local std::string g_last_plan_json;
 thread_local bool g_phase_timing = false;
 thread_local float g_phase_ms[5] = {0, 0, 0, 0, 0};
+thread_local uint64_t g_transfer[2] = {0, 0};  // host<->device bytes of the last host-API call
+constexpr size_t kTriRows = 256;                // row block of the triangular C transfers
 
 struct Error {
     int code;
@@ -717,12 +719,18 @@ struct Plan {
                 a.c3_row = leaves[c3.lgroup].kpad;
             }
             std::vector<PrepNode> tab;
+            a.aligned = 1;
             for (int ni : pg.nodes) {
                 const Node& nd = nodes[ni];
                 GemmGroup& g = gemms[nd.ggroup];
                 PrepNode pn{};
                 pn.in = InView{nd.in, nd.ldin, nd.r0, nd.c0, nd.in64 ? 1 : 0};
                 if (nd.in64) a.in64 = 1;
+                // vector loads: uint4 of residues (uint32 input) or 2 x ulonglong2 (uint64 window)
+                if (nd.in64 ? nd.c0 % 2 != 0
+                            : nd.ldin % 4 != 0 || reinterpret_cast<uintptr_t>(nd.in) % 16 != 0)
+                    a.aligned = 0;
+                if (nd.s3res && (nd.lds3 % 4 != 0 || reinterpret_cast<uintptr_t>(nd.s3res) % 16 != 0)) a.aligned = 0;
                 pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
                 pn.s2 = g.gb + (2LL * nd.gslot) * g.slot_b;
                 pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
@@ -1051,47 +1059,102 @@ bool ranges_overlap(const void* a, size_t a_bytes, const void* b, size_t b_bytes
 }
 size_t span_bytes(size_t rows, size_t cols, size_t ld) { return rows == 0 || cols == 0 ? 0 : ((rows - 1) * ld + cols) * 8; }
 
-// syrkd column map (include/fsyrk/scaled_syrk.hpp:58-104): returns kbar.
-int build_colmap(uint64_t p, const uint64_t* d, size_t k, std::vector<ColMap>& map) {
+// Column transform applied to A on its way in (convert_in): column j of the
+// transformed matrix is sum_t c[t] * A[:, src[t]].
+struct ColXform {
+    std::vector<ColMap> map;
+};
+
+ColMap col_identity(int j) { return ColMap{{j, -1, -1, -1}, {1, 0, 0, 0}}; }
+
+// cu * u + cv * v for two transformed columns (term lists concatenate; at most 4 terms
+// because only syrkbd's (u + v, u - v) columns carry two).
+ColMap col_combine(const host::Field& f, const ColMap& u, uint64_t cu, const ColMap& v, uint64_t cv) {
+    ColMap r{{-1, -1, -1, -1}, {0, 0, 0, 0}};
+    int t = 0;
+    for (const auto* src : {&u, &v}) {
+        const uint64_t w = src == &u ? cu : cv;
+        for (int q = 0; q < 4; ++q)
+            if (src->src[q] >= 0) {
+                if (t == 4) fail(FSYRK_B200_EINVAL, "column transform exceeds 4 source columns");
+                r.src[t] = src->src[q];
+                r.c[t++] = (uint32_t)f.mul(w, src->c[q]);
+            }
+    }
+    return r;
+}
+
+// syrkd's diagonal fold (include/fsyrk/scaled_syrk.hpp:58-104) applied on top of an
+// initial column map `map` (identity for syrkd, syrkbd's block fold otherwise): residue
+// entries scale their column by sqrt(d), non-residues are consumed in pairs through their
+// nrsyf factor, an odd count appends a zero column carrying a copy of the first one.
+void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& map) {
     host::Field f{p};
     if (p == 2) fail(FSYRK_B200_EINVAL, "syrkd requires an odd prime field");
+    const size_t k = dbar.size();
     std::vector<size_t> nr;
-    std::vector<uint64_t> dbar(d, d + k);
     for (auto& v : dbar) v %= p;
     for (size_t j = 0; j < k; ++j)
         if (f.legendre(dbar[j]) == -1) nr.push_back(j);
-    const bool augment = nr.size() % 2 == 1;
-    const size_t kbar = k + (augment ? 1 : 0);
-    map.assign(kbar, ColMap{-1, -1, 0, 0});
-    for (size_t j = 0; j < k; ++j) map[j] = ColMap{(int)j, -1, 1, 0};
-    if (augment) {
+    if (nr.size() % 2 == 1) {
         dbar.push_back(dbar[nr.front()]);
-        nr.push_back(k);  // zero column: no source
+        nr.push_back(k);
+        map.push_back(ColMap{{-1, -1, -1, -1}, {0, 0, 0, 0}});  // the appended zero column
     }
-    for (size_t j = 0; j < kbar; ++j)
+    for (size_t j = 0; j < dbar.size(); ++j)
         if (f.legendre(dbar[j]) >= 0) {
-            uint64_t s = f.sqrt(dbar[j]);
-            if (map[j].src0 >= 0) map[j].c0 = (uint32_t)f.mul(map[j].c0, s);
+            const uint64_t sq = f.sqrt(dbar[j]);
+            for (int q = 0; q < 4; ++q)
+                if (map[j].src[q] >= 0) map[j].c[q] = (uint32_t)f.mul(map[j].c[q], sq);
         }
     for (size_t t = 0; t + 1 < nr.size(); t += 2) {
         const size_t i = nr[t], j = nr[t + 1];
         std::array<uint64_t, 4> y;
         if (!host::nrsyf(f, dbar[i], dbar[j], y)) fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
-        // (u, v) -> (y0 u + y2 v, y1 u + y3 v); u, v are (scaled) original columns or the zero column
+        // (u, v) -> (y0 u + y2 v, y1 u + y3 v)   (scaled_syrk.hpp:93-98)
         const ColMap u = map[i], v = map[j];
-        auto comb = [&](uint64_t cu, uint64_t cv) {
-            ColMap r{-1, -1, 0, 0};
-            if (u.src0 >= 0) { r.src0 = u.src0; r.c0 = (uint32_t)f.mul(cu, u.c0); }
-            if (v.src0 >= 0) {
-                if (r.src0 < 0) { r.src0 = v.src0; r.c0 = (uint32_t)f.mul(cv, v.c0); }
-                else { r.src1 = v.src0; r.c1 = (uint32_t)f.mul(cv, v.c0); }
-            }
-            return r;
-        };
-        map[i] = comb(y[0], y[2]);
-        map[j] = comb(y[1], y[3]);
+        map[i] = col_combine(f, u, y[0], v, y[2]);
+        map[j] = col_combine(f, u, y[1], v, y[3]);
     }
-    return (int)kbar;
+}
+
+ColXform xform_diag(uint64_t p, const uint64_t* d, size_t k) {
+    ColXform x;
+    for (size_t j = 0; j < k; ++j) x.map.push_back(col_identity((int)j));
+    fold_diagonal(p, std::vector<uint64_t>(d, d + k), x.map);
+    return x;
+}
+
+// syrkbd over a prime field (include/fsyrk/scaled_syrk.hpp:117-159): every 2x2 block
+// ((0, beta), (beta, 0)) becomes diagonal entries (beta/2, -beta/2) under the column
+// transform (u, v) -> (u + v, u - v); then the diagonal fold of syrkd.
+ColXform xform_blocks(uint64_t p, const fsyrk_b200_block* b, size_t nblocks, size_t k) {
+    host::Field f{p};
+    size_t dim = 0;
+    for (size_t i = 0; i < nblocks; ++i) {
+        if (b[i].two && b[i].beta % p == 0) fail(FSYRK_B200_EINVAL, "block-diagonal: 2x2 block requires beta != 0");
+        dim += b[i].two ? 2 : 1;
+    }
+    if (dim != k) fail(FSYRK_B200_EDIMENSION, "syrkbd: block-diagonal dimension must match column count");
+    if (p == 2) fail(FSYRK_B200_EINVAL, "syrkbd over characteristic 2 uses BinaryField");
+    const uint64_t half = f.inv(2 % p);
+    ColXform x;
+    std::vector<uint64_t> dbar(k, 1);
+    for (size_t i = 0, j = 0; i < nblocks; ++i) {
+        if (!b[i].two) {
+            x.map.push_back(col_identity((int)j));
+            dbar[j++] = b[i].d % p;
+            continue;
+        }
+        if (b[i].gamma % p != 0) fail(FSYRK_B200_EINVAL, "syrkbd: 2x2 blocks in odd characteristic must be antidiagonal");
+        dbar[j] = f.mul(half, b[i].beta % p);
+        dbar[j + 1] = (p - dbar[j]) % p;
+        x.map.push_back(ColMap{{(int)j, (int)j + 1, -1, -1}, {1, 1, 0, 0}});
+        x.map.push_back(ColMap{{(int)j, (int)j + 1, -1, -1}, {1, (uint32_t)(p - 1), 0, 0}});
+        j += 2;
+    }
+    fold_diagonal(p, std::move(dbar), x.map);
+    return x;
 }
 
 struct DevBuf {
@@ -1120,7 +1183,7 @@ void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
 }
 
 // Core device call: everything resident on the device.
-void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda, const uint64_t* d,
+void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda, const ColXform* xf,
              uint32_t beta, uint64_t* c_dev, size_t ldc, fsyrk_b200_policy pol, bool mirror, cudaStream_t s,
              fsyrk_b200_opcount* ops, int rank = 0, int nranks = 1) {
     validate_field(p);
@@ -1128,23 +1191,24 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     validate_shapes(n, k, lda, ldc);
     require_device();
     if (n == 0) return;
-    int kbar = (int)k;
-    std::vector<ColMap> map;
-    if (d) kbar = build_colmap(p, d, k, map);
+    const int kbar = xf ? (int)xf->map.size() : (int)k;
     if (nranks > 1 && mirror) fail(FSYRK_B200_EINVAL, "mirror_output needs the whole C (not available per rank)");
-    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, d != nullptr, rank, nranks);
-    if (d) ck(cudaMemcpyAsync(plan->dev_colmap, map.data(), map.size() * sizeof(ColMap), cudaMemcpyHostToDevice, s),
-              "upload colmap");
+    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, rank, nranks);
+    if (xf)
+        ck(cudaMemcpyAsync(plan->dev_colmap, xf->map.data(), xf->map.size() * sizeof(ColMap), cudaMemcpyHostToDevice,
+                           s),
+           "upload colmap");
     plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
     fill_ops(ops, plan);
 }
 
 // Host call: stage A (and C when accumulating) through device buffers.
-void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const uint64_t* d,
+void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const ColXform* xf,
               uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy pol, bool mirror, fsyrk_b200_opcount* ops) {
     validate_field(p);
     validate_policy(pol);
     validate_shapes(n, k, lda, ldc);
+    g_transfer[0] = g_transfer[1] = 0;
     if (ranges_overlap(a, span_bytes(n, k, lda), c, span_bytes(n, n, ldc)))
         fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
     require_device();
@@ -1156,15 +1220,44 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     uint64_t* da = static_cast<uint64_t*>(g_stage_a.ptr);
     uint64_t* dc = static_cast<uint64_t*>(g_stage_c.ptr);
     cudaStream_t s = 0;
-    if (k > 0) ck(cudaMemcpy2DAsync(da, k * 8, a, lda * 8, k * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+    uint64_t h2d = 0, d2h = 0;
+    if (k > 0) {
+        ck(cudaMemcpy2DAsync(da, k * 8, a, lda * 8, k * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+        h2d += n * k * 8;
+    }
+    // Only Low(C) crosses PCIe (the strict upper triangle is scratch, fast_syrk.hpp:271-273):
+    // row block [r0, r1) moves columns [0, r1), i.e. its lower part plus the strict upper part
+    // of its diagonal block -- about n^2/2 + n*kTriRows/2 elements instead of n^2.
+    auto tri_copy = [&](bool to_dev) {
+        for (size_t r0 = 0; r0 < n; r0 += kTriRows) {
+            const size_t r1 = std::min(n, r0 + kTriRows);
+            if (to_dev)
+                ck(cudaMemcpy2DAsync(dc + r0 * n, n * 8, c + r0 * ldc, ldc * 8, r1 * 8, r1 - r0,
+                                     cudaMemcpyHostToDevice, s),
+                   "H2D C");
+            else
+                ck(cudaMemcpy2DAsync(c + r0 * ldc, ldc * 8, dc + r0 * n, n * 8, r1 * 8, r1 - r0,
+                                     cudaMemcpyDeviceToHost, s),
+                   "D2H C");
+            (to_dev ? h2d : d2h) += (r1 - r0) * r1 * 8;
+        }
+    };
     const bool need_c = (beta % p) != 0;
-    if (need_c) ck(cudaMemcpy2DAsync(dc, n * 8, c, ldc * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D C");
-    run_dev(p, (uint32_t)(alpha % p), da, n, k, k == 0 ? 1 : k, d, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
-    // The strict upper triangle is scratch in the reference (fast_syrk.hpp:271-273).  When C was
-    // uploaded (beta != 0) it still holds the caller's values; otherwise it is cleared to zero.
-    if (!mirror && !need_c) ck(launch_zero_upper(dc, (long long)n, (int)n, s), "zero_upper");
-    ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+    if (need_c) tri_copy(true);  // syrk_fast_acc reads only Low(C_in)
+    run_dev(p, (uint32_t)(alpha % p), da, n, k, k == 0 ? 1 : k, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
+    if (mirror) {
+        ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+        d2h += n * n * 8;
+    } else {
+        // beta != 0: the diagonal blocks' strict upper parts round-trip the caller's values;
+        // beta = 0: they are cleared, so the returned scratch is deterministic (zeros there,
+        // the caller's values in the rest of the strict upper triangle)
+        if (!need_c) ck(launch_zero_upper(dc, (long long)n, (int)n, (int)kTriRows, s), "zero_upper");
+        tri_copy(false);
+    }
     ck(cudaStreamSynchronize(s), "sync");
+    g_transfer[0] = h2d;
+    g_transfer[1] = d2h;
 }
 
 }  // namespace
@@ -1226,8 +1319,32 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
                      fsyrk_b200_opcount* ops) {
     return guarded([&] {
         if (!d && k > 0) fail(FSYRK_B200_EDIMENSION, "syrkd: diagonal length must match column count");
-        static const uint64_t none = 0;
-        run_host(p, alpha, a, n, k, lda, d ? d : &none, beta, c, ldc, policy, mirror_output != 0, ops);
+        validate_field(p);
+        const ColXform xf = xform_diag(p, d, d ? k : 0);
+        run_host(p, alpha, a, n, k, lda, &xf, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_syrkbd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                      const fsyrk_b200_block* blocks, size_t nblocks, uint64_t beta, uint64_t* c, size_t ldc,
+                      fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        if (!blocks && nblocks) fail(FSYRK_B200_EINVAL, "syrkbd: null block list");
+        const ColXform xf = xform_blocks(p, blocks, nblocks, k);
+        run_host(p, alpha, a, n, k, lda, &xf, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_syrkbd_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda,
+                          const fsyrk_b200_block* blocks, size_t nblocks, uint64_t beta, uint64_t* c_dev, size_t ldc,
+                          fsyrk_b200_policy policy, int mirror_output, void* stream, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        if (!blocks && nblocks) fail(FSYRK_B200_EINVAL, "syrkbd: null block list");
+        const ColXform xf = xform_blocks(p, blocks, nblocks, k);
+        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, &xf, (uint32_t)(beta % p), c_dev, ldc, policy,
+                mirror_output != 0, static_cast<cudaStream_t>(stream), ops);
     });
 }
 
@@ -1236,8 +1353,10 @@ int fsyrk_b200_syrk_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, size_
                         int mirror_output, void* stream, fsyrk_b200_opcount* ops) {
     return guarded([&] {
         validate_field(p);
-        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host, (uint32_t)(beta % p), c_dev, ldc, policy,
-                mirror_output != 0, static_cast<cudaStream_t>(stream), ops);
+        ColXform xf;
+        if (d_host) xf = xform_diag(p, d_host, k);
+        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host ? &xf : nullptr, (uint32_t)(beta % p), c_dev, ldc,
+                policy, mirror_output != 0, static_cast<cudaStream_t>(stream), ops);
     });
 }
 
@@ -1247,8 +1366,10 @@ int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, 
     return guarded([&] {
         validate_field(p);
         if (nranks < 1 || rank < 0 || rank >= nranks) fail(FSYRK_B200_EINVAL, "rank out of range");
-        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host, (uint32_t)(beta % p), c_dev, ldc, policy, false,
-                static_cast<cudaStream_t>(stream), ops, rank, nranks);
+        ColXform xf;
+        if (d_host) xf = xform_diag(p, d_host, k);
+        run_dev(p, (uint32_t)(alpha % p), a_dev, n, k, lda, d_host ? &xf : nullptr, (uint32_t)(beta % p), c_dev, ldc,
+                policy, false, static_cast<cudaStream_t>(stream), ops, rank, nranks);
     });
 }
 
@@ -1272,6 +1393,12 @@ int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, s
 void fsyrk_b200_release_cache(void) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache.clear();
+}
+
+int fsyrk_b200_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = g_transfer[0];
+    if (d2h) *d2h = g_transfer[1];
+    return FSYRK_B200_OK;
 }
 
 int fsyrk_b200_last_launch_count(int* by_kind, int nkinds) {

@@ -42,12 +42,13 @@ __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda,
     (void)kin;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= kout) return;
-    const ColMap cm = map ? map[c] : ColMap{c, -1, 1, 0};
+    const ColMap cm = map ? map[c] : ColMap{{c, -1, -1, -1}, {1, 0, 0, 0}};
     for (int i = blockIdx.y; i < n; i += gridDim.y) {
         const uint64_t* row = a + (long long)i * lda;
         uint32_t v = 0;
-        if (cm.src0 >= 0) v = mulm(mod_u64(row[cm.src0], m), cm.c0, m);
-        if (cm.src1 >= 0) v = addm(v, mulm(mod_u64(row[cm.src1], m), cm.c1, m), m.p);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (cm.src[t] >= 0) v = addm(v, mulm(mod_u64(row[cm.src[t]], m), cm.c[t], m), m.p);
         out[(long long)i * ldo + c] = v;
     }
 }
@@ -554,9 +555,11 @@ __global__ void mirror_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
     }
 }
 
-__global__ void zero_upper_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
+// strict upper triangle of row i, up to the end of i's row block of `rb` rows (rb = 0: whole row)
+__global__ void zero_upper_kernel(uint64_t* __restrict__ c, long long ldc, int n, int rb) {
     const int i = blockIdx.y;
-    for (int j = i + 1 + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    const int end = rb > 0 ? min(n, (i / rb + 1) * rb) : n;
+    for (int j = i + 1 + blockIdx.x * blockDim.x + threadIdx.x; j < end; j += gridDim.x * blockDim.x)
         c[(long long)i * ldc + j] = 0;
 }
 
@@ -586,7 +589,7 @@ int grid_for(long long total, int threads) {
 
 template <int L>
 cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
-    const bool vec = !(a.kh % 4) && !(a.half % 4) && a.kw == a.kh && !(a.g_row % 4) && !(a.c_row % 4) &&
+    const bool vec = a.aligned && !(a.kh % 4) && !(a.half % 4) && a.kw == a.kh && !(a.g_row % 4) && !(a.c_row % 4) &&
                      !(a.c3_row % 4) &&
                      (a.in64 ? !(a.ld64 % 2) && !(reinterpret_cast<uintptr_t>(a.a64) % 16) : true);
     if (vec) {
@@ -687,9 +690,10 @@ cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, cudaStream_t s) {
+cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    zero_upper_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(c, ldc, n);
+    const int w = rb > 0 ? (rb < n ? rb : n) : n;
+    zero_upper_kernel<<<dim3((w + 255) / 256, n), 256, 0, s>>>(c, ldc, n, rb);
     return cudaGetLastError();
 }
 

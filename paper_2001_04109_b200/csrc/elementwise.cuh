@@ -13,9 +13,12 @@ namespace fsyrk_b200 {
 // Output column c of the converted operand is  c0 * A[:, src0] + c1 * A[:, src1]
 // (src < 0: term absent).  Encodes the syrkd column transform
 // (include/fsyrk/scaled_syrk.hpp:77-101); nullptr map = identity.
+// Column j of the transformed input = sum_t c[t] * A[:, src[t]] (src < 0: unused term).
+// syrkd pairs two (scaled) columns (scaled_syrk.hpp:91-100); syrkbd first folds each 2x2
+// antidiagonal block into (u + v, u - v) (:146-153), so a column mixes at most 4 of A's.
 struct ColMap {
-    int src0, src1;
-    uint32_t c0, c1;
+    int src[4];
+    uint32_t c[4];
 };
 
 // Where a node reads its input: an internal uint32 residue buffer, or a
@@ -55,6 +58,7 @@ struct PrepArgs {
     long long c3_plane, c3_row;  // leaf operand planes for S3 (k = kw)
     const PrepNode* nodes;
     int nnodes;
+    int aligned;  // every node's input rows allow 16-byte vector loads at 4-column steps (driver-checked)
 };
 
 struct PostNode {
@@ -99,7 +103,7 @@ cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
                             uint32_t alpha, uint32_t beta, cudaStream_t s);
 cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s);
-cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, cudaStream_t s);
+cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStream_t s);
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s);
 

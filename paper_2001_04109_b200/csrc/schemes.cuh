@@ -69,9 +69,15 @@ struct Scheme<SCHEME_LIMB4> {
     }
 };
 // planes: A = {d0, d1, d2, 2 d1, 2 d2}, B = {e0, e1, e2} (B reads the first 3 planes)
+#ifndef FSYRK_M17_BN
+#define FSYRK_M17_BN 160
+#endif
+#ifndef FSYRK_M17_STAGES
+#define FSYRK_M17_STAGES 3
+#endif
 template <>
 struct Scheme<SCHEME_M17> {
-    static constexpr int PA = 5, PB = 3, NACC = 3, NT = 9, BN = 160, BK = 64, STAGES = 3;
+    static constexpr int PA = 5, PB = 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN, BK = 64, STAGES = FSYRK_M17_STAGES;
     static constexpr bool UNSIGNED = true;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {

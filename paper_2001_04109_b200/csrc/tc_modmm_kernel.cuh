@@ -8,7 +8,8 @@
 //   warp 1      : tcgen05.mma issuer (the scheme's NT terms per 32-deep K step)
 //   warps 2..9  : epilogue; warp w drains TMEM lanes 32*(w%4).. for one part
 //                 of the tile's columns and folds the accumulators mod p
-// TMEM holds the NACC accumulators of one tile (<= 480 columns); the producer
+// TMEM holds the NACC accumulators of one tile (<= 480 columns), twice when two
+// sets fit (the next tile's MMAs then overlap this tile's epilogue); the producer
 // prefetches the next tile's operands while the epilogue runs.
 #pragma once
 
@@ -34,8 +35,11 @@ struct Cfg {
     static constexpr int BN = Sc::BN, BK = Sc::BK, STAGES = Sc::STAGES, NACC = Sc::NACC;
     static_assert(BK == 128 || BK == 64, "BK must match a swizzle mode");
     static constexpr int COLS_USED = NACC * BN;
-    static constexpr int TMEM_COLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
-                                     : COLS_USED <= 256 ? 256 : 512;
+    // two accumulator sets when they fit: the MMAs of tile i+1 run while the epilogue drains tile i
+    static constexpr int NBUF = 2 * COLS_USED <= 512 ? 2 : 1;
+    static constexpr int COLS_ALL = NBUF * COLS_USED;
+    static constexpr int TMEM_COLS = COLS_ALL <= 32 ? 32 : COLS_ALL <= 64 ? 64 : COLS_ALL <= 128 ? 128
+                                     : COLS_ALL <= 256 ? 256 : 512;
     static_assert(COLS_USED <= 512, "accumulators exceed TMEM");
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN: UMMA N for M = 128");
     static constexpr int A_TILE = BM * BK;
@@ -43,6 +47,7 @@ struct Cfg {
     static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
     static constexpr int STAGE_BYTES = Sc::PA * A_TILE + Sc::PB * B_TILE;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 
@@ -61,15 +66,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     using Sc = Scheme<S>;
     constexpr int BN = C::BN, BK = C::BK, STAGES = C::STAGES;
     constexpr int kParts = EPI / 4;  // column slices per lane quadrant
-    static_assert(EPI % 4 == 0 && (BN / kParts) % 16 == 0, "epilogue split must give 16-column chunks");
+    static_assert(EPI % 4 == 0 && BN % 16 == 0, "epilogue works in 16-column chunks");
     constexpr int SW = BK == 128 ? 2 : 4;  // descriptor layout: SWIZZLE_128B / SWIZZLE_64B
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* tmem_full = empty + STAGES;      // [NBUF]
+    uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + C::NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -80,8 +85,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             sm100::mbar_init(&full[s], 1);
             sm100::mbar_init(&empty[s], 1);
         }
-        sm100::mbar_init(tmem_full, 1);
-        sm100::mbar_init(tmem_empty, EPI);
+        for (int b = 0; b < C::NBUF; ++b) {
+            sm100::mbar_init(&tmem_full[b], 1);
+            sm100::mbar_init(&tmem_empty[b], EPI);
+        }
         sm100::fence_mbar_init();
     } else if (warp == 2 && lane == 0) {
         for (int g = 0; g < args.ngroups; ++g) {
@@ -130,8 +137,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             uint32_t it = 0;
             for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
                 const GroupDesc& g = args.g[args.tiles[t].x];
-                sm100::mbar_wait(tmem_empty, (it & 1) ^ 1);  // epilogue drained the previous tile
+                const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
+                const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
+                sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue drained this buffer
                 sm100::tc_fence_after();
+                const uint32_t acc_base = tmem + buf * C::BUF_COLS;
                 for (int kb = 0; kb < g.k_blocks; ++kb) {
                     sm100::mbar_wait(&full[stage], phase);
                     sm100::tc_fence_after();
@@ -147,7 +157,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
                             // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
-                            sm100::mma_i8(tmem + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                            sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                         }
                     }
                     sm100::tc_commit(&empty[stage]);
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         phase ^= 1;
                     }
                 }
-                sm100::tc_commit(tmem_full);
+                sm100::tc_commit(&tmem_full[buf]);
             }
         }
     } else {
@@ -165,18 +175,20 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         const int part = (warp - 2) >> 2;  // column slice of the tile
         const int row = quad * 32 + lane;
         const ModP m = args.modp;
-        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         uint32_t it = 0;
         for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
             const int4 tile = args.tiles[t];
             const GroupDesc& g = args.g[tile.x];
-            sm100::mbar_wait(tmem_full, it & 1);
+            const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
+            const uint32_t use = C::NBUF == 2 ? it >> 1 : it;
+            const uint32_t lane_base = tmem + buf * C::BUF_COLS + ((uint32_t)(quad * 32) << 16);
+            sm100::mbar_wait(&tmem_full[buf], use & 1);
             sm100::tc_fence_after();
             const long long grow = (long long)tile.z * BM + row;
             const bool row_ok = grow < g.M;
             uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
 #pragma unroll 1
-            for (int c0 = part * (BN / kParts); c0 < (part + 1) * (BN / kParts); c0 += 16) {
+            for (int c0 = 16 * part; c0 < BN; c0 += 16 * kParts) {
                 uint32_t raw[C::NACC][16];
 #pragma unroll
                 for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             }
             sm100::tc_fence_before();
             __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tmem_empty);
+            if (lane == 0) sm100::mbar_arrive(&tmem_empty[buf]);
         }
     }
     sm100::tc_fence_before();

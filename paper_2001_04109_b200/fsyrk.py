@@ -29,7 +29,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libfsyrk_b200.so")
+# FSYRK_B200_LIB selects a tuning variant built by build.py --out (experiments only)
+_LIB_PATH = os.environ.get("FSYRK_B200_LIB") or os.path.join(_HERE, "libfsyrk_b200.so")
 
 UNLIMITED_LEVELS = (1 << 64) - 1  # kUnlimitedLevels, winograd.hpp:9
 
@@ -77,6 +78,10 @@ class _Skew(ctypes.Structure):
     _fields_ = [("form", ctypes.c_int), ("a", ctypes.c_uint64), ("b", ctypes.c_uint64), ("ycost", ctypes.c_int)]
 
 
+class _Block(ctypes.Structure):
+    _fields_ = [("two", ctypes.c_int), ("d", ctypes.c_uint64), ("beta", ctypes.c_uint64), ("gamma", ctypes.c_uint64)]
+
+
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _lib = None
 
@@ -86,7 +91,8 @@ EXPORTS = (
     "fsyrk_b200_syrk_fast_into", "fsyrk_b200_syrk_fast_acc", "fsyrk_b200_syrkd", "fsyrk_b200_syrk_dev",
     "fsyrk_b200_release_cache", "fsyrk_b200_last_launch_count", "fsyrk_b200_last_plan_json",
     "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
-    "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners",
+    "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
+    "fsyrk_b200_last_transfer_bytes",
 )
 
 
@@ -114,6 +120,13 @@ def lib() -> ctypes.CDLL:
     L.fsyrk_b200_syrkd.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
                                    ctypes.c_size_t, _u64p, ctypes.c_uint64, _u64p, ctypes.c_size_t, _Policy,
                                    ctypes.c_int, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrkbd.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                    ctypes.c_size_t, ctypes.POINTER(_Block), ctypes.c_size_t, ctypes.c_uint64, _u64p,
+                                    ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_syrkbd_dev.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_size_t, ctypes.c_size_t, ctypes.POINTER(_Block), ctypes.c_size_t,
+                                        ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, _Policy, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.POINTER(_OpCount)]
     L.fsyrk_b200_syrk_dev.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t,
                                       ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, ctypes.c_void_p,
                                       ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.c_void_p,
@@ -125,6 +138,7 @@ def lib() -> ctypes.CDLL:
     L.fsyrk_b200_partition_owners.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int,
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
+    L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
     L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     L.fsyrk_b200_last_phase_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.fsyrk_b200_level_blocks.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
@@ -334,6 +348,76 @@ def syrkd(f: PrimeField, a: np.ndarray, d: Sequence[int], plan: SyrkPlan, ops: O
     return c
 
 
+@dataclass
+class Block:
+    """One block of BlockDiagonal (scaled_syrk.hpp:13-20): scalar d, or ((0, beta), (beta, gamma))."""
+    two: bool = False
+    d: int = 0
+    beta: int = 0
+    gamma: int = 0
+
+
+@dataclass
+class BlockDiagonal:
+    """Middle matrix of A B A^T (scaled_syrk.hpp:12-37)."""
+    blocks: list = field(default_factory=list)
+
+    @staticmethod
+    def scalar(d: int) -> Block:
+        return Block(False, int(d), 0, 0)
+
+    @staticmethod
+    def two_by_two(beta: int, gamma: int) -> Block:
+        return Block(True, 0, int(beta), int(gamma))
+
+    def dimension(self) -> int:
+        return sum(2 if b.two else 1 for b in self.blocks)
+
+    def validate(self, f: PrimeField) -> None:
+        for b in self.blocks:
+            if b.two and b.beta % f.p == 0:
+                raise ValueError("block-diagonal: 2x2 block requires beta != 0")
+
+    def _c(self):
+        arr = (_Block * max(len(self.blocks), 1))()
+        for i, b in enumerate(self.blocks):
+            arr[i] = _Block(int(b.two), int(b.d), int(b.beta), int(b.gamma))
+        return arr
+
+
+def syrkbd(f: PrimeField, a: np.ndarray, b: BlockDiagonal, plan: SyrkPlan, ops: Optional[OpCount] = None,
+           alpha: int = 1, beta: int = 0, c: Optional[np.ndarray] = None) -> np.ndarray:
+    """Low(A B A^T) for block-diagonal B (scaled_syrk.hpp:117-159); alpha/beta/c as in syrkd."""
+    plan.policy.validate()
+    b.validate(f)
+    pa, n, k, lda = _view(a, "a")
+    if b.dimension() != k:
+        raise DimensionError("syrkbd: block-diagonal dimension must match column count")
+    if f.p == 2:
+        raise ValueError("syrkbd over characteristic 2 uses BinaryField")
+    if c is None:
+        c = np.zeros((n, n), dtype=np.uint64)
+    pc, cn, cm, ldc = _view(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrkbd: dimension mismatch")
+    co = _OpCount()
+    _check(lib().fsyrk_b200_syrkbd(f.p, int(alpha) % f.p, pa, n, k, lda, b._c(), len(b.blocks), int(beta) % f.p, pc,
+                                   ldc, plan.policy._c(), int(plan.mirror_output), ctypes.byref(co)))
+    _ops_out(ops, co)
+    return c
+
+
+def syrkbd_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, b: BlockDiagonal, beta: int, c_ptr: int,
+               ldc: int, policy: RecursionPolicy, mirror: bool = False, stream: int = 0,
+               ops: Optional[OpCount] = None) -> None:
+    """Device-resident syrkbd (fsyrk_b200_syrkbd_dev)."""
+    co = _OpCount()
+    _check(lib().fsyrk_b200_syrkbd_dev(int(p), int(alpha) % p, ctypes.c_void_p(a_ptr), int(n), int(k), int(lda),
+                                       b._c(), len(b.blocks), int(beta) % p, ctypes.c_void_p(c_ptr), int(ldc),
+                                       policy._c(), int(mirror), ctypes.c_void_p(stream), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
 def syrk_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta: int, c_ptr: int, ldc: int,
              policy: RecursionPolicy, mirror: bool = False, stream: int = 0, d: Optional[np.ndarray] = None,
              ops: Optional[OpCount] = None) -> None:
@@ -410,6 +494,13 @@ def last_launch_counts() -> dict:
     arr = (ctypes.c_int * 5)()
     total = lib().fsyrk_b200_last_launch_count(arr, 5)
     return {"total": total, "products": arr[0], "pre": arr[1], "post": arr[2], "convert": arr[3], "other": arr[4]}
+
+
+def last_transfer_bytes() -> tuple:
+    """(host->device, device->host) bytes of the last host-API call on this thread."""
+    h, d = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    lib().fsyrk_b200_last_transfer_bytes(ctypes.byref(h), ctypes.byref(d))
+    return int(h.value), int(d.value)
 
 
 def last_plan() -> dict:

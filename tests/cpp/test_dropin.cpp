@@ -80,6 +80,43 @@ int main() {
             CHECK(lower_equal(f, dev.view(), ref.view()), "syrkd p=%llu m=%zu n=%zu", (unsigned long long)p, m, n);
         }
     }
+    // 3b. syrkbd through the shim vs the reference's syrkbd (random block structures,
+    //     acceptance.cpp:277-345 pattern)
+    for (std::uint64_t p : {3ull, 7ull, 13ull, 65537ull, 131071ull, 2147483647ull}) {
+        PrimeField f(p);
+        std::mt19937_64 r4(p * 11 + 3);
+        auto plan = make_syrk_plan(f, {2, kUnlimitedLevels});
+        for (int t = 0; t < 6; ++t) {
+            const std::size_t m = 1 + r4() % 80, want = 1 + r4() % 40;
+            BlockDiagonal<PrimeField> b;
+            std::size_t dim = 0;
+            while (dim < want) {
+                if (r4() % 3 == 0 || dim + 1 == want) {
+                    b.blocks.push_back(BlockDiagonal<PrimeField>::scalar(f.random_element(r4)));
+                    dim += 1;
+                } else {
+                    b.blocks.push_back(BlockDiagonal<PrimeField>::two_by_two(1 + r4() % (p - 1), 0));
+                    dim += 2;
+                }
+            }
+            auto a = random_matrix(f, m, dim, r4());
+            OpCount ops;
+            auto dev = fsyrk_b200::syrkbd(f, a.view(), b, plan, ops);
+            auto ref = syrkbd<PrimeField>(f, a.view(), b, plan, ops);
+            CHECK(lower_equal(f, dev.view(), ref.view()), "syrkbd p=%llu m=%zu k=%zu", (unsigned long long)p, m, dim);
+        }
+        BlockDiagonal<PrimeField> bad;
+        bad.blocks.push_back(BlockDiagonal<PrimeField>::two_by_two(1, 1));
+        Matrix<PrimeField> a2(2, 2, 1);
+        OpCount ops;
+        bool threw = false;
+        try {
+            fsyrk_b200::syrkbd(f, a2.view(), bad, plan, ops);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw, "syrkbd gamma != 0 must throw std::invalid_argument (p=%llu)", (unsigned long long)p);
+    }
     // 4. error convention: aliased output and bad policy throw std::invalid_argument
     {
         PrimeField f(7);

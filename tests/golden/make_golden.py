@@ -49,6 +49,13 @@ for (p, n, k, s) in ((131071, 32, 16, 5001), (3, 12, 9, 5002), (13, 20, 7, 5003)
                      (131071, 48, 31, 5005)):
     CASES.append((p, n, k, s, 2, "inf", "schur", False))
 
+# syrkbd block-diagonal scaling (test_scaled_syrk.cpp:137-205, acceptance.cpp:277-345); D holds the
+# blocks as (two, d, beta, gamma) rows
+for (p, n, k, s) in ((7, 2, 2, 6001), (13, 5, 5, 6002), (131071, 40, 33, 6003), (65537, 24, 17, 6004),
+                     (3, 12, 9, 6005), (11, 30, 12, 6006), (2147483647, 20, 26, 6007), (65521, 64, 48, 6008),
+                     (131071, 96, 64, 6009), (5, 9, 14, 6010)):
+    CASES.append((p, n, k, s, 2, "inf", "syrkbd", False))
+
 
 def run_case(case, tmp):
     p, n, k, seed, thr, lev, mode, mirror = case
@@ -71,6 +78,8 @@ def run_case(case, tmp):
         rec["C0"] = np.fromfile(fc0, dtype=np.uint64).reshape(n, n)
     if mode == "schur":
         rec["D"] = np.fromfile(fd, dtype=np.uint64)
+    if mode == "syrkbd":
+        rec["D"] = np.fromfile(fd, dtype=np.uint64).reshape(-1, 4)
     return rec, info
 
 

@@ -42,6 +42,8 @@ def lib():
         L.orc_syrk_classical.argtypes = [_u64, _u64, _u64p, _sz, _sz, _sz, _u64, _u64p, _sz]
         L.orc_syrk_fast.argtypes = [_u64, _u64p, _sz, _sz, _sz, _u64p, _sz, _sz, _sz]
         L.orc_syrk_fast_acc.argtypes = [_u64, _u64, _u64p, _sz, _sz, _sz, _u64, _u64p, _sz, _sz, _sz]
+        L.orc_abat_classical.argtypes = [_u64, _u64p, _sz, _sz, _sz, ctypes.POINTER(ctypes.c_int), _u64p, _u64p,
+                                         _u64p, _sz, _u64p, _sz]
         L.orc_syrkd.argtypes = [_u64, _u64p, _sz, _sz, _sz, _u64p, _u64p, _sz, _sz, _sz]
         L.orc_syrkd.restype = ctypes.c_long
         L.orc_level_blocks.argtypes = [_u64, _u64p, _sz, _sz, _sz, _sz, _sz] + [_u64p] * 9
@@ -158,3 +160,17 @@ def lower_equal(x, y):
     n = x.shape[0]
     idx = np.tril_indices(n)
     return x.shape == y.shape and np.array_equal(x[idx], y[idx])
+
+
+def abat_classical(p, a, blocks):
+    """Full (A B A^T) mod p for block-diagonal B given as [(two, d, beta, gamma), ...]
+    (abat_oracle, test_scaled_syrk.cpp:25-47)."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    n, k = a.shape
+    nb = len(blocks)
+    two = (ctypes.c_int * max(nb, 1))(*[int(b[0]) for b in blocks])
+    cols = [np.ascontiguousarray(np.array([int(b[i]) for b in blocks] or [0], dtype=np.uint64)) for i in (1, 2, 3)]
+    c = np.zeros((n, n), dtype=np.uint64)
+    if n and k:
+        lib().orc_abat_classical(p, _p(a), n, k, k, two, _p(cols[0]), _p(cols[1]), _p(cols[2]), nb, _p(c), n)
+    return c

@@ -16,6 +16,13 @@ def _policy(fs, case):
     return fs.RecursionPolicy(case["threshold"], UNL if case["levels"] is None else case["levels"])
 
 
+def _blocks(fs, rows):
+    bd = fs.BlockDiagonal()
+    for two, d, beta, gamma in rows:
+        bd.blocks.append(fs.BlockDiagonal.two_by_two(int(beta), int(gamma)) if two else fs.BlockDiagonal.scalar(int(d)))
+    return bd
+
+
 def test_golden_cases(gpu, golden):
     fs = gpu
     for case in golden["cases"]:
@@ -27,6 +34,8 @@ def test_golden_cases(gpu, golden):
         elif case["mode"] == "acc":
             c = case["C0"].copy()
             fs.syrk_fast_acc(f, case["alpha"], a, case["beta"], c, plan)
+        elif case["mode"] == "syrkbd":
+            c = fs.syrkbd(f, a, _blocks(fs, case["D"]), plan)
         else:
             c = case["C0"].copy()
             fs.syrkd(f, a, case["D"], plan, alpha=case["p"] - 1, beta=1, c=c)
@@ -180,3 +189,112 @@ def test_mirror_and_strided_views(gpu):
     c3 = np.full((80, 80), 77, dtype=np.uint64)
     fs.syrk_fast_acc(f, 1, a, 1, c3, fs.make_syrk_plan(f, fs.RecursionPolicy(4)))
     assert (c3[np.triu_indices(80, 1)] == 77).all()
+
+
+def _random_blocks(rng, p, k):
+    rows, dim = [], 0
+    while dim < k:
+        if rng.integers(3) == 0 or dim + 1 == k:
+            rows.append((0, int(rng.integers(p)), 0, 0))
+            dim += 1
+        else:
+            rows.append((1, 0, int(rng.integers(1, p)), 0))
+            dim += 2
+    return rows
+
+
+@pytest.mark.parametrize("p", [3, 7, 13, 65521, 65537, 131071, 2147483647])
+def test_syrkbd_battery(gpu, p):
+    # scaled battery (acceptance.cpp:277-345): syrkbd against the dense A B A^T oracle, plain and in
+    # the accumulating Schur form; odd / even non-residue counts, all-antidiagonal and all-scalar B
+    fs = gpu
+    f = fs.PrimeField(p)
+    rng = np.random.default_rng(p + 17)
+    for t in range(8):
+        n = int(rng.integers(1, 200))
+        k = int(rng.integers(1, 160))
+        rows = _random_blocks(rng, p, k)
+        if t == 6 and k % 2 == 0:
+            rows = [(1, 0, int(rng.integers(1, p)), 0) for _ in range(k // 2)]
+        if t == 7:
+            rows = [(0, int(rng.integers(p)), 0, 0) for _ in range(k)]
+        a = orc.random_matrix(p, n, k, int(rng.integers(1 << 62)))
+        thr = (2, 8, 64)[t % 3]
+        plan = fs.make_syrk_plan(f, fs.RecursionPolicy(thr))
+        want = orc.abat_classical(p, a, rows)
+        c = fs.syrkbd(f, a, _blocks(fs, rows), plan)
+        assert orc.lower_equal(c, want), (p, n, k, t)
+        c0 = orc.random_matrix(p, n, n, 99)
+        c = c0.copy()
+        fs.syrkbd(f, a, _blocks(fs, rows), plan, alpha=p - 1, beta=1, c=c)
+        idx = np.tril_indices(n)
+        exp = c0.copy()
+        exp[idx] = (c0[idx] + np.uint64(p) - want[idx]) % np.uint64(p)
+        assert orc.lower_equal(c, exp), (p, n, k, t, "schur")
+
+
+def test_syrkbd_examples_and_errors(gpu):
+    fs = gpu
+    # antidiagonal over F_7, A = I2, beta = 1 (test_scaled_syrk.cpp:151-161): Low = [[0], [1, 0]]
+    f7 = fs.PrimeField(7)
+    bd = fs.BlockDiagonal([fs.BlockDiagonal.two_by_two(1, 0)])
+    c = fs.syrkbd(f7, np.eye(2, dtype=np.uint64), bd, fs.make_syrk_plan(f7, fs.RecursionPolicy(2)))
+    assert (c[0, 0], c[1, 0], c[1, 1]) == (0, 1, 0)
+    # scalar identity blocks reduce to plain syrk (:139-149)
+    f13 = fs.PrimeField(13)
+    a = fs.random_matrix(f13, 5, 5, 2)
+    plan = fs.make_syrk_plan(f13, fs.RecursionPolicy(2))
+    c = fs.syrkbd(f13, a, fs.BlockDiagonal([fs.BlockDiagonal.scalar(1)] * 5), plan)
+    assert orc.lower_equal(c, fs.syrk_fast(f13, a, plan))
+    # malformed blocks (:192-205): beta = 0, gamma != 0 in odd characteristic, dimension mismatch
+    a2 = np.ones((2, 2), dtype=np.uint64)
+    with pytest.raises(ValueError):
+        fs.syrkbd(f7, a2, fs.BlockDiagonal([fs.BlockDiagonal.two_by_two(0, 0)]), plan)
+    with pytest.raises(ValueError):
+        fs.syrkbd(f7, a2, fs.BlockDiagonal([fs.BlockDiagonal.two_by_two(1, 1)]), plan)
+    with pytest.raises(fs.DimensionError):
+        fs.syrkbd(f7, a2, fs.BlockDiagonal([fs.BlockDiagonal.scalar(1)]), plan)
+
+
+@pytest.mark.parametrize("p", [65521, 131071])
+def test_split_k_child_alignment(gpu, p):
+    # k > n splits k at k1 = (k/2) & ~1 (fast_syrk.hpp:143-150); k1 = 102 puts the second half at a
+    # column offset that is not 16-byte aligned for residue rows while that child (k = 104) is
+    # otherwise vector-shaped -- the prep must take its scalar path there
+    fs = gpu
+    f = fs.PrimeField(p)
+    a = orc.random_matrix(p, 128, 206, 77)
+    d = orc.random_nonzero(p, 206, 78)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(8))
+    assert orc.lower_equal(fs.syrk_fast(f, a, plan), orc.syrk_classical(p, a))
+    want = orc.syrkd(p, a, d, 8)
+    assert orc.lower_equal(fs.syrkd(f, a, d, plan), want)
+
+
+def test_triangular_host_transfers(gpu):
+    # only Low(C) crosses PCIe in 256-row blocks: results stay exact across block edges, the
+    # byte count matches, beta = 0 clears the diagonal blocks' strict upper parts, beta != 0
+    # leaves the caller's strict upper triangle as it was
+    fs = gpu
+    p, n, k = 131071, 600, 200
+    f = fs.PrimeField(p)
+    a = orc.random_matrix(p, n, k, 5)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(16))
+    want = orc.syrk_classical(p, a)
+    c = np.full((n, n), 7, dtype=np.uint64)
+    fs.syrk_fast_into(f, a, c, plan)
+    assert orc.lower_equal(c, want)
+    blocks = [(r0, min(n, r0 + 256)) for r0 in range(0, n, 256)]
+    assert fs.last_transfer_bytes() == (n * k * 8, sum((r1 - r0) * r1 * 8 for r0, r1 in blocks))
+    for r0, r1 in blocks:
+        blk = c[r0:r1, r0:r1]
+        assert (blk[np.triu_indices(r1 - r0, 1)] == 0).all()
+    assert (c[:256, 256:] == 7).all()
+    c0 = orc.random_matrix(p, n, n, 6)
+    c = c0.copy()
+    fs.syrk_fast_acc(f, 3, a, 5, c, plan)
+    idx = np.tril_indices(n)
+    exp = c0.copy()
+    exp[idx] = (want[idx] * np.uint64(3) + c0[idx] * np.uint64(5)) % np.uint64(p)
+    assert orc.lower_equal(c, exp)
+    assert np.array_equal(c[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])

@@ -50,6 +50,8 @@ def test_oracle_matches_reference_outputs(golden):
             assert orc.lower_equal(cls, case["C"]), (p, case["n"], case["k"])
         elif case["mode"] == "acc":
             c = orc.syrk_fast_acc(p, case["alpha"], a, case["beta"], case["C0"], case["threshold"], lev)
+        elif case["mode"] == "syrkbd":  # the dense A B A^T restatement (abat_oracle)
+            c = orc.abat_classical(p, a, [tuple(int(v) for v in row) for row in case["D"]])
         else:  # schur: Low(C0) - Low(A D A^T)
             x = orc.syrkd(p, a, case["D"], case["threshold"], lev)
             c = case["C0"].copy()

@@ -146,9 +146,9 @@ uint64_t pow_mod(uint64_t b, uint64_t e, uint64_t p) {
 // P4 on (I, J) and (J, I), and the post-additions of C11(I, J), C22(I, J),
 // C21(I, J), C21(J, I) -- all local.  Pairs are assigned longest-first to the
 // least-loaded rank (cost ~ rows_I * rows_J, halved on the diagonal).
-int part_block_for(int bn) {
-    int b = 128;
-    while (b % bn) b += 128;  // lcm(128, BN): 128 (BN 64, 128), 384 (96), 640 (160)
+int part_block_for(int bm, int bn) {
+    int b = bm;
+    while (b % bn) b += bm;  // lcm(tile rows, BN), e.g. 640 (128 x 160) or 1280 (256 x 160)
     return b;
 }
 
@@ -267,7 +267,9 @@ struct Plan {
     fsyrk_b200_policy policy;
     bool colmap = false;
     SchemeInfo sch;  // digit scheme of the tensor-core products (schemes.cuh)
-    int L, BN, BK;   // L: digit planes stored per operand
+    int L, BN, BK;   // L: digit planes stored per leaf operand
+    int BMt = 128;   // output rows per product tile (256 on CTA pairs)
+    int ncta = 148;  // CTAs of a persistent product launch
     host::Skew y;
     ModP m;
     uint32_t c32 = 0;
@@ -393,6 +395,7 @@ struct Plan {
         L = sch.planes;
         BN = sch.bn;
         BK = sch.bk;
+        BMt = sch.bm;
         host::Field f{p};
         y = host::skew_orthogonal(f);
         m = make_modp((uint32_t)p);
@@ -405,7 +408,7 @@ struct Plan {
             partitioned = r.kind == LEVEL && nodes[r.ch[0]].kind == LEAF && nodes[r.ch[1]].kind == LEAF &&
                           nodes[r.ch[2]].kind == LEAF;
             if (partitioned) {
-                kPartBlock = part_block_for(BN);
+                kPartBlock = part_block_for(sch.bm, BN);
                 part_nb = (r.h + kPartBlock - 1) / kPartBlock;
                 owner = partition_owners(r.h, pnranks, kPartBlock);
             } else {
@@ -467,14 +470,14 @@ struct Plan {
             lg.off_planes = ar.take((size_t)lg.slot * lg.count, 1024);
             lg.off_x = ar.take((size_t)lg.count * lg.n * lg.n * 4);
             lg.ntiles = 0;
-            for (int tm = 0; tm * 128 < lg.n; ++tm)
-                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn) ++lg.ntiles;
+            for (int tm = 0; tm * BMt < lg.n; ++tm)
+                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * BMt + BMt - 1; ++tn) ++lg.ntiles;
         }
         for (auto& gg : gemms) {
             gg.hpad = (int)round_up(gg.h, 128);
             gg.kpad = (int)round_up(gg.kw, 128);
             gg.plane = (long long)gg.hpad * gg.kpad;
-            gg.slot = gg.plane * L;
+            gg.slot = gg.plane * sch.pa;  // A-role operands (S1, A22)
             gg.off_ga = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
             gg.slot_b = gg.plane * sch.pb;
             gg.off_gb = ar.take((size_t)gg.slot_b * 2 * gg.count, 1024);
@@ -505,16 +508,16 @@ struct Plan {
                     if (!pgs[c].leaf) {
                         const GemmGroup& gg = gemms[pgs[c].idx];
                         for (int b = 0; b < 2 * gg.count; ++b)
-                            for (int tm = 0; tm * 128 < gg.h; ++tm)
+                            for (int tm = 0; tm * BMt < gg.h; ++tm)
                                 for (int tn = 0; tn * BN < gg.h; ++tn)
-                                    if (!idle && owns_block_pair(tm * 128 / kPartBlock, tn * BN / kPartBlock))
+                                    if (!idle && owns_block_pair(tm * BMt / kPartBlock, tn * BN / kPartBlock))
                                         pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
                     } else {
                         const LeafGroup& lg = leaves[pgs[c].idx];
                         for (int b = 0; b < lg.count; ++b)
-                            for (int tm = 0; tm * 128 < lg.n; ++tm)
-                                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * 128 + 127; ++tn)
-                                    if (!idle && owns_block_pair(tm * 128 / kPartBlock, tn * BN / kPartBlock))
+                            for (int tm = 0; tm * BMt < lg.n; ++tm)
+                                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * BMt + BMt - 1; ++tn)
+                                    if (!idle && owns_block_pair(tm * BMt / kPartBlock, tn * BN / kPartBlock))
                                         pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
                     }
                 }
@@ -592,19 +595,20 @@ struct Plan {
             lg.planes = reinterpret_cast<int8_t*>(arena + lg.off_planes);
             lg.xout = reinterpret_cast<uint32_t*>(arena + lg.off_x);
             lg.tA = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, 128, BK);
-            lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, BN, BK);
+            lg.tB = make_plane_map(lg.planes, lg.kpad, lg.rpad, L, lg.count, sch.b_box, BK);
         }
         for (auto& gg : gemms) {
             gg.ga = reinterpret_cast<int8_t*>(arena + gg.off_ga);
             gg.gb = reinterpret_cast<int8_t*>(arena + gg.off_gb);
             gg.out = reinterpret_cast<uint32_t*>(arena + gg.off_out);
-            gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, L, 2 * gg.count, 128, BK);
-            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, sch.pb, 2 * gg.count, BN, BK);
+            gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, sch.pa, 2 * gg.count, 128, BK);
+            gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, sch.pb, 2 * gg.count, sch.b_box, BK);
         }
         {
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            ncta = modmm_grid(sch, nsm);
         }
         for (auto& pl : prods) {
             GroupedArgs& a = pl.args;
@@ -803,12 +807,12 @@ struct Plan {
         for (auto& lg : leaves) {
             uint64_t macs = (uint64_t)lg.count * lg.n * (lg.n + 1) / 2 * lg.k;
             tensor_macs += macs;
-            int8_macs += (uint64_t)lg.count * lg.ntiles * 128ull * BN * lg.kpad * sch.nterms;
+            int8_macs += (uint64_t)lg.count * lg.ntiles * (uint64_t)BMt * BN * lg.kpad * sch.nterms;
         }
         for (auto& gg : gemms) {
             tensor_macs += (uint64_t)2 * gg.count * gg.h * gg.h * gg.kw;
-            int8_macs += (uint64_t)2 * gg.count * (gg.hpad / 128) * ((gg.h + BN - 1) / BN) * 128ull * BN * gg.kpad *
-                         sch.nterms;
+            int8_macs += (uint64_t)2 * gg.count * ((gg.h + BMt - 1) / BMt) * ((gg.h + BN - 1) / BN) * (uint64_t)BMt *
+                         BN * gg.kpad * sch.nterms;
             ew_adds += (uint64_t)gg.count * (4ull * gg.h * gg.kw + 4ull * gg.h * gg.h);
         }
     }
@@ -896,7 +900,7 @@ struct Plan {
         };
         auto run_prod = [&](ProdLaunch& pl, cudaStream_t st) {
             traced("products phase " + std::to_string(pl.phase), st,
-                   [&] { ck(modmm_launch(sch, pl.args, std::min(nsm, pl.args.ntiles), st), "modmm"); });
+                   [&] { ck(modmm_launch(sch, pl.args, std::min(ncta, pl.args.ntiles * (BMt / 128)), st), "modmm"); });
             counts[0]++;
         };
         bool root_done = false;
@@ -1378,7 +1382,8 @@ int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, s
     return guarded([&] {
         if (nranks < 1) fail(FSYRK_B200_EINVAL, "nranks must be >= 1");
         validate_field(p);
-        const int blk = part_block_for(scheme_for(p).bn);
+        const SchemeInfo si = scheme_for(p);
+        const int blk = part_block_for(si.bm, si.bn);
         std::vector<int> own = partition_owners((int)h, nranks, blk);
         const size_t nb = (h + blk - 1) / blk;
         if (nblocks) *nblocks = nb;
@@ -1518,9 +1523,9 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
                                    static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, 0), "split B");
         }
         CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128, BK);
-        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, BN, BK);
+        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, sch.b_box, BK);
         std::vector<int4> tiles;
-        for (int tm = 0; tm * 128 < (int)m; ++tm)
+        for (int tm = 0; tm * sch.bm < (int)m; ++tm)
             for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
         DevBuf dtiles;
         dtiles.ensure(tiles.size() * sizeof(int4));
@@ -1547,7 +1552,8 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         int nsm = 148, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        ck(modmm_launch(sch, args, std::min<int>(nsm, (int)tiles.size()), 0), "modmm");
+        ck(modmm_launch(sch, args, std::min<int>(modmm_grid(sch, nsm), (int)tiles.size() * (sch.bm / 128)), 0),
+           "modmm");
         ck(cudaDeviceSynchronize(), "sync");
         std::vector<uint32_t> buf(m * n);
         ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");

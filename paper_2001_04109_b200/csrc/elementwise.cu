@@ -90,8 +90,9 @@ __device__ __forceinline__ Src make_src(const InView& v, const uint64_t* a64, lo
 }
 
 // The kernels below are templated on the digit scheme S (schemes.cuh): a residue
-// becomes Scheme<S>::PA int8 planes, byte l of encode_planes<S>(x) going to plane l.
-template <int S, int NPL = Scheme<S>::PA>
+// becomes up to planes_of<S>() int8 planes, byte l of encode_planes<S>(x) going to
+// plane l (GEMM operands keep only the planes their A / B role reads).
+template <int S, int NPL = planes_of<S>()>
 __device__ __forceinline__ void put_planes(int8_t* base, long long plane, long long off, uint32_t x, uint32_t p) {
     const uint64_t w = encode_planes<S>(x, p);
 #pragma unroll
@@ -99,7 +100,7 @@ __device__ __forceinline__ void put_planes(int8_t* base, long long plane, long l
 }
 
 // four consecutive columns of one row, one 32-bit store per plane (the first NPL planes)
-template <int S, int NPL = Scheme<S>::PA>
+template <int S, int NPL = planes_of<S>()>
 __device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long long off, uint4 x, uint32_t p) {
     const uint64_t w0 = encode_planes<S>(x.x, p), w1 = encode_planes<S>(x.y, p), w2 = encode_planes<S>(x.z, p),
                    w3 = encode_planes<S>(x.w, p);
@@ -182,8 +183,8 @@ __global__ void prep_kernel(const PrepArgs args) {
         const uint32_t s3 = subm(s1[t], a22[t], p);
         const uint32_t s4 = addm(s3, a12[t], p);
         const long long go = (long long)i * args.g_row + c;
-        put_planes<L>(nd.s1, args.g_plane, go, s1[t], p);
-        put_planes<L>(nd.a22, args.g_plane, go, a22[t], p);
+        put_planes<L, Scheme<L>::PA>(nd.s1, args.g_plane, go, s1[t], p);  // A-role: first PA planes
+        put_planes<L, Scheme<L>::PA>(nd.a22, args.g_plane, go, a22[t], p);
         put_planes<L, Scheme<L>::PB>(nd.s2, args.g_plane, go, s2, p);  // B-role: first PB planes
         put_planes<L, Scheme<L>::PB>(nd.s4, args.g_plane, go, s4, p);
         if (c < kh) {
@@ -298,9 +299,10 @@ __device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNo
         const uint4 s3 = sub4(s1[t], a22[t], p);
         const uint4 s4 = add4(s3, a12[t], p);
         const long long go = (long long)i * args.g_row + c;
-        constexpr int PB = Scheme<S>::PB;  // B-role operands (S2, S4) only need the first PB planes
-        put_planes4<S>(nd.s1, args.g_plane, go, s1[t], p);
-        put_planes4<S>(nd.a22, args.g_plane, go, a22[t], p);
+        // GEMM operands keep the planes of their role; leaf operands (read as A and B) all
+        constexpr int PA = Scheme<S>::PA, PB = Scheme<S>::PB;
+        put_planes4<S, PA>(nd.s1, args.g_plane, go, s1[t], p);
+        put_planes4<S, PA>(nd.a22, args.g_plane, go, a22[t], p);
         put_planes4<S, PB>(nd.s2, args.g_plane, go, s2, p);
         put_planes4<S, PB>(nd.s4, args.g_plane, go, s4, p);
         if (nd.c_a11) put_planes4<S>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);

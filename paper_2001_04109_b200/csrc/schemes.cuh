@@ -35,13 +35,22 @@ struct Term {
     int8_t a, b, acc;
 };
 
+// FSYRK_PAIR = 1: products run on CTA pairs (cta_group::2, 256-row tiles; each SM loads
+// half of B), which halves the B operand bytes an SM pulls from L2 per MAC.  Measured
+// slower than single CTAs on B200 even with the epilogue removed (cfg2 products 166 vs
+// 155 us, cfg5 2.34 vs 2.17 ms; profiles/r01/variants.txt): the single-CTA main loop is
+// not operand-feed bound, so the pair path stays available but off.
+#ifndef FSYRK_PAIR
+#define FSYRK_PAIR 0
+#endif
+
 template <int S>
 struct Scheme;
 
 template <>
 struct Scheme<SCHEME_LIMB2> {
-    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = 128, BK = 128, STAGES = 3;
-    static constexpr bool UNSIGNED = false;
+    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = 128, BK = 128, STAGES = FSYRK_PAIR ? 4 : 3;
+    static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
         return T[q];
@@ -49,8 +58,8 @@ struct Scheme<SCHEME_LIMB2> {
 };
 template <>
 struct Scheme<SCHEME_LIMB3> {
-    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, BN = 96, BK = 128, STAGES = 2;
-    static constexpr bool UNSIGNED = false;
+    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, BN = 96, BK = 128, STAGES = FSYRK_PAIR ? 3 : 2;
+    static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
                                    {2, 0, 2}, {1, 2, 3}, {2, 1, 3}, {2, 2, 4}};
@@ -60,7 +69,7 @@ struct Scheme<SCHEME_LIMB3> {
 template <>
 struct Scheme<SCHEME_LIMB4> {
     static constexpr int PA = 4, PB = 4, NACC = 7, NT = 16, BN = 64, BK = 128, STAGES = 2;
-    static constexpr bool UNSIGNED = false;
+    static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2},
                                    {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}, {1, 3, 4}, {2, 2, 4},
@@ -68,30 +77,35 @@ struct Scheme<SCHEME_LIMB4> {
         return T[q];
     }
 };
-// planes: A = {d0, d1, d2, 2 d1, 2 d2}, B = {e0, e1, e2} (B reads the first 3 planes)
+// planes (stored): {d0, d1, d2, 2 d1, 2 d2}.  Single CTA: A reads all 5, B the first 3.
+// CTA pair: the doubled digits move to the B side (each SM holds only BN/2 rows of B,
+// so the 5-plane operand is the narrow one): A reads {d0, d1, d2}, B all 5.
 #ifndef FSYRK_M17_BN
 #define FSYRK_M17_BN 160
 #endif
 #ifndef FSYRK_M17_STAGES
-#define FSYRK_M17_STAGES 3
+#define FSYRK_M17_STAGES (FSYRK_PAIR ? 4 : 3)
 #endif
 template <>
 struct Scheme<SCHEME_M17> {
-    static constexpr int PA = 5, PB = 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN, BK = 64, STAGES = FSYRK_M17_STAGES;
-    static constexpr bool UNSIGNED = true;
+    static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
+    static constexpr int PA = PAIR ? 3 : 5, PB = PAIR ? 5 : 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN, BK = 64,
+                         STAGES = FSYRK_M17_STAGES;
     __host__ __device__ static constexpr Term term(int q) {
-        constexpr Term T[NT] = {
-        {0, 0, 0}, {3, 2, 0}, {4, 1, 0},   // d0 e0 + 2^18 (d1 e2 + d2 e1) = d0 e0 + (2 d1) e2 + (2 d2) e1
-        {0, 1, 1}, {1, 0, 1}, {4, 2, 1},   // 2^6 (d0 e1 + d1 e0) + 2^24 d2 e2 = 2^6 (... + (2 d2) e2)
-        {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
-        return T[q];
-    }  // 2^12 (d0 e2 + d1 e1 + d2 e0)
+        // acc0: d0 e0 + 2^18 (d1 e2 + d2 e1);  acc1: d0 e1 + d1 e0 + 2^18 d2 e2 (weight 2^6);
+        // acc2: d0 e2 + d1 e1 + d2 e0 (weight 2^12);  2^18 = 2 rides on a doubled digit
+        constexpr Term TA[NT] = {{0, 0, 0}, {3, 2, 0}, {4, 1, 0}, {0, 1, 1}, {1, 0, 1},
+                                 {4, 2, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
+        constexpr Term TB[NT] = {{0, 0, 0}, {1, 4, 0}, {2, 3, 0}, {0, 1, 1}, {1, 0, 1},
+                                 {2, 4, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
+        return PAIR ? TB[q] : TA[q];
+    }
 };
 // planes: A = B = {d0, d1, d2, d3, 2 d3}
 template <>
 struct Scheme<SCHEME_M31> {
-    static constexpr int PA = 5, PB = 5, NACC = 5, NT = 16, BN = 96, BK = 64, STAGES = 3;
-    static constexpr bool UNSIGNED = true;
+    static constexpr int PA = 5, PB = 5, NACC = 5, NT = 16, BN = 96, BK = 64, STAGES = FSYRK_PAIR ? 4 : 3;
+    static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {
         {0, 0, 0}, {1, 4, 0}, {4, 1, 0},             // s=0 and s=4 (2^32 = 2): d1 (2 e3) + (2 d3) e1
@@ -125,9 +139,10 @@ __host__ __device__ inline uint64_t encode_planes(uint32_t x, uint32_t p) {
     }
 }
 
+// planes stored for an operand read in both roles (leaf SYRK operands)
 template <int S>
 constexpr int planes_of() {
-    return Scheme<S>::PA;
+    return Scheme<S>::PA > Scheme<S>::PB ? Scheme<S>::PA : Scheme<S>::PB;
 }
 
 // ------------------------------------------------------------------ fold

@@ -40,7 +40,9 @@ namespace {
 template <int S>
 SchemeInfo info() {
     using Sc = Scheme<S>;
-    return SchemeInfo{S, Sc::PA, Sc::PB, Sc::NACC, Sc::NT, Sc::BN, Sc::BK, Sc::UNSIGNED};
+    return SchemeInfo{S,      planes_of<S>(), Sc::PA,          Sc::PB,
+                      Sc::NACC, Sc::NT,       Sc::BN,          Sc::BK,
+                      Cfg<S>::TILE_M, Cfg<S>::B_ROWS, Sc::UNSIGNED};
 }
 
 uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
@@ -98,6 +100,17 @@ cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid,
         case SCHEME_M17: return launch_cfg<SCHEME_M17>(args, grid, stream);
         case SCHEME_M31: return launch_cfg<SCHEME_M31>(args, grid, stream);
         default: return cudaErrorInvalidValue;
+    }
+}
+
+int modmm_grid(const SchemeInfo& s, int nsm) {
+    switch (s.id) {
+        case SCHEME_LIMB2: return grid_for<SCHEME_LIMB2>(nsm);
+        case SCHEME_LIMB3: return grid_for<SCHEME_LIMB3>(nsm);
+        case SCHEME_LIMB4: return grid_for<SCHEME_LIMB4>(nsm);
+        case SCHEME_M17: return grid_for<SCHEME_M17>(nsm);
+        case SCHEME_M31: return grid_for<SCHEME_M31>(nsm);
+        default: return nsm;
     }
 }
 

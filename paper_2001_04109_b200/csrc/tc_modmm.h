@@ -18,7 +18,7 @@ constexpr int kMaxGroups = 6;
 // problem b reads A slot b * a_mult + a_off and B slot b * b_mult + b_off.
 struct alignas(64) GroupDesc {
     CUtensorMap tmA;  // box BK (K) x 128 rows
-    CUtensorMap tmB;  // box BK (K) x BN rows
+    CUtensorMap tmB;  // box BK (K) x b_box rows
     int M, N;         // output rows / cols
     int k_blocks;     // kpad / BK
     int syrk;         // 1: only j <= i is written (lower triangle)
@@ -42,10 +42,12 @@ struct GroupedArgs {
 // Scheme selection and its parameters (schemes.cuh).
 struct SchemeInfo {
     int id;
-    int planes;   // planes stored per operand (A-role count; B reads the first pb)
-    int pb;
+    int planes;   // planes stored for an operand read in both roles (leaf SYRK operands)
+    int pa, pb;   // planes the A / B role reads (GEMM operands store only these)
     int nacc, nterms;
     int bn, bk;
+    int bm;       // output rows per tile: 128, or 256 on a CTA pair
+    int b_box;    // B rows one CTA stages per tile (bn, or bn / 2 on a CTA pair)
     bool is_unsigned;
 };
 SchemeInfo scheme_for(uint64_t p);
@@ -54,5 +56,7 @@ size_t modmm_k_limit(const SchemeInfo& s, uint64_t p);
 void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w);
 
 cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid, cudaStream_t stream);
+// CTAs per persistent launch on a device with nsm SMs.
+int modmm_grid(const SchemeInfo& s, int nsm);
 
 }  // namespace fsyrk_b200

@@ -6,8 +6,14 @@
 // longest-K-first order.  Warp roles per CTA (one CTA per SM):
 //   warp 0      : TMA producer (runs ahead across tiles)
 //   warp 1      : tcgen05.mma issuer (the scheme's NT terms per 32-deep K step)
-//   warps 2..9  : epilogue; warp w drains TMEM lanes 32*(w%4).. for one part
+//   warps 2..   : epilogue; warp w drains TMEM lanes 32*(w%4).. for one part
 //                 of the tile's columns and folds the accumulators mod p
+// CTA-pair mode (Scheme::PAIR): the CTAs of a 2-CTA cluster share one 256 x BN
+// output tile.  Each loads its 128 rows of A and half of B's BN rows into its
+// own shared memory (completing bytes on the leader's barrier); the leader
+// issues tcgen05.mma.cta_group::2 (M = 256), whose commits arrive in both CTAs;
+// each CTA's epilogue drains its own TMEM rows and reports to the leader.  Per
+// SM this halves the B operand bytes pulled from L2 per MAC.
 // TMEM holds the NACC accumulators of one tile (<= 480 columns), twice when two
 // sets fit (the next tile's MMAs then overlap this tile's epilogue); the producer
 // prefetches the next tile's operands while the epilogue runs.
@@ -26,13 +32,22 @@
 namespace fsyrk_b200 {
 namespace tc {
 
-constexpr int BM = 128;
-constexpr int kEpiWarpsDefault = 8;
+#ifndef FSYRK_EPI_EXPERIMENT
+#define FSYRK_EPI_EXPERIMENT 0
+#endif
+#ifndef FSYRK_EPI_WARPS
+#define FSYRK_EPI_WARPS 8
+#endif
+constexpr int kEpiWarpsDefault = FSYRK_EPI_WARPS;
+constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
 
 template <int S>
 struct Cfg {
     using Sc = Scheme<S>;
+    static constexpr bool PAIR = Sc::PAIR;
     static constexpr int BN = Sc::BN, BK = Sc::BK, STAGES = Sc::STAGES, NACC = Sc::NACC;
+    static constexpr int TILE_M = PAIR ? 2 * BM : BM;  // output rows per tile
+    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA
     static_assert(BK == 128 || BK == 64, "BK must match a swizzle mode");
     static constexpr int COLS_USED = NACC * BN;
     // two accumulator sets when they fit: the MMAs of tile i+1 run while the epilogue drains tile i
@@ -41,9 +56,9 @@ struct Cfg {
     static constexpr int TMEM_COLS = COLS_ALL <= 32 ? 32 : COLS_ALL <= 64 ? 64 : COLS_ALL <= 128 ? 128
                                      : COLS_ALL <= 256 ? 256 : 512;
     static_assert(COLS_USED <= 512, "accumulators exceed TMEM");
-    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN: UMMA N for M = 128");
+    static_assert(BN % (PAIR ? 32 : 16) == 0 && BN >= 16 && BN <= 256, "UMMA N (and 8-row groups per CTA half)");
     static constexpr int A_TILE = BM * BK;
-    static constexpr int B_TILE = BN * BK;
+    static constexpr int B_TILE = B_ROWS * BK;
     static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
     static constexpr int STAGE_BYTES = Sc::PA * A_TILE + Sc::PB * B_TILE;
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
@@ -64,6 +79,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     modmm_kernel(const __grid_constant__ GroupedArgs args) {
     using C = Cfg<S>;
     using Sc = Scheme<S>;
+    constexpr bool PAIR = C::PAIR;
     constexpr int BN = C::BN, BK = C::BK, STAGES = C::STAGES;
     constexpr int kParts = EPI / 4;  // column slices per lane quadrant
     static_assert(EPI % 4 == 0 && BN % 16 == 0, "epilogue works in 16-column chunks");
@@ -72,14 +88,20 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;      // [NBUF]
-    uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF]
+    uint64_t* tmem_full = empty + STAGES;        // [NBUF]
+    uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF] (the leader's counts both CTAs' epilogues)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + C::NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? sm100::cluster_rank() : 0;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // tile-scheduling unit
+    const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     if (warp == 0) {
-        sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
+        if constexpr (PAIR)
+            sm100::tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+        else
+            sm100::tmem_alloc(tmem_slot, C::TMEM_COLS);
     } else if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             sm100::mbar_init(&full[s], 1);
@@ -87,7 +109,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         }
         for (int b = 0; b < C::NBUF; ++b) {
             sm100::mbar_init(&tmem_full[b], 1);
-            sm100::mbar_init(&tmem_empty[b], EPI);
+            sm100::mbar_init(&tmem_empty[b], (PAIR ? 2 : 1) * EPI);
         }
         sm100::fence_mbar_init();
     } else if (warp == 2 && lane == 0) {
@@ -98,29 +120,43 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     }
     sm100::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) sm100::cluster_sync();  // peer barriers initialised before any remote arrive
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ------------------------------------------------ TMA producer
+            // ------------------------------------------------ TMA producer (both CTAs of a pair)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x) {
+            for (int t = unit; t < args.ntiles; t += nunits) {
                 const int4 tile = args.tiles[t];
                 const GroupDesc& g = args.g[tile.x];
                 const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
+                const int arow = tile.z * C::TILE_M + (int)rank * BM;
+                const int brow = tile.w * BN + (int)rank * C::B_ROWS;
                 for (int kb = 0; kb < g.k_blocks; ++kb) {
                     sm100::mbar_wait(&empty[stage], phase ^ 1);
-                    sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
                     uint8_t* st = smem + stage * C::STAGE_BYTES;
+                    if constexpr (PAIR) {
+                        if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
 #pragma unroll
-                    for (int l = 0; l < Sc::PA; ++l)
-                        sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, tile.z * BM, l, bA);
+                        for (int l = 0; l < Sc::PA; ++l)
+                            sm100::tma_load_4d_pair(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
 #pragma unroll
-                    for (int l = 0; l < Sc::PB; ++l)
-                        sm100::tma_load_4d(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage], kb * BK,
-                                           tile.w * BN, l, bB);
+                        for (int l = 0; l < Sc::PB; ++l)
+                            sm100::tma_load_4d_pair(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
+                                                    kb * BK, brow, l, bB);
+                    } else {
+                        sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+#pragma unroll
+                        for (int l = 0; l < Sc::PA; ++l)
+                            sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
+#pragma unroll
+                        for (int l = 0; l < Sc::PB; ++l)
+                            sm100::tma_load_4d(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
+                                               kb * BK, brow, l, bB);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -129,17 +165,17 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
-            constexpr uint32_t idesc = sm100::idesc_i8(BM, BN, !Sc::UNSIGNED);
+        if (lane == 0 && rank == 0) {
+            // ------------------------------------------------ MMA issuer (the leader of a pair)
+            constexpr uint32_t idesc = sm100::idesc_i8(C::TILE_M, BN, !Sc::UNSIGNED);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
-            for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
+            for (int t = unit; t < args.ntiles; t += nunits, ++it) {
                 const GroupDesc& g = args.g[args.tiles[t].x];
                 const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
                 const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
-                sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue drained this buffer
+                sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue(s) drained this buffer
                 sm100::tc_fence_after();
                 const uint32_t acc_base = tmem + buf * C::BUF_COLS;
                 for (int kb = 0; kb < g.k_blocks; ++kb) {
@@ -157,16 +193,25 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         for (int kk = 0; kk < BK / 32; ++kk) {
                             const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
                             // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
-                            sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                            if constexpr (PAIR)
+                                sm100::mma_i8_pair(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                            else
+                                sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                         }
                     }
-                    sm100::tc_commit(&empty[stage]);
+                    if constexpr (PAIR)
+                        sm100::tc_commit_pair(&empty[stage]);
+                    else
+                        sm100::tc_commit(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                sm100::tc_commit(&tmem_full[buf]);
+                if constexpr (PAIR)
+                    sm100::tc_commit_pair(&tmem_full[buf]);
+                else
+                    sm100::tc_commit(&tmem_full[buf]);
             }
         }
     } else {
@@ -176,7 +221,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         const int row = quad * 32 + lane;
         const ModP m = args.modp;
         uint32_t it = 0;
-        for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x, ++it) {
+        for (int t = unit; t < args.ntiles; t += nunits, ++it) {
             const int4 tile = args.tiles[t];
             const GroupDesc& g = args.g[tile.x];
             const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
@@ -184,17 +229,13 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             const uint32_t lane_base = tmem + buf * C::BUF_COLS + ((uint32_t)(quad * 32) << 16);
             sm100::mbar_wait(&tmem_full[buf], use & 1);
             sm100::tc_fence_after();
-            const long long grow = (long long)tile.z * BM + row;
+            const long long grow = (long long)tile.z * C::TILE_M + rank * BM + row;
             const bool row_ok = grow < g.M;
             uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
-#pragma unroll 1
-            for (int c0 = 16 * part; c0 < BN; c0 += 16 * kParts) {
-                uint32_t raw[C::NACC][16];
-#pragma unroll
-                for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
-                sm100::tmem_wait_ld();
+            // fold + store one 16-column chunk of this warp's 32 rows
+            auto emit = [&](const uint32_t (&raw)[C::NACC][16], int c0) {
                 const long long gc0 = (long long)tile.w * BN + c0;
-                if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) continue;
+                if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
                 uint32_t res[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
@@ -203,6 +244,13 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     for (int s = 0; s < C::NACC; ++s) a[s] = raw[s][c];
                     res[c] = fold_acc<S>(a, m, args.w);
                 }
+#if FSYRK_EPI_EXPERIMENT == 3  // timing experiment: fold but do not store
+                uint32_t x = 0;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) x ^= res[c];
+                if (x == 0x7fffffffu) out[gc0] = x;
+                return;
+#endif
                 const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
                 if (full_chunk) {
                     uint4* o = reinterpret_cast<uint4*>(out + gc0);
@@ -216,16 +264,95 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         if (gc < g.N && (!g.syrk || gc <= grow)) out[gc] = res[c];
                     }
                 }
+            };
+            auto load = [&](uint32_t (&raw)[C::NACC][16], int c0) {
+#pragma unroll
+                for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
+            };
+            auto ready = [&](uint32_t (&raw)[C::NACC][16]) {
+                sm100::tmem_wait_ld();
+#pragma unroll
+                for (int s = 0; s < C::NACC; ++s) sm100::reg_fence16(raw[s]);
+            };
+            auto release = [&]() {  // this warp's TMEM reads are complete
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (PAIR)
+                        sm100::mbar_arrive_cluster(&tmem_empty[buf], 0);  // the leader's MMA waits on both CTAs
+                    else
+                        sm100::mbar_arrive(&tmem_empty[buf]);
+                }
+            };
+            // Two register buffers: the TMEM loads of chunk j+1 are in flight while chunk j is
+            // folded and stored; the accumulators are released as soon as the last load lands,
+            // so the next tile's MMAs overlap the last chunk's fold.
+            const int nch = (BN / 16 - part + kParts - 1) / kParts;  // chunks c0 = 16 (part + j kParts)
+#if FSYRK_EPI_EXPERIMENT == 2  // timing experiment: no epilogue at all
+            release();
+            continue;
+#endif
+            uint32_t ra[C::NACC][16];
+            if constexpr (C::NACC > 3) {  // register budget: one buffer for 5 / 7 accumulators
+#pragma unroll 1
+                for (int j = 0; j < nch; ++j) {
+                    load(ra, 16 * (part + j * kParts));
+                    ready(ra);
+                    if (j + 1 == nch) release();
+#if FSYRK_EPI_EXPERIMENT != 1
+                    emit(ra, 16 * (part + j * kParts));
+#endif
+                }
+                continue;
             }
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&tmem_empty[buf]);
+            uint32_t rb[C::NACC][16];
+            load(ra, 16 * part);
+#pragma unroll 1
+            for (int j = 0; j < nch; j += 2) {
+                ready(ra);
+                if (j + 1 < nch) load(rb, 16 * (part + (j + 1) * kParts));
+                else release();
+#if FSYRK_EPI_EXPERIMENT != 1
+                emit(ra, 16 * (part + j * kParts));
+#endif
+                if (j + 1 < nch) {
+                    ready(rb);
+                    if (j + 2 < nch) load(ra, 16 * (part + (j + 2) * kParts));
+                    else release();
+#if FSYRK_EPI_EXPERIMENT != 1
+                    emit(rb, 16 * (part + (j + 1) * kParts));
+#endif
+                }
+            }
         }
     }
     sm100::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) sm100::cluster_sync();  // no CTA leaves while its peer may still signal it
     sm100::tc_fence_after();
-    if (warp == 0) sm100::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (warp == 0) {
+        if constexpr (PAIR)
+            sm100::tmem_dealloc_pair(tmem, C::TMEM_COLS);
+        else
+            sm100::tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+template <int S, int EPI = kEpiWarpsDefault>
+cudaLaunchConfig_t launch_config(int grid, cudaStream_t stream, cudaLaunchAttribute* attr) {
+    using C = Cfg<S>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C::PAIR ? grid & ~1 : grid);
+    cfg.blockDim = dim3(64 + 32 * EPI);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C::PAIR ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
 }
 
 template <int S, int EPI = kEpiWarpsDefault>
@@ -239,8 +366,29 @@ cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
         attr_set = true;
     }
     if (args.ntiles == 0) return cudaSuccess;
-    kern<<<grid, 64 + 32 * EPI, C::SMEM_BYTES, stream>>>(args);
-    return cudaGetLastError();
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);
+    return cudaLaunchKernelEx(&cfg, kern, args);
+}
+
+// CTAs per launch: one per SM, or as many CTA pairs as can be co-resident.
+template <int S, int EPI = kEpiWarpsDefault>
+int grid_for(int nsm) {
+    using C = Cfg<S>;
+    if constexpr (!C::PAIR) {
+        return nsm;
+    } else {
+        auto kern = modmm_kernel<S, EPI>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+        cudaLaunchAttribute attr[1];
+        cudaLaunchConfig_t cfg = launch_config<S, EPI>(nsm, 0, attr);
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+            cudaGetLastError();
+            return nsm & ~1;
+        }
+        return 2 * clusters < nsm ? 2 * clusters : nsm & ~1;
+    }
 }
 
 }  // namespace tc

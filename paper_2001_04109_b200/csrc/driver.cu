@@ -123,7 +123,9 @@ CUtensorMap make_plane_map(void* base, int kpad, int rows, int L, int batch, int
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                        : CU_TENSOR_MAP_SWIZZLE_32B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(FSYRK_B200_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
@@ -636,6 +638,7 @@ struct Plan {
                     g.out = gg.out;
                     g.out_bs = (long long)gg.h * gg.h;
                     g.ldo = gg.h;
+                    modmm_set_output_map(g, 2 * gg.count);
                 } else {
                     const LeafGroup& lg = leaves[pl.members[gi].idx];
                     g.tmA = lg.tA;
@@ -647,6 +650,7 @@ struct Plan {
                     g.out = lg.xout;
                     g.out_bs = (long long)lg.n * lg.n;
                     g.ldo = lg.n;
+                    modmm_set_output_map(g, lg.count);
                 }
             }
         }
@@ -1549,6 +1553,7 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         g.out = static_cast<uint32_t*>(out.ptr);
         g.out_bs = 0;
         g.ldo = (long long)n;
+        modmm_set_output_map(g, 1);
         int nsm = 148, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

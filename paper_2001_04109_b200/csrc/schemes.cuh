@@ -83,14 +83,17 @@ struct Scheme<SCHEME_LIMB4> {
 #ifndef FSYRK_M17_BN
 #define FSYRK_M17_BN 160
 #endif
+#ifndef FSYRK_M17_BK
+#define FSYRK_M17_BK 64
+#endif
 #ifndef FSYRK_M17_STAGES
 #define FSYRK_M17_STAGES (FSYRK_PAIR ? 4 : 3)
 #endif
 template <>
 struct Scheme<SCHEME_M17> {
     static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
-    static constexpr int PA = PAIR ? 3 : 5, PB = PAIR ? 5 : 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN, BK = 64,
-                         STAGES = FSYRK_M17_STAGES;
+    static constexpr int PA = PAIR ? 3 : 5, PB = PAIR ? 5 : 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN,
+                         BK = FSYRK_M17_BK, STAGES = FSYRK_M17_STAGES;
     __host__ __device__ static constexpr Term term(int q) {
         // acc0: d0 e0 + 2^18 (d1 e2 + d2 e1);  acc1: d0 e1 + d1 e0 + 2^18 d2 e2 (weight 2^6);
         // acc2: d0 e2 + d1 e1 + d2 e0 (weight 2^12);  2^18 = 2 rides on a doubled digit
@@ -171,5 +174,30 @@ __device__ __forceinline__ uint32_t fold_acc(const uint32_t* a, const ModP& m, c
         return mod_s64(v, m);
     }
 }
+
+// Two-stage fold for the epilogue: partial() maps the accumulators to one 32-bit word
+// congruent to the result (cheap; runs while the tile holds TMEM), final() reduces it
+// to [0, p) after the accumulators are released.
+template <int S>
+struct SplitFold {
+    static constexpr bool ok = false;
+};
+template <>
+struct SplitFold<SCHEME_M17> {
+    static constexpr bool ok = true;
+    // f(x) = (x mod 2^17) + (x >> 17) = x (mod 2^17 - 1); for x < 2^32: f(x) < 2^17 + 2^15
+    __device__ __forceinline__ static uint32_t f(uint32_t x) { return (x & 0x1FFFFu) + (x >> 17); }
+    __device__ __forceinline__ static uint32_t partial(const uint32_t* a) {  // any a < 2^31
+        return f(a[0]) + (f(a[1]) << 6) + (f(a[2]) << 12);  // < 2^30
+    }
+    // accumulators < 2^26 (K <= 2048): a1 << 6 still fits 32 bits
+    __device__ __forceinline__ static uint32_t partial_short(const uint32_t* a) {
+        return a[0] + f(a[1] << 6) + (f(a[2]) << 12);  // < 2^26 + 2^18 + 2^30
+    }
+    __device__ __forceinline__ static uint32_t final(uint32_t v) {
+        const uint32_t r = f(v);  // < 2^17 + 2^15 < 2p
+        return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
+    }
+};
 
 }  // namespace fsyrk_b200

@@ -103,6 +103,46 @@ cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid,
     }
 }
 
+#ifdef FSYRK_KTRACE
+extern "C" int fsyrk_b200_debug_ktrace(unsigned long long* out, int n) {
+    const int m = n < kTraceTiles * 8 ? n : kTraceTiles * 8;
+    return (int)cudaMemcpyFromSymbol(out, g_ktrace, m * sizeof(unsigned long long));
+}
+#endif
+
+namespace {
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+}  // namespace
+
+void modmm_set_output_map(GroupDesc& g, int batch) {
+    g.tma_ok = 0;
+    const long long bs = g.out_bs > 0 ? g.out_bs : (long long)g.M * g.ldo;
+    if (g.ldo % 4 || bs % 4 || reinterpret_cast<uintptr_t>(g.out) % 16 || g.M <= 0 || g.N <= 0) return;
+    EncodeTiled enc = encode_tiled();
+    if (!enc) return;
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)(batch > 0 ? batch : 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)g.ldo * 4, (cuuint64_t)bs * 4};
+    cuuint32_t box[3] = {16, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&g.tmO, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, g.out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        g.tma_ok = 1;
+}
+
 int modmm_grid(const SchemeInfo& s, int nsm) {
     switch (s.id) {
         case SCHEME_LIMB2: return grid_for<SCHEME_LIMB2>(nsm);

@@ -19,12 +19,13 @@ constexpr int kMaxGroups = 6;
 struct alignas(64) GroupDesc {
     CUtensorMap tmA;  // box BK (K) x 128 rows
     CUtensorMap tmB;  // box BK (K) x b_box rows
+    CUtensorMap tmO;  // outputs [batch][M][N] u32, box 16 x 32 (64-byte swizzle) -- valid if tma_ok
     int M, N;         // output rows / cols
     int k_blocks;     // kpad / BK
     int syrk;         // 1: only j <= i is written (lower triangle)
     int vec_ok;       // ldo % 4 == 0 (16-byte vector stores)
     int a_mult, a_off, b_mult, b_off;
-    int pad_;
+    int tma_ok;       // outputs stored by TMA from shared memory (16-byte aligned rows)
     uint32_t* out;    // residues, problem b at out + b * out_bs
     long long out_bs;
     long long ldo;
@@ -58,5 +59,7 @@ void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w);
 cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid, cudaStream_t stream);
 // CTAs per persistent launch on a device with nsm SMs.
 int modmm_grid(const SchemeInfo& s, int nsm);
+// Output descriptor of a product group (sets g.tmO / g.tma_ok from g.out, M, N, ldo, out_bs).
+void modmm_set_output_map(GroupDesc& g, int batch);
 
 }  // namespace fsyrk_b200

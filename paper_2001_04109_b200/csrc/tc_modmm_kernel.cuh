@@ -35,11 +35,28 @@ namespace tc {
 #ifndef FSYRK_EPI_EXPERIMENT
 #define FSYRK_EPI_EXPERIMENT 0
 #endif
+#ifndef FSYRK_NO_TSTORE
+#define FSYRK_NO_TSTORE 0
+#endif
 #ifndef FSYRK_EPI_WARPS
 #define FSYRK_EPI_WARPS 8
 #endif
 constexpr int kEpiWarpsDefault = FSYRK_EPI_WARPS;
 constexpr int BM = 128;  // accumulator rows per CTA (TMEM lanes)
+
+#ifdef FSYRK_KTRACE
+// timing experiment: per-tile clock64 stamps of CTA 0 (profiles/ktrace.py)
+constexpr int kTraceTiles = 64;
+__device__ unsigned long long g_ktrace[kTraceTiles][8];
+#define KTRACE(it, slot)                                                                        \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && (it) < kTraceTiles) g_ktrace[(it)][(slot)] = clock64();          \
+    } while (0)
+#else
+#define KTRACE(it, slot) \
+    do {                 \
+    } while (0)
+#endif
 
 template <int S>
 struct Cfg {
@@ -48,7 +65,7 @@ struct Cfg {
     static constexpr int BN = Sc::BN, BK = Sc::BK, STAGES = Sc::STAGES, NACC = Sc::NACC;
     static constexpr int TILE_M = PAIR ? 2 * BM : BM;  // output rows per tile
     static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA
-    static_assert(BK == 128 || BK == 64, "BK must match a swizzle mode");
+    static_assert(BK == 128 || BK == 64 || BK == 32, "BK must match a swizzle mode");
     static constexpr int COLS_USED = NACC * BN;
     // two accumulator sets when they fit: the MMAs of tile i+1 run while the epilogue drains tile i
     static constexpr int NBUF = 2 * COLS_USED <= 512 ? 2 : 1;
@@ -61,9 +78,20 @@ struct Cfg {
     static constexpr int B_TILE = B_ROWS * BK;
     static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
     static constexpr int STAGE_BYTES = Sc::PA * A_TILE + Sc::PB * B_TILE;
-    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr int BAR_BYTES = 256;  // mbarriers + TMEM slot
+    static constexpr int EPI_WARPS = kEpiWarpsDefault;
+    static constexpr int NCW = (BN / 16 + EPI_WARPS / 4 - 1) / (EPI_WARPS / 4);  // chunks per epilogue warp
+    // TMA-store staging: one 32 x 16 u32 box (2 KB, 64-byte swizzle) per epilogue warp
+    static constexpr int OUT_BYTES = EPI_WARPS * 2048;
+    // shared memory: [STAGES operand stages][output staging][barriers]; the dynamic window is
+    // 1024-aligned (__align__ on the extern array, checked at entry)
+    // TMA stores: measured faster for the Mersenne schemes (cfg2 products 185 -> 178 us, cfg5
+    // 3.18 -> 2.89 ms), neutral to slightly slower for LIMB2 (cfg3 251 -> 254 us)
+    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (S == SCHEME_M17 || S == SCHEME_M31) &&
+                                   STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES <= 232448;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (TSTORE ? OUT_BYTES : 0) + BAR_BYTES;
     static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1
-    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+    static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
 
 // index of the first term (in issue order) that writes accumulator `acc`
@@ -82,11 +110,13 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     constexpr bool PAIR = C::PAIR;
     constexpr int BN = C::BN, BK = C::BK, STAGES = C::STAGES;
     constexpr int kParts = EPI / 4;  // column slices per lane quadrant
+    static_assert(EPI == C::EPI_WARPS, "staging is sized for the default epilogue width");
     static_assert(EPI % 4 == 0 && BN % 16 == 0, "epilogue works in 16-column chunks");
-    constexpr int SW = BK == 128 ? 2 : 4;  // descriptor layout: SWIZZLE_128B / SWIZZLE_64B
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+    constexpr int SW = BK == 128 ? 2 : BK == 64 ? 4 : 6;  // descriptor layout: SWIZZLE_128B / 64B / 32B
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if (threadIdx.x == 0 && (sm100::smem_u32(smem) & 1023u)) __trap();  // swizzled tiles need 1024-B alignment
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES + (C::TSTORE ? C::OUT_BYTES : 0));
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;        // [NBUF]
     uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF] (the leader's counts both CTAs' epilogues)
@@ -116,6 +146,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         for (int g = 0; g < args.ngroups; ++g) {
             sm100::tma_prefetch(&args.g[g].tmA);
             sm100::tma_prefetch(&args.g[g].tmB);
+            if (C::TSTORE && args.g[g].tma_ok) sm100::tma_prefetch(&args.g[g].tmO);
         }
     }
     sm100::tc_fence_before();
@@ -175,7 +206,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 const GroupDesc& g = args.g[args.tiles[t].x];
                 const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
                 const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
+                KTRACE(it, 0);
                 sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue(s) drained this buffer
+                KTRACE(it, 1);
                 sm100::tc_fence_after();
                 const uint32_t acc_base = tmem + buf * C::BUF_COLS;
                 for (int kb = 0; kb < g.k_blocks; ++kb) {
@@ -212,14 +245,17 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     sm100::tc_commit_pair(&tmem_full[buf]);
                 else
                     sm100::tc_commit(&tmem_full[buf]);
+                KTRACE(it, 2);
             }
         }
     } else {
         // ---------------------------------------------------- epilogue
         const int quad = warp & 3;         // TMEM lane quadrant this warp may access
         const int part = (warp - 2) >> 2;  // column slice of the tile
-        const int row = quad * 32 + lane;
         const ModP m = args.modp;
+        // this warp's output staging: one 32 x 16 swizzled box per chunk (TMA-store path)
+        uint8_t* stg = smem + STAGES * C::STAGE_BYTES + (warp - 2) * 2048;
+        bool stores_pending = false;
         uint32_t it = 0;
         for (int t = unit; t < args.ntiles; t += nunits, ++it) {
             const int4 tile = args.tiles[t];
@@ -228,29 +264,18 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             const uint32_t use = C::NBUF == 2 ? it >> 1 : it;
             const uint32_t lane_base = tmem + buf * C::BUF_COLS + ((uint32_t)(quad * 32) << 16);
             sm100::mbar_wait(&tmem_full[buf], use & 1);
+            if (warp == 2 && lane == 0) KTRACE(it, 3);
             sm100::tc_fence_after();
-            const long long grow = (long long)tile.z * C::TILE_M + rank * BM + row;
+            const int row0 = tile.z * C::TILE_M + (int)rank * BM + quad * 32;  // first row of this warp
+            const long long grow = (long long)row0 + lane;
             const bool row_ok = grow < g.M;
             uint32_t* out = g.out + (long long)tile.y * g.out_bs + grow * g.ldo;
-            // fold + store one 16-column chunk of this warp's 32 rows
-            auto emit = [&](const uint32_t (&raw)[C::NACC][16], int c0) {
+            const int nch = (BN / 16 - part + kParts - 1) / kParts;  // chunks c0 = 16 (part + j kParts)
+            auto col_of = [&](int j) { return 16 * (part + j * kParts); };
+            // direct stores (outputs a TMA box cannot describe): this lane's row, 16 columns
+            auto store_direct = [&](const uint32_t (&res)[16], int c0) {
                 const long long gc0 = (long long)tile.w * BN + c0;
                 if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
-                uint32_t res[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    uint32_t a[C::NACC];
-#pragma unroll
-                    for (int s = 0; s < C::NACC; ++s) a[s] = raw[s][c];
-                    res[c] = fold_acc<S>(a, m, args.w);
-                }
-#if FSYRK_EPI_EXPERIMENT == 3  // timing experiment: fold but do not store
-                uint32_t x = 0;
-#pragma unroll
-                for (int c = 0; c < 16; ++c) x ^= res[c];
-                if (x == 0x7fffffffu) out[gc0] = x;
-                return;
-#endif
                 const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
                 if (full_chunk) {
                     uint4* o = reinterpret_cast<uint4*>(out + gc0);
@@ -265,6 +290,35 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     }
                 }
             };
+            // staged store of chunk j: row `lane` of the warp's 32 x 16 box (64-byte swizzle,
+            // conflict-free), then one TMA store of the box.  The box is reused chunk after chunk:
+            // the previous store must have read it first.
+            auto stage_store = [&](const uint32_t (&res)[16], int j) {
+                const int gc0 = tile.w * BN + col_of(j);
+                if (row0 >= g.M || gc0 >= g.N || (g.syrk && gc0 > row0 + 31)) return;
+                if (stores_pending) {
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                }
+                uint8_t* box = stg + lane * 64;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int qs = q ^ ((lane >> 1) & 3);
+                    *reinterpret_cast<uint4*>(box + qs * 16) =
+                        make_uint4(res[4 * q], res[4 * q + 1], res[4 * q + 2], res[4 * q + 3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                            reinterpret_cast<uint64_t>(&g.tmO)),
+                        "r"(gc0), "r"(row0), "r"(tile.y), "r"(sm100::smem_u32(stg))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                stores_pending = true;
+            };
             auto load = [&](uint32_t (&raw)[C::NACC][16], int c0) {
 #pragma unroll
                 for (int s = 0; s < C::NACC; ++s) sm100::tmem_ld16(lane_base + s * BN + c0, raw[s]);
@@ -275,6 +329,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 for (int s = 0; s < C::NACC; ++s) sm100::reg_fence16(raw[s]);
             };
             auto release = [&]() {  // this warp's TMEM reads are complete
+                if (lane == 0 && warp == 2) KTRACE(it, 4);
+                if (lane == 0 && warp == 9) KTRACE(it, 5);
                 sm100::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -284,47 +340,67 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         sm100::mbar_arrive(&tmem_empty[buf]);
                 }
             };
-            // Two register buffers: the TMEM loads of chunk j+1 are in flight while chunk j is
-            // folded and stored; the accumulators are released as soon as the last load lands,
-            // so the next tile's MMAs overlap the last chunk's fold.
-            const int nch = (BN / 16 - part + kParts - 1) / kParts;  // chunks c0 = 16 (part + j kParts)
+            auto fold = [&](const uint32_t (&raw)[C::NACC][16], uint32_t (&res)[16]) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    uint32_t a[C::NACC];
+#pragma unroll
+                    for (int s = 0; s < C::NACC; ++s) a[s] = raw[s][c];
+                    res[c] = fold_acc<S>(a, m, args.w);
+                }
+            };
 #if FSYRK_EPI_EXPERIMENT == 2  // timing experiment: no epilogue at all
             release();
             continue;
 #endif
+            const bool staged = C::TSTORE && g.tma_ok;
+            uint32_t v[C::NCW][16];  // this warp's folded outputs (TMA-store path)
             uint32_t ra[C::NACC][16];
-            if constexpr (C::NACC > 3) {  // register budget: one buffer for 5 / 7 accumulators
-#pragma unroll 1
-                for (int j = 0; j < nch; ++j) {
-                    load(ra, 16 * (part + j * kParts));
-                    ready(ra);
-                    if (j + 1 == nch) release();
-#if FSYRK_EPI_EXPERIMENT != 1
-                    emit(ra, 16 * (part + j * kParts));
-#endif
+            if constexpr (SplitFold<S>::ok) {
+                // Only a cheap partial fold (one 32-bit word per output) runs while the tile's
+                // accumulators hold TMEM; the final reduction and the stores overlap the next
+                // tile's MMAs.  The short form needs accumulators < 2^26 (K <= 2048).
+                const bool short_k = g.k_blocks * BK <= 2048;
+#pragma unroll
+                for (int j = 0; j < C::NCW; ++j) {
+                    if (j < nch) {
+                        load(ra, col_of(j));
+                        ready(ra);
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            uint32_t a[C::NACC];
+#pragma unroll
+                            for (int s = 0; s < C::NACC; ++s) a[s] = ra[s][c];
+                            v[j][c] = short_k ? SplitFold<S>::partial_short(a) : SplitFold<S>::partial(a);
+                        }
+                    }
                 }
-                continue;
-            }
-            uint32_t rb[C::NACC][16];
-            load(ra, 16 * part);
-#pragma unroll 1
-            for (int j = 0; j < nch; j += 2) {
-                ready(ra);
-                if (j + 1 < nch) load(rb, 16 * (part + (j + 1) * kParts));
-                else release();
-#if FSYRK_EPI_EXPERIMENT != 1
-                emit(ra, 16 * (part + j * kParts));
-#endif
-                if (j + 1 < nch) {
-                    ready(rb);
-                    if (j + 2 < nch) load(ra, 16 * (part + (j + 2) * kParts));
-                    else release();
-#if FSYRK_EPI_EXPERIMENT != 1
-                    emit(rb, 16 * (part + (j + 1) * kParts));
-#endif
+                release();
+#pragma unroll
+                for (int j = 0; j < C::NCW; ++j) {
+                    if (j < nch) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) v[j][c] = SplitFold<S>::final(v[j][c]);
+                        if (staged) stage_store(v[j], j);
+                        else store_direct(v[j], col_of(j));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < C::NCW; ++j) {
+                    if (j < nch) {
+                        load(ra, col_of(j));
+                        ready(ra);
+                        if (j + 1 == nch) release();
+                        fold(ra, v[j]);
+                        if (staged) stage_store(v[j], j);
+                        else store_direct(v[j], col_of(j));
+                    }
                 }
             }
+            if (lane == 0 && warp == 2) KTRACE(it, 6);
         }
+        if (stores_pending && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     sm100::tc_fence_before();
     __syncthreads();

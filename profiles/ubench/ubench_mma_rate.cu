@@ -33,8 +33,8 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int N, int BK, int NACC, bool PAIR>
-__global__ void __launch_bounds__(128, 1) mma_rate(int reps, unsigned long long* cycles) {
+template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512>
+__global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cycles) {
     constexpr int BROWS = PAIR ? N / 2 : N;  // B rows held by this CTA
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -47,11 +47,13 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int reps, unsigned long long*
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         if (PAIR)
-            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sm100::smem_u32(slot))
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(slot)), "n"(TCOLS)
                          : "memory");
-        else
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sm100::smem_u32(slot))
+        else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(slot)), "n"(TCOLS)
                          : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     if (threadIdx.x == 32) {
         sm100::mbar_init(bar, 1);
@@ -106,20 +108,19 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int reps, unsigned long long*
     if (PAIR) cluster_sync();
     if (warp == 0) {
         if (PAIR) {
-            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
         } else {
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
         }
     }
 }
 
-template <int N, int BK, int NACC, bool PAIR>
+template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512>
 void run(int grid) {
     constexpr int BROWS = PAIR ? N / 2 : N;
     const int smem = 1024 + 128 * BK + ((BROWS * BK + 1023) / 1024) * 1024 + 64;
-    auto k = mma_rate<N, BK, NACC, PAIR>;
+    auto k = mma_rate<N, BK, NACC, PAIR, TCOLS>;
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     unsigned long long* d;
     CK(cudaMalloc(&d, grid * sizeof(unsigned long long)));
@@ -148,14 +149,19 @@ void run(int grid) {
         }
     const double cyc = sum / cnt / (reps * (BK / 32));
     const double macs_per_sm = (double)(PAIR ? 256 : 128) * N * 32 / (PAIR ? 2 : 1);
-    printf("N=%3d BK=%3d NACC=%d %-5s grid=%3d : %7.1f cyc/MMA  %7.0f MAC/clk/SM  (smem B/MAC %.4f)\n", N, BK, NACC,
-           PAIR ? "pair" : "1cta", grid, cyc, macs_per_sm / cyc,
+    printf("N=%3d BK=%3d NACC=%d %-5s grid=%3d tmem=%3d : %7.1f cyc/MMA  %7.0f MAC/clk per CTA  (smem B/MAC %.4f)\n", N,
+           BK, NACC, PAIR ? "pair" : "1cta", grid, TCOLS, cyc, macs_per_sm / cyc,
            (128.0 + (PAIR ? N / 2.0 : N)) / (128.0 * N));
     free(h);
     CK(cudaFree(d));
 }
 
 int main() {
+    // two CTAs per SM (grid 296, 256 TMEM columns each): does the tensor pipe overlap two issuers?
+    run<80, 64, 3, false, 256>(296);
+    run<80, 64, 3, false, 256>(148);
+    run<64, 128, 3, false, 256>(296);
+    run<128, 64, 1, false, 256>(296);
     for (int grid : {1, 148}) {
         run<64, 128, 1, false>(grid);
         run<80, 64, 3, false>(grid);

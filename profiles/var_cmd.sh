@@ -1,7 +1,6 @@
-# timing variants (FSYRK_B200_LIB=profiles/variants/<v>.so); epi2 = no epilogue (parity fails by design)
-for v in default single; do
+for c in cfg4 cfg3; do
+for v in default notstore default notstore; do
   if [ $v = default ]; then unset FSYRK_B200_LIB; else export FSYRK_B200_LIB=profiles/variants/$v.so; fi
-  for c in cfg2 cfg3 cfg5; do
     echo "$v $c $(python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["parity"], d["roofline"]["frac"], d["roofline"].get("phase_ms"))')"
   done
 done

@@ -34,6 +34,13 @@
 
 namespace fsyrk_b200 {
 
+#ifndef FSYRK_PREP_MINB
+#define FSYRK_PREP_MINB 3  // measured: cfg2 prep 104 -> 99 us, cfg5 289 -> 278 us (profiles/r01/variants.txt)
+#endif
+#ifndef FSYRK_POST_MINB
+#define FSYRK_POST_MINB 6  // measured: cfg2 post 60 -> 55 us, cfg5 2.53 -> 2.13 ms
+#endif
+
 namespace {
 
 __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda, int n, int kin, int kout,
@@ -315,7 +322,7 @@ __device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNo
 // Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
 // Pair form, their 4 partners) per thread; one specialised body per input kind.
 template <int S, bool PAIR>
-__global__ void __launch_bounds__(256) prep_vec_kernel(const PrepArgs args) {
+__global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const PrepArgs args) {
     const PrepNode& nd = args.nodes[blockIdx.z];
     const int ncg = (PAIR ? args.half : args.kh) / 4;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -452,7 +459,7 @@ __global__ void post_kernel(const PostArgs args) {
 }
 
 // Vector variant (h, all ld % 4 == 0): block (8 x 32), thread = 4 columns of one row.
-__global__ void __launch_bounds__(256) post_vec_kernel(const PostArgs args) {
+__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const PostArgs args) {
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
     const PostNode nd = args.nodes[blockIdx.z];

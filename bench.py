@@ -409,6 +409,8 @@ def main():
                 "kernel": "modmm (tcgen05 kind::i8 limb products)", "launches_per_step": nprod,
                 "avg_launch_ms": round(prod_ms / nprod, 4), "peak_source": peak_src,
                 "algorithmic_int8_ops_per_step": int8_ops, "rank": 0,
+                # ncu's int8 tensor peak: 16384 ops/clk/SM x 148 SMs x 1.965 GHz
+                "nominal_peak": 4765.4, "nominal_frac": round(achieved / 4765.4, 4),
                 "phase_ms": {k2: round(v, 4) for k2, v in phase.items()}}
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_reference(args.config, cfg, 1, 1)
     if cpu is not None:

@@ -404,8 +404,13 @@ def main():
         peak_i8 = 2.0 * peaks.get("bf16_tflops", 1590.0)
         peak_src = "2 x measured bf16 (MEASURED_PEAKS.json)"
     achieved = int8_ops / (prod_ms / 1e3) / 1e12 if prod_ms > 0 else 0.0
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(REPO, "profiles", "traffic.json"))).get(args.config)
+    except Exception:  # noqa: BLE001
+        pass
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_i8, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / peak_i8, 4) if peak_i8 else None, "traffic": None,
+                "frac": round(achieved / peak_i8, 4) if peak_i8 else None, "traffic": traffic,
                 "kernel": "modmm (tcgen05 kind::i8 limb products)", "launches_per_step": nprod,
                 "avg_launch_ms": round(prod_ms / nprod, 4), "peak_source": peak_src,
                 "algorithmic_int8_ops_per_step": int8_ops, "rank": 0,

@@ -94,6 +94,14 @@ int fsyrk_b200_skew_orthogonal(uint64_t p, size_t dim, fsyrk_b200_skew* skew);
  * host-side, so callers can build the same inputs as the reference. */
 int fsyrk_b200_random_matrix(uint64_t p, size_t rows, size_t cols, uint64_t seed, uint64_t* out, size_t ld);
 
+/* PrimeField::sum_of_squares(k) (proj/src/fields.cpp:114-123): a^2 + b^2 = k (mod p), odd p.
+ * Host-only; used by the skew construction and the CLI's `sos` command. */
+int fsyrk_b200_sum_of_squares(uint64_t p, uint64_t k, uint64_t* a, uint64_t* b);
+
+/* nrsyf(f, alpha, beta) (proj/include/fsyrk/skew.hpp:180-194): y = [[a, b], [c, d]] with
+ * Y * Y^T = diag(alpha, beta) for two non-residues (FSYRK_B200_ENONRES otherwise).  Host-only. */
+int fsyrk_b200_nrsyf(uint64_t p, uint64_t alpha, uint64_t beta, uint64_t y[4]);
+
 /* ---------------------------------------------------------------- host API */
 
 /* syrk_fast_into(f, a, c, plan, ops) (include/fsyrk/fast_syrk.hpp:274-282):

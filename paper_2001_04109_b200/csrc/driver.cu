@@ -1300,6 +1300,27 @@ int fsyrk_b200_make_syrk_plan(uint64_t p, fsyrk_b200_policy policy, int mirror_o
     });
 }
 
+int fsyrk_b200_sum_of_squares(uint64_t p, uint64_t k, uint64_t* a, uint64_t* b) {
+    return guarded([&] {
+        validate_field(p);
+        if (p == 2) fail(FSYRK_B200_EDOMAIN, "sum-of-squares decomposition requires odd p");
+        auto ab = host::Field{p}.sum_of_squares(k % p);
+        if (a) *a = ab.first;
+        if (b) *b = ab.second;
+    });
+}
+
+int fsyrk_b200_nrsyf(uint64_t p, uint64_t alpha, uint64_t beta, uint64_t y[4]) {
+    return guarded([&] {
+        validate_field(p);
+        if (p == 2) fail(FSYRK_B200_EDOMAIN, "nrsyf requires an odd prime");
+        std::array<uint64_t, 4> v;
+        if (!host::nrsyf(host::Field{p}, alpha % p, beta % p, v))
+            fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
+        if (y) std::copy(v.begin(), v.end(), y);
+    });
+}
+
 int fsyrk_b200_random_matrix(uint64_t p, size_t rows, size_t cols, uint64_t seed, uint64_t* out, size_t ld) {
     return guarded([&] {
         validate_field(p);

@@ -92,7 +92,7 @@ EXPORTS = (
     "fsyrk_b200_release_cache", "fsyrk_b200_last_launch_count", "fsyrk_b200_last_plan_json",
     "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
     "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
-    "fsyrk_b200_last_transfer_bytes",
+    "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
 )
 
 
@@ -139,6 +139,8 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    L.fsyrk_b200_sum_of_squares.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p]
+    L.fsyrk_b200_nrsyf.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
     L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     L.fsyrk_b200_last_phase_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.fsyrk_b200_level_blocks.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
@@ -250,6 +252,20 @@ class SyrkPlan:
     policy: RecursionPolicy = field(default_factory=RecursionPolicy)
     skew: Optional[SkewOrthogonal] = None
     mirror_output: bool = False
+
+
+def sum_of_squares(f: PrimeField, k: int):
+    """(a, b) with a^2 + b^2 = k mod p (fields.cpp:114-123)."""
+    a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(lib().fsyrk_b200_sum_of_squares(f.p, int(k) % f.p, ctypes.byref(a), ctypes.byref(b)))
+    return int(a.value), int(b.value)
+
+
+def nrsyf(f: PrimeField, alpha: int, beta: int):
+    """[a, b, c, d] with [[a, b], [c, d]] [[a, b], [c, d]]^T = diag(alpha, beta) (skew.hpp:180-194)."""
+    y = (ctypes.c_uint64 * 4)()
+    _check(lib().fsyrk_b200_nrsyf(f.p, int(alpha) % f.p, int(beta) % f.p, y))
+    return [int(v) for v in y]
 
 
 def skew_orthogonal(f: PrimeField, dim: int) -> SkewOrthogonal:

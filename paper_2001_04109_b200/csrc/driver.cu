@@ -302,6 +302,7 @@ struct Plan {
     uint32_t* root_in = nullptr;
     size_t off_root_in = 0;
     ColMap* dev_colmap = nullptr;
+    std::vector<ColMap> colmap_uploaded;  // what dev_colmap holds (repeated calls skip the upload)
     size_t off_colmap = 0;
     uint64_t tensor_macs = 0;  // modular MACs issued on the tensor cores
     uint64_t int8_macs = 0;
@@ -1202,10 +1203,18 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     const int kbar = xf ? (int)xf->map.size() : (int)k;
     if (nranks > 1 && mirror) fail(FSYRK_B200_EINVAL, "mirror_output needs the whole C (not available per rank)");
     Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, rank, nranks);
-    if (xf)
-        ck(cudaMemcpyAsync(plan->dev_colmap, xf->map.data(), xf->map.size() * sizeof(ColMap), cudaMemcpyHostToDevice,
-                           s),
-           "upload colmap");
+    if (xf) {
+        auto same = [](const std::vector<ColMap>& x, const std::vector<ColMap>& y) {
+            return x.size() == y.size() && std::memcmp(x.data(), y.data(), x.size() * sizeof(ColMap)) == 0;
+        };
+        if (!same(xf->map, plan->colmap_uploaded)) {
+            // pageable source: the copy is staged before returning, so the host vector may change after
+            ck(cudaMemcpyAsync(plan->dev_colmap, xf->map.data(), xf->map.size() * sizeof(ColMap),
+                               cudaMemcpyHostToDevice, s),
+               "upload colmap");
+            plan->colmap_uploaded = xf->map;
+        }
+    }
     plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
     fill_ops(ops, plan);
 }

@@ -31,6 +31,7 @@
 #include <cstdint>
 
 #include "elementwise.cuh"
+#include "pdl.cuh"
 
 namespace fsyrk_b200 {
 
@@ -46,6 +47,8 @@ namespace {
 __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda, int n, int kin, int kout,
                                   const ColMap* __restrict__ map, ModP m, uint32_t* __restrict__ out,
                                   long long ldo) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     (void)kin;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= kout) return;
@@ -127,6 +130,8 @@ __device__ __forceinline__ void put_planes4(int8_t* base, long long plane, long 
 template <int L, bool VEC>
 __global__ void split_planes_kernel(InView in, const uint64_t* a64, long long ld64, int rows, int k, ModP m,
                                     int8_t* __restrict__ planes, long long plane, long long rs) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const Src src = make_src(in, a64, ld64);
     constexpr int V = VEC ? 4 : 1;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * V;
@@ -151,6 +156,8 @@ __device__ __forceinline__ void pair_y(uint32_t u, uint32_t v, MulConst ca, MulC
 // Scalar variant: one thread per (row i, column j) or, in Pair form, per column pair (j, j + half).
 template <int L>
 __global__ void prep_kernel(const PrepArgs args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const PrepNode nd = args.nodes[blockIdx.z];
     const ModP m = args.m;
     const uint32_t p = m.p;
@@ -323,6 +330,8 @@ __device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNo
 // Pair form, their 4 partners) per thread; one specialised body per input kind.
 template <int S, bool PAIR>
 __global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const PrepArgs args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const PrepNode& nd = args.nodes[blockIdx.z];
     const int ncg = (PAIR ? args.half : args.kh) / 4;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -412,6 +421,8 @@ __device__ __forceinline__ PostOut make_out(const PostArgs& a, const PostNode& n
 
 // Block (32 x 8) per tile pair (I >= J) of one node.
 __global__ void post_kernel(const PostArgs args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];  // Low(P1 + P5), tile (I, J)
     __shared__ uint32_t sT[TS][TS + 1];  // P4 tile (J, I)
     const PostNode nd = args.nodes[blockIdx.z];
@@ -460,6 +471,8 @@ __global__ void post_kernel(const PostArgs args) {
 
 // Vector variant (h, all ld % 4 == 0): block (8 x 32), thread = 4 columns of one row.
 __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const PostArgs args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
     const PostNode nd = args.nodes[blockIdx.z];
@@ -527,6 +540,8 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const Po
 }
 
 __global__ void add_lower_kernel(const AddNode* __restrict__ nodes, int n, uint32_t p) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const AddNode nd = nodes[blockIdx.z];
     const int i = blockIdx.y;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i && j < n; j += gridDim.x * blockDim.x)
@@ -535,6 +550,8 @@ __global__ void add_lower_kernel(const AddNode* __restrict__ nodes, int n, uint3
 
 __global__ void finalize_kernel(const uint32_t* __restrict__ x, long long ldx, int n, uint64_t* __restrict__ c,
                                 long long ldc, ModP m, uint32_t alpha, uint32_t beta) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const int i = blockIdx.y;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i && j < n; j += gridDim.x * blockDim.x) {
         uint32_t v = x ? x[(long long)i * ldx + j] : 0;
@@ -549,6 +566,8 @@ __global__ void finalize_kernel(const uint32_t* __restrict__ x, long long ldx, i
 
 // C[j][i] <- C[i][j] for i > j, 32 x 32 tiles through shared memory.
 __global__ void mirror_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     __shared__ uint64_t s[TS][TS + 1];
     int I, J;
     tri_decode(blockIdx.x, I, J);
@@ -566,6 +585,8 @@ __global__ void mirror_kernel(uint64_t* __restrict__ c, long long ldc, int n) {
 
 // strict upper triangle of row i, up to the end of i's row block of `rb` rows (rb = 0: whole row)
 __global__ void zero_upper_kernel(uint64_t* __restrict__ c, long long ldc, int n, int rb) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const int i = blockIdx.y;
     const int end = rb > 0 ? min(n, (i / rb + 1) * rb) : n;
     for (int j = i + 1 + blockIdx.x * blockDim.x + threadIdx.x; j < end; j += gridDim.x * blockDim.x)
@@ -574,6 +595,8 @@ __global__ void zero_upper_kernel(uint64_t* __restrict__ c, long long ldc, int n
 
 __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ x, long long ldx, int rows, int cols,
                                   uint64_t* __restrict__ out, long long ldo) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
     const long long total = (long long)rows * cols;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -605,13 +628,13 @@ cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
         const int ncg = (a.pair ? a.half : a.kh) / 4;
         dim3 block(32, 8);
         dim3 grid((ncg + 31) / 32, (a.h + 7) / 8, a.nnodes);
-        if (a.pair) prep_vec_kernel<L, true><<<grid, block, 0, s>>>(a);
-        else prep_vec_kernel<L, false><<<grid, block, 0, s>>>(a);
+        if (a.pair) return launch_pdl(prep_vec_kernel<L, true>, grid, block, 0, s, a);
+        return launch_pdl(prep_vec_kernel<L, false>, grid, block, 0, s, a);
     } else {
         const int ncw = a.pair ? a.half : a.kw;
         dim3 block(32, 8);
         dim3 grid((ncw + 31) / 32, (a.h + 7) / 8, a.nnodes);
-        prep_kernel<L><<<grid, block, 0, s>>>(a);
+        return launch_pdl(prep_kernel<L>, grid, block, 0, s, a);
     }
     return cudaGetLastError();
 }
@@ -622,8 +645,7 @@ cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, 
                               uint32_t p, uint32_t* out, long long ldo, cudaStream_t s) {
     if ((long long)n * kout == 0) return cudaSuccess;
     const dim3 grid((kout + 255) / 256, rows_grid(n, (kout + 255) / 256));
-    convert_in_kernel<<<grid, 256, 0, s>>>(a, lda, n, kin, kout, map, make_modp(p), out, ldo);
-    return cudaGetLastError();
+    return launch_pdl(convert_in_kernel, grid, dim3(256), 0, s, a, lda, n, kin, kout, map, make_modp(p), out, ldo);
 }
 
 cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, long long ld64, int rows, int k,
@@ -672,46 +694,40 @@ cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     dim3 grid(args.pairs ? args.npairs : T * (T + 1) / 2, 1, args.nnodes);
     if (grid.x == 0) return cudaSuccess;
     // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
-    if (args.h % 4 == 0) post_vec_kernel<<<grid, dim3(8, 32), 0, s>>>(args);
-    else post_kernel<<<grid, dim3(32, 8), 0, s>>>(args);
-    return cudaGetLastError();
+    if (args.h % 4 == 0) return launch_pdl(post_vec_kernel, grid, dim3(8, 32), 0, s, args);
+    return launch_pdl(post_kernel, grid, dim3(32, 8), 0, s, args);
 }
 
 cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p, cudaStream_t s) {
     if (n == 0 || nnodes == 0) return cudaSuccess;
     dim3 grid((n + 255) / 256, n, nnodes);
-    add_lower_kernel<<<grid, 256, 0, s>>>(nodes, n, p);
-    return cudaGetLastError();
+    return launch_pdl(add_lower_kernel, grid, dim3(256), 0, s, nodes, n, p);
 }
 
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
                             uint32_t alpha, uint32_t beta, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     dim3 grid((n + 255) / 256, n);
-    finalize_kernel<<<grid, 256, 0, s>>>(x, ldx, n, c, ldc, m, alpha, beta);
-    return cudaGetLastError();
+    return launch_pdl(finalize_kernel, grid, dim3(256), 0, s, x, ldx, n, c, ldc, m, alpha, beta);
 }
 
 cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const int T = (n + TS - 1) / TS;
-    mirror_kernel<<<T * (T + 1) / 2, dim3(32, 8), 0, s>>>(c, ldc, n);
-    return cudaGetLastError();
+    return launch_pdl(mirror_kernel, dim3(T * (T + 1) / 2), dim3(32, 8), 0, s, c, ldc, n);
 }
 
 cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const int w = rb > 0 ? (rb < n ? rb : n) : n;
-    zero_upper_kernel<<<dim3((w + 255) / 256, n), 256, 0, s>>>(c, ldc, n, rb);
-    return cudaGetLastError();
+    return launch_pdl(zero_upper_kernel, dim3((w + 255) / 256, n), dim3(256), 0, s, c, ldc, n, rb);
 }
 
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s) {
     const long long total = (long long)rows * cols;
     if (total == 0) return cudaSuccess;
-    u32_to_u64_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, ldx, rows, cols, out, ldo);
-    return cudaGetLastError();
+    return launch_pdl(u32_to_u64_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ldx, rows, cols, out, ldo);
 }
 
 }  // namespace fsyrk_b200

@@ -25,6 +25,7 @@
 #include <cstdint>
 
 #include "modp.cuh"
+#include "pdl.cuh"
 #include "schemes.cuh"
 #include "sm100.cuh"
 #include "tc_modmm.h"
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     if constexpr (PAIR) sm100::cluster_sync();  // peer barriers initialised before any remote arrive
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // setup above overlaps the previous kernel's tail; operands are ready from here
 
     if (warp == 0) {
         if (lane == 0) {
@@ -402,6 +404,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         }
         if (stores_pending && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
+    pdl_trigger_mm();  // this CTA's work is issued: the next kernel of the call may begin launching
     sm100::tc_fence_before();
     __syncthreads();
     if constexpr (PAIR) sm100::cluster_sync();  // no CTA leaves while its peer may still signal it
@@ -426,8 +429,10 @@ cudaLaunchConfig_t launch_config(int grid, cudaStream_t stream, cudaLaunchAttrib
     attr[0].val.clusterDim.x = C::PAIR ? 2 : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     return cfg;
 }
 
@@ -442,7 +447,7 @@ cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
         attr_set = true;
     }
     if (args.ntiles == 0) return cudaSuccess;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);
     return cudaLaunchKernelEx(&cfg, kern, args);
 }
@@ -456,7 +461,7 @@ int grid_for(int nsm) {
     } else {
         auto kern = modmm_kernel<S, EPI>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         cudaLaunchConfig_t cfg = launch_config<S, EPI>(nsm, 0, attr);
         int clusters = 0;
         if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {

@@ -26,6 +26,7 @@
 #include <random>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -1097,33 +1098,67 @@ ColMap col_combine(const host::Field& f, const ColMap& u, uint64_t cu, const Col
 // initial column map `map` (identity for syrkd, syrkbd's block fold otherwise): residue
 // entries scale their column by sqrt(d), non-residues are consumed in pairs through their
 // nrsyf factor, an odd count appends a zero column carrying a copy of the first one.
+// fn(i) for i in [0, n): O(log p) field work per index (Legendre symbols, square roots,
+// nrsyf factors), split over host threads when n is large enough to pay for them.
+template <class Fn>
+void parallel_for(size_t n, Fn fn) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = n < 256 ? 1 : std::min<size_t>({hw, 16, n / 128});
+    if (nt <= 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (size_t i = t * n / nt; i < (t + 1) * n / nt; ++i) fn(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
 void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& map) {
     host::Field f{p};
     if (p == 2) fail(FSYRK_B200_EINVAL, "syrkd requires an odd prime field");
     const size_t k = dbar.size();
-    std::vector<size_t> nr;
     for (auto& v : dbar) v %= p;
+    std::vector<int> leg(k);
+    parallel_for(k, [&](size_t j) { leg[j] = f.legendre(dbar[j]); });
+    std::vector<size_t> nr;
     for (size_t j = 0; j < k; ++j)
-        if (f.legendre(dbar[j]) == -1) nr.push_back(j);
+        if (leg[j] == -1) nr.push_back(j);
     if (nr.size() % 2 == 1) {
         dbar.push_back(dbar[nr.front()]);
+        leg.push_back(-1);
         nr.push_back(k);
         map.push_back(ColMap{{-1, -1, -1, -1}, {0, 0, 0, 0}});  // the appended zero column
     }
-    for (size_t j = 0; j < dbar.size(); ++j)
-        if (f.legendre(dbar[j]) >= 0) {
-            const uint64_t sq = f.sqrt(dbar[j]);
-            for (int q = 0; q < 4; ++q)
-                if (map[j].src[q] >= 0) map[j].c[q] = (uint32_t)f.mul(map[j].c[q], sq);
-        }
-    for (size_t t = 0; t + 1 < nr.size(); t += 2) {
-        const size_t i = nr[t], j = nr[t + 1];
+    parallel_for(dbar.size(), [&](size_t j) {
+        if (leg[j] < 0) return;
+        const uint64_t sq = f.sqrt(dbar[j]);
+        for (int q = 0; q < 4; ++q)
+            if (map[j].src[q] >= 0) map[j].c[q] = (uint32_t)f.mul(map[j].c[q], sq);
+    });
+    const size_t npairs = nr.size() / 2;
+    std::vector<char> bad(npairs, 0);
+    parallel_for(npairs, [&](size_t t) {
+        const size_t i = nr[2 * t], j = nr[2 * t + 1];
         std::array<uint64_t, 4> y;
-        if (!host::nrsyf(f, dbar[i], dbar[j], y)) fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
+        if (!host::nrsyf(f, dbar[i], dbar[j], y)) {
+            bad[t] = 1;
+            return;
+        }
         // (u, v) -> (y0 u + y2 v, y1 u + y3 v)   (scaled_syrk.hpp:93-98)
-        const ColMap u = map[i], v = map[j];
-        map[i] = col_combine(f, u, y[0], v, y[2]);
-        map[j] = col_combine(f, u, y[1], v, y[3]);
+        try {  // no exception may leave a worker thread
+            const ColMap u = map[i], v = map[j];
+            map[i] = col_combine(f, u, y[0], v, y[2]);
+            map[j] = col_combine(f, u, y[1], v, y[3]);
+        } catch (...) {
+            bad[t] = 2;
+        }
+    });
+    for (char b : bad) {
+        if (b == 1) fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
+        if (b == 2) fail(FSYRK_B200_EINVAL, "column transform exceeds 4 source columns");
     }
 }
 

@@ -24,7 +24,15 @@ inline bool is_prime(uint64_t n) {
 
 struct Field {
     uint64_t p;
-    uint64_t mul(uint64_t a, uint64_t b) const { return (a * b) % p; }
+    uint64_t mu;  // floor(2^64 / p): Barrett reduction of products < 2^62 (p < 2^31)
+    Field(uint64_t p_) : p(p_), mu(p_ > 1 ? (uint64_t)((((unsigned __int128)1) << 64) / p_) : 0) {}
+    uint64_t mul(uint64_t a, uint64_t b) const {
+        const uint64_t x = a * b;  // a, b < p < 2^31
+        if (p < 2) return 0;
+        const uint64_t q = (uint64_t)(((unsigned __int128)x * mu) >> 64);  // floor(x / p) - {0, 1}
+        const uint64_t r = x - q * p;
+        return r >= p ? r - p : r;
+    }
     uint64_t add(uint64_t a, uint64_t b) const { uint64_t s = a + b; return s >= p ? s - p : s; }
     uint64_t sub(uint64_t a, uint64_t b) const { return a >= b ? a - b : a + p - b; }
     uint64_t neg(uint64_t a) const { return a == 0 ? 0 : p - a; }

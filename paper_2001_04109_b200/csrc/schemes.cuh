@@ -175,9 +175,9 @@ __device__ __forceinline__ uint32_t fold_acc(const uint32_t* a, const ModP& m, c
     }
 }
 
-// Two-stage fold for the epilogue: partial() maps the accumulators to one 32-bit word
-// congruent to the result (cheap; runs while the tile holds TMEM), final() reduces it
-// to [0, p) after the accumulators are released.
+// Two-stage fold for the epilogue: partial() maps the accumulators to a compact value V
+// congruent to the result (cheap; runs while the tile holds TMEM), final() reduces it to
+// [0, p) after the accumulators are released.
 template <int S>
 struct SplitFold {
     static constexpr bool ok = false;
@@ -185,19 +185,29 @@ struct SplitFold {
 template <>
 struct SplitFold<SCHEME_M17> {
     static constexpr bool ok = true;
+    using V = uint32_t;
     // f(x) = (x mod 2^17) + (x >> 17) = x (mod 2^17 - 1); for x < 2^32: f(x) < 2^17 + 2^15
     __device__ __forceinline__ static uint32_t f(uint32_t x) { return (x & 0x1FFFFu) + (x >> 17); }
-    __device__ __forceinline__ static uint32_t partial(const uint32_t* a) {  // any a < 2^31
-        return f(a[0]) + (f(a[1]) << 6) + (f(a[2]) << 12);  // < 2^30
+    // short_k: accumulators < 2^26 (K <= 2048), so a1 << 6 still fits 32 bits
+    __device__ __forceinline__ static V partial(const uint32_t* a, bool short_k) {
+        return short_k ? a[0] + f(a[1] << 6) + (f(a[2]) << 12)      // < 2^26 + 2^18 + 2^30
+                       : f(a[0]) + (f(a[1]) << 6) + (f(a[2]) << 12);  // any a < 2^31: < 2^30
     }
-    // accumulators < 2^26 (K <= 2048): a1 << 6 still fits 32 bits
-    __device__ __forceinline__ static uint32_t partial_short(const uint32_t* a) {
-        return a[0] + f(a[1] << 6) + (f(a[2]) << 12);  // < 2^26 + 2^18 + 2^30
-    }
-    __device__ __forceinline__ static uint32_t final(uint32_t v) {
+    __device__ __forceinline__ static uint32_t final(V v, const ModP&) {
         const uint32_t r = f(v);  // < 2^17 + 2^15 < 2p
         return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
     }
+};
+// LIMB2 (p <= 2^16): the exact integer  sum_x r_x r_y = a0 + 2^8 a1 + 2^16 a2  of the balanced
+// representatives, |.| <= K 2^30 < 2^62 within the scheme's K bound; reduced mod p afterwards.
+template <>
+struct SplitFold<SCHEME_LIMB2> {
+    static constexpr bool ok = true;
+    using V = int64_t;
+    __device__ __forceinline__ static V partial(const uint32_t* a, bool) {
+        return (int64_t)(int32_t)a[0] + (int64_t)(int32_t)a[1] * 256 + (int64_t)(int32_t)a[2] * 65536;
+    }
+    __device__ __forceinline__ static uint32_t final(V v, const ModP& m) { return mod_s64(v, m); }
 };
 
 }  // namespace fsyrk_b200

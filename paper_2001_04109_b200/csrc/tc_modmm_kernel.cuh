@@ -36,6 +36,9 @@ namespace tc {
 #ifndef FSYRK_EPI_EXPERIMENT
 #define FSYRK_EPI_EXPERIMENT 0
 #endif
+#ifndef FSYRK_TSTORE_ALL
+#define FSYRK_TSTORE_ALL 0
+#endif
 #ifndef FSYRK_NO_TSTORE
 #define FSYRK_NO_TSTORE 0
 #endif
@@ -88,7 +91,7 @@ struct Cfg {
     // 1024-aligned (__align__ on the extern array, checked at entry)
     // TMA stores: measured faster for the Mersenne schemes (cfg2 products 185 -> 178 us, cfg5
     // 3.18 -> 2.89 ms), neutral to slightly slower for LIMB2 (cfg3 251 -> 254 us)
-    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (S == SCHEME_M17 || S == SCHEME_M31) &&
+    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (S == SCHEME_M17 || S == SCHEME_M31 || FSYRK_TSTORE_ALL) &&
                                    STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES <= 232448;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (TSTORE ? OUT_BYTES : 0) + BAR_BYTES;
     static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1
@@ -356,13 +359,14 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             continue;
 #endif
             const bool staged = C::TSTORE && g.tma_ok;
-            uint32_t v[C::NCW][16];  // this warp's folded outputs (TMA-store path)
             uint32_t ra[C::NACC][16];
             if constexpr (SplitFold<S>::ok) {
-                // Only a cheap partial fold (one 32-bit word per output) runs while the tile's
+                // Only a cheap partial fold (one compact value per output) runs while the tile's
                 // accumulators hold TMEM; the final reduction and the stores overlap the next
-                // tile's MMAs.  The short form needs accumulators < 2^26 (K <= 2048).
+                // tile's MMAs.
+                using V = typename SplitFold<S>::V;
                 const bool short_k = g.k_blocks * BK <= 2048;
+                V v[C::NCW][16];
 #pragma unroll
                 for (int j = 0; j < C::NCW; ++j) {
                     if (j < nch) {
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                             uint32_t a[C::NACC];
 #pragma unroll
                             for (int s = 0; s < C::NACC; ++s) a[s] = ra[s][c];
-                            v[j][c] = short_k ? SplitFold<S>::partial_short(a) : SplitFold<S>::partial(a);
+                            v[j][c] = SplitFold<S>::partial(a, short_k);
                         }
                     }
                 }
@@ -381,13 +385,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
 #pragma unroll
                 for (int j = 0; j < C::NCW; ++j) {
                     if (j < nch) {
+                        uint32_t res[16];
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) v[j][c] = SplitFold<S>::final(v[j][c]);
-                        if (staged) stage_store(v[j], j);
-                        else store_direct(v[j], col_of(j));
+                        for (int c = 0; c < 16; ++c) res[c] = SplitFold<S>::final(v[j][c], m);
+                        if (staged) stage_store(res, j);
+                        else store_direct(res, col_of(j));
                     }
                 }
             } else {
+                uint32_t v[C::NCW][16];  // this warp's folded outputs
 #pragma unroll
                 for (int j = 0; j < C::NCW; ++j) {
                     if (j < nch) {

@@ -141,6 +141,17 @@ int fsyrk_b200_syrkbd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, s
                       const fsyrk_b200_block* blocks, size_t nblocks, uint64_t beta, uint64_t* c, size_t ldc,
                       fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
 
+/* Quadratic extension F_{p^2} = F_p[x] / (x^2 - ns), ns the least quadratic non-residue
+ * (fsyrk::QuadExtField, include/fsyrk/fields.hpp:142-212).  Matrices hold (a, b) uint64 pairs
+ * (QuadExtElement, fields.hpp:142-146) row-major; lda / ldc count pairs.
+ * herk_fast_into (include/fsyrk/fast_syrk.hpp:307-313): Low(C) <- Low(A * conj(A)^T);
+ * the fp2 syrk_fast_into (fast_syrk.hpp:274-282 over QuadExtField): Low(C) <- Low(A * A^T).
+ * mirror_output fills the upper triangle with the (conjugate) transpose; otherwise it is zero. */
+int fsyrk_b200_herk_fast_into(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c, size_t ldc,
+                              fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
+int fsyrk_b200_syrk_fast_into_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c,
+                                  size_t ldc, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
+
 /* -------------------------------------------------------------- device API */
 
 /* Same operations on device-resident uint64 matrices (pointers from

@@ -119,6 +119,32 @@ inline fsyrk::Matrix<Field> syrkbd(const Field& f, CView a, const fsyrk::BlockDi
     return c;
 }
 
+// replaces herk_fast_into / herk_fast (include/fsyrk/fast_syrk.hpp:305-320) over QuadExtField:
+// Low(C) <- Low(A * conj(A)^T).  (The reference's versions are non-template inline functions,
+// so there is no FSYRK_B200_OVERRIDE form; call these by name.)
+inline void herk_fast_into(const fsyrk::QuadExtField& f, fsyrk::ConstMatrixView<fsyrk::QuadExtField> a,
+                           fsyrk::MatrixView<fsyrk::QuadExtField> c, const fsyrk::SyrkPlan<fsyrk::QuadExtField>& plan,
+                           fsyrk::OpCount& ops) {
+    if (!plan.conjugate) throw std::invalid_argument("herk_fast: plan must be built by make_herk_plan");
+    plan.policy.validate();
+    if (c.rows != c.cols || c.rows != a.rows) throw fsyrk::DimensionError("syrk_fast: dimension mismatch");
+    static_assert(sizeof(fsyrk::QuadExtElement) == 2 * sizeof(uint64_t), "QuadExtElement is an (a, b) pair");
+    fsyrk_b200_opcount oc{0, 0};
+    detail::check(fsyrk_b200_herk_fast_into(f.characteristic(), reinterpret_cast<const uint64_t*>(a.data), a.rows,
+                                            a.cols, a.stride, reinterpret_cast<uint64_t*>(c.data), c.stride,
+                                            detail::policy(plan.policy), plan.mirror_output ? 1 : 0, &oc));
+    detail::add_ops(ops, oc);
+}
+
+inline fsyrk::Matrix<fsyrk::QuadExtField> herk_fast(const fsyrk::QuadExtField& f,
+                                                    fsyrk::ConstMatrixView<fsyrk::QuadExtField> a,
+                                                    const fsyrk::SyrkPlan<fsyrk::QuadExtField>& plan,
+                                                    fsyrk::OpCount& ops) {
+    fsyrk::Matrix<fsyrk::QuadExtField> c(a.rows, a.rows, f.zero());
+    fsyrk_b200::herk_fast_into(f, a, c.view(), plan, ops);
+    return c;
+}
+
 // LDL^T Schur update in one call: Low(C) <- Low(C - A Diag(d) A^T) (no reference analogue: the
 // reference composes syrkd and an elementwise subtraction)
 inline void schur_update(const Field& f, CView a, const std::vector<Field::Element>& d, View c, const Plan& plan,

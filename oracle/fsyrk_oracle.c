@@ -280,6 +280,32 @@ void orc_abat_classical(uint64_t p, const uint64_t* A, size_t n, size_t k, size_
     free(AB);
 }
 
+/* Classical product over F_{p^2} = F_p[x] / (x^2 - ns) (QuadExtField, fields.hpp:148-176):
+ * C[i][j] = sum_l A[i][l] * (conj ? conj(A[j][l]) : A[j][l]) for j <= i (lower triangle; the
+ * reference's syrk_classical with conjugate, matrix.hpp:369-407).  Elements are (a, b) pairs. */
+void orc_fp2_syrk_classical(uint64_t p, uint64_t ns, const uint64_t* A, size_t n, size_t k, int conj, uint64_t* C) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (long long ii = 0; ii < (long long)n; ++ii) {
+        const size_t i = (size_t)ii;
+        for (size_t j = 0; j <= i; ++j) {
+            u128 re = 0, im = 0, nsbb = 0, neg = 0;
+            for (size_t l = 0; l < k; ++l) {
+                const uint64_t a = A[2 * (i * k + l)], b = A[2 * (i * k + l) + 1];
+                const uint64_t c = A[2 * (j * k + l)], d0 = A[2 * (j * k + l) + 1];
+                const uint64_t d = conj ? (d0 ? p - d0 : 0) : d0;
+                /* (a + bx)(c + dx) = ac + ns bd + (ad + bc) x */
+                re += (u128)a * c;
+                nsbb += (u128)b * d;
+                im += (u128)a * d + (u128)b * c;
+            }
+            (void)neg;
+            const uint64_t bd = (uint64_t)(nsbb % p);
+            C[2 * (i * n + j)] = (uint64_t)((re % p + (u128)bd * ns % p) % p);
+            C[2 * (i * n + j) + 1] = (uint64_t)(im % p);
+        }
+    }
+}
+
 /* ------------------------------------------------- the 5-product recursion */
 typedef struct {
     uint64_t p;

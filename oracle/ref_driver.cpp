@@ -56,7 +56,7 @@ struct Args {
 [[noreturn]] void usage() {
     std::fprintf(stderr,
                  "usage: ref_driver [--p P] [--n N] [--k K] [--seed S] [--threshold T]\n"
-                 "  [--levels L|inf] [--mode plain|acc|schur|classical|syrkbd] [--cseed S] [--abseed S]\n"
+                 "  [--levels L|inf] [--mode plain|acc|schur|classical|syrkbd|herk|syrk2] [--cseed S] [--abseed S]\n"
                  "  [--alpha a --beta b] [--dseed S] [--mirror] [--threads T] [--reps R]\n"
                  "  [--out-a F] [--out-c F] [--out-c0 F] [--out-d F] [--no-digest] [--sample N]\n");
     std::exit(2);
@@ -189,8 +189,32 @@ double run_instance(const PrimeField& f, const Args& g, Instance& in) {
 
 }  // namespace
 
+// F_{p^2} modes (QuadExtField, proj/include/fsyrk/fields.hpp:142-212): "herk" runs
+// herk_fast (make_herk_plan, fast_syrk.hpp:26-29, 305-320), "syrk2" runs syrk_fast over the
+// extension.  Matrices are dumped as (a, b) uint64 pairs; C is the full n x n matrix.
+int main_fp2(const Args& g) {
+    QuadExtField f(g.p);
+    auto a = random_matrix(f, g.n, g.k, g.seed);
+    OpCount ops;
+    Matrix<QuadExtField> c(g.n, g.n, f.zero());
+    if (g.mode == "herk") {
+        auto plan = make_herk_plan(f, RecursionPolicy{g.threshold, g.levels}, g.mirror);
+        herk_fast_into(f, a.view(), c.view(), plan, ops);
+    } else {
+        auto plan = make_syrk_plan(f, RecursionPolicy{g.threshold, g.levels}, g.mirror);
+        syrk_fast_into(f, a.view(), c.view(), plan, ops);
+    }
+    dump(g.out_a, a.data().data(), a.data().size() * sizeof(QuadExtElement));
+    dump(g.out_c, c.data().data(), c.data().size() * sizeof(QuadExtElement));
+    std::printf("{\"p\": %" PRIu64 ", \"n\": %zu, \"k\": %zu, \"mode\": \"%s\", \"seed\": %" PRIu64
+                ", \"non_residue\": %" PRIu64 ", \"alpha\": 1, \"beta\": 0, \"digest\": \"\"}\n",
+                g.p, g.n, g.k, g.mode.c_str(), g.seed, f.non_residue());
+    return 0;
+}
+
 int main(int argc, char** argv) {
     Args g = parse(argc, argv);
+    if (g.mode == "herk" || g.mode == "syrk2") return main_fp2(g);
     PrimeField f(g.p);
     auto y = skew_orthogonal(f, 2);
 

@@ -1226,6 +1226,63 @@ void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
     ops->adds += plan->ew_adds;
 }
 
+// C = A * B^T mod p on the tensor cores for device-resident uint64 A (m x k, lda) and B
+// (n x k, ldb) into uint32 `out` (m x n, ldo): digit split, one grouped product launch.
+// Scratch buffers are call-local (general products outside the recursion are not hot).
+void gemm_nt_dev(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
+                 size_t ldb, uint32_t* out, long long ldo, cudaStream_t s) {
+    const SchemeInfo sch = scheme_for(p);
+    const int L = sch.planes, BN = sch.bn, BK = sch.bk;
+    if (k > modmm_k_limit(sch, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
+    if (m == 0 || n == 0) return;
+    const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
+    const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
+    DevBuf pa, pb, dtiles;
+    pa.ensure((size_t)(mpad * kpad * L));
+    pb.ensure((size_t)(npad * kpad * L));
+    ck(cudaMemsetAsync(pa.ptr, 0, pa.bytes, s), "memset");
+    ck(cudaMemsetAsync(pb.ptr, 0, pb.bytes, s), "memset");
+    if (k > 0) {
+        const InView top{nullptr, 0, 0, 0, 1};
+        ck(launch_split_planes(sch.id, top, a, (long long)lda, (int)m, (int)k, (uint32_t)p,
+                               static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, s),
+           "split A");
+        ck(launch_split_planes(sch.id, top, b, (long long)ldb, (int)n, (int)k, (uint32_t)p,
+                               static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, s),
+           "split B");
+    }
+    std::vector<int4> tiles;
+    for (int tm = 0; tm * sch.bm < (int)m; ++tm)
+        for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
+    dtiles.ensure(tiles.size() * sizeof(int4));
+    ck(cudaMemcpyAsync(dtiles.ptr, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s), "tiles");
+    GroupedArgs args;
+    std::memset(&args, 0, sizeof(args));
+    args.modp = make_modp((uint32_t)p);
+    fill_fold_weights(sch, p, args.w);
+    args.ngroups = 1;
+    args.ntiles = (int)tiles.size();
+    args.tiles = static_cast<int4*>(dtiles.ptr);
+    GroupDesc& g = args.g[0];
+    g.tmA = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128, BK);
+    g.tmB = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, sch.b_box, BK);
+    g.M = (int)m;
+    g.N = (int)n;
+    g.k_blocks = (int)(kpad / BK);
+    g.syrk = 0;
+    g.vec_ok = ldo % 4 == 0;
+    g.a_mult = g.b_mult = 1;
+    g.out = out;
+    g.out_bs = 0;
+    g.ldo = ldo;
+    modmm_set_output_map(g, 1);
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    ck(modmm_launch(sch, args, std::min<int>(modmm_grid(sch, nsm), (int)tiles.size() * (sch.bm / 128)), s), "modmm");
+    ck(cudaStreamSynchronize(s), "sync");  // scratch buffers are released on return
+}
+
 // Core device call: everything resident on the device.
 void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t k, size_t lda, const ColXform* xf,
              uint32_t beta, uint64_t* c_dev, size_t ldc, fsyrk_b200_policy pol, bool mirror, cudaStream_t s,
@@ -1310,6 +1367,66 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     ck(cudaStreamSynchronize(s), "sync");
     g_transfer[0] = h2d;
     g_transfer[1] = d2h;
+}
+
+// Products over F_{p^2} = F_p[x] / (x^2 - ns), ns the least non-residue (the reference's
+// QuadExtField, proj/include/fsyrk/fields.hpp:148-212).  With A = X + x Y:
+//   herk (conj):  A conj(A)^T = (X X^T - ns Y Y^T) + x (Y X^T - X Y^T)
+//   syrk:         A A^T       = (X X^T + ns Y Y^T) + x (Y X^T + X Y^T)
+// The real part is the syrkd of [X | Y] with D = (1, .., 1, -+ns, .., -+ns) on the device path
+// (recursion, digit-plane products); the imaginary part is G +- G^T with G = Y X^T from one
+// tensor-core product.  Exact, so equal to the reference's herk_fast / syrk_fast over F_{p^2}
+// (fast_syrk.hpp:305-320) for any policy.  a, c: (a, b) uint64 pairs, lda / ldc in pairs.
+void run_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c, size_t ldc,
+             fsyrk_b200_policy pol, bool mirror, bool conj, fsyrk_b200_opcount* ops) {
+    validate_field(p);
+    validate_policy(pol);
+    if (p == 2) fail(FSYRK_B200_EINVAL, "QuadExtField requires an odd prime");
+    validate_shapes(n, 2 * k, 2 * lda, 2 * ldc);
+    if (ranges_overlap(a, span_bytes(n, 2 * k, 2 * lda), c, span_bytes(n, 2 * n, 2 * ldc)))
+        fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
+    require_device();
+    if (n == 0) return;
+    host::Field f{p};
+    const uint64_t ns = f.lqnr();
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    const size_t kk = std::max<size_t>(k, 1);
+    DevBuf dA, dX, dY, dR, dG, dC;
+    dA.ensure(n * 2 * kk * 8);
+    dX.ensure(n * kk * 8);
+    dY.ensure(n * kk * 8);
+    dR.ensure(n * n * 8);
+    dG.ensure(n * n * 4);
+    dC.ensure(n * n * 16);
+    cudaStream_t s = 0;
+    auto* A = static_cast<uint64_t*>(dA.ptr);
+    auto* R = static_cast<uint64_t*>(dR.ptr);
+    auto* G = static_cast<uint32_t*>(dG.ptr);
+    if (k == 0) {
+        ck(cudaMemsetAsync(dR.ptr, 0, n * n * 8, s), "memset");
+        ck(cudaMemsetAsync(dG.ptr, 0, n * n * 4, s), "memset");
+    } else {
+        ck(cudaMemcpy2DAsync(A, 2 * k * 8, a, 2 * lda * 8, 2 * k * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+        // real part: columns [a parts | b parts] scaled by (1 | -+ns) through syrkd's diagonal fold
+        ColXform xf;
+        for (size_t j = 0; j < 2 * k; ++j)
+            xf.map.push_back(ColMap{{(int)(j < k ? 2 * j : 2 * (j - k) + 1), -1, -1, -1}, {1, 0, 0, 0}});
+        std::vector<uint64_t> dbar(2 * k, 1);
+        for (size_t j = k; j < 2 * k; ++j) dbar[j] = conj ? p - ns : ns;
+        fold_diagonal(p, std::move(dbar), xf.map);
+        run_dev(p, 1, A, n, 2 * k, 2 * k, &xf, 0, R, n, pol, false, s, ops);
+        // imaginary part: G = Y X^T
+        ck(launch_deinterleave(A, (long long)k, (int)n, (int)k, static_cast<uint64_t*>(dX.ptr),
+                               static_cast<uint64_t*>(dY.ptr), s),
+           "deinterleave");
+        gemm_nt_dev(p, static_cast<uint64_t*>(dY.ptr), n, k, k, static_cast<uint64_t*>(dX.ptr), n, k, G, (long long)n,
+                    s);
+    }
+    ck(launch_fp2_combine(R, (long long)n, G, (long long)n, (int)n, (uint32_t)p, conj ? 1 : 0, mirror ? 1 : 0,
+                          static_cast<uint64_t*>(dC.ptr), (long long)n, s),
+       "fp2 combine");
+    ck(cudaMemcpy2DAsync(c, 2 * ldc * 8, dC.ptr, 2 * n * 8, 2 * n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+    ck(cudaStreamSynchronize(s), "sync");
 }
 
 }  // namespace
@@ -1568,68 +1685,32 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         if (lda < k || ldb < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "gemm_nt: dimension mismatch");
         require_device();
         if (m == 0 || n == 0) return;
-        const SchemeInfo sch = scheme_for(p);
-        const int L = sch.planes, BN = sch.bn, BK = sch.bk;
-        if (k > modmm_k_limit(sch, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
-        const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
-        const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
-        DevBuf d64a, d64b, r32, pa, pb, out;
-        d64a.ensure(m * std::max<size_t>(k, 1) * 8);
-        d64b.ensure(n * std::max<size_t>(k, 1) * 8);
-        r32.ensure(std::max(m, n) * std::max<size_t>(k, 1) * 4);
-        pa.ensure((size_t)(mpad * kpad * L));
-        pb.ensure((size_t)(npad * kpad * L));
+        const size_t kk = std::max<size_t>(k, 1);
+        DevBuf d64a, d64b, out;
+        d64a.ensure(m * kk * 8);
+        d64b.ensure(n * kk * 8);
         out.ensure(m * n * 4);
-        ck(cudaMemset(pa.ptr, 0, pa.bytes), "memset");
-        ck(cudaMemset(pb.ptr, 0, pb.bytes), "memset");
         if (k > 0) {
             ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
             ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
-            const InView top{nullptr, 0, 0, 0, 1};
-            ck(launch_split_planes(sch.id, top, static_cast<uint64_t*>(d64a.ptr), (long long)k, (int)m, (int)k, (uint32_t)p,
-                                   static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, 0), "split A");
-            ck(launch_split_planes(sch.id, top, static_cast<uint64_t*>(d64b.ptr), (long long)k, (int)n, (int)k, (uint32_t)p,
-                                   static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, 0), "split B");
         }
-        CUtensorMap ta = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128, BK);
-        CUtensorMap tb = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, sch.b_box, BK);
-        std::vector<int4> tiles;
-        for (int tm = 0; tm * sch.bm < (int)m; ++tm)
-            for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
-        DevBuf dtiles;
-        dtiles.ensure(tiles.size() * sizeof(int4));
-        ck(cudaMemcpy(dtiles.ptr, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice), "tiles");
-        GroupedArgs args;
-        std::memset(&args, 0, sizeof(args));
-        args.modp = make_modp((uint32_t)p);
-        fill_fold_weights(sch, p, args.w);
-        args.ngroups = 1;
-        args.ntiles = (int)tiles.size();
-        args.tiles = static_cast<int4*>(dtiles.ptr);
-        GroupDesc& g = args.g[0];
-        g.tmA = ta;
-        g.tmB = tb;
-        g.M = (int)m;
-        g.N = (int)n;
-        g.k_blocks = (int)(kpad / BK);
-        g.syrk = 0;
-        g.vec_ok = n % 4 == 0;
-        g.a_mult = g.b_mult = 1;
-        g.out = static_cast<uint32_t*>(out.ptr);
-        g.out_bs = 0;
-        g.ldo = (long long)n;
-        modmm_set_output_map(g, 1);
-        int nsm = 148, dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        ck(modmm_launch(sch, args, std::min<int>(modmm_grid(sch, nsm), (int)tiles.size() * (sch.bm / 128)), 0),
-           "modmm");
-        ck(cudaDeviceSynchronize(), "sync");
+        gemm_nt_dev(p, static_cast<uint64_t*>(d64a.ptr), m, k, kk, static_cast<uint64_t*>(d64b.ptr), n, kk,
+                    static_cast<uint32_t*>(out.ptr), (long long)n, 0);
         std::vector<uint32_t> buf(m * n);
         ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");
         for (size_t i = 0; i < m; ++i)
             for (size_t j = 0; j < n; ++j) c[i * ldc + j] = buf[i * n + j];
     });
+}
+
+int fsyrk_b200_herk_fast_into(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c, size_t ldc,
+                              fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
+    return guarded([&] { run_fp2(p, a, n, k, lda, c, ldc, policy, mirror_output != 0, true, ops); });
+}
+
+int fsyrk_b200_syrk_fast_into_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c,
+                                  size_t ldc, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
+    return guarded([&] { run_fp2(p, a, n, k, lda, c, ldc, policy, mirror_output != 0, false, ops); });
 }
 
 }  // extern "C"

@@ -605,6 +605,44 @@ __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ x, long long ldx,
     }
 }
 
+// F_{p^2} helpers (herk / syrk over the quadratic extension, see driver.cu run_fp2)
+// (a, b) pairs -> X = a parts, Y = b parts, both n x k row-major
+__global__ void deinterleave_kernel(const uint64_t* __restrict__ a, long long ldp, int n, int k,
+                                    uint64_t* __restrict__ x, uint64_t* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    for (int i = blockIdx.y; i < n; i += gridDim.y) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(a + 2 * ((long long)i * ldp + j));
+        x[(long long)i * k + j] = v.x;
+        y[(long long)i * k + j] = v.y;
+    }
+}
+
+// C = R + x * I as (a, b) pairs: R = Low(re part) (uint64, ld ldr), I from G = Y X^T (conj:
+// I = G - G^T, herk) or G = X Y^T (I = G + G^T, syrk); upper triangle = conj / plain mirror of
+// the lower one when `mirror`, zeros otherwise.
+__global__ void fp2_combine_kernel(const uint64_t* __restrict__ r, long long ldr, const uint32_t* __restrict__ g,
+                                   long long ldg, int n, uint32_t p, int conj, int mirror, uint64_t* __restrict__ c,
+                                   long long ldcp) {
+    pdl_wait();
+    pdl_trigger();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    for (int i = blockIdx.y; i < n; i += gridDim.y) {
+        const int lo = i >= j ? i : j, hi = i >= j ? j : i;  // (lo, hi) = the lower-triangle position
+        const uint32_t g_lh = g[(long long)lo * ldg + hi], g_hl = g[(long long)hi * ldg + lo];
+        uint32_t re = (uint32_t)r[(long long)lo * ldr + hi];
+        uint32_t im = conj ? subm(g_lh, g_hl, p) : addm(g_lh, g_hl, p);
+        if (i < j) {  // upper triangle
+            if (!mirror) re = im = 0;
+            else if (conj) im = im ? p - im : 0;  // conj(C[j][i])
+        }
+        *reinterpret_cast<ulonglong2*>(c + 2 * ((long long)i * ldcp + j)) = make_ulonglong2(re, im);
+    }
+}
+
 // rows covered by grid.y (each block loops over rows with stride gridDim.y): about 8 waves of 148 SMs
 int rows_grid(int rows, int gx) {
     int gy = (148 * 32 + gx - 1) / gx;
@@ -728,6 +766,21 @@ cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int co
     const long long total = (long long)rows * cols;
     if (total == 0) return cudaSuccess;
     return launch_pdl(u32_to_u64_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ldx, rows, cols, out, ldo);
+}
+
+cudaError_t launch_deinterleave(const uint64_t* a, long long ldp, int n, int k, uint64_t* x, uint64_t* y,
+                                cudaStream_t s) {
+    if ((long long)n * k == 0) return cudaSuccess;
+    const int gx = (k + 255) / 256;
+    return launch_pdl(deinterleave_kernel, dim3(gx, rows_grid(n, gx)), dim3(256), 0, s, a, ldp, n, k, x, y);
+}
+
+cudaError_t launch_fp2_combine(const uint64_t* r, long long ldr, const uint32_t* g, long long ldg, int n, uint32_t p,
+                               int conj, int mirror, uint64_t* c, long long ldcp, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int gx = (n + 255) / 256;
+    return launch_pdl(fp2_combine_kernel, dim3(gx, rows_grid(n, gx)), dim3(256), 0, s, r, ldr, g, ldg, n, p, conj,
+                      mirror, c, ldcp);
 }
 
 }  // namespace fsyrk_b200

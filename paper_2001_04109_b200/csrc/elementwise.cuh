@@ -103,6 +103,11 @@ cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
                             uint32_t alpha, uint32_t beta, cudaStream_t s);
 cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s);
+// F_{p^2}: split (a, b) pairs into X, Y; combine R (real part) and G into C pairs
+cudaError_t launch_deinterleave(const uint64_t* a, long long ldp, int n, int k, uint64_t* x, uint64_t* y,
+                                cudaStream_t s);
+cudaError_t launch_fp2_combine(const uint64_t* r, long long ldr, const uint32_t* g, long long ldg, int n, uint32_t p,
+                               int conj, int mirror, uint64_t* c, long long ldcp, cudaStream_t s);
 cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStream_t s);
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s);

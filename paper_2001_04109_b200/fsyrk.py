@@ -93,6 +93,7 @@ EXPORTS = (
     "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
     "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
     "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
+    "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2",
 )
 
 
@@ -139,6 +140,9 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    for name in ("fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2"):
+        getattr(L, name).argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
+                                     _u64p, ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.POINTER(_OpCount)]
     L.fsyrk_b200_sum_of_squares.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p]
     L.fsyrk_b200_nrsyf.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
     L.fsyrk_b200_last_launch_count.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int]
@@ -252,6 +256,7 @@ class SyrkPlan:
     policy: RecursionPolicy = field(default_factory=RecursionPolicy)
     skew: Optional[SkewOrthogonal] = None
     mirror_output: bool = False
+    conjugate: bool = False  # herk plans (make_herk_plan, fast_syrk.hpp:17, 26-29)
 
 
 def sum_of_squares(f: PrimeField, k: int):
@@ -432,6 +437,70 @@ def syrkbd_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, b: Bloc
                                        b._c(), len(b.blocks), int(beta) % p, ctypes.c_void_p(c_ptr), int(ldc),
                                        policy._c(), int(mirror), ctypes.c_void_p(stream), ctypes.byref(co)))
     _ops_out(ops, co)
+
+
+class QuadExtField:
+    """F_{p^2} = F_p[x] / (x^2 - ns), ns the least quadratic non-residue (fields.hpp:148-212).
+    Matrices over it are numpy uint64 arrays of shape (rows, cols, 2): (a, b) = a + b x."""
+
+    def __init__(self, p: int):
+        self.base = PrimeField(p)
+        if self.base.p == 2:
+            raise ValueError("QuadExtField requires an odd prime")
+        self.p = self.base.p
+
+    def characteristic(self) -> int:
+        return self.p
+
+    def name(self) -> str:
+        return f"F_{self.p}^2"
+
+
+def _view_fp2(m: np.ndarray, name: str):
+    if not isinstance(m, np.ndarray) or m.dtype != np.uint64 or m.ndim != 3 or m.shape[2] != 2:
+        raise DimensionError(f"{name} must be a (rows, cols, 2) numpy uint64 array of (a, b) pairs")
+    if m.size > 0 and (m.strides[2] != 8 or (m.shape[1] > 1 and m.strides[1] != 16)):
+        raise DimensionError(f"{name} rows must be contiguous pairs")
+    ld = m.strides[0] // 16 if m.shape[0] > 1 and m.size > 0 else max(m.shape[1], 1)
+    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(max(ld, m.shape[1]))
+
+
+def make_herk_plan(f: QuadExtField, policy: Optional[RecursionPolicy] = None, mirror_output: bool = False) -> SyrkPlan:
+    """make_herk_plan (fast_syrk.hpp:26-29): a conjugating plan."""
+    policy = policy or RecursionPolicy()
+    policy.validate()
+    return SyrkPlan(policy, None, bool(mirror_output), True)
+
+
+def _fp2_call(fn, f: QuadExtField, a: np.ndarray, c: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount]):
+    plan.policy.validate()
+    pa, n, k, lda = _view_fp2(a, "a")
+    pc, cn, cm, ldc = _view_fp2(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrk_fast: dimension mismatch")
+    co = _OpCount()
+    _check(fn(f.p, pa, n, k, lda, pc, ldc, plan.policy._c(), int(plan.mirror_output), ctypes.byref(co)))
+    _ops_out(ops, co)
+
+
+def herk_fast_into(f: QuadExtField, a: np.ndarray, c: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount] = None):
+    """Low(C) <- Low(A conj(A)^T) over F_{p^2} (fast_syrk.hpp:307-313)."""
+    if not getattr(plan, "conjugate", False):
+        raise ValueError("herk_fast: plan must be built by make_herk_plan")
+    _fp2_call(lib().fsyrk_b200_herk_fast_into, f, a, c, plan, ops)
+
+
+def herk_fast(f: QuadExtField, a: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount] = None) -> np.ndarray:
+    c = np.zeros((a.shape[0], a.shape[0], 2), dtype=np.uint64)
+    herk_fast_into(f, a, c, plan, ops)
+    return c
+
+
+def syrk_fast_fp2(f: QuadExtField, a: np.ndarray, plan: SyrkPlan, ops: Optional[OpCount] = None) -> np.ndarray:
+    """Low(A A^T) over F_{p^2} (syrk_fast, fast_syrk.hpp:284-289, for QuadExtField)."""
+    c = np.zeros((a.shape[0], a.shape[0], 2), dtype=np.uint64)
+    _fp2_call(lib().fsyrk_b200_syrk_fast_into_fp2, f, a, c, plan, ops)
+    return c
 
 
 def syrk_dev(p: int, alpha: int, a_ptr: int, n: int, k: int, lda: int, beta: int, c_ptr: int, ldc: int,

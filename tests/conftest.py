@@ -33,6 +33,8 @@ def golden():
             rec["C0"] = data[pre + "C0"]
         if pre + "D" in data:
             rec["D"] = data[pre + "D"]
+        if pre + "ns" in data:
+            rec["ns"] = int(data[pre + "ns"])
         cases.append(rec)
     return {"cases": cases, "skew_p": data["skew_p"], "skew_form": data["skew_form"],
             "skew_a": data["skew_a"], "skew_b": data["skew_b"]}

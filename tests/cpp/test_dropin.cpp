@@ -117,6 +117,20 @@ int main() {
         }
         CHECK(threw, "syrkbd gamma != 0 must throw std::invalid_argument (p=%llu)", (unsigned long long)p);
     }
+    // 3c. herk_fast over F_{p^2} through the shim vs the reference's herk_fast
+    for (std::uint64_t p : {7ull, 13ull, 131071ull, 2147483647ull}) {
+        QuadExtField f(p);
+        std::mt19937_64 r5(p * 13 + 5);
+        for (int t = 0; t < 4; ++t) {
+            const std::size_t n = 1 + r5() % 70, k = 1 + r5() % 50;
+            auto a = random_matrix(f, n, k, r5());
+            auto plan = make_herk_plan(f, {4, kUnlimitedLevels}, t % 2 == 1);
+            OpCount ops;
+            auto dev = fsyrk_b200::herk_fast(f, a.view(), plan, ops);
+            auto ref = herk_fast(f, a.view(), plan, ops);
+            CHECK(lower_equal(f, dev.view(), ref.view()), "herk_fast p=%llu n=%zu k=%zu", (unsigned long long)p, n, k);
+        }
+    }
     // 4. error convention: aliased output and bad policy throw std::invalid_argument
     {
         PrimeField f(7);

@@ -56,6 +56,14 @@ for (p, n, k, s) in ((7, 2, 2, 6001), (13, 5, 5, 6002), (131071, 40, 33, 6003), 
                      (131071, 96, 64, 6009), (5, 9, 14, 6010)):
     CASES.append((p, n, k, s, 2, "inf", "syrkbd", False))
 
+# F_{p^2}: herk_fast (conjugate) and syrk_fast over the quadratic extension (QuadExtField);
+# A and C are stored as (rows, cols, 2) arrays of (a, b) pairs
+for (p, n, k, s) in ((7, 3, 2, 7001), (13, 20, 11, 7002), (131071, 48, 40, 7003), (65521, 33, 64, 7004),
+                     (2147483647, 24, 30, 7005), (11, 64, 17, 7006)):
+    CASES.append((p, n, k, s, 4, "inf", "herk", False))
+for (p, n, k, s) in ((7, 9, 5, 7101), (131071, 40, 24, 7102), (65537, 30, 30, 7103)):
+    CASES.append((p, n, k, s, 4, "inf", "syrk2", False))
+
 
 def run_case(case, tmp):
     p, n, k, seed, thr, lev, mode, mirror = case
@@ -66,6 +74,16 @@ def run_case(case, tmp):
     if mirror:
         cmd.append("--mirror")
     info = json.loads(subprocess.run(cmd, check=True, capture_output=True, text=True).stdout)
+    if mode in ("herk", "syrk2"):
+        return {
+            "A": np.fromfile(fa, dtype=np.uint64).reshape(n, k, 2),
+            "C": np.fromfile(fc, dtype=np.uint64).reshape(n, n, 2),
+            "meta": np.array([p, n, k, seed, thr, -1 if lev == "inf" else int(lev), int(mirror), 1, 0],
+                             dtype=np.int64),
+            "mode": np.array(mode),
+            "digest": np.array(""),
+            "ns": np.array(info["non_residue"], dtype=np.uint64),
+        }, {"skew_form": "none", "skew_a": 0, "skew_b": 0}
     rec = {
         "A": np.fromfile(fa, dtype=np.uint64).reshape(n, k),
         "C": np.fromfile(fc, dtype=np.uint64).reshape(n, n),
@@ -91,7 +109,8 @@ def main():
             rec, info = run_case(case, tmp)
             for key, val in rec.items():
                 out[f"c{i:03d}_{key}"] = val
-            skews[int(case[0])] = (info["skew_form"], info["skew_a"], info["skew_b"])
+            if info["skew_form"] != "none":
+                skews[int(case[0])] = (info["skew_form"], info["skew_a"], info["skew_b"])
     out["ncases"] = np.array(len(CASES))
     primes = sorted(skews)
     out["skew_p"] = np.array(primes, dtype=np.uint64)

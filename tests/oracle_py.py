@@ -44,6 +44,7 @@ def lib():
         L.orc_syrk_fast_acc.argtypes = [_u64, _u64, _u64p, _sz, _sz, _sz, _u64, _u64p, _sz, _sz, _sz]
         L.orc_abat_classical.argtypes = [_u64, _u64p, _sz, _sz, _sz, ctypes.POINTER(ctypes.c_int), _u64p, _u64p,
                                          _u64p, _sz, _u64p, _sz]
+        L.orc_fp2_syrk_classical.argtypes = [_u64, _u64, _u64p, _sz, _sz, ctypes.c_int, _u64p]
         L.orc_syrkd.argtypes = [_u64, _u64p, _sz, _sz, _sz, _u64p, _u64p, _sz, _sz, _sz]
         L.orc_syrkd.restype = ctypes.c_long
         L.orc_level_blocks.argtypes = [_u64, _u64p, _sz, _sz, _sz, _sz, _sz] + [_u64p] * 9
@@ -173,4 +174,19 @@ def abat_classical(p, a, blocks):
     c = np.zeros((n, n), dtype=np.uint64)
     if n and k:
         lib().orc_abat_classical(p, _p(a), n, k, k, two, _p(cols[0]), _p(cols[1]), _p(cols[2]), nb, _p(c), n)
+    return c
+
+
+def lqnr(p):
+    """Least quadratic non-residue (the QuadExtField modulus x^2 - ns, fields.hpp:148-150)."""
+    return int(lib().orc_lqnr(p))
+
+
+def fp2_syrk_classical(p, a_pairs, conj):
+    """Lower triangle of A * conj(A)^T (conj) or A * A^T over F_{p^2}; a_pairs: (n, k, 2) uint64."""
+    a = np.ascontiguousarray(a_pairs, dtype=np.uint64)
+    n, k = a.shape[0], a.shape[1]
+    c = np.zeros((n, n, 2), dtype=np.uint64)
+    if n and k:
+        lib().orc_fp2_syrk_classical(p, lqnr(p), _p(a), n, k, 1 if conj else 0, _p(c))
     return c

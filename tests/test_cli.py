@@ -61,6 +61,29 @@ def test_file_roundtrips(tmp_path):
 def test_verify_and_bench():
     rc, out, _ = run("verify", "--field", "fp", "--prime", 131071, "--n", 48, "--cases", 10)
     assert rc == 0 and out.strip().endswith("PASS overall"), out
+    # cli_syrk_roundtrip.cmake:29: the F_{p^2} battery (syrk_fast and herk_fast)
+    rc, out, _ = run("verify", "--field", "fp2", "--prime", 13, "--n", 24, "--cases", 6)
+    assert rc == 0 and "herk_fast" in out and out.strip().endswith("PASS overall"), out
     rc, out, _ = run("bench", "--prime", 131071, "--min-n", 256, "--max-n", 512, "--threshold", 128)
     lines = out.strip().splitlines()
     assert rc == 0 and lines[0] == "algorithm,n,seconds,effective_gfops" and len(lines) == 3
+
+
+@pytest.mark.gpu
+def test_fp2_file_syrk(tmp_path):
+    import numpy as np
+    import sys
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import oracle_py as orc
+    p, n, k = 13, 5, 4
+    a = orc.random_matrix(p, n, 2 * k, 9).reshape(n, k, 2)
+    f = tmp_path / "a2.txt"
+    f.write_text(f"{n} {k}\n" + "\n".join(" ".join(str(int(x[0] + x[1] * p)) for x in row) for row in a) + "\n")
+    rc, out, err = run("syrk", "--field", "fp2", "--prime", p, "--input", f)
+    assert rc == 0, err
+    rows = [list(map(int, l.split())) for l in out.strip().splitlines()[1:]]
+    want = orc.fp2_syrk_classical(p, a, False)
+    for i in range(n):
+        for j in range(n):
+            enc = int(want[i, j, 0] + want[i, j, 1] * p) if j <= i else 0
+            assert rows[i][j] == enc, (i, j)

@@ -34,6 +34,15 @@ def test_golden_cases(gpu, golden):
         elif case["mode"] == "acc":
             c = case["C0"].copy()
             fs.syrk_fast_acc(f, case["alpha"], a, case["beta"], c, plan)
+        elif case["mode"] in ("herk", "syrk2"):
+            q = fs.QuadExtField(case["p"])
+            if case["mode"] == "herk":
+                c = fs.herk_fast(q, a, fs.make_herk_plan(q, _policy(fs, case)))
+            else:
+                c = fs.syrk_fast_fp2(q, a, fs.make_syrk_plan(f, _policy(fs, case)))
+            for i in range(case["n"]):
+                assert np.array_equal(c[i, :i + 1], case["C"][i, :i + 1]), (case["mode"], case["p"], case["n"], i)
+            continue
         elif case["mode"] == "syrkbd":
             c = fs.syrkbd(f, a, _blocks(fs, case["D"]), plan)
         else:
@@ -298,3 +307,30 @@ def test_triangular_host_transfers(gpu):
     exp[idx] = (want[idx] * np.uint64(3) + c0[idx] * np.uint64(5)) % np.uint64(p)
     assert orc.lower_equal(c, exp)
     assert np.array_equal(c[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])
+
+
+@pytest.mark.parametrize("p", [3, 7, 13, 65521, 131071, 2147483647])
+def test_fp2_herk_and_syrk_battery(gpu, p):
+    # herk_fast / syrk_fast over F_{p^2} (fast_syrk.hpp:305-320; verify_herk_battery, fsyrk.cpp)
+    # against the classical conjugate product; mirror gives conj(C)^T / C^T above the diagonal
+    fs = gpu
+    q = fs.QuadExtField(p)
+    rng = np.random.default_rng(p + 3)
+    for t in range(4):
+        n = int(rng.integers(1, 150))
+        k = int(rng.integers(1, 120))
+        a = orc.random_matrix(p, n, 2 * k, int(rng.integers(1 << 62))).reshape(n, k, 2)
+        pol = fs.RecursionPolicy((2, 8, 64, 16)[t])
+        want_h = orc.fp2_syrk_classical(p, a, True)
+        want_s = orc.fp2_syrk_classical(p, a, False)
+        c = fs.herk_fast(q, a, fs.make_herk_plan(q, pol, mirror_output=True))
+        cs = fs.syrk_fast_fp2(q, a, fs.make_syrk_plan(q.base, pol, mirror_output=True))
+        for i in range(n):
+            assert np.array_equal(c[i, :i + 1], want_h[i, :i + 1]), (p, n, k, i)
+            assert np.array_equal(cs[i, :i + 1], want_s[i, :i + 1]), (p, n, k, i)
+        iu = np.triu_indices(n, 1)
+        assert np.array_equal(c[iu][:, 0], c.transpose(1, 0, 2)[iu][:, 0])                # Hermitian
+        assert np.array_equal(c[iu][:, 1], (np.uint64(p) - c.transpose(1, 0, 2)[iu][:, 1]) % np.uint64(p))
+        assert np.array_equal(cs[iu], cs.transpose(1, 0, 2)[iu])                           # symmetric
+    with pytest.raises(ValueError):
+        fs.herk_fast(q, np.zeros((2, 2, 2), np.uint64), fs.make_syrk_plan(q.base))       # not a herk plan

@@ -12,7 +12,10 @@ import oracle_py as orc
 def test_random_matrix_stream_matches_reference(golden):
     # random_matrix(f, n, k, seed) (matrix.hpp:411-419): mt19937_64 + libstdc++ uniform_int_distribution
     for case in golden["cases"]:
-        a = orc.random_matrix(case["p"], case["n"], case["k"], case["seed"])
+        if case["mode"] in ("herk", "syrk2"):  # QuadExtField::random_element draws a, then b
+            a = orc.random_matrix(case["p"], case["n"], 2 * case["k"], case["seed"]).reshape(case["n"], case["k"], 2)
+        else:
+            a = orc.random_matrix(case["p"], case["n"], case["k"], case["seed"])
         assert np.array_equal(a, case["A"]), (case["p"], case["n"], case["k"])
 
 
@@ -43,6 +46,13 @@ def test_skew_known_answers():
 def test_oracle_matches_reference_outputs(golden):
     for case in golden["cases"]:
         p, a = case["p"], case["A"]
+        if case["mode"] in ("herk", "syrk2"):  # F_{p^2}: classical (conjugate) product
+            assert orc.lqnr(p) == case["ns"]
+            c = orc.fp2_syrk_classical(p, a, case["mode"] == "herk")
+            n = case["n"]
+            for i in range(n):
+                assert np.array_equal(c[i, :i + 1], case["C"][i, :i + 1]), (case["mode"], p, n, case["k"], i)
+            continue
         lev = orc.UNLIMITED if case["levels"] is None else case["levels"]
         if case["mode"] == "plain":
             c = orc.syrk_fast(p, a, case["threshold"], lev)

@@ -9,8 +9,9 @@
 //   fsyrk_b200 bench  --prime P [--min-n N0] [--max-n N1] [--threshold T] [--rec R] [--seed S] [--output F]
 //   fsyrk_b200 sos    --prime P --value V
 //   fsyrk_b200 nrsyf  --prime P --alpha A --beta B
-// `--field` accepts only `fp` (the other fields are outside the B200 path); `count` (the
-// reference's operation-count model) is not part of this tool.
+// `--field` accepts `fp` and, for `syrk` / `verify`, `fp2` (F_{p^2}: syrk_fast and herk_fast);
+// gf2k / complex are outside the B200 path and `count` (the operation-count model) is not part
+// of this tool.
 #include <cerrno>
 #include <chrono>
 #include <cstdint>
@@ -100,8 +101,10 @@ Options parse_args(int argc, char** argv) {
         if (i + 1 >= argc) throw UsageError("--" + k + " needs a value");
         o.kv[k] = argv[++i];
     }
-    if (o.has("field") && o.str("field") != "fp")
-        throw UsageError("--field " + o.str("field") + ": only fp runs on the B200 path");
+    if (o.has("field") && o.str("field") != "fp" && o.str("field") != "fp2")
+        throw UsageError("--field " + o.str("field") + ": only fp and fp2 run on the B200 path");
+    if (o.str("field") == "fp2" && o.cmd != "syrk" && o.cmd != "verify")
+        throw UsageError(o.cmd + ": only --field fp is supported");
     return o;
 }
 
@@ -219,8 +222,149 @@ bool lower_equal(const Matrix& x, const Matrix& y) {
     return true;
 }
 
+// F_{p^2} = F_p[x] / (x^2 - ns) (QuadExtField): matrices of (a, b) pairs; the text format
+// prints the integer encoding a + b p (fields.hpp:194-198).
+struct Fp2 {
+    Field base;
+    uint64_t ns;
+    explicit Fp2(uint64_t p) : base(p), ns(0) {
+        if (p == 2) throw UsageError("QuadExtField requires an odd prime");
+        for (uint64_t s = 2;; ++s) {  // least non-residue (Euler's criterion)
+            uint64_t r = 1, b = s % p, e = (p - 1) / 2;
+            while (e) {
+                if (e & 1) r = base.mul(r, b);
+                b = base.mul(b, b);
+                e >>= 1;
+            }
+            if (r == p - 1) {
+                ns = s;
+                break;
+            }
+        }
+    }
+    uint64_t p() const { return base.p; }
+    void parse_into(const std::string& t, uint64_t* ab) const {
+        char* end = nullptr;
+        errno = 0;
+        unsigned long long v = std::strtoull(t.c_str(), &end, 10);
+        if (errno != 0 || end == t.c_str() || *end != '\0' || v >= p() * p())
+            throw ParseError("invalid F_" + std::to_string(p()) + "^2 element: '" + t + "'");
+        ab[0] = v % p();
+        ab[1] = v / p();
+    }
+};
+
+struct Matrix2 {  // rows x cols of (a, b) pairs
+    size_t rows = 0, cols = 0;
+    std::vector<uint64_t> data;
+    Matrix2() = default;
+    Matrix2(size_t r, size_t c) : rows(r), cols(c), data(2 * r * c, 0) {}
+    uint64_t* at(size_t i, size_t j) { return &data[2 * (i * cols + j)]; }
+    const uint64_t* at(size_t i, size_t j) const { return &data[2 * (i * cols + j)]; }
+};
+
+Matrix2 read_matrix2(const Fp2& f, std::istream& is) {
+    size_t rows = 0, cols = 0;
+    if (!(is >> rows >> cols)) throw ParseError("matrix header must be 'rows cols'");
+    Matrix2 m(rows, cols);
+    std::string token;
+    for (size_t i = 0; i < rows; ++i)
+        for (size_t j = 0; j < cols; ++j) {
+            if (!(is >> token)) throw ParseError("matrix body ended early at row " + std::to_string(i));
+            f.parse_into(token, m.at(i, j));
+        }
+    return m;
+}
+
+void write_matrix2(const Fp2& f, std::ostream& os, const Matrix2& m) {
+    os << m.rows << ' ' << m.cols << '\n';
+    for (size_t i = 0; i < m.rows; ++i) {
+        for (size_t j = 0; j < m.cols; ++j) {
+            if (j) os << ' ';
+            os << m.at(i, j)[0] + m.at(i, j)[1] * f.p();
+        }
+        os << '\n';
+    }
+}
+
+// Low(A conj(A)^T) (conj) or Low(A A^T) over F_{p^2}, classical, on the host (the oracle of the
+// verify batteries, fsyrk.cpp verify_herk_battery)
+Matrix2 classical2(const Fp2& f, const Matrix2& a, bool conj) {
+    const uint64_t p = f.p();
+    Matrix2 c(a.rows, a.rows);
+    for (size_t i = 0; i < a.rows; ++i)
+        for (size_t j = 0; j <= i; ++j) {
+            uint64_t re = 0, im = 0;
+            for (size_t l = 0; l < a.cols; ++l) {
+                const uint64_t* x = a.at(i, l);
+                const uint64_t* y = a.at(j, l);
+                const uint64_t yb = conj ? (p - y[1]) % p : y[1];
+                re = (re + f.base.mul(x[0], y[0]) + f.base.mul(f.ns, f.base.mul(x[1], yb))) % p;
+                im = (im + f.base.mul(x[0], yb) + f.base.mul(x[1], y[0])) % p;
+            }
+            c.at(i, j)[0] = re;
+            c.at(i, j)[1] = im;
+        }
+    return c;
+}
+
+int cmd_syrk_fp2(const Options& o) {
+    Fp2 f(o.u64("prime", 131071));
+    if (!o.has("input")) throw UsageError("syrk: --input is required");
+    if (o.has("scaling") || o.has("alpha") || o.has("beta") || o.has("acc"))
+        throw UsageError("--field fp2: only the plain product runs on the B200 path");
+    std::ifstream in(o.str("input"));
+    if (!in) throw std::runtime_error("cannot open input file: " + o.str("input"));
+    Matrix2 a = read_matrix2(f, in);
+    Matrix2 c(a.rows, a.rows);
+    check(fsyrk_b200_syrk_fast_into_fp2(f.p(), a.data.data(), a.rows, a.cols, a.cols ? a.cols : 1, c.data.data(),
+                                        a.rows ? a.rows : 1, policy_of(o), o.flag("mirror"), nullptr));
+    if (o.has("output")) {
+        std::ofstream out(o.str("output"));
+        if (!out) throw std::runtime_error("cannot open output file: " + o.str("output"));
+        write_matrix2(f, out, c);
+    } else {
+        write_matrix2(f, std::cout, c);
+    }
+    return kExitOk;
+}
+
+int cmd_verify_fp2(const Options& o) {
+    Fp2 f(o.u64("prime", 131071));
+    const size_t nmax = o.u64("n", 64), kmax = o.u64("cols", 0) ? o.u64("cols", 0) : nmax;
+    const int cases = (int)o.u64("cases", 100);
+    const uint64_t seed = o.u64("seed", 0);
+    const fsyrk_b200_policy pol = policy_of(o);
+    bool all = true;
+    for (int conj = 0; conj < 2; ++conj) {  // syrk_fast, then herk_fast (verify_herk_battery)
+        std::mt19937_64 rng(seed + 3 * conj);
+        bool ok = true;
+        const int nc = conj ? std::max(1, cases / 4) : cases;
+        for (int t = 0; t < nc; ++t) {
+            const size_t n = 1 + rng() % (conj ? std::min<size_t>(nmax, 64) : nmax);
+            const size_t k = 1 + rng() % (conj ? std::min<size_t>(nmax, 64) : kmax);
+            Matrix2 a(n, k);
+            std::vector<uint64_t> flat(2 * n * k);
+            check(fsyrk_b200_random_matrix(f.p(), n, 2 * k, rng(), flat.data(), 2 * k));  // a, then b per element
+            a.data = flat;
+            Matrix2 c(n, n);
+            check((conj ? fsyrk_b200_herk_fast_into : fsyrk_b200_syrk_fast_into_fp2)(
+                f.p(), a.data.data(), n, k, k, c.data.data(), n, pol, 0, nullptr));
+            Matrix2 ref = classical2(f, a, conj);
+            for (size_t i = 0; i < n && ok; ++i)
+                for (size_t j = 0; j <= i; ++j) ok &= c.at(i, j)[0] == ref.at(i, j)[0] && c.at(i, j)[1] == ref.at(i, j)[1];
+        }
+        std::cout << (ok ? "PASS" : "FAIL") << (conj ? " herk_fast" : " syrk_fast") << " vs classical (" << nc
+                  << " cases, F_" << f.p() << "^2)\n";
+        all &= ok;
+    }
+    std::cout << (all ? "PASS" : "FAIL") << " overall\n";
+    return all ? kExitOk : kExitVerifyFailed;
+}
+
 // ------------------------------------------------------------------ commands
 int cmd_syrk(const Options& o) {
+    if (o.str("field") == "fp2") return cmd_syrk_fp2(o);
     Field f(o.u64("prime", 131071));
     if (!o.has("input")) throw UsageError("syrk: --input is required");
     std::ifstream in(o.str("input"));
@@ -266,6 +410,7 @@ int cmd_syrk(const Options& o) {
 }
 
 int cmd_verify(const Options& o) {
+    if (o.str("field") == "fp2") return cmd_verify_fp2(o);
     Field f(o.u64("prime", 131071));
     const size_t nmax = o.u64("n", 64), kmax = o.u64("cols", 0) ? o.u64("cols", 0) : nmax;
     const int cases = (int)o.u64("cases", 100);

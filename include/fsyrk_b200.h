@@ -226,6 +226,16 @@ int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, s
 int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
                        size_t ldb, uint64_t* c, size_t ldc);
 
+/* Strassen-Winograd general product C = A * B^T mod p (replaces gemm_winograd_nt_into,
+ * include/fsyrk/winograd.hpp:195-202): policy.max_levels Winograd levels over the tensor-core
+ * product while every dimension is even and >= policy.threshold; exact, so identical to
+ * fsyrk_b200_gemm_nt.  Host pointers; _dev takes device pointers (C is m x n uint64). */
+int fsyrk_b200_gemm_winograd_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b,
+                                size_t n, size_t ldb, uint64_t* c, size_t ldc, fsyrk_b200_policy policy);
+int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m, size_t k, size_t lda,
+                                    const uint64_t* b_dev, size_t n, size_t ldb, uint64_t* c_dev, size_t ldc,
+                                    fsyrk_b200_policy policy, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,11 @@ void ck(cudaError_t e, const char* what) {
     }
 }
 
+// rethrow the status of a nested entry point (its message is in g_last_error)
+void check_status(int st) {
+    if (st != FSYRK_B200_OK) fail(st, g_last_error);
+}
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -1226,34 +1231,48 @@ void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
     ops->adds += plan->ew_adds;
 }
 
-// C = A * B^T mod p on the tensor cores for device-resident uint64 A (m x k, lda) and B
-// (n x k, ldb) into uint32 `out` (m x n, ldo): digit split, one grouped product launch.
-// Scratch buffers are call-local (general products outside the recursion are not hot).
-void gemm_nt_dev(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
-                 size_t ldb, uint32_t* out, long long ldo, cudaStream_t s) {
+// One operand of a batched product: a uint32 residue view, or a window of a uint64 matrix.
+struct GemmOperand {
+    InView v;
+    const uint64_t* a64 = nullptr;
+    long long ld64 = 0;
+};
+GemmOperand operand_u64(const uint64_t* a, long long lda) { return GemmOperand{InView{nullptr, 0, 0, 0, 1}, a, lda}; }
+GemmOperand operand_u32(const uint32_t* a, long long lda) { return GemmOperand{InView{a, lda, 0, 0, 0}, nullptr, 0}; }
+
+// out[b] = A[b] * B[b]^T mod p (b = 0 .. batch-1; A[b] m x k, B[b] n x k, out[b] at out + b * out_bs,
+// row stride ldo) on the tensor cores: digit split per operand, ONE grouped product launch.
+// Scratch buffers are call-local (products outside the recursion plan are not hot).
+void gemm_batch_dev(uint64_t p, size_t m, size_t n, size_t k, const std::vector<GemmOperand>& A,
+                    const std::vector<GemmOperand>& B, uint32_t* out, long long ldo, long long out_bs,
+                    cudaStream_t s) {
     const SchemeInfo sch = scheme_for(p);
     const int L = sch.planes, BN = sch.bn, BK = sch.bk;
     if (k > modmm_k_limit(sch, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
-    if (m == 0 || n == 0) return;
+    const int batch = (int)A.size();
+    if (m == 0 || n == 0 || batch == 0) return;
     const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
     const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
-    DevBuf pa, pb, dtiles;
-    pa.ensure((size_t)(mpad * kpad * L));
-    pb.ensure((size_t)(npad * kpad * L));
-    ck(cudaMemsetAsync(pa.ptr, 0, pa.bytes, s), "memset");
-    ck(cudaMemsetAsync(pb.ptr, 0, pb.bytes, s), "memset");
-    if (k > 0) {
-        const InView top{nullptr, 0, 0, 0, 1};
-        ck(launch_split_planes(sch.id, top, a, (long long)lda, (int)m, (int)k, (uint32_t)p,
-                               static_cast<int8_t*>(pa.ptr), mpad * kpad, kpad, s),
+    // scratch kept across calls (grows to the largest product seen); one product at a time
+    static std::mutex mu;
+    static DevBuf pa, pb, dtiles;
+    std::lock_guard<std::mutex> lk(mu);
+    pa.ensure((size_t)(mpad * kpad * L * batch));
+    pb.ensure((size_t)(npad * kpad * L * batch));
+    ck(cudaMemsetAsync(pa.ptr, 0, (size_t)(mpad * kpad * L * batch), s), "memset");
+    ck(cudaMemsetAsync(pb.ptr, 0, (size_t)(npad * kpad * L * batch), s), "memset");
+    for (int b = 0; k > 0 && b < batch; ++b) {
+        ck(launch_split_planes(sch.id, A[b].v, A[b].a64, A[b].ld64, (int)m, (int)k, (uint32_t)p,
+                               static_cast<int8_t*>(pa.ptr) + (long long)b * L * mpad * kpad, mpad * kpad, kpad, s),
            "split A");
-        ck(launch_split_planes(sch.id, top, b, (long long)ldb, (int)n, (int)k, (uint32_t)p,
-                               static_cast<int8_t*>(pb.ptr), npad * kpad, kpad, s),
+        ck(launch_split_planes(sch.id, B[b].v, B[b].a64, B[b].ld64, (int)n, (int)k, (uint32_t)p,
+                               static_cast<int8_t*>(pb.ptr) + (long long)b * L * npad * kpad, npad * kpad, kpad, s),
            "split B");
     }
     std::vector<int4> tiles;
-    for (int tm = 0; tm * sch.bm < (int)m; ++tm)
-        for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, 0, tm, tn));
+    for (int b = 0; b < batch; ++b)
+        for (int tm = 0; tm * sch.bm < (int)m; ++tm)
+            for (int tn = 0; tn * BN < (int)n; ++tn) tiles.push_back(make_int4(0, b, tm, tn));
     dtiles.ensure(tiles.size() * sizeof(int4));
     ck(cudaMemcpyAsync(dtiles.ptr, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s), "tiles");
     GroupedArgs args;
@@ -1264,23 +1283,130 @@ void gemm_nt_dev(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, 
     args.ntiles = (int)tiles.size();
     args.tiles = static_cast<int4*>(dtiles.ptr);
     GroupDesc& g = args.g[0];
-    g.tmA = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, 1, 128, BK);
-    g.tmB = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, 1, sch.b_box, BK);
+    g.tmA = make_plane_map(pa.ptr, (int)kpad, (int)mpad, L, batch, 128, BK);
+    g.tmB = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, batch, sch.b_box, BK);
     g.M = (int)m;
     g.N = (int)n;
     g.k_blocks = (int)(kpad / BK);
     g.syrk = 0;
-    g.vec_ok = ldo % 4 == 0;
+    g.vec_ok = ldo % 4 == 0 && out_bs % 4 == 0;
     g.a_mult = g.b_mult = 1;
     g.out = out;
-    g.out_bs = 0;
+    g.out_bs = out_bs;
     g.ldo = ldo;
-    modmm_set_output_map(g, 1);
+    modmm_set_output_map(g, batch);
     int nsm = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     ck(modmm_launch(sch, args, std::min<int>(modmm_grid(sch, nsm), (int)tiles.size() * (sch.bm / 128)), s), "modmm");
-    ck(cudaStreamSynchronize(s), "sync");  // scratch buffers are released on return
+    ck(cudaStreamSynchronize(s), "sync");  // the scratch is reused by the next call
+}
+
+// C = A * B^T mod p for device-resident uint64 A (m x k, lda) and B (n x k, ldb) into uint32 out.
+void gemm_nt_dev(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b, size_t n,
+                 size_t ldb, uint32_t* out, long long ldo, cudaStream_t s) {
+    gemm_batch_dev(p, m, n, k, {operand_u64(a, (long long)lda)}, {operand_u64(b, (long long)ldb)}, out, ldo, 0, s);
+}
+
+// Strassen-Winograd levels over the tensor-core product (the reference's generic-product
+// engine gemm_winograd_nt_into, include/fsyrk/winograd.hpp:118-169, 195-202): C = A B^T for
+// uint32 residue matrices A (m x k) and B (n x k, the stored form of B^T).  Each level splits
+// every problem into 7 half-size products with the pre-additions
+//   S1 = A21 + A22, S2 = S1 - A11, S3 = A11 - A21, S4 = A12 - S2,
+//   T1 = B'12 - B'11, T2 = B'22 - T1, T3 = B'22 - B'12, T4 = T2 - B'21     (B' = B^T blocks)
+// and the post-additions C11 = M1 + M2, C12 = M1 + M6 + M5 + M3, C21 = M1 + M6 + M7 - M4,
+// C22 = M1 + M6 + M7 + M5; all 7^levels base products of a call run as ONE grouped
+// tensor-core launch.  Levels stop where a dimension is odd or below the policy threshold
+// (the reference peels odd dimensions instead; the result is the same exact product).
+void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const uint32_t* B, long long ldb, size_t n,
+                   size_t k, uint32_t* C, long long ldc, fsyrk_b200_policy pol, cudaStream_t s) {
+    struct Prob {
+        GemmOperand a, b;
+        uint32_t* c;
+        long long ldc;
+    };
+    std::vector<Prob> cur{{operand_u32(A, lda), operand_u32(B, ldb), C, ldc}};
+    struct Level {
+        std::vector<Prob> parents;
+        uint32_t* m_out;  // 7 x parents.size() products of hm x hn, child-major order
+        long long hm, hn;
+    };
+    std::vector<Level> levels;
+    static std::mutex mu;  // per-level scratch kept across calls
+    static std::vector<std::unique_ptr<DevBuf>> pool;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t cm = m, cn = n, ck_ = k;
+    const uint32_t pp = (uint32_t)p;
+    for (uint64_t lev = 0; lev < pol.max_levels; ++lev) {
+        if (cm % 2 || cn % 2 || ck_ % 2 || std::min({cm, cn, ck_}) < pol.threshold) break;
+        const long long hm = (long long)cm / 2, hn = (long long)cn / 2, hk = (long long)ck_ / 2;
+        Level L;
+        L.hm = hm;
+        L.hn = hn;
+        const size_t np = cur.size();
+        // per parent: S1..S4 (hm x hk), T1..T4 (hn x hk); per level: 7 np products (hm x hn)
+        const size_t per = (size_t)(4 * hm * hk + 4 * hn * hk);
+        if (pool.size() <= lev) pool.push_back(std::make_unique<DevBuf>());
+        pool[lev]->ensure((per * np + (size_t)7 * np * hm * hn) * 4);
+        auto* base = static_cast<uint32_t*>(pool[lev]->ptr);
+        L.m_out = base + per * np;
+        std::vector<Prob> next;
+        for (size_t q = 0; q < np; ++q) {
+            const Prob& pr = cur[q];
+            uint32_t* S = base + per * q;
+            uint32_t* T = S + 4 * hm * hk;
+            const uint32_t* a = pr.a.v.p32;
+            const long long la = pr.a.v.ld32;
+            const uint32_t* b = pr.b.v.p32;
+            const long long lb = pr.b.v.ld32;
+            ck(launch_wino_pre(a, a + hk, a + hm * la, a + hm * la + hk, la, (int)hm, (int)hk, pp, 0, S, hk,
+                               hm * hk, s),
+               "winograd pre A");
+            // stored blocks of B: B'11 = B[0:hn, 0:hk], B'12 = B[hn:, 0:hk], B'21 = B[0:hn, hk:], B'22 = B[hn:, hk:]
+            ck(launch_wino_pre(b, b + hn * lb, b + hk, b + hn * lb + hk, lb, (int)hn, (int)hk, pp, 1, T, hk,
+                               hn * hk, s),
+               "winograd pre B");
+            const uint32_t *S1 = S, *S2 = S + hm * hk, *S3 = S + 2 * hm * hk, *S4 = S + 3 * hm * hk;
+            const uint32_t *T1 = T, *T2 = T + hn * hk, *T3 = T + 2 * hn * hk, *T4 = T + 3 * hn * hk;
+            const GemmOperand ops[7][2] = {
+                {operand_u32(a, la), operand_u32(b, lb)},                               // M1 = A11 B'11
+                {operand_u32(a + hk, la), operand_u32(b + hk, lb)},                     // M2 = A12 B'21
+                {operand_u32(S4, hk), operand_u32(b + hn * lb + hk, lb)},               // M3 = S4 B'22
+                {operand_u32(a + hm * la + hk, la), operand_u32(T4, hk)},               // M4 = A22 T4
+                {operand_u32(S1, hk), operand_u32(T1, hk)},                             // M5 = S1 T1
+                {operand_u32(S2, hk), operand_u32(T2, hk)},                             // M6 = S2 T2
+                {operand_u32(S3, hk), operand_u32(T3, hk)}};                            // M7 = S3 T3
+            for (int i = 0; i < 7; ++i)
+                next.push_back(Prob{ops[i][0], ops[i][1], L.m_out + ((long long)q * 7 + i) * hm * hn, hn});
+        }
+        L.parents = std::move(cur);
+        levels.push_back(std::move(L));
+        cur = std::move(next);
+        cm /= 2;
+        cn /= 2;
+        ck_ /= 2;
+    }
+    // base products: one grouped launch (outputs are either C itself or a level's contiguous M batch)
+    std::vector<GemmOperand> ea, eb;
+    for (auto& pr : cur) {
+        ea.push_back(pr.a);
+        eb.push_back(pr.b);
+    }
+    if (levels.empty())
+        gemm_batch_dev(p, cm, cn, ck_, ea, eb, C, ldc, 0, s);
+    else
+        gemm_batch_dev(p, cm, cn, ck_, ea, eb, levels.back().m_out, (long long)cn, (long long)cm * cn, s);
+    // post-additions, deepest level first
+    for (size_t l = levels.size(); l-- > 0;) {
+        Level& L = levels[l];
+        for (size_t q = 0; q < L.parents.size(); ++q) {
+            const Prob& pr = L.parents[q];
+            ck(launch_wino_post(L.m_out + (long long)q * 7 * L.hm * L.hn, L.hm * L.hn, L.hn, (int)L.hm, (int)L.hn, pp,
+                                pr.c, pr.ldc, s),
+               "winograd post");
+        }
+    }
+    ck(cudaStreamSynchronize(s), "sync");
 }
 
 // Core device call: everything resident on the device.
@@ -1700,6 +1826,64 @@ int fsyrk_b200_gemm_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t
         ck(cudaMemcpy(buf.data(), out.ptr, m * n * 4, cudaMemcpyDeviceToHost), "D2H");
         for (size_t i = 0; i < m; ++i)
             for (size_t j = 0; j < n; ++j) c[i * ldc + j] = buf[i * n + j];
+    });
+}
+
+int fsyrk_b200_gemm_winograd_nt(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, const uint64_t* b,
+                                size_t n, size_t ldb, uint64_t* c, size_t ldc, fsyrk_b200_policy policy) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (lda < k || ldb < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "gemm_winograd_nt: dimension mismatch");
+        require_device();
+        if (m == 0 || n == 0) return;
+        const size_t kk = std::max<size_t>(k, 1);
+        DevBuf d64a, d64b, d64c;
+        d64a.ensure(m * kk * 8);
+        d64b.ensure(n * kk * 8);
+        d64c.ensure(m * n * 8);
+        if (k > 0) {
+            ck(cudaMemcpy2D(d64a.ptr, k * 8, a, lda * 8, k * 8, m, cudaMemcpyHostToDevice), "H2D A");
+            ck(cudaMemcpy2D(d64b.ptr, k * 8, b, ldb * 8, k * 8, n, cudaMemcpyHostToDevice), "H2D B");
+        }
+        check_status(fsyrk_b200_gemm_winograd_nt_dev(p, static_cast<uint64_t*>(d64a.ptr), m, k, kk,
+                                                     static_cast<uint64_t*>(d64b.ptr), n, kk,
+                                                     static_cast<uint64_t*>(d64c.ptr), n, policy, nullptr));
+        ck(cudaMemcpy2D(c, ldc * 8, d64c.ptr, n * 8, n * 8, m, cudaMemcpyDeviceToHost), "D2H C");
+    });
+}
+
+int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m, size_t k, size_t lda,
+                                    const uint64_t* b_dev, size_t n, size_t ldb, uint64_t* c_dev, size_t ldc,
+                                    fsyrk_b200_policy policy, void* stream) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (lda < k || ldb < k || ldc < n) fail(FSYRK_B200_EDIMENSION, "gemm_winograd_nt: dimension mismatch");
+        require_device();
+        if (m == 0 || n == 0) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t kk = std::max<size_t>(k, 1);
+        static std::mutex mu;
+        static DevBuf ra, rb, rc;
+        std::lock_guard<std::mutex> lk(mu);
+        ra.ensure(m * kk * 4);
+        rb.ensure(n * kk * 4);
+        rc.ensure(m * n * 4);
+        auto* A = static_cast<uint32_t*>(ra.ptr);
+        auto* B = static_cast<uint32_t*>(rb.ptr);
+        auto* C = static_cast<uint32_t*>(rc.ptr);
+        if (k == 0) {
+            ck(cudaMemsetAsync(C, 0, m * n * 4, s), "memset");
+        } else {
+            ck(launch_convert_in(a_dev, (long long)lda, (int)m, (int)k, (int)k, nullptr, (uint32_t)p, A, (long long)k, s),
+               "convert A");
+            ck(launch_convert_in(b_dev, (long long)ldb, (int)n, (int)k, (int)k, nullptr, (uint32_t)p, B, (long long)k, s),
+               "convert B");
+            wino_gemm_dev(p, A, (long long)k, m, B, (long long)k, n, k, C, (long long)n, policy, s);
+        }
+        ck(launch_u32_to_u64(C, (long long)n, (int)m, (int)n, c_dev, (long long)ldc, s), "widen C");
+        ck(cudaStreamSynchronize(s), "sync");
     });
 }
 

@@ -643,6 +643,66 @@ __global__ void fp2_combine_kernel(const uint64_t* __restrict__ r, long long ldr
     }
 }
 
+// ------------------------------------------------------------- Winograd
+// Pre-additions of one Strassen-Winograd level (winograd.hpp:118-169) on uint32 residue
+// blocks x11, x12, x21, x22 (rows x cols, stride ld); out = 4 contiguous blocks (stride ldo,
+// block stride bs).  side 0 (A): S1 = x21 + x22, S2 = S1 - x11, S3 = x11 - x21, S4 = x12 - S2.
+// side 1 (stored blocks of B, x11 = B'11, x12 = B'12, x21 = B'21, x22 = B'22):
+//   T1 = x12 - x11, T2 = x22 - T1, T3 = x22 - x12, T4 = T2 - x21.
+__global__ void wino_pre_kernel(const uint32_t* __restrict__ x11, const uint32_t* __restrict__ x12,
+                                const uint32_t* __restrict__ x21, const uint32_t* __restrict__ x22, long long ld,
+                                int rows, int cols, uint32_t p, int side, uint32_t* __restrict__ out, long long ldo,
+                                long long bs) {
+    pdl_wait();
+    pdl_trigger();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+        const long long o = (long long)i * ld + j;
+        const uint32_t a = x11[o], b = x12[o], c = x21[o], d = x22[o];
+        uint32_t r0, r1, r2, r3;
+        if (side == 0) {
+            r0 = addm(c, d, p);
+            r1 = subm(r0, a, p);
+            r2 = subm(a, c, p);
+            r3 = subm(b, r1, p);
+        } else {
+            r0 = subm(b, a, p);
+            r1 = subm(d, r0, p);
+            r2 = subm(d, b, p);
+            r3 = subm(r1, c, p);
+        }
+        const long long q = (long long)i * ldo + j;
+        out[q] = r0;
+        out[bs + q] = r1;
+        out[2 * bs + q] = r2;
+        out[3 * bs + q] = r3;
+    }
+}
+
+// Post-additions: M1..M7 (rows x cols each, block stride bs, row stride ldm) -> the four
+// quadrants of C (stride ldc): C11 = M1 + M2, U2 = M1 + M6, U3 = U2 + M7, U4 = U2 + M5,
+// C12 = U4 + M3, C21 = U3 - M4, C22 = U3 + M5.
+__global__ void wino_post_kernel(const uint32_t* __restrict__ mm, long long bs, long long ldm, int rows, int cols,
+                                 uint32_t p, uint32_t* __restrict__ c, long long ldc) {
+    pdl_wait();
+    pdl_trigger();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+        const long long o = (long long)i * ldm + j;
+        const uint32_t m1 = mm[o], m2 = mm[bs + o], m3 = mm[2 * bs + o], m4 = mm[3 * bs + o], m5 = mm[4 * bs + o],
+                       m6 = mm[5 * bs + o], m7 = mm[6 * bs + o];
+        const uint32_t u2 = addm(m1, m6, p), u3 = addm(u2, m7, p), u4 = addm(u2, m5, p);
+        uint32_t* r0 = c + (long long)i * ldc + j;
+        uint32_t* r1 = c + (long long)(i + rows) * ldc + j;
+        r0[0] = addm(m1, m2, p);
+        r0[cols] = addm(u4, m3, p);
+        r1[0] = subm(u3, m4, p);
+        r1[cols] = addm(u3, m5, p);
+    }
+}
+
 // rows covered by grid.y (each block loops over rows with stride gridDim.y): about 8 waves of 148 SMs
 int rows_grid(int rows, int gx) {
     int gy = (148 * 32 + gx - 1) / gx;
@@ -766,6 +826,23 @@ cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int co
     const long long total = (long long)rows * cols;
     if (total == 0) return cudaSuccess;
     return launch_pdl(u32_to_u64_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ldx, rows, cols, out, ldo);
+}
+
+cudaError_t launch_wino_pre(const uint32_t* x11, const uint32_t* x12, const uint32_t* x21, const uint32_t* x22,
+                            long long ld, int rows, int cols, uint32_t p, int side, uint32_t* out, long long ldo,
+                            long long bs, cudaStream_t s) {
+    if ((long long)rows * cols == 0) return cudaSuccess;
+    const int gx = (cols + 255) / 256;
+    return launch_pdl(wino_pre_kernel, dim3(gx, rows_grid(rows, gx)), dim3(256), 0, s, x11, x12, x21, x22, ld, rows,
+                      cols, p, side, out, ldo, bs);
+}
+
+cudaError_t launch_wino_post(const uint32_t* m, long long bs, long long ldm, int rows, int cols, uint32_t p,
+                             uint32_t* c, long long ldc, cudaStream_t s) {
+    if ((long long)rows * cols == 0) return cudaSuccess;
+    const int gx = (cols + 255) / 256;
+    return launch_pdl(wino_post_kernel, dim3(gx, rows_grid(rows, gx)), dim3(256), 0, s, m, bs, ldm, rows, cols, p, c,
+                      ldc);
 }
 
 cudaError_t launch_deinterleave(const uint64_t* a, long long ldp, int n, int k, uint64_t* x, uint64_t* y,

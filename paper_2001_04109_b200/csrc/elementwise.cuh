@@ -103,6 +103,13 @@ cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,
                             uint32_t alpha, uint32_t beta, cudaStream_t s);
 cudaError_t launch_mirror(uint64_t* c, long long ldc, int n, cudaStream_t s);
+// Strassen-Winograd level: pre-additions (side 0: A blocks -> S1..S4, side 1: stored B blocks ->
+// T1..T4) and post-additions (M1..M7 -> the four quadrants of C)
+cudaError_t launch_wino_pre(const uint32_t* x11, const uint32_t* x12, const uint32_t* x21, const uint32_t* x22,
+                            long long ld, int rows, int cols, uint32_t p, int side, uint32_t* out, long long ldo,
+                            long long bs, cudaStream_t s);
+cudaError_t launch_wino_post(const uint32_t* m, long long bs, long long ldm, int rows, int cols, uint32_t p,
+                             uint32_t* c, long long ldc, cudaStream_t s);
 // F_{p^2}: split (a, b) pairs into X, Y; combine R (real part) and G into C pairs
 cudaError_t launch_deinterleave(const uint64_t* a, long long ldp, int n, int k, uint64_t* x, uint64_t* y,
                                 cudaStream_t s);

@@ -93,7 +93,8 @@ EXPORTS = (
     "fsyrk_b200_set_phase_timing", "fsyrk_b200_last_phase_ms", "fsyrk_b200_level_blocks", "fsyrk_b200_gemm_nt",
     "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
     "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
-    "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2",
+    "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2", "fsyrk_b200_gemm_winograd_nt",
+    "fsyrk_b200_gemm_winograd_nt_dev",
 )
 
 
@@ -140,6 +141,12 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    L.fsyrk_b200_gemm_winograd_nt.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                              ctypes.c_size_t, _u64p, ctypes.c_size_t, ctypes.c_size_t, _u64p,
+                                              ctypes.c_size_t, _Policy]
+    L.fsyrk_b200_gemm_winograd_nt_dev.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
+                                                  ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
+                                                  ctypes.c_void_p, ctypes.c_size_t, _Policy, ctypes.c_void_p]
     for name in ("fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2"):
         getattr(L, name).argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
                                      _u64p, ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.POINTER(_OpCount)]
@@ -557,6 +564,27 @@ def gemm_nt(f: PrimeField, a: np.ndarray, b: np.ndarray) -> np.ndarray:
     c = np.zeros((m, n), dtype=np.uint64)
     _check(lib().fsyrk_b200_gemm_nt(f.p, pa, m, k, lda, pb, n, ldb, c.ctypes.data_as(_u64p), max(n, 1)))
     return c
+
+
+def gemm_winograd_nt(f: PrimeField, a: np.ndarray, b: np.ndarray, policy: Optional[RecursionPolicy] = None) -> np.ndarray:
+    """C = A B^T by Strassen-Winograd levels over the tensor-core product (winograd.hpp:195-202)."""
+    policy = policy or RecursionPolicy()
+    policy.validate()
+    pa, m, k, lda = _view(a, "a")
+    pb, n, kb, ldb = _view(b, "b")
+    if kb != k:
+        raise DimensionError("gemm_winograd_nt: dimension mismatch")
+    c = np.zeros((m, n), dtype=np.uint64)
+    pc, _, _, ldc = _view(c, "c")
+    _check(lib().fsyrk_b200_gemm_winograd_nt(f.p, pa, m, k, lda, pb, n, ldb, pc, ldc, policy._c()))
+    return c
+
+
+def gemm_winograd_nt_dev(p: int, a_ptr: int, m: int, k: int, lda: int, b_ptr: int, n: int, ldb: int, c_ptr: int,
+                         ldc: int, policy: RecursionPolicy, stream: int = 0) -> None:
+    _check(lib().fsyrk_b200_gemm_winograd_nt_dev(int(p), ctypes.c_void_p(a_ptr), int(m), int(k), int(lda),
+                                                 ctypes.c_void_p(b_ptr), int(n), int(ldb), ctypes.c_void_p(c_ptr),
+                                                 int(ldc), policy._c(), ctypes.c_void_p(stream)))
 
 
 def level_blocks(f: PrimeField, a: np.ndarray):

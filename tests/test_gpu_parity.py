@@ -334,3 +334,20 @@ def test_fp2_herk_and_syrk_battery(gpu, p):
         assert np.array_equal(cs[iu], cs.transpose(1, 0, 2)[iu])                           # symmetric
     with pytest.raises(ValueError):
         fs.herk_fast(q, np.zeros((2, 2, 2), np.uint64), fs.make_syrk_plan(q.base))       # not a herk plan
+
+
+@pytest.mark.parametrize("p", [65521, 131071, 2147483647, 13])
+def test_winograd_general_product(gpu, p):
+    # Strassen-Winograd levels over the tensor-core product (winograd.hpp:118-169, test_winograd.cpp):
+    # exact, so bit-identical to the direct product for every depth, odd sizes stopping the recursion
+    fs = gpu
+    f = fs.PrimeField(p)
+    for (m, n, k, thr, lev) in ((64, 64, 64, 2, 1), (256, 128, 192, 16, 2), (96, 160, 64, 8, 3),
+                                (130, 98, 70, 2, 4), (512, 512, 512, 64, 2), (33, 40, 50, 2, 3)):
+        a = orc.random_matrix(p, m, k, m + k)
+        b = orc.random_matrix(p, n, k, n + 3 * k)
+        c = fs.gemm_winograd_nt(f, a, b, fs.RecursionPolicy(thr, lev))
+        assert np.array_equal(c, fs.gemm_nt(f, a, b)), (p, m, n, k, lev)
+    a = np.full((128, 128), p - 1, dtype=np.uint64)  # extreme residues through every level
+    c = fs.gemm_winograd_nt(f, a, a, fs.RecursionPolicy(8, 3))
+    assert np.array_equal(c, fs.gemm_nt(f, a, a))

@@ -395,7 +395,8 @@ def main():
         return
 
     peaks = load_peaks()
-    int8_ops = 2.0 * plan.get("terms", 9) * plan.get("tensor_macs", 0)  # NT int8 MMAs per modular MAC
+    # algorithmic int8 ops: 2 x (distinct digit-plane products per modular MAC) x modular MACs
+    int8_ops = 2.0 * plan.get("terms", 9) * plan.get("tensor_macs", 0)
     nprod = max(1, launches.get("products", 1))
     prod_ms = phase["products"]
     peak_i8 = peaks.get("int8_tops")

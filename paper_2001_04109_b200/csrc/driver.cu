@@ -832,7 +832,8 @@ struct Plan {
         std::ostringstream o;
         static const char* scheme_names[] = {"limb2", "limb3", "limb4", "m17", "m31"};
         o << "{\"p\": " << p << ", \"n\": " << n << ", \"k\": " << k << ", \"scheme\": \"" << scheme_names[sch.id]
-          << "\", \"planes\": " << L << ", \"terms\": " << sch.nterms << ", \"accumulators\": " << sch.nacc
+          << "\", \"planes\": " << L << ", \"terms\": " << sch.products << ", \"mmas_per_kstep\": " << sch.nterms
+          << ", \"accumulators\": " << sch.nacc
           << ", \"limbs\": " << L << ", \"block_n\": " << BN
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
           << "}, \"nodes\": " << nodes.size() << ", \"arena_bytes\": " << arena_bytes

@@ -105,19 +105,39 @@ struct Scheme<SCHEME_M17> {
     }
 };
 // planes: A = B = {d0, d1, d2, d3, 2 d3}
+// FSYRK_M31_ACC4 = 1: the weight-2 term d2 e2 is issued twice into accumulator 0 instead of
+// getting its own accumulator: 17 MMAs into 4 accumulators, which fit 128-column tiles
+// (4 x 128 = 512 TMEM columns) -- full MMA rate (N = 96 runs at 86%, ubench_mma_rate.cu).
+// Accumulators are read as unsigned 32-bit (K <= 13210); 0: 16 MMAs, 5 accumulators, N = 96.
+#ifndef FSYRK_M31_ACC4
+#define FSYRK_M31_ACC4 1  // measured: cfg4 products 23.5 -> 20.2 ms (profiles/r01/variants.txt)
+#endif
+#ifndef FSYRK_M31_BK
+#define FSYRK_M31_BK 64
+#endif
+#ifndef FSYRK_M31_STAGES
+#define FSYRK_M31_STAGES (FSYRK_M31_ACC4 ? (FSYRK_M31_BK == 32 ? 5 : 2) : (FSYRK_PAIR ? 4 : 3))
+#endif
 template <>
 struct Scheme<SCHEME_M31> {
-    static constexpr int PA = 5, PB = 5, NACC = 5, NT = 16, BN = 96, BK = 64, STAGES = FSYRK_PAIR ? 4 : 3;
+    static constexpr bool ACC4 = FSYRK_M31_ACC4;
+    static constexpr int PA = 5, PB = 5, NACC = ACC4 ? 4 : 5, NT = ACC4 ? 17 : 16, BN = ACC4 ? 128 : 96,
+                         BK = FSYRK_M31_BK, STAGES = FSYRK_M31_STAGES;
     static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
-        constexpr Term T[NT] = {
+        constexpr Term T5[16] = {
         {0, 0, 0}, {1, 4, 0}, {4, 1, 0},             // s=0 and s=4 (2^32 = 2): d1 (2 e3) + (2 d3) e1
         {0, 1, 1}, {1, 0, 1}, {2, 4, 1}, {4, 2, 1},  // s=1 and s=5 (2^40 = 2 * 2^8)
         {0, 2, 2}, {1, 1, 2}, {2, 0, 2}, {4, 3, 2},  // s=2 and s=6 (2^48 = 2 * 2^16): (2 d3) e3
         {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3},  // s=3
-        {2, 2, 4}};
-        return T[q];
-    }                                  // d2 e2, weight 2^32 = 2
+        {2, 2, 4}};                                  // d2 e2, weight 2^32 = 2
+        constexpr Term T4[17] = {
+        {0, 0, 0}, {1, 4, 0}, {4, 1, 0}, {2, 2, 0}, {2, 2, 0},  // s=0, s=4: ... + 2 d2 e2 as two MMAs
+        {0, 1, 1}, {1, 0, 1}, {2, 4, 1}, {4, 2, 1},
+        {0, 2, 2}, {1, 1, 2}, {2, 0, 2}, {4, 3, 2},
+        {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}};
+        return ACC4 ? T4[q] : T5[q];
+    }
 };
 
 // --------------------------------------------------------------- encoding
@@ -161,8 +181,8 @@ __device__ __forceinline__ uint32_t fold_acc(const uint32_t* a, const ModP& m, c
         uint32_t r = (uint32_t)v;
         return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
     } else if constexpr (S == SCHEME_M31) {
-        uint64_t v = (uint64_t)a[0] + ((uint64_t)a[1] << 8) + ((uint64_t)a[2] << 16) + ((uint64_t)a[3] << 24) +
-                     ((uint64_t)a[4] << 1);  // < 2^56
+        uint64_t v = (uint64_t)a[0] + ((uint64_t)a[1] << 8) + ((uint64_t)a[2] << 16) + ((uint64_t)a[3] << 24);
+        if constexpr (!Scheme<S>::ACC4) v += (uint64_t)a[Scheme<S>::NACC - 1] << 1;  // < 2^57
         v = (v & 0x7FFFFFFFull) + (v >> 31);  // < 2^31 + 2^25
         v = (v & 0x7FFFFFFFull) + (v >> 31);
         uint32_t r = (uint32_t)v;

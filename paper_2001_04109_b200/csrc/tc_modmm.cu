@@ -40,9 +40,10 @@ namespace {
 template <int S>
 SchemeInfo info() {
     using Sc = Scheme<S>;
-    return SchemeInfo{S,      planes_of<S>(), Sc::PA,          Sc::PB,
-                      Sc::NACC, Sc::NT,       Sc::BN,          Sc::BK,
-                      Cfg<S>::TILE_M, Cfg<S>::B_ROWS, Sc::UNSIGNED};
+    // M31 with 4 accumulators issues d2 e2 twice (weight 2): 17 MMAs for 16 digit products
+    const int products = (S == SCHEME_M31 && Sc::NT == 17) ? 16 : Sc::NT;
+    return SchemeInfo{S,      planes_of<S>(), Sc::PA,   Sc::PB,         Sc::NACC,       Sc::NT,
+                      products, Sc::BN,       Sc::BK,   Cfg<S>::TILE_M, Cfg<S>::B_ROWS, Sc::UNSIGNED};
 }
 
 uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
@@ -71,8 +72,10 @@ size_t modmm_k_limit(const SchemeInfo& s, uint64_t p) {
     switch (s.id) {
         case SCHEME_M17:  // <= 3 terms of (2 d) e <= 126 * 63 per accumulator
             return (size_t)(i32 / (3ull * 126 * 63));
-        case SCHEME_M31:  // <= 4 terms of <= 255 * 254 per accumulator
-            return (size_t)(i32 / (4ull * 255 * 254));
+        case SCHEME_M31:
+            if (Scheme<SCHEME_M31>::ACC4)  // accumulator 0: 5 terms of <= 255 * 255, read as uint32
+                return (size_t)(0xFFFFFFFFull / (5ull * 255 * 255));
+            return (size_t)(i32 / (4ull * 255 * 254));  // <= 4 terms of <= 255 * 254 per accumulator
         default: {
             const int L = s.planes;
             const uint64_t k32 = i32 / ((uint64_t)L * 16384ull);  // |T_s| <= L K 2^14

@@ -45,7 +45,8 @@ struct SchemeInfo {
     int id;
     int planes;   // planes stored for an operand read in both roles (leaf SYRK operands)
     int pa, pb;   // planes the A / B role reads (GEMM operands store only these)
-    int nacc, nterms;
+    int nacc, nterms;  // accumulators; MMAs issued per 32-deep K step
+    int products;      // distinct digit-plane products per modular MAC (the algorithmic count)
     int bn, bk;
     int bm;       // output rows per tile: 128, or 256 on a CTA pair
     int b_box;    // B rows one CTA stages per tile (bn, or bn / 2 on a CTA pair)

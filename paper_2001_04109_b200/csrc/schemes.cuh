@@ -47,9 +47,12 @@ struct Term {
 template <int S>
 struct Scheme;
 
+#ifndef FSYRK_LIMB2_BN
+#define FSYRK_LIMB2_BN 128
+#endif
 template <>
 struct Scheme<SCHEME_LIMB2> {
-    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = 128, BK = 128, STAGES = FSYRK_PAIR ? 4 : 3;
+    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = FSYRK_LIMB2_BN, BK = 128, STAGES = FSYRK_PAIR ? 4 : 3;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
@@ -208,13 +211,14 @@ struct SplitFold<SCHEME_M17> {
     using V = uint32_t;
     // f(x) = (x mod 2^17) + (x >> 17) = x (mod 2^17 - 1); for x < 2^32: f(x) < 2^17 + 2^15
     __device__ __forceinline__ static uint32_t f(uint32_t x) { return (x & 0x1FFFFu) + (x >> 17); }
-    // short_k: accumulators < 2^26 (K <= 2048), so a1 << 6 still fits 32 bits
+    // short_k (K <= 2048): per k, a0 <= 63*63 + 2*126*63 = 19845, a1 <= 15876, a2 <= 11907, so
+    // a0 + 2^6 a1 + 2^12 f(a2) <= 40.6e6 + 2.08e9 + 2^29.0 < 2^32 -- five integer ops
     __device__ __forceinline__ static V partial(const uint32_t* a, bool short_k) {
-        return short_k ? a[0] + f(a[1] << 6) + (f(a[2]) << 12)      // < 2^26 + 2^18 + 2^30
+        return short_k ? a[0] + (a[1] << 6) + (f(a[2]) << 12)
                        : f(a[0]) + (f(a[1]) << 6) + (f(a[2]) << 12);  // any a < 2^31: < 2^30
     }
     __device__ __forceinline__ static uint32_t final(V v, const ModP&) {
-        const uint32_t r = f(v);  // < 2^17 + 2^15 < 2p
+        const uint32_t r = f(v);  // v < 2^32: r < 2^17 + 2^15 < 2p
         return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
     }
 };

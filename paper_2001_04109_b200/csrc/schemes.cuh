@@ -167,7 +167,7 @@ __host__ __device__ inline uint64_t encode_planes(uint32_t x, uint32_t p) {
 
 // planes stored for an operand read in both roles (leaf SYRK operands)
 template <int S>
-constexpr int planes_of() {
+__host__ __device__ constexpr int planes_of() {
     return Scheme<S>::PA > Scheme<S>::PB ? Scheme<S>::PA : Scheme<S>::PB;
 }
 

@@ -39,6 +39,9 @@ namespace tc {
 #ifndef FSYRK_TSTORE_ALL
 #define FSYRK_TSTORE_ALL 0
 #endif
+#ifndef FSYRK_STG256
+#define FSYRK_STG256 0  // 256-bit direct stores from the epilogue (experiment; with FSYRK_NO_TSTORE)
+#endif
 #ifndef FSYRK_NO_TSTORE
 #define FSYRK_NO_TSTORE 0
 #endif
@@ -283,6 +286,18 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
                 const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
                 if (full_chunk) {
+#if FSYRK_STG256
+                    if ((reinterpret_cast<uintptr_t>(out + gc0) & 31) == 0) {  // two full 32-byte sectors
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+                            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + gc0 + 8 * q),
+                                         "r"(res[8 * q]), "r"(res[8 * q + 1]), "r"(res[8 * q + 2]), "r"(res[8 * q + 3]),
+                                         "r"(res[8 * q + 4]), "r"(res[8 * q + 5]), "r"(res[8 * q + 6]),
+                                         "r"(res[8 * q + 7])
+                                         : "memory");
+                        return;
+                    }
+#endif
                     uint4* o = reinterpret_cast<uint4*>(out + gc0);
 #pragma unroll
                     for (int q = 0; q < 4; ++q)

@@ -172,13 +172,28 @@ std::vector<int> partition_owners(int h, int nranks, int kPartBlock) {
     for (int i = 0; i < nb; ++i)
         for (int j = 0; j <= i; ++j) pc.push_back({rows(i) * rows(j) * (i == j ? 0.5 : 1.0), i, j});
     std::stable_sort(pc.begin(), pc.end(), [](const PairCost& a, const PairCost& b) { return a.cost > b.cost; });
+    // Each rank also prepares the operand rows of every block its pairs touch (the pre-additions
+    // of the top level), so a block new to a rank costs about one block pair of products
+    // (kBlockCost); pairs go, longest first, to the rank where they add the least total work.
+    constexpr double kBlockCost = 1.0;
     std::vector<double> load(nranks, 0.0);
+    std::vector<std::vector<char>> need(nranks, std::vector<char>(nb, 0));
     for (const auto& q : pc) {
-        int r = 0;
-        for (int t = 1; t < nranks; ++t)
-            if (load[t] < load[r]) r = t;
-        load[r] += q.cost;
-        owner[(size_t)q.i * nb + q.j] = r;
+        int best = 0;
+        double best_score = 0;
+        for (int t = 0; t < nranks; ++t) {
+            double extra = q.cost;
+            if (!need[t][q.i]) extra += kBlockCost * rows(q.i) * kPartBlock;
+            if (q.j != q.i && !need[t][q.j]) extra += kBlockCost * rows(q.j) * kPartBlock;
+            const double score = load[t] + extra;
+            if (t == 0 || score < best_score) {
+                best = t;
+                best_score = score;
+            }
+        }
+        load[best] = best_score;
+        need[best][q.i] = need[best][q.j] = 1;
+        owner[(size_t)q.i * nb + q.j] = best;
     }
     return owner;
 }
@@ -400,7 +415,7 @@ struct Plan {
         colmap = colmap_;
         prank = rank_;
         pnranks = nranks_;
-        sch = scheme_for(p);
+        sch = scheme_for(p, nranks_);
         L = sch.planes;
         BN = sch.bn;
         BK = sch.bk;
@@ -735,6 +750,16 @@ struct Plan {
             }
             std::vector<PrepNode> tab;
             a.aligned = 1;
+            a.part_block = 0;
+            a.need_mask = ~0ull;
+            if (partitioned && n0.parent < 0 && part_nb <= 64) {  // the root: this rank's row blocks only
+                unsigned long long need = 0;
+                for (int bi = 0; bi < part_nb; ++bi)
+                    for (int bj = 0; bj <= bi; ++bj)
+                        if (owns_block_pair(bi, bj)) need |= (1ull << bi) | (1ull << bj);
+                a.part_block = kPartBlock;
+                a.need_mask = need;
+            }
             for (int ni : pg.nodes) {
                 const Node& nd = nodes[ni];
                 GemmGroup& g = gemms[nd.ggroup];
@@ -1695,7 +1720,7 @@ int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, s
     return guarded([&] {
         if (nranks < 1) fail(FSYRK_B200_EINVAL, "nranks must be >= 1");
         validate_field(p);
-        const SchemeInfo si = scheme_for(p);
+        const SchemeInfo si = scheme_for(p, nranks);
         const int blk = part_block_for(si.bm, si.bn);
         std::vector<int> own = partition_owners((int)h, nranks, blk);
         const size_t nb = (h + blk - 1) / blk;
@@ -1765,8 +1790,9 @@ int fsyrk_b200_level_blocks(uint64_t p, const uint64_t* a, size_t n, size_t k, s
         // recombine digit planes -> residues on the host (white-box readback only): the first
         // `nd` planes are the digits of base 2^bits, signed for the balanced LIMB schemes
         const int sid = plan.sch.id;
-        const int nd = sid == SCHEME_M17 ? 3 : sid == SCHEME_M31 ? 4 : L;
-        const int bits = sid == SCHEME_M17 ? 6 : 8;
+        const bool m17 = sid == SCHEME_M17 || sid == SCHEME_M17N;
+        const int nd = m17 ? 3 : sid == SCHEME_M31 ? 4 : L;
+        const int bits = m17 ? 6 : 8;
         const bool sgn = !plan.sch.is_unsigned;
         auto read_planes = [&](const int8_t* base, long long plane, long long row, int rows, int cols, uint64_t* out) {
             std::vector<int8_t> buf((size_t)plane * nd);

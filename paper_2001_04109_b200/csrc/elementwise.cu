@@ -117,7 +117,7 @@ __device__ __forceinline__ uint32_t bytes_k(const uint4& x, int k) { return gath
 
 template <int S>
 __device__ __forceinline__ void planes4(uint4 x, uint32_t p, uint32_t (&w)[planes_of<S>()]) {
-    if constexpr (S == SCHEME_M17) {  // x < 2^17: d0 = x[0:6), d1 = x[6:12), d2 = x[12:17)
+    if constexpr (digits_of<S> == SCHEME_M17) {  // x < 2^17: d0 = x[0:6), d1 = x[6:12), d2 = x[12:17)
         const uint32_t lo = bytes_k(x, 0), hi = bytes_k(x, 1), top = bytes_k(x, 2);
         w[0] = lo & 0x3F3F3F3Fu;
         w[1] = ((lo >> 6) & 0x03030303u) | ((hi << 2) & 0x3C3C3C3Cu);
@@ -189,6 +189,7 @@ __global__ void prep_kernel(const PrepArgs args) {
     const int jp = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (jp >= ncw || i >= h) return;
+    if (args.part_block && !((args.need_mask >> (i / args.part_block)) & 1ull)) return;  // not this rank's rows
     const Src src = make_src(nd.in, args.a64, args.ld64);
 
     const int nc = args.pair ? 2 : 1;
@@ -360,6 +361,7 @@ __global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const Pr
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (g >= ncg || i >= args.h) return;
+    if (args.part_block && !((args.need_mask >> (i / args.part_block)) & 1ull)) return;  // not this rank's rows
     const PrepNode local = nd;
     if (local.in.in64) prep_vec_body<S, PAIR, true>(args, local, i, g);
     else prep_vec_body<S, PAIR, false>(args, local, i, g);
@@ -790,6 +792,7 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
         case SCHEME_LIMB3: FSYRK_SPLIT(SCHEME_LIMB3) break;
         case SCHEME_LIMB4: FSYRK_SPLIT(SCHEME_LIMB4) break;
         case SCHEME_M17: FSYRK_SPLIT(SCHEME_M17) break;
+        case SCHEME_M17N: FSYRK_SPLIT(SCHEME_M17N) break;
         case SCHEME_M31: FSYRK_SPLIT(SCHEME_M31) break;
         default: return cudaErrorInvalidValue;
     }
@@ -804,6 +807,7 @@ cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s) {
         case SCHEME_LIMB3: return prep_dispatch<SCHEME_LIMB3>(args, s);
         case SCHEME_LIMB4: return prep_dispatch<SCHEME_LIMB4>(args, s);
         case SCHEME_M17: return prep_dispatch<SCHEME_M17>(args, s);
+        case SCHEME_M17N: return prep_dispatch<SCHEME_M17N>(args, s);
         case SCHEME_M31: return prep_dispatch<SCHEME_M31>(args, s);
         default: return cudaErrorInvalidValue;
     }

@@ -59,6 +59,10 @@ struct PrepArgs {
     const PrepNode* nodes;
     int nnodes;
     int aligned;  // every node's input rows allow 16-byte vector loads at 4-column steps (driver-checked)
+    // multi-GPU partition: only rows i of blocks (i / part_block) set in need_mask are prepared
+    // (the row blocks of this rank's block pairs); part_block = 0: all rows
+    int part_block;
+    unsigned long long need_mask;
 };
 
 struct PostNode {

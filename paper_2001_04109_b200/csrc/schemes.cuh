@@ -29,7 +29,17 @@
 
 namespace fsyrk_b200 {
 
-enum SchemeId { SCHEME_LIMB2 = 0, SCHEME_LIMB3 = 1, SCHEME_LIMB4 = 2, SCHEME_M17 = 3, SCHEME_M31 = 4 };
+enum SchemeId {
+    SCHEME_LIMB2 = 0,
+    SCHEME_LIMB3 = 1,
+    SCHEME_LIMB4 = 2,
+    SCHEME_M17 = 3,
+    SCHEME_M31 = 4,
+    SCHEME_M17N = 5  // M17 digits with 128-column tiles (fine multi-GPU partitions: blocks of 128)
+};
+// the digit arithmetic a scheme shares with another one (M17N is M17 with narrower tiles)
+template <int S>
+inline constexpr int digits_of = S == SCHEME_M17N ? SCHEME_M17 : S;
 
 struct Term {
     int8_t a, b, acc;
@@ -107,6 +117,11 @@ struct Scheme<SCHEME_M17> {
         return PAIR ? TB[q] : TA[q];
     }
 };
+template <>
+struct Scheme<SCHEME_M17N> : Scheme<SCHEME_M17> {
+    static constexpr int BN = 128;
+};
+
 // planes: A = B = {d0, d1, d2, d3, 2 d3}
 // FSYRK_M31_ACC4 = 1: the weight-2 term d2 e2 is issued twice into accumulator 0 instead of
 // getting its own accumulator: 17 MMAs into 4 accumulators, which fit 128-column tiles
@@ -147,7 +162,7 @@ struct Scheme<SCHEME_M31> {
 // Byte l of the result is plane l of residue x (canonical, x < p).
 template <int S>
 __host__ __device__ inline uint64_t encode_planes(uint32_t x, uint32_t p) {
-    if constexpr (S == SCHEME_M17) {
+    if constexpr (digits_of<S> == SCHEME_M17) {
         const uint32_t d0 = x & 63u, d1 = (x >> 6) & 63u, d2 = x >> 12;
         return (uint64_t)d0 | (uint64_t)d1 << 8 | (uint64_t)d2 << 16 | (uint64_t)(2 * d1) << 24 |
                (uint64_t)(2 * d2) << 32;
@@ -176,7 +191,7 @@ __host__ __device__ constexpr int planes_of() {
 // w: balanced weights (LIMB schemes only).
 template <int S>
 __device__ __forceinline__ uint32_t fold_acc(const uint32_t* a, const ModP& m, const int32_t* w) {
-    if constexpr (S == SCHEME_M17) {
+    if constexpr (digits_of<S> == SCHEME_M17) {
         // unsigned accumulators < 2^31: v < 2^44
         uint64_t v = (uint64_t)a[0] + ((uint64_t)a[1] << 6) + ((uint64_t)a[2] << 12);
         v = (v & 0x1FFFFull) + (v >> 17);  // < 2^28
@@ -222,6 +237,8 @@ struct SplitFold<SCHEME_M17> {
         return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
     }
 };
+template <>
+struct SplitFold<SCHEME_M17N> : SplitFold<SCHEME_M17> {};
 // LIMB2 (p <= 2^16): the exact integer  sum_x r_x r_y = a0 + 2^8 a1 + 2^16 a2  of the balanced
 // representatives, |.| <= K 2^30 < 2^62 within the scheme's K bound; reduced mod p afterwards.
 template <>

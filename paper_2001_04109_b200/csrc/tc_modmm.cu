@@ -31,6 +31,10 @@
 #include "tc_modmm.h"
 #include "tc_modmm_kernel.cuh"
 
+#ifndef FSYRK_M17N_RANKS
+#define FSYRK_M17N_RANKS 0
+#endif
+
 namespace fsyrk_b200 {
 
 using namespace tc;
@@ -59,8 +63,12 @@ uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
 
 }  // namespace
 
-SchemeInfo scheme_for(uint64_t p) {
-    if (p == 131071ull) return info<SCHEME_M17>();
+SchemeInfo scheme_for(uint64_t p, int nranks) {
+    // FSYRK_M17N_RANKS (0 = never): partitioned plans over at least this many ranks use 128-column
+    // M17 tiles so the partition blocks are 128 instead of 640 rows (measured: finer blocks
+    // balance better but every rank then touches most blocks' pre-additions; off by default)
+    if (p == 131071ull)
+        return FSYRK_M17N_RANKS > 0 && nranks >= FSYRK_M17N_RANKS ? info<SCHEME_M17N>() : info<SCHEME_M17>();
     if (p == 2147483647ull) return info<SCHEME_M31>();
     if (p <= 65536ull) return info<SCHEME_LIMB2>();
     if (p <= 16777216ull) return info<SCHEME_LIMB3>();
@@ -71,6 +79,7 @@ size_t modmm_k_limit(const SchemeInfo& s, uint64_t p) {
     const uint64_t i32 = (1ull << 31) - 1;
     switch (s.id) {
         case SCHEME_M17:  // <= 3 terms of (2 d) e <= 126 * 63 per accumulator
+        case SCHEME_M17N:
             return (size_t)(i32 / (3ull * 126 * 63));
         case SCHEME_M31:
             if (Scheme<SCHEME_M31>::ACC4)  // accumulator 0: 5 terms of <= 255 * 255, read as uint32
@@ -88,7 +97,7 @@ size_t modmm_k_limit(const SchemeInfo& s, uint64_t p) {
 
 void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w) {
     for (int i = 0; i < 8; ++i) w[i] = 0;
-    if (s.id == SCHEME_M17 || s.id == SCHEME_M31) return;  // constant weights inside fold_acc
+    if (s.id == SCHEME_M17 || s.id == SCHEME_M17N || s.id == SCHEME_M31) return;  // constants inside fold_acc
     for (int i = 0; i < 8; ++i) {
         uint64_t v = powmod(256, (uint64_t)i, p);
         w[i] = v > p / 2 ? (int32_t)((int64_t)v - (int64_t)p) : (int32_t)v;
@@ -101,6 +110,7 @@ cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid,
         case SCHEME_LIMB3: return launch_cfg<SCHEME_LIMB3>(args, grid, stream);
         case SCHEME_LIMB4: return launch_cfg<SCHEME_LIMB4>(args, grid, stream);
         case SCHEME_M17: return launch_cfg<SCHEME_M17>(args, grid, stream);
+        case SCHEME_M17N: return launch_cfg<SCHEME_M17N>(args, grid, stream);
         case SCHEME_M31: return launch_cfg<SCHEME_M31>(args, grid, stream);
         default: return cudaErrorInvalidValue;
     }
@@ -152,6 +162,7 @@ int modmm_grid(const SchemeInfo& s, int nsm) {
         case SCHEME_LIMB3: return grid_for<SCHEME_LIMB3>(nsm);
         case SCHEME_LIMB4: return grid_for<SCHEME_LIMB4>(nsm);
         case SCHEME_M17: return grid_for<SCHEME_M17>(nsm);
+        case SCHEME_M17N: return grid_for<SCHEME_M17N>(nsm);
         case SCHEME_M31: return grid_for<SCHEME_M31>(nsm);
         default: return nsm;
     }

@@ -52,7 +52,9 @@ struct SchemeInfo {
     int b_box;    // B rows one CTA stages per tile (bn, or bn / 2 on a CTA pair)
     bool is_unsigned;
 };
-SchemeInfo scheme_for(uint64_t p);
+// nranks >= 3: partitioned multi-GPU plans use narrower tiles where that makes the partition
+// blocks (lcm of the tile sides) finer (p = 2^17 - 1: 128 instead of 640)
+SchemeInfo scheme_for(uint64_t p, int nranks = 1);
 // Largest inner dimension for which the scheme's int32 accumulators and fold stay exact.
 size_t modmm_k_limit(const SchemeInfo& s, uint64_t p);
 void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w);

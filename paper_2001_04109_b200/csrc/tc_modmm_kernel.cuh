@@ -94,7 +94,7 @@ struct Cfg {
     // 1024-aligned (__align__ on the extern array, checked at entry)
     // TMA stores: measured faster for the Mersenne schemes (cfg2 products 185 -> 178 us, cfg5
     // 3.18 -> 2.89 ms), neutral to slightly slower for LIMB2 (cfg3 251 -> 254 us)
-    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (S == SCHEME_M17 || S == SCHEME_M31 || FSYRK_TSTORE_ALL) &&
+    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (digits_of<S> == SCHEME_M17 || S == SCHEME_M31 || FSYRK_TSTORE_ALL) &&
                                    STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES <= 232448;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (TSTORE ? OUT_BYTES : 0) + BAR_BYTES;
     static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1

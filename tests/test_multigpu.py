@@ -42,12 +42,19 @@ def test_partition_owners_complete_and_balanced(fsyrk, p, h, nranks):
     assert (lower >= 0).all() and (lower < nranks).all()
     assert (own[np.triu_indices(nb, 1)] == -1).all()
     rows = [min(BLOCK, h - b * BLOCK) for b in range(nb)]
+    # per-rank work: its block pairs' products plus the pre-additions of every block they touch
+    # (one block ~ one block pair of products, the planner's cost model)
     load = np.zeros(nranks)
+    touched = [set() for _ in range(nranks)]
     for bi in range(nb):
         for bj in range(bi + 1):
-            load[own[bi, bj]] += rows[bi] * rows[bj] * (0.5 if bi == bj else 1.0)
+            r = own[bi, bj]
+            load[r] += rows[bi] * rows[bj] * (0.5 if bi == bj else 1.0)
+            touched[r] |= {bi, bj}
+    for r in range(nranks):
+        load[r] += sum(rows[b] * BLOCK for b in touched[r])
     if nb * (nb + 1) // 2 >= 4 * nranks:
-        assert load.max() / load.mean() < 1.15
+        assert load.max() / load.mean() < 1.2
 
 
 def _gloo_worker(rank, world, port, n, p, result_q):

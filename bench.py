@@ -425,7 +425,9 @@ def main():
     line = {"metric": METRIC, "value": round(value, 2), "unit": "GOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
             "scaling": "strong" if part else "weak", "vs_baseline": None,
-            "dtype": "u32 residues / s8 limbs, s32 accumulate",
+            "dtype": "int8",  # tensor-core digit products (int32 accumulate); uint32 residues elsewhere
+            "dtype_detail": "int8 digit planes x int8 -> int32 TMEM accumulators; uint32 mod-p residues in the "
+                            "elementwise kernels; uint64 at the API boundary",
             "data": "synthetic (reference random_matrix stream)",
             "config": {"workload": args.config, "p": p, "n": n, "k": k, "mode": cfg["mode"],
                        "threshold": cfg["threshold"], "levels": "inf" if cfg["levels"] == UNL else cfg["levels"],

@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfsyrk_b200.so")
-SOURCES = ["driver.cu", "tc_modmm.cu", "elementwise.cu"]
-HEADERS = ["modp.cuh", "sm100.cuh", "tc_modmm.h", "elementwise.cuh", "field_host.h"]
+SOURCES = ["driver.cu", "tc_modmm.cu", "elementwise.cu", "host_io.cu"]
+HEADERS = ["host_io.h", "modp.cuh", "sm100.cuh", "tc_modmm.h", "elementwise.cuh", "field_host.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

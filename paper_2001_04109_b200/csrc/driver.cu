@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cstdio>
 #include <cstring>
@@ -33,6 +34,7 @@
 #include "../../include/fsyrk_b200.h"
 #include "elementwise.cuh"
 #include "field_host.h"
+#include "host_io.h"
 #include "modp.cuh"
 #include "tc_modmm.h"
 
@@ -1463,7 +1465,52 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     fill_ops(ops, plan);
 }
 
-// Host call: stage A (and C when accumulating) through device buffers.
+// Host call: the caller's A (and Low(C_in) when accumulating) cross PCIe through host_io
+// (uint32 on the wire, narrowed / widened by host threads), the device computes, Low(C) comes
+// back the same way.  Only Low(C) is moved (the strict upper triangle is scratch,
+// fast_syrk.hpp:271-273); with beta = 0 the strict upper parts of the diagonal 256-row blocks
+// are cleared, the rest of the strict upper triangle is left as the caller had it.
+//
+// Accumulating into pinned C (FSYRK_B200_HOSTIO=auto|duplex): the uint64 row blocks of C_in
+// and of the result move unnarrowed but at the same time in both PCIe directions -- the device
+// computes alpha X into a side buffer while C_in streams in, then per chunk of row blocks
+// combines beta C_in + alpha X and sends the chunk back while later chunks still arrive.
+enum class IoMode { Auto, Narrow, Duplex };
+IoMode io_mode() {
+    static const IoMode m = [] {
+        const char* e = getenv("FSYRK_B200_HOSTIO");
+        if (!e) return IoMode::Auto;
+        if (!strcmp(e, "narrow")) return IoMode::Narrow;
+        if (!strcmp(e, "duplex")) return IoMode::Duplex;
+        return IoMode::Auto;
+    }();
+    return m;
+}
+
+struct IoStreams {
+    cudaStream_t main = nullptr, cin = nullptr, cout = nullptr;
+    cudaEvent_t a_done = nullptr;
+    std::vector<cudaEvent_t> in_ev, fin_ev;
+    void init() {
+        if (main) return;
+        ck(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&a_done, cudaEventDisableTiming), "event");
+    }
+    void events(size_t n) {
+        while (in_ev.size() < n) {
+            cudaEvent_t a, b;
+            ck(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+            in_ev.push_back(a);
+            fin_ev.push_back(b);
+        }
+    }
+};
+IoStreams g_io;
+DevBuf g_stage_x;
+
 void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const ColXform* xf,
               uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy pol, bool mirror, fsyrk_b200_opcount* ops) {
     validate_field(p);
@@ -1475,50 +1522,112 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     require_device();
     if (n == 0) return;
     std::lock_guard<std::mutex> lk(g_stage_mu);
+    g_io.init();
     const size_t abytes = n * std::max<size_t>(k, 1) * 8, cbytes = n * n * 8;
     g_stage_a.ensure(abytes);
     g_stage_c.ensure(cbytes);
     uint64_t* da = static_cast<uint64_t*>(g_stage_a.ptr);
     uint64_t* dc = static_cast<uint64_t*>(g_stage_c.ptr);
-    cudaStream_t s = 0;
+    cudaStream_t s = g_io.main;
     uint64_t h2d = 0, d2h = 0;
-    if (k > 0) {
-        ck(cudaMemcpy2DAsync(da, k * 8, a, lda * 8, k * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
-        h2d += n * k * 8;
-    }
-    // Only Low(C) crosses PCIe (the strict upper triangle is scratch, fast_syrk.hpp:271-273):
-    // row block [r0, r1) moves columns [0, r1), i.e. its lower part plus the strict upper part
-    // of its diagonal block -- about n^2/2 + n*kTriRows/2 elements instead of n^2.
-    auto tri_copy = [&](bool to_dev) {
-        for (size_t r0 = 0; r0 < n; r0 += kTriRows) {
-            const size_t r1 = std::min(n, r0 + kTriRows);
-            if (to_dev)
-                ck(cudaMemcpy2DAsync(dc + r0 * n, n * 8, c + r0 * ldc, ldc * 8, r1 * 8, r1 - r0,
-                                     cudaMemcpyHostToDevice, s),
+    static const bool io_trace = getenv("FSYRK_B200_IO_TRACE") != nullptr;
+    auto tnow = [] {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    double tr[4] = {tnow(), 0, 0, 0};
+    hio::g_io_stats = hio::IoStats{};
+    const size_t lda_dev = k == 0 ? 1 : k;
+    const bool need_c = (beta % p) != 0;
+    const bool duplex = need_c && !mirror && io_mode() != IoMode::Narrow &&
+                        (io_mode() == IoMode::Duplex || hio::is_pinned(c));
+    // duplex: chunks of whole kTriRows-row blocks of C, ~32 MB each
+    std::vector<std::pair<size_t, size_t>> chunks;
+    auto blocks = [&](size_t r0, size_t r1, bool in) {
+        for (size_t b0 = r0; b0 < r1; b0 += kTriRows) {
+            const size_t b1 = std::min(r1, b0 + kTriRows);
+            if (in)
+                ck(cudaMemcpy2DAsync(dc + b0 * n, n * 8, c + b0 * ldc, ldc * 8, b1 * 8, b1 - b0,
+                                     cudaMemcpyHostToDevice, g_io.cin),
                    "H2D C");
             else
-                ck(cudaMemcpy2DAsync(c + r0 * ldc, ldc * 8, dc + r0 * n, n * 8, r1 * 8, r1 - r0,
-                                     cudaMemcpyDeviceToHost, s),
+                ck(cudaMemcpy2DAsync(c + b0 * ldc, ldc * 8, dc + b0 * n, n * 8, b1 * 8, b1 - b0,
+                                     cudaMemcpyDeviceToHost, g_io.cout),
                    "D2H C");
-            (to_dev ? h2d : d2h) += (r1 - r0) * r1 * 8;
+            (in ? h2d : d2h) += (b1 - b0) * b1 * 8;
         }
     };
-    const bool need_c = (beta % p) != 0;
-    if (need_c) tri_copy(true);  // syrk_fast_acc reads only Low(C_in)
-    run_dev(p, (uint32_t)(alpha % p), da, n, k, k == 0 ? 1 : k, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
-    if (mirror) {
-        ck(cudaMemcpy2DAsync(c, ldc * 8, dc, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
-        d2h += n * n * 8;
+    auto queue_cin = [&] {
+        for (size_t q = 0; q < chunks.size(); ++q) {
+            blocks(chunks[q].first, chunks[q].second, true);
+            ck(cudaEventRecord(g_io.in_ev[q], g_io.cin), "event");
+        }
+    };
+    // C_in follows A on the wire (A gates the compute); FSYRK_B200_CIN_EARLY=1 queues it first,
+    // sharing the H2D direction with A's narrowed chunks
+    static const bool cin_early = getenv("FSYRK_B200_CIN_EARLY") != nullptr;
+    if (duplex) {
+        for (size_t r0 = 0; r0 < n;) {
+            size_t r1 = r0, elems = 0;
+            while (r1 < n && (elems == 0 || elems < (size_t(4) << 20))) {
+                const size_t b1 = std::min(n, r1 + kTriRows);
+                elems += (b1 - r1) * b1;
+                r1 = b1;
+            }
+            chunks.push_back({r0, r1});
+            r0 = r1;
+        }
+        g_io.events(chunks.size());
+        if (cin_early) queue_cin();
+    }
+    if (k > 0) ck(hio::upload(a, lda, hio::Region{n, k, false}, da, k, s, &h2d), "H2D A");
+    if (io_trace) {
+        ck(cudaStreamSynchronize(s), "sync");
+        tr[1] = tnow();
+    }
+    if (!duplex) {
+        if (need_c) ck(hio::upload(c, ldc, hio::Region{n, n, true}, dc, n, s, &h2d), "H2D C");
+        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
+        if (io_trace) {
+            ck(cudaStreamSynchronize(s), "sync");
+            tr[2] = tnow();
+        }
+        ck(hio::download(dc, n, hio::Region{n, n, !mirror}, c, ldc, (need_c || mirror) ? 0 : kTriRows, s, &d2h),
+           "D2H C");
     } else {
-        // beta != 0: the diagonal blocks' strict upper parts round-trip the caller's values;
-        // beta = 0: they are cleared, so the returned scratch is deterministic (zeros there,
-        // the caller's values in the rest of the strict upper triangle)
-        if (!need_c) ck(launch_zero_upper(dc, (long long)n, (int)n, (int)kTriRows, s), "zero_upper");
-        tri_copy(false);
+        g_stage_x.ensure(cbytes);
+        uint64_t* dx = static_cast<uint64_t*>(g_stage_x.ptr);
+        if (!cin_early) {
+            ck(cudaEventRecord(g_io.a_done, s), "event");
+            ck(cudaStreamWaitEvent(g_io.cin, g_io.a_done, 0), "wait");
+            queue_cin();
+        }
+        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, 0, dx, n, pol, false, s, ops);
+        if (io_trace) {
+            ck(cudaStreamSynchronize(s), "sync");
+            tr[2] = tnow();
+        }
+        const ModP m = make_modp((uint32_t)p);
+        for (size_t q = 0; q < chunks.size(); ++q) {
+            ck(cudaStreamWaitEvent(s, g_io.in_ev[q], 0), "wait");
+            ck(hio::launch_acc_combine(dx, (long long)n, dc, (long long)n, (int)chunks[q].first, (int)chunks[q].second,
+                                       m, (uint32_t)(beta % p), s),
+               "acc_combine");
+            ck(cudaEventRecord(g_io.fin_ev[q], s), "event");
+            ck(cudaStreamWaitEvent(g_io.cout, g_io.fin_ev[q], 0), "wait");
+            blocks(chunks[q].first, chunks[q].second, false);
+        }
+        ck(cudaStreamSynchronize(g_io.cout), "sync");
     }
     ck(cudaStreamSynchronize(s), "sync");
     g_transfer[0] = h2d;
     g_transfer[1] = d2h;
+    if (io_trace) {
+        tr[3] = tnow();
+        fprintf(stderr, "[io] n=%zu k=%zu %s: A %.3f ms, C_in+compute %.3f ms, out %.3f ms, total %.3f ms; pool %.3f ms, slot waits %.3f ms, threads %d\n",
+                n, k, duplex ? "duplex" : "narrow", (tr[1] - tr[0]) * 1e3, (tr[2] - tr[1]) * 1e3,
+                (tr[3] - tr[2]) * 1e3, (tr[3] - tr[0]) * 1e3, hio::g_io_stats.host * 1e3, hio::g_io_stats.wait * 1e3,
+                hio::host_threads());
+    }
 }
 
 // Products over F_{p^2} = F_p[x] / (x^2 - ns), ns the least non-residue (the reference's

@@ -281,8 +281,8 @@ def test_split_k_child_alignment(gpu, p):
 
 
 def test_triangular_host_transfers(gpu):
-    # only Low(C) crosses PCIe in 256-row blocks: results stay exact across block edges, the
-    # byte count matches, beta = 0 clears the diagonal blocks' strict upper parts, beta != 0
+    # only Low(C) crosses PCIe: results stay exact across chunk edges, the byte count matches,
+    # beta = 0 clears the diagonal blocks' strict upper parts, beta != 0
     # leaves the caller's strict upper triangle as it was
     fs = gpu
     p, n, k = 131071, 600, 200
@@ -294,7 +294,8 @@ def test_triangular_host_transfers(gpu):
     fs.syrk_fast_into(f, a, c, plan)
     assert orc.lower_equal(c, want)
     blocks = [(r0, min(n, r0 + 256)) for r0 in range(0, n, 256)]
-    assert fs.last_transfer_bytes() == (n * k * 8, sum((r1 - r0) * r1 * 8 for r0, r1 in blocks))
+    # residues cross PCIe as uint32 (narrowed / widened by host threads, host_io.h)
+    assert fs.last_transfer_bytes() == (n * k * 4, n * (n + 1) // 2 * 4)
     for r0, r1 in blocks:
         blk = c[r0:r1, r0:r1]
         assert (blk[np.triu_indices(r1 - r0, 1)] == 0).all()
@@ -307,6 +308,68 @@ def test_triangular_host_transfers(gpu):
     exp[idx] = (want[idx] * np.uint64(3) + c0[idx] * np.uint64(5)) % np.uint64(p)
     assert orc.lower_equal(c, exp)
     assert np.array_equal(c[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])
+
+
+def _pinned(shape):
+    torch = pytest.importorskip("torch")
+    t = torch.empty(shape, dtype=torch.int64, pin_memory=True)
+    return t.numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_io_chunked_paths(gpu, pinned):
+    # host_io: several 2 Mi-element chunks each way (A narrowed in host threads, Low(C) widened),
+    # strided caller views, and with pinned C the accumulate duplex path (raw row blocks of C_in
+    # and C out at the same time); pageable C takes the narrowed path for C_in too
+    fs = gpu
+    p, n, k = 2147483647, 2300, 1500
+    f = fs.PrimeField(p)
+    big = orc.random_matrix(p, n, k + 7, 11)
+    a = big[:, 3:3 + k]
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(256, 2))
+    want = orc.syrk_classical(p, np.ascontiguousarray(a))
+    cbig = _pinned((n, n + 5)) if pinned else np.empty((n, n + 5), dtype=np.uint64)
+    cbig[:] = 9
+    c = cbig[:, 2:2 + n]
+    fs.syrk_fast_into(f, a, c, plan)
+    assert orc.lower_equal(np.ascontiguousarray(c), want)
+    assert (cbig[:, :2] == 9).all() and (cbig[:, 2 + n:] == 9).all()
+    h2d, d2h = fs.last_transfer_bytes()  # pinned C: a share of the rows also moves unnarrowed
+    assert h2d == n * k * 4 and (d2h >= n * (n + 1) // 2 * 4 if pinned else d2h == n * (n + 1) // 2 * 4)
+    c0 = orc.random_matrix(p, n, n, 12)
+    c[:] = c0
+    alpha, beta = 123456789, 987654321
+    fs.syrk_fast_acc(f, alpha, a, beta, c, plan)
+    idx = np.tril_indices(n)
+    exp = c0.copy()
+    exp[idx] = np.array([(int(w) * alpha + int(x) * beta) % p for w, x in zip(want[idx], c0[idx])], dtype=np.uint64)
+    assert np.array_equal(np.ascontiguousarray(c)[idx], exp[idx])
+    assert np.array_equal(np.ascontiguousarray(c)[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])
+    assert (cbig[:, :2] == 9).all() and (cbig[:, 2 + n:] == 9).all()
+    h2d, d2h = fs.last_transfer_bytes()
+    assert h2d >= n * k * 4 and d2h >= n * (n + 1) // 2 * 4
+
+
+def test_host_io_noncanonical_inputs(gpu):
+    # values >= 2^32 cannot be narrowed: their chunk crosses PCIe as uint64 and the device
+    # reduces them (the reference's PrimeField treats stored words as residues mod p only
+    # after reduction; the device path reduces any uint64)
+    fs = gpu
+    p, n, k = 131071, 300, 200
+    f = fs.PrimeField(p)
+    a = orc.random_matrix(p, n, k, 21)
+    big = a.copy()
+    big[5, 7] += np.uint64(p) * np.uint64(1 << 40)
+    big[250, 3] += np.uint64(p) * np.uint64(3)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(32))
+    want = orc.syrk_classical(p, a)
+    assert orc.lower_equal(fs.syrk_fast(f, big, plan), want)
+    c0 = orc.random_matrix(p, n, n, 22)
+    c = c0.copy()
+    c[10, 2] += np.uint64(p) * np.uint64(1 << 33)
+    fs.syrk_fast_acc(f, 1, a, 1, c, plan)
+    idx = np.tril_indices(n)
+    assert np.array_equal(c[idx], (want[idx] + c0[idx]) % np.uint64(p))
 
 
 @pytest.mark.parametrize("p", [3, 7, 13, 65521, 131071, 2147483647])

@@ -202,6 +202,15 @@ int fsyrk_b200_last_launch_count(int* by_kind, int nkinds);
  * lower-triangle row blocks of C unless mirror_output). */
 int fsyrk_b200_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
+/* Host-only check of the host transfer format (no device needed): the rows of `a`
+ * (lower != 0: row i holds columns [0, i]) are packed exactly as the host entry points put
+ * them on the wire -- `bits` in [8, 24] bit-packed groups, 32 = uint32 -- by the library's host
+ * worker pool, then unpacked into `out` (same shape, stride ldo).  Returns the number of
+ * chunks that would cross unnarrowed (a value >= 2^bits) in *raw_chunks and the seconds
+ * spent packing / unpacking in secs[2].  Diagnostic / test hook. */
+int fsyrk_b200_hostio_roundtrip(const uint64_t* a, size_t rows, size_t cols, size_t lda, int lower, int bits,
+                                uint64_t* out, size_t ldo, size_t* raw_chunks, double* secs);
+
 /* Describe the last executed plan as a JSON string (tree, groups, limbs, bytes). */
 const char* fsyrk_b200_last_plan_json(void);
 

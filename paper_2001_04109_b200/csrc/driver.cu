@@ -1536,10 +1536,13 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     };
     double tr[4] = {tnow(), 0, 0, 0};
     hio::g_io_stats = hio::IoStats{};
+    const int bits = hio::transfer_bits(p);
     const size_t lda_dev = k == 0 ? 1 : k;
     const bool need_c = (beta % p) != 0;
+    // auto: duplex for pinned C unless residues pack to 16 bits or less (then the packed path
+    // moves 4x fewer PCIe bytes than the raw duplex and wins, profiles/r01/hostio.txt)
     const bool duplex = need_c && !mirror && io_mode() != IoMode::Narrow &&
-                        (io_mode() == IoMode::Duplex || hio::is_pinned(c));
+                        (io_mode() == IoMode::Duplex || (hio::is_pinned(c) && bits > 16));
     // duplex: chunks of whole kTriRows-row blocks of C, ~32 MB each
     std::vector<std::pair<size_t, size_t>> chunks;
     auto blocks = [&](size_t r0, size_t r1, bool in) {
@@ -1579,19 +1582,19 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
         g_io.events(chunks.size());
         if (cin_early) queue_cin();
     }
-    if (k > 0) ck(hio::upload(a, lda, hio::Region{n, k, false}, da, k, s, &h2d), "H2D A");
+    if (k > 0) ck(hio::upload(a, lda, hio::Region{n, k, false}, da, k, bits, s, &h2d), "H2D A");
     if (io_trace) {
         ck(cudaStreamSynchronize(s), "sync");
         tr[1] = tnow();
     }
     if (!duplex) {
-        if (need_c) ck(hio::upload(c, ldc, hio::Region{n, n, true}, dc, n, s, &h2d), "H2D C");
+        if (need_c) ck(hio::upload(c, ldc, hio::Region{n, n, true}, dc, n, bits, s, &h2d), "H2D C");
         run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
         if (io_trace) {
             ck(cudaStreamSynchronize(s), "sync");
             tr[2] = tnow();
         }
-        ck(hio::download(dc, n, hio::Region{n, n, !mirror}, c, ldc, (need_c || mirror) ? 0 : kTriRows, s, &d2h),
+        ck(hio::download(dc, n, hio::Region{n, n, !mirror}, c, ldc, (need_c || mirror) ? 0 : kTriRows, bits, s, &d2h),
            "D2H C");
     } else {
         g_stage_x.ensure(cbytes);
@@ -1845,6 +1848,21 @@ int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, s
 void fsyrk_b200_release_cache(void) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache.clear();
+}
+
+int fsyrk_b200_hostio_roundtrip(const uint64_t* a, size_t rows, size_t cols, size_t lda, int lower, int bits,
+                                uint64_t* out, size_t ldo, size_t* raw_chunks, double* secs) {
+    return guarded([&] {
+        if (lower && cols < rows) fail(FSYRK_B200_EDIMENSION, "hostio_roundtrip: lower region needs cols >= rows");
+        if (lda < cols || ldo < cols) fail(FSYRK_B200_EDIMENSION, "hostio_roundtrip: stride < cols");
+        double t[2];
+        const size_t raw = hio::roundtrip(a, lda, hio::Region{rows, cols, lower != 0}, bits, out, ldo, t);
+        if (raw_chunks) *raw_chunks = raw;
+        if (secs) {
+            secs[0] = t[0];
+            secs[1] = t[1];
+        }
+    });
 }
 
 int fsyrk_b200_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {

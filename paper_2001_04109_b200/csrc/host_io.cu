@@ -25,6 +25,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "elementwise.cuh"
@@ -193,6 +194,107 @@ inline void widen_run(const uint32_t* s, uint64_t* o, size_t n) {
     else widen_avx2<false>(s, o, n);
 }
 
+// ---- B-bit packing (B < 32): groups of 32 residues -> B little-endian 32-bit words ----
+template <int B, size_t... T>
+inline void pack32_impl(const uint32_t* v, uint32_t* w, std::index_sequence<T...>) {
+    ((w[(T * B) / 32] |= v[T] << ((T * B) % 32),
+      w[(T * B) / 32 + 1] |= ((T * B) % 32 + B > 32) ? v[T] >> ((32 - (T * B) % 32) & 31) : 0u),
+     ...);
+}
+template <int B>
+inline void pack32(const uint32_t* v, uint32_t* out) {
+    uint32_t w[B + 1] = {};
+    pack32_impl<B>(v, w, std::make_index_sequence<32>{});
+    for (int i = 0; i < B; ++i) _mm_stream_si32(reinterpret_cast<int*>(out + i), (int)w[i]);
+}
+template <int B, size_t... T>
+inline void unpack32_impl(const uint32_t* w, uint32_t* v, std::index_sequence<T...>) {
+    constexpr uint32_t mask = (1u << B) - 1;
+    ((v[T] = ((w[(T * B) / 32] >> ((T * B) % 32)) |
+              (((T * B) % 32 + B > 32) ? w[(T * B) / 32 + 1] << ((32 - (T * B) % 32) & 31) : 0u)) &
+             mask),
+     ...);
+}
+template <int B>
+inline void unpack32(const uint32_t* in, uint32_t* v) {
+    uint32_t w[B + 1];
+    for (int i = 0; i < B; ++i) w[i] = in[i];
+    w[B] = 0;
+    unpack32_impl<B>(w, v, std::make_index_sequence<32>{});
+}
+
+// Packs a worker's run of row segments (starting at a group boundary) into consecutive groups.
+template <int B>
+struct Packer {
+    uint32_t v[32];
+    int n = 0;
+    uint32_t* out;
+    uint64_t hi = 0;
+    void push(const uint64_t* s, size_t cnt) {
+        while (cnt) {
+            if (n == 0 && cnt >= 32) {  // whole groups straight from the row
+                for (; cnt >= 32; cnt -= 32, s += 32, out += B) {
+                    uint64_t h = 0;
+                    for (int t = 0; t < 32; ++t) {
+                        h |= s[t];
+                        v[t] = (uint32_t)s[t];
+                    }
+                    hi |= h;
+                    pack32<B>(v, out);
+                }
+                continue;
+            }
+            const size_t t = std::min<size_t>(32 - n, cnt);
+            for (size_t j = 0; j < t; ++j) {
+                hi |= s[j];
+                v[n + j] = (uint32_t)s[j];
+            }
+            n += (int)t;
+            s += t;
+            cnt -= t;
+            if (n == 32) {
+                pack32<B>(v, out);
+                out += B;
+                n = 0;
+            }
+        }
+    }
+    void flush() {
+        if (!n) return;
+        for (int t = n; t < 32; ++t) v[t] = 0;
+        pack32<B>(v, out);
+        out += B;
+        n = 0;
+    }
+};
+template <int B>
+struct Unpacker {
+    uint32_t v[32];
+    int n = 32;  // values of v already handed out
+    const uint32_t* in;
+    void pull(uint64_t* o, size_t cnt) {
+        while (cnt) {
+            if (n == 32 && cnt >= 32) {
+                for (; cnt >= 32; cnt -= 32, o += 32, in += B) {
+                    unpack32<B>(in, v);
+                    for (int t = 0; t < 32; ++t) _mm_stream_si64(reinterpret_cast<long long*>(o + t), (long long)v[t]);
+                }
+                continue;
+            }
+            if (n == 32) {
+                unpack32<B>(in, v);
+                in += B;
+                n = 0;
+            }
+            const size_t t = std::min<size_t>(32 - n, cnt);
+            for (size_t j = 0; j < t; ++j) _mm_stream_si64(reinterpret_cast<long long*>(o + j), (long long)v[n + j]);
+            n += (int)t;
+            o += t;
+            cnt -= t;
+        }
+    }
+};
+
 // ---- staging ----
 struct Slot {
     uint32_t* buf = nullptr;
@@ -246,6 +348,18 @@ cudaError_t acquire(Slot& s) {
     return e;
 }
 
+struct Staging g_devw;  // packed words on the device
+
+cudaError_t ensure_devw(size_t n) {
+    if (g_devw.n >= n) return cudaSuccess;
+    if (g_devw.ptr) cudaFree(g_devw.ptr);
+    g_devw.ptr = nullptr;
+    g_devw.n = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&g_devw.ptr), n * 4);
+    if (e == cudaSuccess) g_devw.n = n;
+    return e;
+}
+
 cudaError_t ensure_dev32(size_t n) {
     if (g_dev32.n >= n) return cudaSuccess;
     if (g_dev32.ptr) cudaFree(g_dev32.ptr);
@@ -272,9 +386,11 @@ std::vector<Chunk> make_chunks(const Region& r, size_t rows, size_t cap) {
 }
 
 // Worker w's slice of a chunk, walked row by row: fn(row, c0, c1, packed index of (row, c0)).
+// Slices start at multiples of 32 chunk elements (whole groups of the bit-packed format).
 template <class Fn>
 void slice(const Region& r, const Chunk& ch, int w, int nw, Fn&& fn) {
-    const size_t b = ch.off + ch.len * w / nw, e = ch.off + ch.len * (w + 1) / nw;
+    const size_t b = ch.off + ch.len * w / nw / 32 * 32;
+    const size_t e = w + 1 == nw ? ch.off + ch.len : ch.off + ch.len * (w + 1) / nw / 32 * 32;
     if (b >= e) return;
     size_t lo = ch.r0, hi = ch.r1 - 1;  // first row whose packed range contains b
     while (lo < hi) {
@@ -288,6 +404,41 @@ void slice(const Region& r, const Chunk& ch, int w, int nw, Fn&& fn) {
         pos = rb + c1;
     }
 }
+
+// Worker entry points per bit width (8..24), dispatched through tables.
+using PackFn = uint64_t (*)(const Region&, const Chunk&, int, int, const uint64_t*, size_t, uint32_t*);
+using UnpackFn = void (*)(const Region&, const Chunk&, int, int, const uint32_t*, uint64_t*, size_t, size_t);
+template <int B>
+uint64_t pack_slice(const Region& r, const Chunk& ch, int w, int nw, const uint64_t* h, size_t ldh, uint32_t* words) {
+    Packer<B> pk;
+    pk.out = words + (ch.len * w / nw / 32) * B;
+    slice(r, ch, w, nw, [&](size_t i, size_t c0, size_t c1, size_t) { pk.push(h + i * ldh + c0, c1 - c0); });
+    pk.flush();
+    return pk.hi >> B;
+}
+template <int B>
+void unpack_slice(const Region& r, const Chunk& ch, int w, int nw, const uint32_t* words, uint64_t* h, size_t ldh,
+                  size_t zero_rb) {
+    Unpacker<B> up;
+    up.in = words + (ch.len * w / nw / 32) * B;
+    slice(r, ch, w, nw, [&](size_t i, size_t c0, size_t c1, size_t) {
+        uint64_t* o = h + i * ldh;
+        up.pull(o + c0, c1 - c0);
+        if (zero_rb && c1 == r.width(i)) {
+            const size_t end = std::min(r.rows, (i / zero_rb + 1) * zero_rb);
+            if (end > i + 1) std::memset(o + i + 1, 0, (end - i - 1) * 8);
+        }
+    });
+}
+constexpr int kMinBits = 8, kMaxBits = 24;
+template <int... Bs>
+struct Tables {
+    static constexpr PackFn pack[] = {&pack_slice<Bs>...};
+    static constexpr UnpackFn unpack[] = {&unpack_slice<Bs>...};
+};
+using Tab = Tables<8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24>;
+
+size_t packed_words(size_t len, int bits) { return bits >= 32 ? len : (len + 31) / 32 * (size_t)bits; }
 
 // Chunks through the workers.  prepare(c) (calling thread) makes chunk c's slot usable,
 // work(c, w, nw) is worker w's share, finish(c) (calling thread) runs once every share is in.
@@ -393,6 +544,36 @@ __global__ void narrow_kernel(const uint64_t* __restrict__ d, long long ldd, int
     }
 }
 
+// Bit-packed transfer format on the device: value t of group g sits at bits [t B, t B + B) of
+// words [g B, g B + B).
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, size_t n, int B, uint32_t* __restrict__ out) {
+    const uint32_t mask = (1u << B) - 1;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t g = idx / 32;
+        const unsigned bit = (unsigned)(idx % 32) * B;
+        const size_t wi = g * B + bit / 32;
+        const unsigned sh = bit % 32;
+        uint32_t v = words[wi] >> sh;
+        if (sh + B > 32) v |= words[wi + 1] << (32 - sh);
+        out[idx] = v & mask;
+    }
+}
+__global__ void pack_kernel(const uint32_t* __restrict__ vals, size_t n, int B, uint32_t* __restrict__ words,
+                            size_t nwords) {
+    for (size_t wi = blockIdx.x * (size_t)blockDim.x + threadIdx.x; wi < nwords; wi += (size_t)gridDim.x * blockDim.x) {
+        const size_t g = wi / B;
+        const int b0 = (int)(wi % B) * 32;  // first bit of the word inside its group
+        uint32_t w = 0;
+        for (int t = b0 / B; t < 32 && t * B < b0 + 32; ++t) {
+            const size_t idx = g * 32 + t;
+            const uint32_t v = idx < n ? vals[idx] : 0;
+            const int off = t * B - b0;
+            w |= off >= 0 ? v << off : v >> -off;
+        }
+        words[wi] = w;
+    }
+}
+
 __global__ void acc_combine_kernel(const uint64_t* __restrict__ x, long long ldx, uint64_t* __restrict__ c,
                                    long long ldc, int r0, int r1, ModP m, uint32_t beta) {
     for (int i = r0 + blockIdx.y; i < r1; i += gridDim.y)
@@ -431,10 +612,19 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t ldd, cudaStream_t s,
+int transfer_bits(uint64_t p) {
+    static const bool pack = env_size("FSYRK_B200_PACK", 1) != 0;
+    int b = 0;
+    while (b < 64 && ((p - 1) >> b) != 0) ++b;  // bit length of the largest residue
+    if (!pack || b > kMaxBits) return 32;
+    return std::max(b, kMinBits);
+}
+
+cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t ldd, int bits, cudaStream_t s,
                    uint64_t* bytes) {
     const size_t total = r.offset(r.rows);
     if (total == 0) return cudaSuccess;
+    if (bits < 32 && (bits < kMinBits || bits > kMaxBits)) bits = 32;
     const size_t cap = std::max(kChunk, r.lower ? r.rows : r.cols);
     cudaError_t e;
     if ((e = ensure_slots(cap)) != cudaSuccess) return e;
@@ -448,17 +638,25 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
         if ((e = cudaEventRecord(g_raw_done, g_raw)) != cudaSuccess) return e;
     }
     const std::vector<Chunk> chunks = make_chunks(r, split, cap);
+    std::vector<size_t> wofs(chunks.size() + 1, 0);  // packed words of each chunk in the device word buffer
+    for (size_t c = 0; c < chunks.size(); ++c) wofs[c + 1] = wofs[c] + packed_words(chunks[c].len, bits);
+    if (bits < 32 && (e = ensure_devw(wofs.back())) != cudaSuccess) return e;
+    const PackFn packer = bits < 32 ? Tab::pack[bits - kMinBits] : nullptr;
     const size_t nw = (size_t)workers().size();
-    std::vector<uint64_t> high(chunks.size() * nw, 0);  // high words seen, per chunk and worker
+    std::vector<uint64_t> high(chunks.size() * nw, 0);  // out-of-range bits seen, per chunk and worker
     e = run_chunks(
         chunks.size(), kSlots - 1, [&](size_t c) { return acquire(g_slot[c % kSlots]); },
         [&](size_t c, int w, int nwk) {
             const Chunk& ch = chunks[c];
-            uint32_t* dst = g_slot[c % kSlots].buf - ch.off;
             uint64_t hi = 0;
-            slice(r, ch, w, nwk, [&](size_t i, size_t c0, size_t c1, size_t pos) {
-                hi |= narrow_run(h + i * ldh + c0, dst + pos, c1 - c0);
-            });
+            if (packer) {
+                hi = packer(r, ch, w, nwk, h, ldh, g_slot[c % kSlots].buf);
+            } else {
+                uint32_t* dst = g_slot[c % kSlots].buf - ch.off;
+                slice(r, ch, w, nwk, [&](size_t i, size_t c0, size_t c1, size_t pos) {
+                    hi |= narrow_run(h + i * ldh + c0, dst + pos, c1 - c0);
+                });
+            }
             high[c * nw + (size_t)w] = hi;
         },
         [&](size_t c) -> cudaError_t {
@@ -466,7 +664,7 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
             uint64_t hi = 0;
             for (size_t w = 0; w < nw; ++w) hi |= high[c * nw + w];
             cudaError_t e2;
-            if (hi) {  // a value >= 2^32 (non-canonical input): this chunk crosses unnarrowed
+            if (hi) {  // a value that does not fit the transfer width (non-canonical input): unnarrowed
                 const size_t wd = r.width(ch.r1 - 1);
                 *bytes += (ch.r1 - ch.r0) * wd * 8;
                 return cudaMemcpy2DAsync(d + ch.r0 * ldd, ldd * 8, h + ch.r0 * ldh, ldh * 8, wd * 8, ch.r1 - ch.r0,
@@ -474,10 +672,17 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
             }
             Slot& sl = g_slot[c % kSlots];
             uint32_t* d32 = g_dev32.ptr + ch.off;
-            if ((e2 = cudaMemcpyAsync(d32, sl.buf, ch.len * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e2;
+            const size_t nwords = wofs[c + 1] - wofs[c];
+            uint32_t* dst = bits < 32 ? g_devw.ptr + wofs[c] : d32;
+            if ((e2 = cudaMemcpyAsync(dst, sl.buf, nwords * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e2;
             if ((e2 = cudaEventRecord(sl.ev, s)) != cudaSuccess) return e2;
             sl.pending = true;
-            *bytes += ch.len * 4;
+            *bytes += nwords * 4;
+            if (bits < 32) {
+                unpack_kernel<<<(unsigned)std::min<size_t>(4096, (ch.len + 255) / 256), 256, 0, s>>>(dst, ch.len, bits,
+                                                                                                    d32);
+                if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+            }
             widen_kernel<<<rows_grid(ch.r1 - ch.r0, r.width(ch.r1 - 1)), 256, 0, s>>>(
                 d32, ch.off, (int)ch.r0, (int)ch.r1, (int)r.cols, r.lower ? 1 : 0, d, (long long)ldd);
             return cudaGetLastError();
@@ -487,10 +692,11 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
     return e;
 }
 
-cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_t ldh, size_t zero_rb,
+cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_t ldh, size_t zero_rb, int bits,
                      cudaStream_t s, uint64_t* bytes) {
     const size_t total = r.offset(r.rows);
     if (total == 0) return cudaSuccess;
+    if (bits < 32 && (bits < kMinBits || bits > kMaxBits)) bits = 32;
     const size_t cap = std::max(kChunk, r.lower ? r.rows : r.cols);
     cudaError_t e;
     if ((e = ensure_slots(cap)) != cudaSuccess) return e;
@@ -509,29 +715,45 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
         if ((e = cudaEventRecord(g_raw_done, g_raw)) != cudaSuccess) return e;
     }
     const std::vector<Chunk> chunks = make_chunks(r, split, cap);
+    std::vector<size_t> wofs(chunks.size() + 1, 0);
+    for (size_t c = 0; c < chunks.size(); ++c) wofs[c + 1] = wofs[c] + packed_words(chunks[c].len, bits);
+    if (bits < 32 && (e = ensure_devw(wofs.back())) != cudaSuccess) return e;
     if (!chunks.empty()) {
         narrow_kernel<<<rows_grid(split, r.lower ? split : r.cols), 256, 0, s>>>(
             d, (long long)ldd, (int)split, (int)r.cols, r.lower ? 1 : 0, g_dev32.ptr);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (bits < 32)
+            for (size_t c = 0; c < chunks.size(); ++c) {
+                const size_t nwords = wofs[c + 1] - wofs[c];
+                pack_kernel<<<(unsigned)std::min<size_t>(4096, (nwords + 255) / 256), 256, 0, s>>>(
+                    g_dev32.ptr + chunks[c].off, chunks[c].len, bits, g_devw.ptr + wofs[c], nwords);
+            }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     auto issue = [&](size_t c) -> cudaError_t {
         Slot& sl = g_slot[c % kSlots];
         cudaError_t e2 = acquire(sl);
         if (e2 != cudaSuccess) return e2;
-        const Chunk& ch = chunks[c];
-        e2 = cudaMemcpyAsync(sl.buf, g_dev32.ptr + ch.off, ch.len * 4, cudaMemcpyDeviceToHost, s);
+        const size_t nwords = wofs[c + 1] - wofs[c];
+        const uint32_t* src = bits < 32 ? g_devw.ptr + wofs[c] : g_dev32.ptr + chunks[c].off;
+        e2 = cudaMemcpyAsync(sl.buf, src, nwords * 4, cudaMemcpyDeviceToHost, s);
         if (e2 != cudaSuccess) return e2;
         e2 = cudaEventRecord(sl.ev, s);
         sl.pending = true;
-        *bytes += ch.len * 4;
+        *bytes += nwords * 4;
         return e2;
     };
     for (size_t c = 0; c < chunks.size() && c < (size_t)kSlots; ++c)
         if ((e = issue(c)) != cudaSuccess) return e;
+    const UnpackFn unpacker = bits < 32 ? Tab::unpack[bits - kMinBits] : nullptr;
     e = run_chunks(
         chunks.size(), 1, [&](size_t c) { return acquire(g_slot[c % kSlots]); },
         [&](size_t c, int w, int nw) {
             const Chunk& ch = chunks[c];
+            if (unpacker) {
+                unpacker(r, ch, w, nw, g_slot[c % kSlots].buf, h, ldh, zero_rb);
+                return;
+            }
             const uint32_t* src = g_slot[c % kSlots].buf - ch.off;
             slice(r, ch, w, nw, [&](size_t i, size_t c0, size_t c1, size_t pos) {
                 uint64_t* o = h + i * ldh;
@@ -546,6 +768,59 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
     if (e != cudaSuccess) return e;
     if (split < r.rows) e = cudaEventSynchronize(g_raw_done);
     return e;
+}
+
+size_t roundtrip(const uint64_t* h, size_t ldh, Region r, int bits, uint64_t* out, size_t ldo, double* secs) {
+    if (bits < 32 && (bits < kMinBits || bits > kMaxBits)) bits = 32;
+    const size_t cap = std::max(kChunk, r.lower ? r.rows : r.cols);
+    const std::vector<Chunk> chunks = make_chunks(r, r.rows, cap);
+    const PackFn packer = bits < 32 ? Tab::pack[bits - kMinBits] : nullptr;
+    const UnpackFn unpacker = bits < 32 ? Tab::unpack[bits - kMinBits] : nullptr;
+    std::vector<uint32_t> buf(cap + 64);
+    const size_t nw = (size_t)workers().size();
+    std::vector<uint64_t> high(nw);
+    size_t raw = 0;
+    secs[0] = secs[1] = 0;
+    auto none = [](size_t) { return cudaSuccess; };
+    for (const Chunk& ch : chunks) {
+        const Chunk* pc = &ch;
+        double t0 = now_s();
+        run_chunks(
+            1, 0, none,
+            [&](size_t, int w, int nwk) {
+                uint64_t hi = 0;
+                if (packer) {
+                    hi = packer(r, *pc, w, nwk, h, ldh, buf.data());
+                } else {
+                    uint32_t* dst = buf.data() - pc->off;
+                    slice(r, *pc, w, nwk, [&](size_t i, size_t c0, size_t c1, size_t pos) {
+                        hi |= narrow_run(h + i * ldh + c0, dst + pos, c1 - c0);
+                    });
+                }
+                high[(size_t)w] = hi;
+            },
+            none);
+        double t1 = now_s();
+        uint64_t hi = 0;
+        for (uint64_t x : high) hi |= x;
+        raw += hi != 0;
+        run_chunks(
+            1, 0, none,
+            [&](size_t, int w, int nwk) {
+                if (unpacker) {
+                    unpacker(r, *pc, w, nwk, buf.data(), out, ldo, 0);
+                    return;
+                }
+                const uint32_t* src = buf.data() - pc->off;
+                slice(r, *pc, w, nwk, [&](size_t i, size_t c0, size_t c1, size_t pos) {
+                    widen_run(src + pos, out + i * ldo + c0, c1 - c0);
+                });
+            },
+            none);
+        secs[0] += t1 - t0;
+        secs[1] += now_s() - t1;
+    }
+    return raw;
 }
 
 cudaError_t launch_acc_combine(const uint64_t* x, long long ldx, uint64_t* c, long long ldc, int r0, int r1,

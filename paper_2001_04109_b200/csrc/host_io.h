@@ -36,19 +36,29 @@ bool is_pinned(const void* p);
 
 // Host rows -> device uint64 rows (row stride ldd).  Returns after the last chunk is queued on
 // `s` (host work done; the device side completes in stream order).  *bytes += PCIe bytes.
-cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t ldd, cudaStream_t s,
+// `bits` < 32: residues cross as a B-bit packed stream (groups of 32 values in B words; B from
+// transfer_bits(p)); 32: as uint32.
+cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t ldd, int bits, cudaStream_t s,
                    uint64_t* bytes);
 
 // Device uint64 rows (every value < 2^32) -> host rows; synchronous.  zero_rb > 0 also writes
 // zeros at (i, j) for i < j < min(rows, (i / zero_rb + 1) * zero_rb) (the strict upper parts of
 // the diagonal zero_rb-row blocks) without moving them.  *bytes += PCIe bytes.
-cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_t ldh, size_t zero_rb,
+cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_t ldh, size_t zero_rb, int bits,
                      cudaStream_t s, uint64_t* bytes);
+
+// Transfer width for residues mod p: the bit length of p - 1 (at least 8) when it is at most 24,
+// else 32 (FSYRK_B200_PACK=0: always 32).
+int transfer_bits(uint64_t p);
 
 // c[i][j] <- (x[i][j] + beta * (c[i][j] mod p)) mod p on the lower triangle of rows [r0, r1)
 // (x already reduced; c any uint64).  The accumulate step of the pinned-memory duplex path.
 cudaError_t launch_acc_combine(const uint64_t* x, long long ldx, uint64_t* c, long long ldc, int r0, int r1,
                                const ModP& m, uint32_t beta, cudaStream_t s);
+
+// Host-only pack -> unpack of a region through the worker pool (format check and host
+// bandwidth probe; fsyrk_b200_hostio_roundtrip).  Returns the chunks that would go unnarrowed.
+size_t roundtrip(const uint64_t* h, size_t ldh, Region r, int bits, uint64_t* out, size_t ldo, double* secs);
 
 // Host seconds spent converting on the pool / waiting for staging slots (FSYRK_B200_IO_TRACE).
 struct IoStats {

@@ -94,7 +94,7 @@ EXPORTS = (
     "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
     "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
     "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2", "fsyrk_b200_gemm_winograd_nt",
-    "fsyrk_b200_gemm_winograd_nt_dev",
+    "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip",
 )
 
 
@@ -141,6 +141,9 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    L.fsyrk_b200_hostio_roundtrip.argtypes = [_u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int,
+                                              ctypes.c_int, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                                              ctypes.POINTER(ctypes.c_double)]
     L.fsyrk_b200_gemm_winograd_nt.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
                                               ctypes.c_size_t, _u64p, ctypes.c_size_t, ctypes.c_size_t, _u64p,
                                               ctypes.c_size_t, _Policy]
@@ -614,6 +617,25 @@ def last_transfer_bytes() -> tuple:
     h, d = ctypes.c_uint64(0), ctypes.c_uint64(0)
     lib().fsyrk_b200_last_transfer_bytes(ctypes.byref(h), ctypes.byref(d))
     return int(h.value), int(d.value)
+
+
+def transfer_bits(p: int) -> int:
+    """Width of a residue on the wire for the host entry points (host_io.cu transfer_bits)."""
+    b = max(8, (int(p) - 1).bit_length())
+    return b if b <= 24 and os.environ.get("FSYRK_B200_PACK", "1") != "0" else 32
+
+
+def hostio_roundtrip(a: np.ndarray, lower: bool, bits: int):
+    """Host-only pack -> unpack of `a`'s rows (lower: row i holds columns [0, i]) in the host
+    transfer format (fsyrk_b200_hostio_roundtrip).  Returns (out, raw_chunks, (pack_s, unpack_s));
+    entries outside the region stay zero."""
+    pa, rows, cols, lda = _view(a, "a")
+    out = np.zeros((rows, cols), dtype=np.uint64)
+    raw = ctypes.c_size_t(0)
+    secs = (ctypes.c_double * 2)()
+    _check(lib().fsyrk_b200_hostio_roundtrip(pa, rows, cols, lda, int(bool(lower)), int(bits),
+                                             out.ctypes.data_as(_u64p), max(cols, 1), ctypes.byref(raw), secs))
+    return out, int(raw.value), (secs[0], secs[1])
 
 
 def last_plan() -> dict:

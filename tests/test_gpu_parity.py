@@ -280,6 +280,24 @@ def test_split_k_child_alignment(gpu, p):
     assert orc.lower_equal(fs.syrkd(f, a, d, plan), want)
 
 
+def _xfer_bytes(p, rows, cols, lower):
+    """PCIe bytes host_io moves for a region (host_io.cu make_chunks / transfer_bits): row-aligned
+    chunks of <= 2^20 elements, each a stream of B-bit groups of 32 residues (B = bit length of
+    p - 1, at least 8, when <= 24) or of uint32."""
+    b = max(8, (p - 1).bit_length())
+    width = (lambda i: i + 1) if lower else (lambda i: cols)
+    cap = max(1 << 20, rows if lower else cols)
+    total, r0 = 0, 0
+    while r0 < rows:
+        r1, ln = r0, 0
+        while r1 < rows and (ln == 0 or ln + width(r1) <= cap):
+            ln += width(r1)
+            r1 += 1
+        total += (ln + 31) // 32 * b * 4 if b <= 24 else ln * 4
+        r0 = r1
+    return total
+
+
 def test_triangular_host_transfers(gpu):
     # only Low(C) crosses PCIe: results stay exact across chunk edges, the byte count matches,
     # beta = 0 clears the diagonal blocks' strict upper parts, beta != 0
@@ -294,8 +312,8 @@ def test_triangular_host_transfers(gpu):
     fs.syrk_fast_into(f, a, c, plan)
     assert orc.lower_equal(c, want)
     blocks = [(r0, min(n, r0 + 256)) for r0 in range(0, n, 256)]
-    # residues cross PCIe as uint32 (narrowed / widened by host threads, host_io.h)
-    assert fs.last_transfer_bytes() == (n * k * 4, n * (n + 1) // 2 * 4)
+    # residues cross PCIe bit-packed (17 bits here; packed / unpacked by host threads, host_io.h)
+    assert fs.last_transfer_bytes() == (_xfer_bytes(p, n, k, False), _xfer_bytes(p, n, n, True))
     for r0, r1 in blocks:
         blk = c[r0:r1, r0:r1]
         assert (blk[np.triu_indices(r1 - r0, 1)] == 0).all()
@@ -317,12 +335,13 @@ def _pinned(shape):
 
 
 @pytest.mark.parametrize("pinned", [False, True])
-def test_host_io_chunked_paths(gpu, pinned):
+@pytest.mark.parametrize("p", [2147483647, 131071, 65521])
+def test_host_io_chunked_paths(gpu, pinned, p):
     # host_io: several 2 Mi-element chunks each way (A narrowed in host threads, Low(C) widened),
     # strided caller views, and with pinned C the accumulate duplex path (raw row blocks of C_in
     # and C out at the same time); pageable C takes the narrowed path for C_in too
     fs = gpu
-    p, n, k = 2147483647, 2300, 1500
+    n, k = 2300, 1500
     f = fs.PrimeField(p)
     big = orc.random_matrix(p, n, k + 7, 11)
     a = big[:, 3:3 + k]
@@ -335,7 +354,8 @@ def test_host_io_chunked_paths(gpu, pinned):
     assert orc.lower_equal(np.ascontiguousarray(c), want)
     assert (cbig[:, :2] == 9).all() and (cbig[:, 2 + n:] == 9).all()
     h2d, d2h = fs.last_transfer_bytes()  # pinned C: a share of the rows also moves unnarrowed
-    assert h2d == n * k * 4 and (d2h >= n * (n + 1) // 2 * 4 if pinned else d2h == n * (n + 1) // 2 * 4)
+    want_a, want_c = _xfer_bytes(p, n, k, False), _xfer_bytes(p, n, n, True)
+    assert h2d == want_a and (d2h >= want_c if pinned else d2h == want_c)
     c0 = orc.random_matrix(p, n, n, 12)
     c[:] = c0
     alpha, beta = 123456789, 987654321
@@ -347,7 +367,7 @@ def test_host_io_chunked_paths(gpu, pinned):
     assert np.array_equal(np.ascontiguousarray(c)[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])
     assert (cbig[:, :2] == 9).all() and (cbig[:, 2 + n:] == 9).all()
     h2d, d2h = fs.last_transfer_bytes()
-    assert h2d >= n * k * 4 and d2h >= n * (n + 1) // 2 * 4
+    assert h2d >= want_a and d2h >= want_c
 
 
 def test_host_io_noncanonical_inputs(gpu):
@@ -361,8 +381,13 @@ def test_host_io_noncanonical_inputs(gpu):
     big = a.copy()
     big[5, 7] += np.uint64(p) * np.uint64(1 << 40)
     big[250, 3] += np.uint64(p) * np.uint64(3)
+    a[100, 100] = 0
+    big[100, 100] = p
     plan = fs.make_syrk_plan(f, fs.RecursionPolicy(32))
     want = orc.syrk_classical(p, a)
+    fits = a.copy()
+    fits[100, 100] = p  # fits the 17-bit transfer width: crosses packed, the device reduces it
+    assert orc.lower_equal(fs.syrk_fast(f, fits, plan), want)
     assert orc.lower_equal(fs.syrk_fast(f, big, plan), want)
     c0 = orc.random_matrix(p, n, n, 22)
     c = c0.copy()

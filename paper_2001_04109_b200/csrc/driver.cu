@@ -334,6 +334,16 @@ struct Plan {
     // side stream + events: the top level's general products overlap the deeper pre/post-additions
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // Root post-addition overlapped with the products (one-level plans, FSYRK_B200_POST_ROUNDS=R,
+    // off by default -- measured slower, profiles/r01/variants.txt): the product tiles run in R
+    // rounds of output rows (a round holds every tile whose first needed post pair lies in its
+    // rows) on FSYRK_B200_ROUND_CTAS SMs, and the root post runs as the product kernel's
+    // programmatic dependent on the other SMs, each pair once its round's tiles are stored.
+    int nrounds = 0;                 // 0: off
+    std::vector<int> round_target;   // epilogue-warp reports of each round (its tiles x epilogue warps)
+    size_t off_rounds = 0;           // device: [round_done[nrounds] | next_pair | target[nrounds]]
+    int* dev_rounds = nullptr;
+    int round_ctas = 0;  // product CTAs (the remaining SMs run the post)
 
     ~Plan() {
         if (arena) cudaFree(arena);
@@ -552,6 +562,55 @@ struct Plan {
                 c0 = c;
             }
         }
+        // post-overlap rounds (one-level plans: the root's P1, P2, P5 are leaf products)
+        {
+            static const int want = [] {
+                const char* e = getenv("FSYRK_B200_POST_ROUNDS");
+                return e ? atoi(e) : 0;  // measured slower (profiles/r01/variants.txt): off
+            }();
+            const Node& r0 = nodes[0];
+            if (want > 1 && !partitioned && !idle && r0.kind == LEVEL && nodes[r0.ch[0]].kind == LEAF &&
+                nodes[r0.ch[1]].kind == LEAF && nodes[r0.ch[2]].kind == LEAF && prods.size() == 1 &&
+                r0.h >= 2048) {
+                const ProdLaunch& pl = prods[0];
+                const int T = (r0.h + 31) / 32;
+                // a tile covering 32-row blocks [a, ..) and 32-column blocks [c, ..) is first needed
+                // by the post pairs (I, J), I >= J, with I = max(a, c)
+                auto first_u = [&](const int4& t) { return std::max(t.z * BMt, t.w * BN) / 32; };
+                std::vector<long long> cnt(T + 1, 0);
+                for (const int4& t : pl.host_tiles) cnt[first_u(t)]++;
+                const int R = std::min(want, T);
+                std::vector<int> bound(1, 0);  // round r covers 32-row blocks [bound[r], bound[r + 1])
+                long long acc = 0, tot = (long long)pl.host_tiles.size();
+                for (int u = 0; u < T; ++u) {
+                    acc += cnt[u];
+                    if ((int)bound.size() < R && acc * R >= tot * (long long)bound.size() && u + 1 < T)
+                        bound.push_back(u + 1);
+                }
+                bound.push_back(T);
+                std::vector<int> round_of(T + 1, 0);
+                for (size_t r = 0; r + 1 < bound.size(); ++r)
+                    for (int u = bound[r]; u < bound[r + 1]; ++u) round_of[u] = (int)r;
+                const int nr = (int)bound.size() - 1;
+                // one launch, tiles in round order, the round in the tile's group field
+                ProdLaunch& pm = prods[0];
+                std::vector<int4> sorted;
+                round_target.assign(nr, 0);
+                for (int r = 0; r < nr; ++r)
+                    for (const int4& t : pm.host_tiles)
+                        if (round_of[first_u(t)] == r) {
+                            sorted.push_back(make_int4(t.x | (r << kTileGroupBits), t.y, t.z, t.w));
+                            round_target[r] += modmm_epilogue_warps();
+                        }
+                pm.host_tiles = std::move(sorted);
+                for (int r = 0; r < nr; ++r)
+                    for (int I = bound[r]; I < bound[r + 1]; ++I)
+                        for (int J = 0; J <= I; ++J) root_pairs.push_back(make_int2(I | (r << 20), J));
+                nrounds = nr;
+                off_rounds = ar.take((2 * (size_t)nr + 1) * sizeof(int));
+                off_pairs = ar.take(root_pairs.size() * sizeof(int2));
+            }
+        }
         std::vector<size_t> off_x(nodes.size(), 0), off_s3(nodes.size(), 0);
         for (size_t i = 0; i < nodes.size(); ++i) {
             Node& nd = nodes[i];
@@ -677,6 +736,16 @@ struct Plan {
                     modmm_set_output_map(g, lg.count);
                 }
             }
+        }
+        if (nrounds) {
+            dev_rounds = reinterpret_cast<int*>(arena + off_rounds);
+            ck(cudaMemcpy(dev_rounds + nrounds + 1, round_target.data(), nrounds * sizeof(int), cudaMemcpyHostToDevice),
+               "upload round targets");
+            static const int ctas = [] {
+                const char* e = getenv("FSYRK_B200_ROUND_CTAS");
+                return e ? atoi(e) : 0;
+            }();
+            round_ctas = ctas > 0 ? std::min(ctas, ncta) : std::max(1, ncta - ncta / 6);
         }
         // node pointers (top-down: a node's input is set before its children read it)
         for (size_t i = 0; i < nodes.size(); ++i) {
@@ -816,7 +885,7 @@ struct Plan {
                 pg.dev_post = reinterpret_cast<PostNode*>(arena + pg.off_nodes);
                 ck(cudaMemcpy(pg.dev_post, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
                    "upload post table");
-                if (partitioned && pg.depth == 0 && !root_pairs.empty()) {
+                if ((partitioned || nrounds) && pg.depth == 0 && !root_pairs.empty()) {
                     dev_pairs = reinterpret_cast<int2*>(arena + off_pairs);
                     ck(cudaMemcpy(dev_pairs, root_pairs.data(), root_pairs.size() * sizeof(int2),
                                   cudaMemcpyHostToDevice),
@@ -863,7 +932,8 @@ struct Plan {
           << ", \"accumulators\": " << sch.nacc
           << ", \"limbs\": " << L << ", \"block_n\": " << BN
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
-          << "}, \"nodes\": " << nodes.size() << ", \"arena_bytes\": " << arena_bytes
+          << "}, \"nodes\": " << nodes.size() << ", \"post_rounds\": " << nrounds
+          << ", \"arena_bytes\": " << arena_bytes
           << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs << ", \"leaf_groups\": [";
         for (size_t i = 0; i < leaves.size(); ++i)
             o << (i ? ", " : "") << "{\"n\": " << leaves[i].n << ", \"k\": " << leaves[i].k
@@ -970,7 +1040,41 @@ struct Plan {
             counts[2]++;
         };
         const bool overlap = !g_phase_timing && !prods.empty() && prods[0].phase == 0;
-        if (!overlap) {
+        const bool post_rounds = !g_phase_timing && nrounds > 0 && !trace;
+        if (post_rounds) {
+            ck(cudaMemsetAsync(dev_rounds, 0, (nrounds + 1) * sizeof(int), s), "clear round counters");
+            for (auto& pg : preps) run_prep(pg, s);
+            mark(2);
+            ProdLaunch& pm = prods[0];
+            GroupedArgs ga = pm.args;
+            ga.round_done = dev_rounds;
+            ck(modmm_launch(sch, ga, std::min(round_ctas, ga.ntiles * (BMt / 128)), s), "modmm");
+            counts[0]++;
+            const PostGroup& root_post = posts[0];
+            PostArgs a{};
+            a.m = m;
+            a.h = root_post.n / 2;
+            a.nodes = root_post.dev_post;
+            a.nnodes = 1;
+            a.out64 = 1;
+            a.c64 = c_dev;
+            a.ldc = ldc;
+            a.alpha = alpha;
+            a.beta = beta;
+            a.pairs = dev_pairs;
+            a.npairs = (int)root_pairs.size();
+            static const int post_blocks = [] {
+                const char* e = getenv("FSYRK_B200_POST_BLOCKS");
+                return e ? atoi(e) : 0;
+            }();
+            const int blocks = post_blocks > 0 ? post_blocks : 6 * nsm;
+            ck(launch_post_rounds(a, dev_rounds, dev_rounds + nrounds + 1, dev_rounds + nrounds, blocks, s),
+               "post rounds");
+            counts[2]++;
+            root_done = true;
+            mark(3);
+            mark(4);
+        } else if (!overlap) {
             // 3. fused pre-additions, top-down; 4. products; 5. post-additions, bottom-up
             for (auto& pg : preps) run_prep(pg, s);
             mark(2);

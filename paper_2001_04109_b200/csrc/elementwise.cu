@@ -495,22 +495,12 @@ __global__ void post_kernel(const PostArgs args) {
 }
 
 // Vector variant (h, all ld % 4 == 0): block (8 x 32), thread = 4 columns of one row.
-__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const PostArgs args) {
-    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
-    pdl_trigger();
-    __shared__ uint32_t sU[TS][TS + 1];
-    __shared__ uint32_t sT[TS][TS + 1];
-    const PostNode nd = args.nodes[blockIdx.z];
+// One 32 x 32 tile pair (I >= J) of a node's post-addition, 8 x 32 threads.
+__device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNode& nd, int I, int J,
+                                              uint32_t (&sU)[TS][TS + 1], uint32_t (&sT)[TS][TS + 1]) {
     const uint32_t p = args.m.p;
     const int h = args.h;
     const PostOut out = make_out(args, nd);
-    int I, J;
-    if (args.pairs) {
-        I = args.pairs[blockIdx.x].x;
-        J = args.pairs[blockIdx.x].y;
-    } else {
-        tri_decode(blockIdx.x, I, J);
-    }
     const int tx = threadIdx.x, r = threadIdx.y;
     const int c0 = 4 * tx;
     const int i = I * TS + r, j = J * TS + c0;        // tile (I, J)
@@ -561,6 +551,67 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const Po
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = addm(sU[c0 + e][r], sT[r][c0 + e], p);
         out.put4(h + it, jt, add4(make_uint4(v[0], v[1], v[2], v[3]), p3t, p));
+    }
+}
+
+__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const PostArgs args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
+    __shared__ uint32_t sU[TS][TS + 1];
+    __shared__ uint32_t sT[TS][TS + 1];
+    const PostNode nd = args.nodes[blockIdx.z];
+    int I, J;
+    if (args.pairs) {
+        I = args.pairs[blockIdx.x].x;
+        J = args.pairs[blockIdx.x].y;
+    } else {
+        tri_decode(blockIdx.x, I, J);
+    }
+    post_vec_pair(args, nd, I, J, sU, sT);
+}
+
+// Root post-addition overlapped with the product kernel (driver.cu, Plan::rounds).  Launched as
+// the product kernel's programmatic dependent, so it starts while the products run, on the SMs
+// they leave free.  Blocks take tile pairs in round order from a shared counter and, before a
+// pair of round r, wait until every product tile of rounds <= r has been stored
+// (round_done[r] >= target[r], counted by the product kernel's epilogue warps).  No
+// griddepcontrol.wait: the products are still running.  A wait that never ends (a broken
+// count) traps after ~4 s instead of hanging the device.
+__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_rounds_kernel(const PostArgs args,
+                                                                          const int* round_done,
+                                                                          const int* target, int* next_pair) {
+    __shared__ uint32_t sU[TS][TS + 1];
+    __shared__ uint32_t sT[TS][TS + 1];
+    __shared__ int s_idx;
+    const PostNode nd = args.nodes[0];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    int ready_round = -1;  // rounds <= ready_round are known complete
+    for (;;) {
+        if (tid == 0) s_idx = atomicAdd(next_pair, 1);
+        __syncthreads();
+        const int idx = s_idx;
+        __syncthreads();
+        if (idx >= args.npairs) break;
+        const int2 pr = args.pairs[idx];
+        const int r = pr.x >> 20, I = pr.x & ((1 << 20) - 1), J = pr.y;
+        if (r > ready_round) {
+            if (tid == 0) {
+                const long long t0 = clock64();
+                for (int q = ready_round + 1; q <= r; ++q) {
+                    int v;
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(round_done + q) : "memory");
+                        if (v >= target[q]) break;
+                        __nanosleep(500);
+                        if (clock64() - t0 > (8ll << 30)) __trap();
+                    }
+                }
+            }
+            __syncthreads();
+            ready_round = r;
+        }
+        post_vec_pair(args, nd, I, J, sU, sT);
+        __syncthreads();  // sU / sT are reused by the next pair
     }
 }
 
@@ -821,6 +872,13 @@ cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
     if (args.h % 4 == 0) return launch_pdl(post_vec_kernel, grid, dim3(8, 32), 0, s, args);
     return launch_pdl(post_kernel, grid, dim3(32, 8), 0, s, args);
+}
+
+cudaError_t launch_post_rounds(const PostArgs& args, const int* round_done, const int* target, int* next_pair,
+                               int blocks, cudaStream_t s) {
+    if (args.h == 0 || args.npairs == 0) return cudaSuccess;
+    if (args.h % 4 != 0) return cudaErrorInvalidValue;
+    return launch_pdl(post_rounds_kernel, dim3(blocks), dim3(8, 32), 0, s, args, round_done, target, next_pair);
 }
 
 cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p, cudaStream_t s) {

@@ -94,6 +94,10 @@ struct AddNode {
     long long ldx;
 };
 
+// Root post-addition overlapped with the products: pairs (I | round << 20, J) in round order,
+// taken through *next_pair (zeroed per call); waits for round_done[r] >= target[r].
+cudaError_t launch_post_rounds(const PostArgs& args, const int* round_done, const int* target, int* next_pair,
+                               int blocks, cudaStream_t s);
 cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, int kout, const ColMap* map,
                               uint32_t p, uint32_t* out, long long ldo, cudaStream_t s);
 // Residues (uint32 view, or the caller's uint64 window) -> limb planes.

@@ -156,6 +156,8 @@ void modmm_set_output_map(GroupDesc& g, int batch) {
         g.tma_ok = 1;
 }
 
+int modmm_epilogue_warps() { return kEpiWarpsDefault; }
+
 int modmm_grid(const SchemeInfo& s, int nsm) {
     switch (s.id) {
         case SCHEME_LIMB2: return grid_for<SCHEME_LIMB2>(nsm);

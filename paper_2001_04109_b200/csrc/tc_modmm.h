@@ -37,8 +37,16 @@ struct GroupedArgs {
     int32_t w[8];       // balanced fold weights (LIMB schemes)
     int ngroups;
     int ntiles;
-    const int4* tiles;  // (group, batch, tm, tn), longest K first
+    const int4* tiles;  // (group | round << 8, batch, tm, tn), longest K first
+    // Root post overlap (driver.cu, Plan::rounds): every epilogue warp adds 1 to round_done[round
+    // of the tile] once its stores of the tile are globally visible, and the launch lets its
+    // programmatic dependent (the round-aware post kernel) start as soon as every CTA is past
+    // its prologue.  nullptr: off.
+    int* round_done;
 };
+constexpr int kTileGroupBits = 8;
+// epilogue warps per CTA of the product kernel (each reports once per tile to round_done)
+int modmm_epilogue_warps();
 
 // Scheme selection and its parameters (schemes.cuh).
 struct SchemeInfo {

@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_wait();  // setup above overlaps the previous kernel's tail; operands are ready from here
+    // round-aware post kernel: may launch once every CTA is resident and past the wait (it only
+    // spins on round_done, so it can never hold resources this grid or its producers need)
+    if (args.round_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         if (lane == 0) {
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             uint32_t phase = 0;
             for (int t = unit; t < args.ntiles; t += nunits) {
                 const int4 tile = args.tiles[t];
-                const GroupDesc& g = args.g[tile.x];
+                const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
                 const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
                 const int arow = tile.z * C::TILE_M + (int)rank * BM;
                 const int brow = tile.w * BN + (int)rank * C::B_ROWS;
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             uint32_t phase = 0;
             uint32_t it = 0;
             for (int t = unit; t < args.ntiles; t += nunits, ++it) {
-                const GroupDesc& g = args.g[args.tiles[t].x];
+                const GroupDesc& g = args.g[args.tiles[t].x & ((1 << kTileGroupBits) - 1)];
                 const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
                 const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
                 KTRACE(it, 0);
@@ -264,13 +267,30 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         // this warp's output staging: one 32 x 16 swizzled box per chunk (TMA-store path)
         uint8_t* stg = smem + STAGES * C::STAGE_BYTES + (warp - 2) * 2048;
         bool stores_pending = false;
+        // round-aware post (args.round_done): the previous tile's outputs are reported once this
+        // warp would idle anyway (before it waits for the next accumulators), not right after
+        // its stores were issued
+        int report_round = -1;
+        auto report = [&]() {
+            if (report_round < 0) return;
+            if (stores_pending && lane == 0) {
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete, not just read
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            stores_pending = false;
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(args.round_done + report_round, 1);
+            report_round = -1;
+        };
         uint32_t it = 0;
         for (int t = unit; t < args.ntiles; t += nunits, ++it) {
             const int4 tile = args.tiles[t];
-            const GroupDesc& g = args.g[tile.x];
+            const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
             const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
             const uint32_t use = C::NBUF == 2 ? it >> 1 : it;
             const uint32_t lane_base = tmem + buf * C::BUF_COLS + ((uint32_t)(quad * 32) << 16);
+            report();
             sm100::mbar_wait(&tmem_full[buf], use & 1);
             if (warp == 2 && lane == 0) KTRACE(it, 3);
             sm100::tc_fence_after();
@@ -421,8 +441,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     }
                 }
             }
+            if (args.round_done) report_round = tile.x >> kTileGroupBits;  // reported when the warp next idles
             if (lane == 0 && warp == 2) KTRACE(it, 6);
         }
+        report();
         if (stores_pending && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     pdl_trigger_mm();  // this CTA's work is issued: the next kernel of the call may begin launching

@@ -2,6 +2,8 @@
 against the reference's golden outputs and the pinned C oracle.
 
 Bit-exact on every entry of Low(C) (integer arithmetic; no tolerance)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -439,3 +441,36 @@ def test_winograd_general_product(gpu, p):
     a = np.full((128, 128), p - 1, dtype=np.uint64)  # extreme residues through every level
     c = fs.gemm_winograd_nt(f, a, a, fs.RecursionPolicy(8, 3))
     assert np.array_equal(c, fs.gemm_nt(f, a, a))
+
+
+@pytest.mark.parametrize("p", [131071, 65521, 65537, 2147483647])
+def test_root_post_overlapped_with_products(gpu, p):
+    # FSYRK_B200_POST_ROUNDS (off by default, read at first plan creation: this test runs in
+    # its own process): one-level plans with h >= 2048 run the root post-addition as the
+    # product kernel's programmatic dependent, pair by pair as the product rounds complete
+    # (driver.cu Plan::nrounds); exact against the oracle, accumulating with alpha, beta
+    import subprocess
+    import sys
+    if os.environ.get("FSYRK_B200_POST_ROUNDS") is None:
+        env = dict(os.environ, FSYRK_B200_POST_ROUNDS="8", FSYRK_B200_ROUND_CTAS="120")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                            f"{__file__}::test_root_post_overlapped_with_products[{p}]"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+        return
+    fs = gpu
+    f = fs.PrimeField(p)
+    n, k = 4096, 96
+    a = orc.random_matrix(p, n, k, 31)
+    c0 = orc.random_matrix(p, n, n, 32)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(2, 1))
+    alpha, beta = 12345 % p, 54321 % p
+    c = c0.copy()
+    fs.syrk_fast_acc(f, alpha, a, beta, c, plan)
+    assert fs.last_plan()["post_rounds"] > 1
+    want = orc.syrk_classical(p, a)
+    idx = np.tril_indices(n)
+    exp = (want[idx] * np.uint64(alpha) % np.uint64(p) + c0[idx] * np.uint64(beta) % np.uint64(p)) % np.uint64(p)
+    assert np.array_equal(c[idx], exp)
+    c2 = fs.syrk_fast(f, a, plan)
+    assert orc.lower_equal(c2, want)

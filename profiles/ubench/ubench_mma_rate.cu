@@ -1,3 +1,4 @@
+#include <string>
 // Microbenchmark: raw tcgen05.mma.kind::i8 issue rate with operands resident in shared
 // memory (no TMA, no epilogue) -- how the per-SM int8 MAC rate depends on the tile width N,
 // the swizzle/K-block (BK), the number of accumulators the MMAs rotate over, and 1-CTA
@@ -33,7 +34,7 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512>
+template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512, bool SIGNED = false>
 __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cycles) {
     constexpr int BROWS = PAIR ? N / 2 : N;  // B rows held by this CTA
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
         const int layout = BK == 128 ? 2 : 4;
         const uint64_t ad = sm100::sdesc_kmajor(sm100::smem_u32(A), layout, 8 * BK);
         const uint64_t bd = sm100::sdesc_kmajor(sm100::smem_u32(B), layout, 8 * BK);
-        const uint32_t idesc = sm100::idesc_i8(PAIR ? 256 : 128, N, false);
+        const uint32_t idesc = sm100::idesc_i8(PAIR ? 256 : 128, N, SIGNED);
         long long t0 = clock64();
         int q = 0;
         for (int r = 0; r < reps; ++r) {
@@ -116,11 +117,11 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
     }
 }
 
-template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512>
+template <int N, int BK, int NACC, bool PAIR, int TCOLS = 512, bool SIGNED = false>
 void run(int grid) {
     constexpr int BROWS = PAIR ? N / 2 : N;
     const int smem = 1024 + 128 * BK + ((BROWS * BK + 1023) / 1024) * 1024 + 64;
-    auto k = mma_rate<N, BK, NACC, PAIR, TCOLS>;
+    auto k = mma_rate<N, BK, NACC, PAIR, TCOLS, SIGNED>;
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     unsigned long long* d;
     CK(cudaMalloc(&d, grid * sizeof(unsigned long long)));
@@ -149,14 +150,24 @@ void run(int grid) {
         }
     const double cyc = sum / cnt / (reps * (BK / 32));
     const double macs_per_sm = (double)(PAIR ? 256 : 128) * N * 32 / (PAIR ? 2 : 1);
-    printf("N=%3d BK=%3d NACC=%d %-5s grid=%3d tmem=%3d : %7.1f cyc/MMA  %7.0f MAC/clk per CTA  (smem B/MAC %.4f)\n", N,
-           BK, NACC, PAIR ? "pair" : "1cta", grid, TCOLS, cyc, macs_per_sm / cyc,
+    printf("N=%3d BK=%3d NACC=%d %-5s %s grid=%3d tmem=%3d : %7.1f cyc/MMA  %7.0f MAC/clk per CTA  (smem B/MAC %.4f)\n", N,
+           BK, NACC, PAIR ? "pair" : "1cta", SIGNED ? "s8" : "u8", grid, TCOLS, cyc, macs_per_sm / cyc,
            (128.0 + (PAIR ? N / 2.0 : N)) / (128.0 * N));
     free(h);
     CK(cudaFree(d));
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "signed") {  // s8 x s8 vs u8 x u8 at the tile shapes in use
+        for (int grid : {1, 148}) {
+            run<128, 128, 3, false, 512, false>(grid);
+            run<128, 128, 3, false, 512, true>(grid);
+            run<160, 64, 3, false, 512, false>(grid);
+            run<160, 64, 3, false, 512, true>(grid);
+            run<96, 128, 5, false, 512, true>(grid);
+        }
+        return 0;
+    }
     // two CTAs per SM (grid 296, 256 TMEM columns each): does the tensor pipe overlap two issuers?
     run<80, 64, 3, false, 256>(296);
     run<80, 64, 3, false, 256>(148);

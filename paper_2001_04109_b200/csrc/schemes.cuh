@@ -232,6 +232,10 @@ struct SplitFold<SCHEME_M17> {
         return short_k ? a[0] + (a[1] << 6) + (f(a[2]) << 12)
                        : f(a[0]) + (f(a[1]) << 6) + (f(a[2]) << 12);  // any a < 2^31: < 2^30
     }
+    // accumulator s's share of partial() (the staggered epilogue adds them one by one)
+    __device__ __forceinline__ static V term(int s, uint32_t a, bool short_k) {
+        return s == 0 ? (short_k ? a : f(a)) : s == 1 ? (short_k ? a << 6 : f(a) << 6) : f(a) << 12;
+    }
     __device__ __forceinline__ static uint32_t final(V v, const ModP&) {
         const uint32_t r = f(v);  // v < 2^32: r < 2^17 + 2^15 < 2p
         return r >= 0x1FFFFu ? r - 0x1FFFFu : r;
@@ -247,6 +251,9 @@ struct SplitFold<SCHEME_LIMB2> {
     using V = int64_t;
     __device__ __forceinline__ static V partial(const uint32_t* a, bool) {
         return (int64_t)(int32_t)a[0] + (int64_t)(int32_t)a[1] * 256 + (int64_t)(int32_t)a[2] * 65536;
+    }
+    __device__ __forceinline__ static V term(int s, uint32_t a, bool) {
+        return (int64_t)(int32_t)a << (8 * s);
     }
     __device__ __forceinline__ static uint32_t final(V v, const ModP& m) { return mod_s64(v, m); }
 };

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "modp.cuh"
 #include "pdl.cuh"
@@ -44,6 +45,9 @@ namespace tc {
 #endif
 #ifndef FSYRK_NO_TSTORE
 #define FSYRK_NO_TSTORE 0
+#endif
+#ifndef FSYRK_STAGGER
+#define FSYRK_STAGGER 1
 #endif
 #ifndef FSYRK_EPI_WARPS
 #define FSYRK_EPI_WARPS 8
@@ -98,8 +102,23 @@ struct Cfg {
                                    STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES <= 232448;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (TSTORE ? OUT_BYTES : 0) + BAR_BYTES;
     static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1
+    // Staggered accumulator release (single TMEM buffer, separable partial fold): the epilogue
+    // drains the tile accumulator by accumulator, adding each one's share of the partial fold,
+    // and frees it at once; the next tile's first MMAs into that accumulator wait only for it.
+    // Measured (profiles/r01/variants.txt): M17 products -1% (cfg2) / -2% (cfg5); LIMB2 +4% (off).
+    static constexpr bool STAGGER =
+        FSYRK_STAGGER && NBUF == 1 && !PAIR && SplitFold<S>::ok && digits_of<S> == SCHEME_M17;
     static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
+
+// compile-time loop: fn(std::integral_constant<int, i>) for i in [0, N)
+template <int N, int I = 0, class Fn>
+__device__ __forceinline__ void static_for(Fn&& fn) {
+    if constexpr (I < N) {
+        fn(std::integral_constant<int, I>{});
+        static_for<N, I + 1>(fn);
+    }
+}
 
 // index of the first term (in issue order) that writes accumulator `acc`
 template <int S>
@@ -127,7 +146,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;        // [NBUF]
     uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF] (the leader's counts both CTAs' epilogues)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + C::NBUF);
+    uint64_t* acc_empty = tmem_empty + C::NBUF;  // [NACC] staggered release: accumulator s drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::NACC);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? sm100::cluster_rank() : 0;
@@ -148,6 +168,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             sm100::mbar_init(&tmem_full[b], 1);
             sm100::mbar_init(&tmem_empty[b], (PAIR ? 2 : 1) * EPI);
         }
+        for (int s = 0; s < C::NACC; ++s) sm100::mbar_init(&acc_empty[s], EPI);
         sm100::fence_mbar_init();
     } else if (warp == 2 && lane == 0) {
         for (int g = 0; g < args.ngroups; ++g) {
@@ -218,39 +239,84 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
                 const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
                 KTRACE(it, 0);
-                sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue(s) drained this buffer
+                if constexpr (!C::STAGGER) {
+                    sm100::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);  // epilogue(s) drained this buffer
+                    sm100::tc_fence_after();
+                }
                 KTRACE(it, 1);
-                sm100::tc_fence_after();
                 const uint32_t acc_base = tmem + buf * C::BUF_COLS;
-                for (int kb = 0; kb < g.k_blocks; ++kb) {
+                // issue term q of the scheme for K-block kb from the stage at shared address st
+                auto issue = [&](auto qc, uint32_t st, int kb) {
+                    constexpr int q = decltype(qc)::value;
+                    constexpr Term tm = Sc::term(q);
+                    constexpr bool first = first_term<S>(tm.acc) == q;
+                    const uint64_t ad = sm100::sdesc_kmajor(st + tm.a * C::A_TILE, SW, 8 * BK);
+                    const uint64_t bd = sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk) {
+                        const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
+                        // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
+                        if constexpr (PAIR)
+                            sm100::mma_i8_pair(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                        else
+                            sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
+                    }
+                };
+                auto advance = [&](int& s, uint32_t& ph) {
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                };
+                int kb0 = 0;
+                if constexpr (C::STAGGER) {
+                    // The epilogue frees the accumulators one by one (0 first).  The terms of every
+                    // accumulator but the last start as soon as theirs is free, for as many K-blocks
+                    // as there are stages; the last accumulator's terms of those K-blocks follow once
+                    // it is free (per accumulator the sums run in the same K order, so the int32
+                    // results are the same).  The tensor pipe thus works while the epilogue drains.
+                    constexpr int LAST = C::NACC - 1;
+                    const int L = g.k_blocks < STAGES ? g.k_blocks : STAGES;
+                    int s1 = stage;
+                    uint32_t ph1 = phase;
+                    for (int kb = 0; kb < L; ++kb) {
+                        sm100::mbar_wait(&full[s1], ph1);
+                        sm100::tc_fence_after();
+                        const uint32_t st = sm100::smem_u32(smem + s1 * C::STAGE_BYTES);
+                        static_for<Sc::NT>([&](auto qc) {
+                            constexpr Term tm = Sc::term(decltype(qc)::value);
+                            if constexpr (tm.acc != LAST) {
+                                if (kb == 0 && first_term<S>(tm.acc) == decltype(qc)::value) {
+                                    sm100::mbar_wait(&acc_empty[tm.acc], (use & 1) ^ 1);
+                                    sm100::tc_fence_after();
+                                }
+                                issue(qc, st, kb);
+                            }
+                        });
+                        advance(s1, ph1);
+                    }
+                    sm100::mbar_wait(&acc_empty[LAST], (use & 1) ^ 1);
+                    sm100::tc_fence_after();
+                    for (int kb = 0; kb < L; ++kb) {
+                        const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
+                        static_for<Sc::NT>([&](auto qc) {
+                            if constexpr (Sc::term(decltype(qc)::value).acc == LAST) issue(qc, st, kb);
+                        });
+                        sm100::tc_commit(&empty[stage]);
+                        advance(stage, phase);
+                    }
+                    kb0 = L;
+                }
+                for (int kb = kb0; kb < g.k_blocks; ++kb) {
                     sm100::mbar_wait(&full[stage], phase);
                     sm100::tc_fence_after();
                     const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
-#pragma unroll
-                    for (int q = 0; q < Sc::NT; ++q) {
-                        const Term tm = Sc::term(q);
-                        const bool first = first_term<S>(tm.acc) == q;
-                        const uint64_t ad = sm100::sdesc_kmajor(st + tm.a * C::A_TILE, SW, 8 * BK);
-                        const uint64_t bd =
-                            sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
-#pragma unroll
-                        for (int kk = 0; kk < BK / 32; ++kk) {
-                            const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
-                            // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
-                            if constexpr (PAIR)
-                                sm100::mma_i8_pair(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                            else
-                                sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
-                        }
-                    }
+                    static_for<Sc::NT>([&](auto qc) { issue(qc, st, kb); });
                     if constexpr (PAIR)
                         sm100::tc_commit_pair(&empty[stage]);
                     else
                         sm100::tc_commit(&empty[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    advance(stage, phase);
                 }
                 if constexpr (PAIR)
                     sm100::tc_commit_pair(&tmem_full[buf]);
@@ -395,7 +461,45 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
 #endif
             const bool staged = C::TSTORE && g.tma_ok;
             uint32_t ra[C::NACC][16];
-            if constexpr (SplitFold<S>::ok) {
+            if constexpr (C::STAGGER) {
+                using V = typename SplitFold<S>::V;
+                const bool short_k = g.k_blocks * BK <= 2048;
+                V v[C::NCW][16];
+#pragma unroll
+                for (int s = 0; s < C::NACC; ++s) {
+                    uint32_t raw[C::NCW][16];
+#pragma unroll
+                    for (int j = 0; j < C::NCW; ++j)
+                        if (j < nch) sm100::tmem_ld16(lane_base + s * BN + col_of(j), raw[j]);
+                    sm100::tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < C::NCW; ++j) sm100::reg_fence16(raw[j]);
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) sm100::mbar_arrive(&acc_empty[s]);  // accumulator s may be overwritten
+#pragma unroll
+                    for (int j = 0; j < C::NCW; ++j) {
+                        if (j < nch) {
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) {
+                                const V t = SplitFold<S>::term(s, raw[j][c], short_k);
+                                v[j][c] = s == 0 ? t : v[j][c] + t;
+                            }
+                        }
+                    }
+                }
+                if (lane == 0 && warp == 2) KTRACE(it, 4);
+#pragma unroll
+                for (int j = 0; j < C::NCW; ++j) {
+                    if (j < nch) {
+                        uint32_t res[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) res[c] = SplitFold<S>::final(v[j][c], m);
+                        if (staged) stage_store(res, j);
+                        else store_direct(res, col_of(j));
+                    }
+                }
+            } else if constexpr (SplitFold<S>::ok) {
                 // Only a cheap partial fold (one compact value per output) runs while the tile's
                 // accumulators hold TMEM; the final reduction and the stores overlap the next
                 // tile's MMAs.

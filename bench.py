@@ -418,6 +418,19 @@ def main():
                 # ncu's int8 tensor peak: 16384 ops/clk/SM x 148 SMs x 1.965 GHz
                 "nominal_peak": 4765.4, "nominal_frac": round(achieved / 4765.4, 4),
                 "phase_ms": {k2: round(v, 4) for k2, v in phase.items()}}
+    # the elementwise phases against HBM: algorithmic bytes (plan JSON, driver.cu) / phase time
+    hbm_peak = peaks.get("hbm_gbs")
+    post_b = plan.get("post_bytes", 0) + (plan.get("post_cin_bytes", 0) if beta % p else 0)
+    hbm = {}
+    for key, nbytes in (("convert", plan.get("convert_bytes", 0)), ("pre", plan.get("prep_bytes", 0)),
+                        ("post", post_b)):
+        t = phase.get(key, 0.0)
+        if t > 0 and nbytes:
+            gbs = nbytes / (t / 1e3) / 1e9
+            hbm[key] = {"algorithmic_bytes": nbytes, "ms": round(t, 4), "achieved": round(gbs, 1),
+                        "frac": round(gbs / hbm_peak, 4) if hbm_peak else None}
+    roofline["elementwise_hbm"] = {"peak": hbm_peak, "unit": "GB/s",
+                                   "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs)", **hbm}
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_reference(args.config, cfg, 1, 1)
     if cpu is not None:
         cpu.pop("seconds", None)

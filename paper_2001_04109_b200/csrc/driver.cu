@@ -330,6 +330,7 @@ struct Plan {
     uint64_t tensor_macs = 0;  // modular MACs issued on the tensor cores
     uint64_t int8_macs = 0;
     uint64_t ew_adds = 0;
+    uint64_t prep_bytes = 0, post_bytes = 0, post_cin_bytes = 0, convert_bytes = 0;  // algorithmic HBM bytes
 
     // side stream + events: the top level's general products overlap the deeper pre/post-additions
     cudaStream_t side = nullptr;
@@ -922,6 +923,30 @@ struct Plan {
                          BN * gg.kpad * sch.nterms;
             ew_adds += (uint64_t)gg.count * (4ull * gg.h * gg.kw + 4ull * gg.h * gg.h);
         }
+        // algorithmic HBM bytes of the elementwise phases (what each kernel must read and write;
+        // bench.py divides them by the phase times for the HBM roofline fraction)
+        prep_bytes = post_bytes = post_cin_bytes = 0;
+        convert_bytes = colmap ? (uint64_t)n * kin * 8 + (uint64_t)n * k * 4 : 0;  // caller's A in, residues out
+        auto lower = [](uint64_t m) { return m * (m + 1) / 2; };
+        for (const Node& nd : nodes) {
+            if (nd.kind == LEVEL) {
+                const uint64_t h = nd.h, kh = nd.kh, kw = nd.kw;
+                prep_bytes += (uint64_t)nd.n * nd.k * (nd.in64 ? 8 : 4);        // the four quadrants
+                prep_bytes += 2 * h * kw * (uint64_t)(sch.pa + sch.pb);          // S1, A22 / S2, S4 planes
+                for (int c = 0; c < 3; ++c) {
+                    const Node& ch = nodes[nd.ch[c]];
+                    if (ch.kind == LEAF) prep_bytes += h * (uint64_t)ch.k * L;   // leaf operand planes
+                    else if (c == 2) prep_bytes += h * kw * 4;                    // S3 residues
+                }
+                post_bytes += 3 * lower(h) * 4 + 2 * h * h * 4;                  // P1, P2, P5 (lower), P3, P4
+            } else if (nd.kind == SPLITK) {
+                post_bytes += 2 * lower(nd.n) * 4;
+            } else {
+                continue;
+            }
+            post_bytes += lower(nd.n) * (nd.parent < 0 ? 8 : 4);  // X (the root: the caller's uint64 C)
+            if (nd.parent < 0) post_cin_bytes = lower(nd.n) * 8;   // + C_in when beta != 0
+        }
     }
 
     std::string json() const {
@@ -934,7 +959,10 @@ struct Plan {
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
           << "}, \"nodes\": " << nodes.size() << ", \"post_rounds\": " << nrounds
           << ", \"arena_bytes\": " << arena_bytes
-          << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs << ", \"leaf_groups\": [";
+          << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs
+          << ", \"prep_bytes\": " << prep_bytes << ", \"post_bytes\": " << post_bytes
+          << ", \"post_cin_bytes\": " << post_cin_bytes << ", \"convert_bytes\": " << convert_bytes
+          << ", \"leaf_groups\": [";
         for (size_t i = 0; i < leaves.size(); ++i)
             o << (i ? ", " : "") << "{\"n\": " << leaves[i].n << ", \"k\": " << leaves[i].k
               << ", \"count\": " << leaves[i].count << ", \"tiles\": " << leaves[i].ntiles << "}";
@@ -962,11 +990,16 @@ struct Plan {
         }
         mark(0);
         const Node& root = nodes[0];
+        cudaEvent_t ev_conv = nullptr;  // phase timing: end of the conversion pass
         // 1. syrkd: convert the reference-layout input with the column transform folded in;
         //    otherwise the top-level pre-additions read the caller's uint64 matrix directly
         if (colmap) {
             ck(launch_convert_in(a_dev, lda, n, kin, k, dev_colmap, (uint32_t)p, root_in, root.ldin, s), "convert_in");
             counts[3]++;
+        }
+        if (g_phase_timing) {
+            ck(cudaEventCreate(&ev_conv), "event");
+            ck(cudaEventRecord(ev_conv, s), "event record");
         }
         // 2. leaf operands that are plain views (root leaf, split-on-k children)
         for (int li : split_leaves) {
@@ -1142,15 +1175,16 @@ struct Plan {
             float t;
             // kinds: 0 products, 1 pre (split + prep), 2 post, 3 convert/finalize
             cudaEventElapsedTime(&t, ev[2], ev[3]); g_phase_ms[0] = t;
-            float t1, t2;
-            cudaEventElapsedTime(&t1, ev[0], ev[1]);
+            float tc = 0, t1 = 0, t2 = 0;  // convert (ev0 -> ev_conv), pre (ev_conv -> ev2)
+            cudaEventElapsedTime(&tc, ev[0], ev_conv);
+            cudaEventElapsedTime(&t1, ev_conv, ev[1]);
             cudaEventElapsedTime(&t2, ev[1], ev[2]);
             g_phase_ms[1] = t1 + t2;
-            t1 = 0;
             cudaEventElapsedTime(&t, ev[3], ev[4]); g_phase_ms[2] = t;
             float t5;
             cudaEventElapsedTime(&t5, ev[4], ev[5]);
-            g_phase_ms[3] = t1 + t5;
+            g_phase_ms[3] = tc + t5;
+            cudaEventDestroy(ev_conv);
             g_phase_ms[4] = 0;
             for (auto& e : ev) cudaEventDestroy(e);
         }

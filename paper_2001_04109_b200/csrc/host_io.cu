@@ -14,6 +14,7 @@
 #include "host_io.h"
 
 #include <immintrin.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -117,8 +118,14 @@ class Workers {
 };
 
 Workers& workers() {
-    static Workers w(std::max(1, host_threads() - 1));  // the calling thread orchestrates
-    return w;
+    // the calling thread orchestrates; a forked child (whose copy has no threads) builds its own
+    static Workers* w = nullptr;
+    static pid_t owner = 0;
+    if (!w || owner != getpid()) {
+        w = new Workers(std::max(1, host_threads() - 1));  // the parent's copy is abandoned on purpose
+        owner = getpid();
+    }
+    return *w;
 }
 
 // ---- conversions (AVX2 when the CPU has it) ----

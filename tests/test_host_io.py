@@ -40,3 +40,21 @@ def test_transfer_bits(fsyrk):
     assert fsyrk.transfer_bits(65537) == 17
     assert fsyrk.transfer_bits(131071) == 17
     assert fsyrk.transfer_bits(2147483647) == 32
+
+
+def test_roundtrip_in_forked_child(fsyrk):
+    # the worker pool is per process: a child forked after the pool started builds its own
+    import multiprocessing as mp
+    a = np.arange(64 * 100, dtype=np.uint64).reshape(64, 100) % 65521
+    fsyrk.hostio_roundtrip(a, False, 16)  # start the parent's pool
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+
+    def child(queue):
+        out, raw, _ = fsyrk.hostio_roundtrip(a, False, 16)
+        queue.put(bool(np.array_equal(out, a)) and raw == 0)
+
+    proc = ctx.Process(target=child, args=(q,))
+    proc.start()
+    proc.join(60)
+    assert proc.exitcode == 0 and q.get(timeout=5)

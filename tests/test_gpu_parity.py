@@ -474,3 +474,38 @@ def test_root_post_overlapped_with_products(gpu, p):
     assert np.array_equal(c[idx], exp)
     c2 = fs.syrk_fast(f, a, plan)
     assert orc.lower_equal(c2, want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("p", [5, 13, 131041, 3, 7, 11, 131071, 65521, 65537, 2147483647])
+def test_acceptance_battery(gpu, p):
+    # the reference's main parity gate at its own scale (acceptance.cpp:45-74): 500 seeded
+    # cases per prime, n, k <= 256, thresholds {2, 8, 64}; every third case accumulates with
+    # random alpha, beta (test_fast_syrk.cpp:312-375) and every fifth mirrors.  The reference's
+    # seven primes plus the BASELINE primes of the other digit schemes (LIMB2, LIMB3, M31).
+    fs = gpu
+    f = fs.PrimeField(p)
+    rng = np.random.default_rng(p * 7919 + 1)
+    for t in range(500):
+        n = int(rng.integers(1, 257))
+        k = int(rng.integers(1, 257))
+        thr = (2, 8, 64)[t % 3]
+        a = orc.random_matrix(p, n, k, int(rng.integers(1 << 62)))
+        plan = fs.make_syrk_plan(f, fs.RecursionPolicy(thr), mirror_output=(t % 5 == 4))
+        want = orc.syrk_classical(p, a)
+        if t % 3 == 1:
+            alpha, beta = int(rng.integers(p)), int(rng.integers(p))
+            c0 = orc.random_matrix(p, n, n, int(rng.integers(1 << 62)))
+            c = c0.copy()
+            fs.syrk_fast_acc(f, alpha, a, beta, c, plan)
+            idx = np.tril_indices(n)
+            exp = (want[idx] * np.uint64(alpha) % np.uint64(p) + c0[idx] * np.uint64(beta) % np.uint64(p)) % np.uint64(p)
+            assert np.array_equal(c[idx], exp), (p, n, k, thr, t)
+        else:
+            c = fs.syrk_fast(f, a, plan)
+            assert orc.lower_equal(c, want), (p, n, k, thr, t)
+            if t % 5 == 4:
+                assert np.array_equal(c, c.T), (p, n, k, t)
+        if t % 100 == 99:
+            fs.release_cache()
+    fs.release_cache()

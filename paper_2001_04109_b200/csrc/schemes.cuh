@@ -60,9 +60,16 @@ struct Scheme;
 #ifndef FSYRK_LIMB2_BN
 #define FSYRK_LIMB2_BN 128
 #endif
+#ifndef FSYRK_LIMB2_BK
+#define FSYRK_LIMB2_BK 128
+#endif
+#ifndef FSYRK_LIMB2_STAGES
+#define FSYRK_LIMB2_STAGES (FSYRK_PAIR ? 4 : 3)
+#endif
 template <>
 struct Scheme<SCHEME_LIMB2> {
-    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = FSYRK_LIMB2_BN, BK = 128, STAGES = FSYRK_PAIR ? 4 : 3;
+    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK,
+                         STAGES = FSYRK_LIMB2_STAGES;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};

@@ -539,23 +539,33 @@ struct Plan {
                 ProdLaunch pl;
                 pl.phase = pgs[c0].phase;
                 size_t c = c0;
+                // Tiles of one product in groups of kGroupRows tile rows, column by column inside a
+                // group: the ~ncta tiles in flight then share kGroupRows A row panels and ~ncta /
+                // kGroupRows B column panels in L2, instead of every B panel being streamed again
+                // for each tile row (cfg4's 8192^2 products: 11x re-reads from DRAM in row order).
+                static const int kGroupRows = [] {
+                    const char* e = getenv("FSYRK_B200_GROUP_ROWS");
+                    return e ? atoi(e) : 12;
+                }();
+                auto push_tiles = [&](int gi, int b, int nrow, int ncol, bool lower) {
+                    const int ntm = (nrow + BMt - 1) / BMt, ntn = (ncol + BN - 1) / BN;
+                    const int gm = kGroupRows > 0 ? kGroupRows : ntm;
+                    for (int tm0 = 0; tm0 < ntm; tm0 += gm)
+                        for (int tn = 0; tn < ntn; ++tn)
+                            for (int tm = tm0; tm < std::min(ntm, tm0 + gm); ++tm)
+                                if ((!lower || tn * BN <= tm * BMt + BMt - 1) && !idle &&
+                                    owns_block_pair(tm * BMt / kPartBlock, tn * BN / kPartBlock))
+                                    pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                };
                 for (; c < pgs.size() && c < c0 + kMaxGroups && pgs[c].phase == pl.phase; ++c) {
                     const int gi = (int)(c - c0);
                     pl.members.push_back({pgs[c].leaf, pgs[c].idx});
                     if (!pgs[c].leaf) {
                         const GemmGroup& gg = gemms[pgs[c].idx];
-                        for (int b = 0; b < 2 * gg.count; ++b)
-                            for (int tm = 0; tm * BMt < gg.h; ++tm)
-                                for (int tn = 0; tn * BN < gg.h; ++tn)
-                                    if (!idle && owns_block_pair(tm * BMt / kPartBlock, tn * BN / kPartBlock))
-                                        pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                        for (int b = 0; b < 2 * gg.count; ++b) push_tiles(gi, b, gg.h, gg.h, false);
                     } else {
                         const LeafGroup& lg = leaves[pgs[c].idx];
-                        for (int b = 0; b < lg.count; ++b)
-                            for (int tm = 0; tm * BMt < lg.n; ++tm)
-                                for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * BMt + BMt - 1; ++tn)
-                                    if (!idle && owns_block_pair(tm * BMt / kPartBlock, tn * BN / kPartBlock))
-                                        pl.host_tiles.push_back(make_int4(gi, b, tm, tn));
+                        for (int b = 0; b < lg.count; ++b) push_tiles(gi, b, lg.n, lg.n, true);
                     }
                 }
                 pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4));

@@ -18,3 +18,5 @@ python profiles/run_config.py cfg5 --iters 2 > /dev/null 2>&1; echo run_config5 
 ncu --set full --clock-control none -k regex:modmm --launch-skip 1 -c 1 -f -o gpurun_out/r01/modmm_cfg5 python profiles/run_config.py cfg5 --iters 2 > gpurun_out/r01/ncu_modmm5.log 2>&1; echo ncu5 rc=$?
 python profiles/run_config.py cfg3 --iters 2 > /dev/null 2>&1; echo run_config3 rc=$?
 ncu --set full --clock-control none -k regex:modmm --launch-skip 1 -c 1 -f -o gpurun_out/r01/modmm_cfg3 python profiles/run_config.py cfg3 --iters 2 > gpurun_out/r01/ncu_modmm3.log 2>&1; echo ncu6 rc=$?
+python profiles/run_config.py cfg4 --iters 2 > /dev/null 2>&1; echo run_config4 rc=$?
+ncu --set full --clock-control none -k regex:modmm --launch-skip 1 -c 1 -f -o gpurun_out/r01/modmm_cfg4 python profiles/run_config.py cfg4 --iters 2 > gpurun_out/r01/ncu_modmm4.log 2>&1; echo ncu7 rc=$?

@@ -1669,6 +1669,8 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
         fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
     require_device();
     if (n == 0) return;
+    if ((k > 0 && hio::is_device(a)) || hio::is_device(c))
+        fail(FSYRK_B200_EINVAL, "host entry point called with device memory (use fsyrk_b200_syrk_dev)");
     std::lock_guard<std::mutex> lk(g_stage_mu);
     g_io.init();
     const size_t abytes = n * std::max<size_t>(k, 1) * 8, cbytes = n * n * 8;

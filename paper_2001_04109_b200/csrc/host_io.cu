@@ -627,6 +627,15 @@ int transfer_bits(uint64_t p) {
     return std::max(b, kMinBits);
 }
 
+bool is_device(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice;
+}
+
 cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t ldd, int bits, cudaStream_t s,
                    uint64_t* bytes) {
     const size_t total = r.offset(r.rows);

@@ -33,6 +33,8 @@ struct Region {
 
 // true when `p` is page-locked host memory (cudaHostAlloc / cudaHostRegister)
 bool is_pinned(const void* p);
+// true when `p` is device memory (not readable by host threads)
+bool is_device(const void* p);
 
 // Host rows -> device uint64 rows (row stride ldd).  Returns after the last chunk is queued on
 // `s` (host work done; the device side completes in stream order).  *bytes += PCIe bytes.

@@ -509,3 +509,19 @@ def test_acceptance_battery(gpu, p):
         if t % 100 == 99:
             fs.release_cache()
     fs.release_cache()
+
+
+def test_host_entry_rejects_device_memory(gpu):
+    # the host entry points stage through host threads: device pointers are refused (EINVAL),
+    # not dereferenced on the host
+    torch = pytest.importorskip("torch")
+    import ctypes
+    fs = gpu
+    lib = fs.lib()
+    a = torch.zeros((64, 32), dtype=torch.int64, device="cuda")
+    c = np.zeros((64, 64), dtype=np.uint64)
+    pol = fs.RecursionPolicy(8)._c()
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    st = lib.fsyrk_b200_syrk_fast_into(131071, ctypes.cast(a.data_ptr(), u64p), 64, 32, 32,
+                                       c.ctypes.data_as(u64p), 64, pol, 0, None)
+    assert st == 2 and b"device memory" in lib.fsyrk_b200_last_error()

@@ -150,6 +150,16 @@ def cpu_reference(cfgname, cfg, threads, reps=1):
             "seconds": out["wall_seconds"]}
 
 
+def cpu_reference_bounded(cfgname, cfg, target_s=10.0):
+    """The reference on one core, repeated until about target_s seconds of CPU work (the
+    cpu_baseline leg: a bounded sample of the workload, timed on the box's own host)."""
+    first = cpu_reference(cfgname, cfg, 1, 1)
+    if first is None:
+        return None
+    reps = max(1, min(50, int(target_s / max(first["seconds"], 1e-3) + 0.5)))
+    return cpu_reference(cfgname, cfg, 1, reps) if reps > 1 else first
+
+
 def run_reference(args, cfgname, cfg, world, rank):
     if rank != 0:
         return
@@ -431,7 +441,7 @@ def main():
                         "frac": round(gbs / hbm_peak, 4) if hbm_peak else None}
     roofline["elementwise_hbm"] = {"peak": hbm_peak, "unit": "GB/s",
                                    "peak_source": "measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs)", **hbm}
-    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_reference(args.config, cfg, 1, 1)
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_reference_bounded(args.config, cfg)
     if cpu is not None:
         cpu.pop("seconds", None)
     clocks = clk.summary()

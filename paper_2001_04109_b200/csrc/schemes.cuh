@@ -137,6 +137,9 @@ struct Scheme<SCHEME_M17N> : Scheme<SCHEME_M17> {
 #ifndef FSYRK_M31_ACC4
 #define FSYRK_M31_ACC4 1  // measured: cfg4 products 23.5 -> 20.2 ms (profiles/r01/variants.txt)
 #endif
+#ifndef FSYRK_M31_PAIR
+#define FSYRK_M31_PAIR FSYRK_PAIR  // CTA pairs for M31 only (experiment, profiles/r01/variants.txt)
+#endif
 #ifndef FSYRK_M31_BK
 #define FSYRK_M31_BK 64
 #endif
@@ -148,7 +151,7 @@ struct Scheme<SCHEME_M31> {
     static constexpr bool ACC4 = FSYRK_M31_ACC4;
     static constexpr int PA = 5, PB = 5, NACC = ACC4 ? 4 : 5, NT = ACC4 ? 17 : 16, BN = ACC4 ? 128 : 96,
                          BK = FSYRK_M31_BK, STAGES = FSYRK_M31_STAGES;
-    static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
+    static constexpr bool UNSIGNED = true, PAIR = FSYRK_M31_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T5[16] = {
         {0, 0, 0}, {1, 4, 0}, {4, 1, 0},             // s=0 and s=4 (2^32 = 2): d1 (2 e3) + (2 d3) e1

@@ -117,6 +117,10 @@ cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid,
 }
 
 #ifdef FSYRK_KTRACE
+extern "C" int fsyrk_b200_debug_cta_span(unsigned long long* out, int n) {
+    const int m = n < 1024 * 3 ? n : 1024 * 3;
+    return (int)cudaMemcpyFromSymbol(out, g_cta_span, m * sizeof(unsigned long long));
+}
 extern "C" int fsyrk_b200_debug_ktrace(unsigned long long* out, int n) {
     const int m = n < kTraceTiles * 8 ? n : kTraceTiles * 8;
     return (int)cudaMemcpyFromSymbol(out, g_ktrace, m * sizeof(unsigned long long));

@@ -63,6 +63,13 @@ __device__ unsigned long long g_ktrace[kTraceTiles][8];
     do {                                                                                        \
         if (blockIdx.x == 0 && (it) < kTraceTiles) g_ktrace[(it)][(slot)] = clock64();          \
     } while (0)
+// per-CTA span (globaltimer ns): [0] past the prologue, [1] last epilogue warp done, [2] tiles
+__device__ unsigned long long g_cta_span[1024][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #else
 #define KTRACE(it, slot) \
     do {                 \
@@ -183,6 +190,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_wait();  // setup above overlaps the previous kernel's tail; operands are ready from here
+#ifdef FSYRK_KTRACE
+    if (threadIdx.x == 0) g_cta_span[blockIdx.x][0] = gtimer();
+#endif
     // round-aware post kernel: may launch once every CTA is resident and past the wait (it only
     // spins on round_done, so it can never hold resources this grid or its producers need)
     if (args.round_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -550,6 +560,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         }
         report();
         if (stores_pending && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef FSYRK_KTRACE
+        if (lane == 0) {
+            atomicMax(&g_cta_span[blockIdx.x][1], gtimer());
+            g_cta_span[blockIdx.x][2] = it;
+        }
+#endif
     }
     pdl_trigger_mm();  // this CTA's work is issued: the next kernel of the call may begin launching
     sm100::tc_fence_before();

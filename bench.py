@@ -117,9 +117,14 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # FSYRK_B200_BENCH_PART1=1: run the multi-GPU partition path as a single rank (one-GPU test
+    # of its NCCL / staging plumbing; the result is the single-GPU problem)
+    if world > 1 or os.environ.get("FSYRK_B200_BENCH_PART1"):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         import torch
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -240,8 +245,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    part = world > 1 and args.mgpu == "partition"
-    if world > 1:
+    part = (world > 1 or bool(os.environ.get("FSYRK_B200_BENCH_PART1"))) and args.mgpu == "partition"
+    if world > 1 or part:
         import torch.distributed as dist
     p, n, k = cfg["p"], cfg["n"], cfg["k"]
     f = fs.PrimeField(p)
@@ -363,16 +368,22 @@ def main():
             c_np[:] = c0_host
         plan_obj = fs.make_syrk_plan(f, policy)
 
+        up_bytes = [0, 0]
+
         def host_step():
             if part:  # rank 0 uploads A, NCCL broadcast, per-rank shares, NCCL reduce of C, rank 0 downloads
+                # rank 0's host copies go through the library's staging path (bit-packed residues,
+                # fsyrk_b200_upload / _download: Low(C) only), like the single-GPU host entry points
                 if rank == 0:
-                    a_dev.copy_(a_pin, non_blocking=True)
+                    fs.upload(p, a_np, a_dev.data_ptr(), k, stream=sh)
+                    up_bytes[0] = fs.last_transfer_bytes()[0]
                 dist.broadcast(a_dev, src=0)
                 c_dev.zero_()
                 step()
                 dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
                 if rank == 0:
-                    c_pin.copy_(c_dev)
+                    fs.download(p, c_dev.data_ptr(), n, c_np, lower=True, stream=sh)
+                    up_bytes[1] = fs.last_transfer_bytes()[1]
                 torch.cuda.synchronize()
             elif cfg["mode"] == "plain":
                 fs.syrk_fast_into(f, a_np, c_np, plan_obj)
@@ -391,8 +402,8 @@ def main():
             host_step()
         t1 = time.perf_counter()
         secs = max_over_ranks(t1 - t0, world)
-        if part:  # rank 0's copies around the NCCL broadcast / reduce
-            h2d, d2h = n * k * 8, n * n * 8
+        if part:  # rank 0's staged copies around the NCCL broadcast / reduce
+            h2d, d2h = up_bytes
         else:     # what the host API moved (A, and the lower-triangle row blocks of C)
             h2d, d2h = fs.last_transfer_bytes()
             h2d, d2h = h2d * world, d2h * world
@@ -400,7 +411,7 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
     if rank != 0:
-        if world > 1:
+        if world > 1 or part:
             dist.destroy_process_group()
         return
 
@@ -461,7 +472,7 @@ def main():
             "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("scheme", "terms", "block_n", "nodes", "leaf_groups",
                                                                      "gemm_groups", "arena_bytes")}}
     print(json.dumps(line))
-    if world > 1:
+    if world > 1 or part:
         dist.destroy_process_group()
 
 

@@ -182,6 +182,18 @@ int fsyrk_b200_syrk_part_dev(uint64_t p, uint64_t alpha, const uint64_t* a_dev, 
                              const uint64_t* d_host, uint64_t beta, uint64_t* c_dev, size_t ldc,
                              fsyrk_b200_policy policy, int rank, int nranks, void* stream, fsyrk_b200_opcount* ops);
 
+/* Host <-> device staging of residue matrices through the library's transfer path (bit-packed
+ * residues of p on the wire, host worker threads, pinned slots; see host_io.h) -- what the host
+ * entry points use internally, for callers that keep A / C on the device (e.g. rank 0 of a
+ * multi-GPU call before an NCCL broadcast).  lower != 0: only row i's columns [0, i] move.
+ * upload returns once the transfer is queued on `stream` (the caller's host rows may be reused);
+ * download is synchronous; device values must be < 2^32.  Host-to-device / device-to-host byte
+ * counts land in fsyrk_b200_last_transfer_bytes. */
+int fsyrk_b200_upload(uint64_t p, const uint64_t* h, size_t rows, size_t cols, size_t ldh, int lower, uint64_t* d_dev,
+                      size_t ldd, void* stream);
+int fsyrk_b200_download(uint64_t p, const uint64_t* d_dev, size_t rows, size_t cols, size_t ldd, int lower,
+                        uint64_t* h, size_t ldh, void* stream);
+
 /* Owner rank of every top-level block pair (I >= J) for quadrant size h = n/2:
  * owners[I * nblocks + J]; blocks are `block` rows/columns (lcm of 128 and the
  * product tile width of p's digit scheme).  Host-only. */

@@ -2000,6 +2000,41 @@ void fsyrk_b200_release_cache(void) {
     g_cache.clear();
 }
 
+int fsyrk_b200_upload(uint64_t p, const uint64_t* h, size_t rows, size_t cols, size_t ldh, int lower, uint64_t* d_dev,
+                      size_t ldd, void* stream) {
+    return guarded([&] {
+        validate_field(p);
+        if (ldh < cols || ldd < cols || (lower && cols < rows)) fail(FSYRK_B200_EDIMENSION, "upload: bad shape");
+        require_device();
+        if (rows == 0 || cols == 0) return;
+        if (hio::is_device(h)) fail(FSYRK_B200_EINVAL, "upload: host rows are device memory");
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        uint64_t bytes = 0;
+        ck(hio::upload(h, ldh, hio::Region{rows, cols, lower != 0}, d_dev, ldd, hio::transfer_bits(p),
+                       static_cast<cudaStream_t>(stream), &bytes),
+           "upload");
+        g_transfer[0] = bytes;
+        g_transfer[1] = 0;
+    });
+}
+
+int fsyrk_b200_download(uint64_t p, const uint64_t* d_dev, size_t rows, size_t cols, size_t ldd, int lower,
+                        uint64_t* h, size_t ldh, void* stream) {
+    return guarded([&] {
+        validate_field(p);
+        if (ldh < cols || ldd < cols || (lower && cols < rows)) fail(FSYRK_B200_EDIMENSION, "download: bad shape");
+        require_device();
+        if (rows == 0 || cols == 0) return;
+        if (hio::is_device(h)) fail(FSYRK_B200_EINVAL, "download: host rows are device memory");
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        uint64_t bytes = 0;
+        ck(hio::download(d_dev, ldd, hio::Region{rows, cols, lower != 0}, h, ldh, 0, hio::transfer_bits(p),
+                         static_cast<cudaStream_t>(stream), &bytes),
+           "download");
+        g_transfer[1] = bytes;
+    });
+}
+
 int fsyrk_b200_hostio_roundtrip(const uint64_t* a, size_t rows, size_t cols, size_t lda, int lower, int bits,
                                 uint64_t* out, size_t ldo, size_t* raw_chunks, double* secs) {
     return guarded([&] {

@@ -94,7 +94,7 @@ EXPORTS = (
     "fsyrk_b200_syrk_part_dev", "fsyrk_b200_partition_owners", "fsyrk_b200_syrkbd", "fsyrk_b200_syrkbd_dev",
     "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
     "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2", "fsyrk_b200_gemm_winograd_nt",
-    "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip",
+    "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip", "fsyrk_b200_upload", "fsyrk_b200_download",
 )
 
 
@@ -141,6 +141,10 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    L.fsyrk_b200_upload.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    L.fsyrk_b200_download.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
+                                       ctypes.c_size_t, ctypes.c_int, _u64p, ctypes.c_size_t, ctypes.c_void_p]
     L.fsyrk_b200_hostio_roundtrip.argtypes = [_u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int,
                                               ctypes.c_int, _u64p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
                                               ctypes.POINTER(ctypes.c_double)]
@@ -623,6 +627,20 @@ def transfer_bits(p: int) -> int:
     """Width of a residue on the wire for the host entry points (host_io.cu transfer_bits)."""
     b = max(8, (int(p) - 1).bit_length())
     return b if b <= 24 and os.environ.get("FSYRK_B200_PACK", "1") != "0" else 32
+
+
+def upload(p: int, h: np.ndarray, d_ptr: int, ldd: int, lower: bool = False, stream: int = 0) -> None:
+    """Host rows -> device uint64 rows through the library's staging path (fsyrk_b200_upload)."""
+    ph, rows, cols, ldh = _view(h, "h")
+    _check(lib().fsyrk_b200_upload(int(p), ph, rows, cols, ldh, int(bool(lower)), ctypes.c_void_p(d_ptr), int(ldd),
+                                   ctypes.c_void_p(stream)))
+
+
+def download(p: int, d_ptr: int, ldd: int, h: np.ndarray, lower: bool = False, stream: int = 0) -> None:
+    """Device uint64 rows (residues) -> host rows (fsyrk_b200_download; synchronous)."""
+    ph, rows, cols, ldh = _view(h, "h")
+    _check(lib().fsyrk_b200_download(int(p), ctypes.c_void_p(d_ptr), rows, cols, int(ldd), int(bool(lower)), ph, ldh,
+                                     ctypes.c_void_p(stream)))
 
 
 def hostio_roundtrip(a: np.ndarray, lower: bool, bits: int):

@@ -525,3 +525,26 @@ def test_host_entry_rejects_device_memory(gpu):
     st = lib.fsyrk_b200_syrk_fast_into(131071, ctypes.cast(a.data_ptr(), u64p), 64, 32, 32,
                                        c.ctypes.data_as(u64p), 64, pol, 0, None)
     assert st == 2 and b"device memory" in lib.fsyrk_b200_last_error()
+
+
+@pytest.mark.parametrize("p", [131071, 2147483647])
+def test_upload_download_staging(gpu, p):
+    # fsyrk_b200_upload / _download (the staging path of the host entry points, exposed for
+    # device-resident callers such as rank 0 of a multi-GPU call): exact round trips, Low only
+    torch = pytest.importorskip("torch")
+    fs = gpu
+    n, k = 1500, 1100
+    a = orc.random_matrix(p, n, k, 41)
+    a_dev = torch.zeros((n, k + 3), dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    fs.upload(p, a, a_dev.data_ptr(), k + 3, stream=s)
+    torch.cuda.synchronize()
+    assert np.array_equal(a_dev[:, :k].cpu().numpy().view(np.uint64), a)
+    c = orc.random_matrix(p, n, n, 42)
+    c_dev = torch.from_numpy(c.view(np.int64)).cuda()
+    out = np.full((n, n), 7, dtype=np.uint64)
+    fs.download(p, c_dev.data_ptr(), n, out, lower=True, stream=s)
+    idx = np.tril_indices(n)
+    assert np.array_equal(out[idx], c[idx]) and (out[np.triu_indices(n, 1)] == 7).all()
+    up = fs.last_transfer_bytes()[1]
+    assert 0 < up < n * (n + 1) // 2 * 8

@@ -346,7 +346,13 @@ struct Plan {
     int* dev_rounds = nullptr;
     int round_ctas = 0;  // product CTAs (the remaining SMs run the post)
 
+    // Calls that share this plan share its arena: each call's stream first waits for the
+    // previous call's last kernel (ev_done), whatever stream that call used.
+    std::mutex use_mu;
+    cudaEvent_t ev_done = nullptr;
+
     ~Plan() {
+        if (ev_done) cudaEventDestroy(ev_done);
         if (arena) cudaFree(arena);
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1216,19 +1222,22 @@ struct PlanKey {
 };
 
 std::mutex g_cache_mu;
-std::map<PlanKey, std::unique_ptr<Plan>> g_cache;
+std::map<PlanKey, std::shared_ptr<Plan>> g_cache;  // guarded by g_cache_mu
 
-Plan* get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap, int rank = 0, int nranks = 1) {
+// The cache lookup / creation is serialised; a call keeps its plan alive (shared ownership)
+// even if fsyrk_b200_release_cache drops the cache's reference meanwhile.
+std::shared_ptr<Plan> get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap, int rank = 0,
+                               int nranks = 1) {
     int dev = 0;
     cudaGetDevice(&dev);
     PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev, rank, nranks};
+    std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
-    if (it != g_cache.end()) return it->second.get();
-    auto plan = std::make_unique<Plan>();
+    if (it != g_cache.end()) return it->second;
+    auto plan = std::make_shared<Plan>();
     plan->create(p, n, kin, k, pol, colmap, rank, nranks);
-    Plan* raw = plan.get();
-    g_cache[key] = std::move(plan);
-    return raw;
+    g_cache[key] = plan;
+    return plan;
 }
 
 // ------------------------------------------------------------- validation
@@ -1596,7 +1605,11 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     if (n == 0) return;
     const int kbar = xf ? (int)xf->map.size() : (int)k;
     if (nranks > 1 && mirror) fail(FSYRK_B200_EINVAL, "mirror_output needs the whole C (not available per rank)");
-    Plan* plan = get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, rank, nranks);
+    const std::shared_ptr<Plan> plan_ref = get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, rank, nranks);
+    Plan* plan = plan_ref.get();
+    std::lock_guard<std::mutex> use(plan->use_mu);
+    if (!plan->ev_done) ck(cudaEventCreateWithFlags(&plan->ev_done, cudaEventDisableTiming), "event");
+    else ck(cudaStreamWaitEvent(s, plan->ev_done, 0), "wait for the plan's previous call");
     if (xf) {
         auto same = [](const std::vector<ColMap>& x, const std::vector<ColMap>& y) {
             return x.size() == y.size() && std::memcmp(x.data(), y.data(), x.size() * sizeof(ColMap)) == 0;
@@ -1610,6 +1623,7 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
         }
     }
     plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
+    ck(cudaEventRecord(plan->ev_done, s), "event record");
     fill_ops(ops, plan);
 }
 

@@ -548,3 +548,70 @@ def test_upload_download_staging(gpu, p):
     assert np.array_equal(out[idx], c[idx]) and (out[np.triu_indices(n, 1)] == 7).all()
     up = fs.last_transfer_bytes()[1]
     assert 0 < up < n * (n + 1) // 2 * 8
+
+
+def test_concurrent_host_calls(gpu):
+    # host entry points called from several host threads at once (the staging path, plan cache
+    # and worker pool are shared): every result exact
+    import threading
+    fs = gpu
+    results = {}
+
+    def work(tid):
+        p = (131071, 65521, 2147483647, 65537)[tid % 4]
+        f = fs.PrimeField(p)
+        ok = True
+        for it in range(6):
+            n, k = 200 + 37 * tid + it, 150 + 11 * it
+            a = orc.random_matrix(p, n, k, 1000 * tid + it)
+            plan = fs.make_syrk_plan(f, fs.RecursionPolicy(16))
+            if it % 2:
+                c0 = orc.random_matrix(p, n, n, 7 + it)
+                c = c0.copy()
+                fs.syrk_fast_acc(f, 2, a, 3, c, plan)
+                want = orc.syrk_classical(p, a)
+                idx = np.tril_indices(n)
+                ok &= bool(np.array_equal(c[idx], (want[idx] * np.uint64(2) % np.uint64(p)
+                                                   + c0[idx] * np.uint64(3) % np.uint64(p)) % np.uint64(p)))
+            else:
+                ok &= orc.lower_equal(fs.syrk_fast(f, a, plan), orc.syrk_classical(p, a))
+        results[tid] = ok
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(300)
+    assert len(results) == 6 and all(results.values()), results
+
+
+def test_concurrent_device_calls_share_a_plan(gpu):
+    # device entry point from two host threads on two streams with the same shape: the calls
+    # share one cached plan (arena), ordered by the plan's completion event; results exact
+    import threading
+    torch = pytest.importorskip("torch")
+    fs = gpu
+    p, n, k = 131071, 512, 384
+    pol = fs.RecursionPolicy(64)
+    inputs = [orc.random_matrix(p, n, k, 60 + t) for t in range(2)]
+    wants = [orc.syrk_classical(p, a) for a in inputs]
+    results = {}
+
+    def work(t):
+        stream = torch.cuda.Stream()
+        a_dev = torch.from_numpy(inputs[t].view(np.int64)).cuda()
+        ok = True
+        with torch.cuda.stream(stream):
+            for it in range(20):
+                c_dev = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+                fs.syrk_dev(p, 1, a_dev.data_ptr(), n, k, k, 0, c_dev.data_ptr(), n, pol, False, stream.cuda_stream)
+                stream.synchronize()
+                ok &= orc.lower_equal(c_dev.cpu().numpy().view(np.uint64), wants[t])
+        results[t] = ok
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(300)
+    assert results == {0: True, 1: True}

@@ -2055,6 +2055,7 @@ int fsyrk_b200_hostio_roundtrip(const uint64_t* a, size_t rows, size_t cols, siz
         if (lower && cols < rows) fail(FSYRK_B200_EDIMENSION, "hostio_roundtrip: lower region needs cols >= rows");
         if (lda < cols || ldo < cols) fail(FSYRK_B200_EDIMENSION, "hostio_roundtrip: stride < cols");
         double t[2];
+        std::lock_guard<std::mutex> lk(g_stage_mu);  // one user of the host worker pool at a time
         const size_t raw = hio::roundtrip(a, lda, hio::Region{rows, cols, lower != 0}, bits, out, ldo, t);
         if (raw_chunks) *raw_chunks = raw;
         if (secs) {

@@ -58,3 +58,25 @@ def test_roundtrip_in_forked_child(fsyrk):
     proc.start()
     proc.join(60)
     assert proc.exitcode == 0 and q.get(timeout=5)
+
+
+def test_roundtrip_from_several_threads(fsyrk):
+    # the host worker pool serves one transfer at a time; concurrent callers queue up
+    import threading
+    rng = np.random.default_rng(5)
+    mats = [rng.integers(0, 1 << 17, size=(700, 900), dtype=np.uint64) for _ in range(4)]
+    ok = {}
+
+    def work(t):
+        good = True
+        for _ in range(5):
+            out, raw, _ = fsyrk.hostio_roundtrip(mats[t], t % 2 == 1 and False, 17)
+            good &= bool(np.array_equal(out, mats[t])) and raw == 0
+        ok[t] = good
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join(60)
+    assert ok == {0: True, 1: True, 2: True, 3: True}

@@ -603,12 +603,9 @@ template <int S, int EPI = kEpiWarpsDefault>
 cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<S>;
     auto kern = modmm_kernel<S, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static const cudaError_t attr =  // thread-safe one-time setup
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (attr != cudaSuccess) return attr;
     if (args.ntiles == 0) return cudaSuccess;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);

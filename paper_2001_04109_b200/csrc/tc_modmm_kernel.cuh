@@ -603,9 +603,9 @@ template <int S, int EPI = kEpiWarpsDefault>
 cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<S>;
     auto kern = modmm_kernel<S, EPI>;
-    static const cudaError_t attr =  // thread-safe one-time setup
+    static const cudaError_t smem_attr =  // thread-safe one-time setup
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (attr != cudaSuccess) return attr;
+    if (smem_attr != cudaSuccess) return smem_attr;
     if (args.ntiles == 0) return cudaSuccess;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);

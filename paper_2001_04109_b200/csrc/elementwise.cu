@@ -38,6 +38,9 @@ namespace fsyrk_b200 {
 #ifndef FSYRK_PREP_MINB
 #define FSYRK_PREP_MINB 3  // measured: cfg2 prep 104 -> 99 us, cfg5 289 -> 278 us (profiles/r01/variants.txt)
 #endif
+#ifndef FSYRK_CONVERT_ROWS
+#define FSYRK_CONVERT_ROWS 1  // rows per iteration of the conversion (4: 0.161 vs 0.149 ms on cfg5)
+#endif
 #ifndef FSYRK_POST_MINB
 #define FSYRK_POST_MINB 6  // measured: cfg2 post 60 -> 55 us, cfg5 2.53 -> 2.13 ms
 #endif
@@ -53,13 +56,34 @@ __global__ void convert_in_kernel(const uint64_t* __restrict__ a, long long lda,
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= kout) return;
     const ColMap cm = map ? map[c] : ColMap{{c, -1, -1, -1}, {1, 0, 0, 0}};
-    for (int i = blockIdx.y; i < n; i += gridDim.y) {
-        const uint64_t* row = a + (long long)i * lda;
-        uint32_t v = 0;
+    // Shoup constants of this column's coefficients, once per thread: the per-element work is
+    // then a 32-bit mul-hi and two multiplies per source (the 64-bit Barrett products made the
+    // kernel instruction-bound at 22% of HBM bandwidth, ncu)
+    MulConst mc[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (cm.src[t] >= 0) v = addm(v, mulm(mod_u64(row[cm.src[t]], m), cm.c[t], m), m.p);
-        out[(long long)i * ldo + c] = v;
+    for (int t = 0; t < 4; ++t) mc[t] = make_mulconst(cm.src[t] >= 0 ? cm.c[t] : 0, m.p);
+    // R rows per iteration with every load issued first (memory-level parallelism)
+    constexpr int R = FSYRK_CONVERT_ROWS;
+    for (int i0 = blockIdx.y * R; i0 < n; i0 += gridDim.y * R) {
+        uint64_t x[R][4];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const uint64_t* row = a + (long long)min(i0 + q, n - 1) * lda;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) x[q][t] = cm.src[t] >= 0 ? row[cm.src[t]] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (i0 + q >= n) break;
+            uint32_t v = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (cm.src[t] >= 0) {
+                    const uint32_t r = x[q][t] < m.p ? (uint32_t)x[q][t] : mod_u64(x[q][t], m);  // canonical: no reduction
+                    v = addm(v, mulc(r, mc[t], m.p), m.p);
+                }
+            out[(long long)(i0 + q) * ldo + c] = v;
+        }
     }
 }
 
@@ -818,7 +842,7 @@ cudaError_t prep_dispatch(const PrepArgs& a, cudaStream_t s) {
 cudaError_t launch_convert_in(const uint64_t* a, long long lda, int n, int kin, int kout, const ColMap* map,
                               uint32_t p, uint32_t* out, long long ldo, cudaStream_t s) {
     if ((long long)n * kout == 0) return cudaSuccess;
-    const dim3 grid((kout + 255) / 256, rows_grid(n, (kout + 255) / 256));
+    const dim3 grid((kout + 255) / 256, rows_grid((n + FSYRK_CONVERT_ROWS - 1) / FSYRK_CONVERT_ROWS, (kout + 255) / 256));
     return launch_pdl(convert_in_kernel, grid, dim3(256), 0, s, a, lda, n, kin, kout, map, make_modp(p), out, ldo);
 }
 

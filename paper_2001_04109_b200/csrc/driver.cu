@@ -1075,6 +1075,8 @@ struct Plan {
                     a.ldc = ldc;
                     a.alpha = alpha;
                     a.beta = beta;
+                    a.calpha = make_mulconst(alpha, (uint32_t)p);
+                    a.cbeta = make_mulconst(beta, (uint32_t)p);
                     root_done = true;
                     if (partitioned) {
                         if (root_pairs.empty()) return;  // this rank owns no block pair
@@ -1110,6 +1112,8 @@ struct Plan {
             a.ldc = ldc;
             a.alpha = alpha;
             a.beta = beta;
+            a.calpha = make_mulconst(alpha, (uint32_t)p);
+            a.cbeta = make_mulconst(beta, (uint32_t)p);
             a.pairs = dev_pairs;
             a.npairs = (int)root_pairs.size();
             static const int post_blocks = [] {

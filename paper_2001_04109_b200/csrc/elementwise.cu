@@ -409,6 +409,7 @@ struct PostOut {
     long long ldc;
     bool out64, vec64;
     uint32_t alpha, beta;
+    MulConst ca, cb;  // Shoup constants of alpha, beta (32-bit products instead of 64-bit Barrett)
     ModP m;
     // write element (i, j) of the node output (lower triangle for out64)
     __device__ __forceinline__ void put(long long i, long long j, uint32_t v) const {
@@ -416,18 +417,13 @@ struct PostOut {
             x[i * ldx + j] = v;
             return;
         }
-        uint32_t r = alpha == 1 ? v : mulm(v, alpha, m);
-        if (beta != 0) {
-            const uint32_t ci = mod_u64(c[i * ldc + j], m);
-            r = addm(r, beta == 1 ? ci : mulm(ci, beta, m), m.p);
-        }
-        c[i * ldc + j] = r;
+        c[i * ldc + j] = acc(v, beta != 0 ? c[i * ldc + j] : 0);
     }
     __device__ __forceinline__ uint32_t acc(uint32_t v, uint64_t cin) const {
-        uint32_t r = alpha == 1 ? v : mulm(v, alpha, m);
+        uint32_t r = alpha == 1 ? v : mulc(v, ca, m.p);
         if (beta != 0) {
-            const uint32_t ci = mod_u64(cin, m);
-            r = addm(r, beta == 1 ? ci : mulm(ci, beta, m), m.p);
+            const uint32_t ci = cin < m.p ? (uint32_t)cin : mod_u64(cin, m);  // canonical C_in: no reduction
+            r = addm(r, beta == 1 ? ci : mulc(ci, cb, m.p), m.p);
         }
         return r;
     }
@@ -464,6 +460,8 @@ __device__ __forceinline__ PostOut make_out(const PostArgs& a, const PostNode& n
     o.vec64 = o.out64 && !(a.ldc % 2) && !(reinterpret_cast<uintptr_t>(a.c64) % 16);
     o.alpha = a.alpha;
     o.beta = a.beta;
+    o.ca = a.calpha;
+    o.cb = a.cbeta;
     o.m = a.m;
     return o;
 }

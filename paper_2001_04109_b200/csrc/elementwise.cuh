@@ -82,6 +82,7 @@ struct PostArgs {
     uint64_t* c64;
     long long ldc;
     uint32_t alpha, beta;
+    MulConst calpha, cbeta;  // make_mulconst(alpha / beta, p), set by the host with alpha, beta
     // multi-GPU partition: only these 32 x 32 tile pairs (I >= J); nullptr = all pairs
     const int2* pairs;
     int npairs;

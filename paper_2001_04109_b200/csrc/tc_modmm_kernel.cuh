@@ -43,6 +43,9 @@ namespace tc {
 #ifndef FSYRK_STG256
 #define FSYRK_STG256 0  // 256-bit direct stores from the epilogue (experiment; with FSYRK_NO_TSTORE)
 #endif
+#ifndef FSYRK_LIMB2_TSTORE
+#define FSYRK_LIMB2_TSTORE 0  // measured: products +3%, call within noise (profiles/r01/variants.txt)
+#endif
 #ifndef FSYRK_NO_TSTORE
 #define FSYRK_NO_TSTORE 0
 #endif
@@ -105,7 +108,10 @@ struct Cfg {
     // 1024-aligned (__align__ on the extern array, checked at entry)
     // TMA stores: measured faster for the Mersenne schemes (cfg2 products 185 -> 178 us, cfg5
     // 3.18 -> 2.89 ms), neutral to slightly slower for LIMB2 (cfg3 251 -> 254 us)
-    static constexpr bool TSTORE = !FSYRK_NO_TSTORE && (digits_of<S> == SCHEME_M17 || S == SCHEME_M31 || FSYRK_TSTORE_ALL) &&
+    // TMA stores: M17 / M31 measured faster; LIMB2 optional (FSYRK_LIMB2_TSTORE)
+    static constexpr bool TSTORE = !FSYRK_NO_TSTORE &&
+                                   (digits_of<S> == SCHEME_M17 || S == SCHEME_M31 || (S == SCHEME_LIMB2 && FSYRK_LIMB2_TSTORE) ||
+                                    FSYRK_TSTORE_ALL) &&
                                    STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES <= 232448;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + (TSTORE ? OUT_BYTES : 0) + BAR_BYTES;
     static constexpr int BUF_COLS = 2 * COLS_USED <= 512 ? COLS_USED : 0;  // column offset of buffer 1

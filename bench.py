@@ -392,7 +392,7 @@ def main():
             else:
                 fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
 
-        for _ in range(2):
+        for _ in range(6):  # warm-up (also lets host_io settle its raw-DMA shares)
             host_step()
         e2e_steps = max(3, min(args.steps, 10))
         # three timed rounds of e2e_steps calls, the median round reported: the host side of the

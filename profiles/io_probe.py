@@ -26,7 +26,7 @@ def main():
     c[:] = 1
     plan = fs.make_syrk_plan(f, fs.RecursionPolicy(512, 1))
     ts = []
-    for it in range(6):
+    for it in range(int(os.environ.get('PROBE_CALLS', '6'))):
         t0 = time.perf_counter()
         if mode == "plain":
             fs.syrk_fast_into(f, a, c, plan)

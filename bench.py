@@ -7,12 +7,15 @@ A "step" is one full call of the hot path on one input of the chosen config
 (default cfg2 = configs[1]: p = 131071, A 4096 x 4096, recursion to 512-leaves).
 `value` is effective n^2 k / t (GOPS) over device-resident inputs (CUDA
 events on the launching stream, L2 flushed between steps); `e2e` is the same
-metric through the host C-ABI entry point (pinned host A -> device -> host C).
-Under torchrun every rank runs independent instances of the config ("replicas",
-weak scaling); the timed region is bracketed by barriers and the max over
-ranks is reported.  `--impl reference` times the reference's own CPU
-implementation (oracle/_ref/ref_driver, built from the reference sources) on
-the host cores instead.
+metric through the host C-ABI entry point from the caller's pageable numpy
+buffers (`e2e_pinned`: from pinned buffers).
+N > 1 ranks: launched by torchrun (one process per GPU), or by this script itself
+when `--gpus N` is given without WORLD_SIZE in the environment.  Default
+`--mgpu partition`: the ranks split one problem's top-level tile pairs (strong
+scaling); `--mgpu replicas`: one independent problem per rank (weak
+scaling).  The timed region is bracketed by barriers and the max over ranks is
+reported.  `--impl reference` times the reference's own CPU implementation
+(oracle/_ref/ref_driver, built from the reference sources) on the host cores.
 """
 from __future__ import annotations
 
@@ -43,14 +46,25 @@ CONFIGS = {
                  dseed=5002),
 }
 METRIC = "mod-p SYRK C=AAᵀ effective GOPS (n²k/t) at 1–8 B200; % of tensor-core peak"
-# CPU-baseline samples: same prime / leaf size / mode as the config, smaller n (bounded CPU time)
+# CPU samples of the reference (cpu_baseline leg and --impl reference): configs 1-2 run the
+# config itself (n = k = 4096 for cfg2: ~25-35 s per single-threaded call); configs 3-5 take
+# 1-25 min per call single-threaded, so they run a bounded sample (same prime / mode / leaf size,
+# smaller n) and say so in the line's `sample` and `same_config: false`
 CPU_SAMPLE = {
     "cfg1": dict(n=1024, k=1024, threshold=64, levels="1"),
-    "cfg2": dict(n=2048, k=2048, threshold=1024, levels="inf"),
+    "cfg2": dict(n=4096, k=4096, threshold=1024, levels="inf"),
     "cfg3": dict(n=2048, k=512, threshold=512, levels="inf"),
     "cfg4": dict(n=2048, k=2048, threshold=512, levels="inf"),
     "cfg5": dict(n=4096, k=256, threshold=512, levels="inf"),
 }
+# the reference arm's warm-up waves: a 64x smaller instance of the same prime and policy (a warm-up
+# only pages in the binary and settles the host clocks; a full cfg2 wave is ~30 s)
+CPU_WARM = dict(n=1024, k=1024)
+
+
+def same_config(cfgname, cfg):
+    s = CPU_SAMPLE[cfgname]
+    return s["n"] == cfg["n"] and s["k"] == cfg["k"]
 
 
 def load_peaks():
@@ -131,12 +145,15 @@ def dist_init():
     return world, rank, local
 
 
-def cpu_reference(cfgname, cfg, threads, reps=1):
-    """Run the unmodified reference (oracle/_ref/ref_driver) on a bounded sample."""
+def cpu_reference(cfgname, cfg, threads, reps=1, sample=None):
+    """Run the unmodified reference (oracle/_ref/ref_driver): `threads` concurrent independent
+    instances of the sample (default CPU_SAMPLE[cfgname]), each `reps` calls."""
     drv = os.path.join(REPO, "oracle", "_ref", "ref_driver")
     if not os.path.exists(drv):
         return None
-    s = CPU_SAMPLE[cfgname]
+    s = dict(CPU_SAMPLE[cfgname])
+    if sample:
+        s.update(sample)
     cmd = [drv, "--p", str(cfg["p"]), "--n", str(s["n"]), "--k", str(s["k"]), "--seed", str(cfg["seed"]),
            "--threshold", str(s["threshold"]), "--levels", s["levels"], "--mode", cfg["mode"],
            "--threads", str(threads), "--reps", str(reps), "--no-digest"]
@@ -152,47 +169,81 @@ def cpu_reference(cfgname, cfg, threads, reps=1):
     return {"value": round(gops, 4), "unit": "GOPS", "cores": threads, "kind": "reference",
             "sample": f"reference syrk ({cfg['mode']}) p={cfg['p']} n={s['n']} k={s['k']} threshold={s['threshold']}"
                       f" levels={s['levels']}, {threads} concurrent instance(s) x {reps}",
+            "same_config": s["n"] == cfg["n"] and s["k"] == cfg["k"],
             "seconds": out["wall_seconds"]}
 
 
 def cpu_reference_bounded(cfgname, cfg, target_s=10.0):
-    """The reference on one core, repeated until about target_s seconds of CPU work (the
-    cpu_baseline leg: a bounded sample of the workload, timed on the box's own host)."""
+    """The reference on one core (the cpu_baseline leg, timed on the box's own host): one call of
+    the config itself when that is cfg1 / cfg2 (cfg2: ~25-35 s), else the bounded sample repeated
+    to about target_s seconds of CPU work."""
     first = cpu_reference(cfgname, cfg, 1, 1)
-    if first is None:
-        return None
+    if first is None or first["same_config"]:
+        return first
     reps = max(1, min(50, int(target_s / max(first["seconds"], 1e-3) + 0.5)))
     return cpu_reference(cfgname, cfg, 1, reps) if reps > 1 else first
 
 
 def run_reference(args, cfgname, cfg, world, rank):
+    """--impl reference: the reference's own CPU implementation on all host cores, one
+    independent single-threaded instance per core (the reference has no threaded mode,
+    proj/README.md:149); a step is one wave of those instances on the config (cfg1 / cfg2:
+    the config itself, e.g. 16 x cfg2 per ~30 s step)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    base = cpu_reference(cfgname, cfg, threads, reps=1)
-    if base is None:
+    if not os.path.exists(os.path.join(REPO, "oracle", "_ref", "ref_driver")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built"}))
         return
-    times = []
     for _ in range(args.warmup):
-        cpu_reference(cfgname, cfg, threads, reps=1)
-    for _ in range(args.steps):
+        cpu_reference(cfgname, cfg, threads, reps=1, sample=CPU_WARM)
+    budget = float(os.environ.get("FSYRK_B200_REF_BUDGET_S", "1500"))
+    times, base = [], None
+    t_start = time.perf_counter()
+    for i in range(args.steps):
         r = cpu_reference(cfgname, cfg, threads, reps=1)
+        base = base or r
         times.append(r["seconds"])
+        # stay inside the driver's per-command limit: stop once the next wave would not fit
+        if (time.perf_counter() - t_start) * (i + 2) / (i + 1) > budget:
+            break
     s = CPU_SAMPLE[cfgname]
     e = float(s["n"]) ** 2 * float(s["k"]) * threads
     total = sum(times)
     value = e * len(times) / total / 1e9
-    line = {"metric": METRIC, "value": round(value, 4), "unit": "GOPS", "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GOPS", "n_gpus": max(world, args.gpus),
+            "steps": len(times), "steps_requested": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference random_matrix)",
             "impl": "reference",
             "config": {"workload": cfgname, **{k: v for k, v in cfg.items() if k != "levels"},
-                       "levels": "inf" if cfg["levels"] == UNL else cfg["levels"], "sample": base["sample"]},
+                       "levels": "inf" if cfg["levels"] == UNL else cfg["levels"], "sample": base["sample"],
+                       "warmup_sample": f"n={CPU_WARM['n']} k={CPU_WARM['k']}"},
+            "vs_reference": {"same_config": base["same_config"]},
             "cpu_baseline": {"value": round(value, 4), "unit": "GOPS", "cores": threads, "kind": "reference",
-                             "sample": base["sample"]},
+                             "sample": base["sample"], "same_config": base["same_config"]},
             "e2e": {"value": round(value, 4), "unit": "GOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def spawn_ranks(ngpus):
+    """`--gpus N` without a launcher: start N ranks (one process per GPU) with torchrun on this
+    node and pass rank 0's JSON line through.  NCCL_DEBUG=INFO stays on so every rank's NCCL
+    init is visible in the log."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < ngpus:
+        print(f"bench.py: --gpus {ngpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def max_over_ranks(value, world):
@@ -230,6 +281,8 @@ def main():
     ap.add_argument("--threshold", type=int, default=None, help="override the config's recursion threshold")
     ap.add_argument("--levels", type=int, default=None, help="override the config's max recursion levels")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
     cfg = dict(CONFIGS[args.config])
     if args.threshold is not None:
         cfg["threshold"] = args.threshold
@@ -357,63 +410,70 @@ def main():
     fs.set_phase_timing(False)
     torch.cuda.synchronize()
 
-    # end-to-end: host A (pinned) -> device(s) -> host C, through the public API
-    e2e = None
+    # end-to-end through the public API: host A -> device(s) -> host Low(C).  Default: pageable
+    # numpy buffers, the memory a drop-in caller hands in (the reference's Matrix is a
+    # std::vector, matrix.hpp:122-126); the same from pinned buffers is reported beside it.
+    e2e = e2e_pinned = None
     if not args.no_e2e and (not part or cfg["mode"] == "plain"):
-        a_pin = torch.from_numpy(a_host.view(np.int64)).pin_memory()
-        c_pin = torch.zeros((n, n), dtype=torch.int64).pin_memory()
-        a_np = a_pin.numpy().view(np.uint64)
-        c_np = c_pin.numpy().view(np.uint64)
-        if cfg["mode"] != "plain":
-            c_np[:] = c0_host
         plan_obj = fs.make_syrk_plan(f, policy)
 
-        up_bytes = [0, 0]
+        def measure(a_np, c_np):
+            up_bytes = [0, 0]
+            if cfg["mode"] != "plain":
+                c_np[:] = c0_host
 
-        def host_step():
-            if part:  # rank 0 uploads A, NCCL broadcast, per-rank shares, NCCL reduce of C, rank 0 downloads
-                # rank 0's host copies go through the library's staging path (bit-packed residues,
-                # fsyrk_b200_upload / _download: Low(C) only), like the single-GPU host entry points
-                if rank == 0:
-                    fs.upload(p, a_np, a_dev.data_ptr(), k, stream=sh)
-                    up_bytes[0] = fs.last_transfer_bytes()[0]
-                dist.broadcast(a_dev, src=0)
-                c_dev.zero_()
-                step()
-                dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
-                if rank == 0:
-                    fs.download(p, c_dev.data_ptr(), n, c_np, lower=True, stream=sh)
-                    up_bytes[1] = fs.last_transfer_bytes()[1]
-                torch.cuda.synchronize()
-            elif cfg["mode"] == "plain":
-                fs.syrk_fast_into(f, a_np, c_np, plan_obj)
-            elif cfg["mode"] == "acc":  # C accumulates across steps (any C_in is a valid input)
-                fs.syrk_fast_acc(f, alpha, a_np, beta, c_np, plan_obj)
-            else:
-                fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
+            def host_step():
+                if part:  # rank 0 uploads A, NCCL broadcast, per-rank shares, NCCL reduce of C, rank 0 downloads
+                    # rank 0's host copies go through the library's staging path (bit-packed residues,
+                    # fsyrk_b200_upload / _download: Low(C) only), like the single-GPU host entry points
+                    if rank == 0:
+                        fs.upload(p, a_np, a_dev.data_ptr(), k, stream=sh)
+                        up_bytes[0] = fs.last_transfer_bytes()[0]
+                    dist.broadcast(a_dev, src=0)
+                    c_dev.zero_()
+                    step()
+                    dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
+                    if rank == 0:
+                        fs.download(p, c_dev.data_ptr(), n, c_np, lower=True, stream=sh)
+                        up_bytes[1] = fs.last_transfer_bytes()[1]
+                    torch.cuda.synchronize()
+                elif cfg["mode"] == "plain":
+                    fs.syrk_fast_into(f, a_np, c_np, plan_obj)
+                elif cfg["mode"] == "acc":  # C accumulates across steps (any C_in is a valid input)
+                    fs.syrk_fast_acc(f, alpha, a_np, beta, c_np, plan_obj)
+                else:
+                    fs.syrkd(f, a_np, d, plan_obj, alpha=alpha, beta=beta, c=c_np)
 
-        for _ in range(6):  # warm-up (also lets host_io settle its raw-DMA shares)
-            host_step()
-        e2e_steps = max(3, min(args.steps, 10))
-        # three timed rounds of e2e_steps calls, the median round reported: the host side of the
-        # transfers is sensitive to host-CPU noise (e.g. right after an all-core CPU run)
-        round_secs = []
-        for _ in range(3):
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            for _ in range(e2e_steps):
+            for _ in range(6):  # warm-up (also lets host_io settle its raw-DMA shares)
                 host_step()
-            t1 = time.perf_counter()
-            round_secs.append(max_over_ranks(t1 - t0, world))
-        secs = statistics.median(round_secs)
-        if part:  # rank 0's staged copies around the NCCL broadcast / reduce
-            h2d, d2h = up_bytes
-        else:     # what the host API moved (A, and the lower-triangle row blocks of C)
-            h2d, d2h = fs.last_transfer_bytes()
-            h2d, d2h = h2d * world, d2h * world
-        e2e = {"value": round(E * e2e_steps * problems / secs / 1e9, 3), "unit": "GOPS",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            e2e_steps = max(3, min(args.steps, 10))
+            # three timed rounds of e2e_steps calls, the median round reported: the host side of the
+            # transfers is sensitive to host-CPU noise (e.g. right after an all-core CPU run)
+            round_secs = []
+            for _ in range(3):
+                if world > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                for _ in range(e2e_steps):
+                    host_step()
+                t1 = time.perf_counter()
+                round_secs.append(max_over_ranks(t1 - t0, world))
+            secs = statistics.median(round_secs)
+            if part:  # rank 0's staged copies around the NCCL broadcast / reduce
+                h2d, d2h = up_bytes
+            else:     # what the host API moved (A, and the lower-triangle row blocks of C)
+                h2d, d2h = fs.last_transfer_bytes()
+                h2d, d2h = h2d * world, d2h * world
+            return {"value": round(E * e2e_steps * problems / secs / 1e9, 3), "unit": "GOPS",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+        # pageable (the default e2e): the numpy arrays the caller owns
+        e2e = measure(np.ascontiguousarray(a_host), np.zeros((n, n), dtype=np.uint64))
+        e2e["host_memory"] = "pageable"
+        a_pin = torch.from_numpy(a_host.view(np.int64)).pin_memory()
+        c_pin = torch.zeros((n, n), dtype=torch.int64).pin_memory()
+        e2e_pinned = measure(a_pin.numpy().view(np.uint64), c_pin.numpy().view(np.uint64))
+        e2e_pinned["host_memory"] = "pinned"
 
     if rank != 0:
         if world > 1 or part:
@@ -473,7 +533,10 @@ def main():
                        "parallelism": (f"top-level tile-pair partition x{world}" if part else f"replicas x{world}"),
                        "l2": "flushed between steps (256 MiB write)"},
             "parity": parity, "gpu_launches": launches["total"] * args.steps,
-            "launches_per_step": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "launches_per_step": launches, "roofline": roofline, "cpu_baseline": cpu,
+            "vs_reference": {"same_config": bool(cpu and cpu.get("same_config")),
+                             "reference_sample": cpu and cpu.get("sample")},
+            "e2e": e2e, "e2e_pinned": e2e_pinned,
             "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("scheme", "terms", "block_n", "nodes", "leaf_groups",
                                                                      "gemm_groups", "arena_bytes")}}
     print(json.dumps(line))

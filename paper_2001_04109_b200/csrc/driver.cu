@@ -458,11 +458,9 @@ struct Plan {
                 idle = prank != 0;  // not partitionable: rank 0 computes everything
             }
         }
-        for (auto& nd : nodes)
-            if ((nd.kind == LEAF && (uint64_t)nd.k > modmm_k_limit(sch, p)) ||
-                (nd.kind == LEVEL && (uint64_t)nd.kw > modmm_k_limit(sch, p)))
-                fail(FSYRK_B200_EINVAL, "inner dimension " + std::to_string(nd.k) +
-                                            " exceeds the exact int32 accumulation bound");
+        // any K is exact: the product kernel drains its int32 accumulators mod p every
+        // modmm_k_limit(sch, p) of K (chunk_blocks), like the reference's __int128 dot
+        // products accept any k (matrix.hpp:144-160)
         // ---- input sources: views of the caller's matrix stay uint64 windows (no conversion
         // pass); only S3 (and, for syrkd, the transformed root) live in residue buffers.
         // Nodes are in DFS order, so parents are visited before their children.
@@ -732,7 +730,7 @@ struct Plan {
                     g.tmA = gg.tA;
                     g.tmB = gg.tB;
                     g.M = g.N = gg.h;
-                    g.k_blocks = gg.kpad / BK;
+                    modmm_set_k(g, sch, p, gg.kpad);
                     g.syrk = 0;
                     g.vec_ok = gg.h % 4 == 0;
                     g.out = gg.out;
@@ -744,7 +742,7 @@ struct Plan {
                     g.tmA = lg.tA;
                     g.tmB = lg.tB;
                     g.M = g.N = lg.n;
-                    g.k_blocks = lg.kpad / BK;
+                    modmm_set_k(g, sch, p, lg.kpad);
                     g.syrk = 1;
                     g.vec_ok = lg.n % 4 == 0;
                     g.out = lg.xout;
@@ -1437,7 +1435,6 @@ void gemm_batch_dev(uint64_t p, size_t m, size_t n, size_t k, const std::vector<
                     cudaStream_t s) {
     const SchemeInfo sch = scheme_for(p);
     const int L = sch.planes, BN = sch.bn, BK = sch.bk;
-    if (k > modmm_k_limit(sch, p)) fail(FSYRK_B200_EINVAL, "gemm_nt: inner dimension exceeds the exact bound");
     const int batch = (int)A.size();
     if (m == 0 || n == 0 || batch == 0) return;
     const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
@@ -1476,7 +1473,7 @@ void gemm_batch_dev(uint64_t p, size_t m, size_t n, size_t k, const std::vector<
     g.tmB = make_plane_map(pb.ptr, (int)kpad, (int)npad, L, batch, sch.b_box, BK);
     g.M = (int)m;
     g.N = (int)n;
-    g.k_blocks = (int)(kpad / BK);
+    modmm_set_k(g, sch, p, kpad);
     g.syrk = 0;
     g.vec_ok = ldo % 4 == 0 && out_bs % 4 == 0;
     g.a_mult = g.b_mult = 1;

@@ -95,6 +95,12 @@ size_t modmm_k_limit(const SchemeInfo& s, uint64_t p) {
     }
 }
 
+void modmm_set_k(GroupDesc& g, const SchemeInfo& s, uint64_t p, long long kpad) {
+    g.k_blocks = (int)(kpad / s.bk);
+    const long long cb = (long long)(modmm_k_limit(s, p) / (size_t)s.bk);
+    g.chunk_blocks = (int)(cb < 1 ? 1 : cb < g.k_blocks ? cb : g.k_blocks > 0 ? g.k_blocks : 1);
+}
+
 void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w) {
     for (int i = 0; i < 8; ++i) w[i] = 0;
     if (s.id == SCHEME_M17 || s.id == SCHEME_M17N || s.id == SCHEME_M31) return;  // constants inside fold_acc

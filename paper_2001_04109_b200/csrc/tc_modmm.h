@@ -22,6 +22,8 @@ struct alignas(64) GroupDesc {
     CUtensorMap tmO;  // outputs [batch][M][N] u32, box 16 x 32 (64-byte swizzle) -- valid if tma_ok
     int M, N;         // output rows / cols
     int k_blocks;     // kpad / BK
+    int chunk_blocks; // K-blocks per exact chunk: the accumulators are drained (folded mod p into
+                      // a running residue) every chunk_blocks K-blocks, so any K stays exact
     int syrk;         // 1: only j <= i is written (lower triangle)
     int vec_ok;       // ldo % 4 == 0 (16-byte vector stores)
     int a_mult, a_off, b_mult, b_off;
@@ -63,8 +65,11 @@ struct SchemeInfo {
 // nranks >= 3: partitioned multi-GPU plans use narrower tiles where that makes the partition
 // blocks (lcm of the tile sides) finer (p = 2^17 - 1: 128 instead of 640)
 SchemeInfo scheme_for(uint64_t p, int nranks = 1);
-// Largest inner dimension for which the scheme's int32 accumulators and fold stay exact.
+// Largest inner dimension for which the scheme's int32 accumulators and fold stay exact: the
+// product kernel drains its accumulators at least this often along K (chunk_blocks).
 size_t modmm_k_limit(const SchemeInfo& s, uint64_t p);
+// g.k_blocks / g.chunk_blocks for an operand K padded to kpad (a multiple of 128).
+void modmm_set_k(GroupDesc& g, const SchemeInfo& s, uint64_t p, long long kpad);
 void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w);
 
 cudaError_t modmm_launch(const SchemeInfo& s, const GroupedArgs& args, int grid, cudaStream_t stream);

@@ -250,8 +250,12 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
-            for (int t = unit; t < args.ntiles; t += nunits, ++it) {
-                const GroupDesc& g = args.g[args.tiles[t].x & ((1 << kTileGroupBits) - 1)];
+            for (int t = unit; t < args.ntiles; t += nunits) {
+              const GroupDesc& g = args.g[args.tiles[t].x & ((1 << kTileGroupBits) - 1)];
+              // K chunks: the accumulators are drained every chunk_blocks K-blocks (exactness
+              // bound of the int32 accumulators); one chunk is one use of the TMEM buffer
+              for (int kc = 0; kc < g.k_blocks; kc += g.chunk_blocks, ++it) {
+                const int kend = min(g.k_blocks, kc + g.chunk_blocks);
                 const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
                 const uint32_t use = C::NBUF == 2 ? it >> 1 : it;  // uses of this buffer so far
                 KTRACE(it, 0);
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 }
                 KTRACE(it, 1);
                 const uint32_t acc_base = tmem + buf * C::BUF_COLS;
-                // issue term q of the scheme for K-block kb from the stage at shared address st
+                // issue term q of the scheme for K-block kb of the chunk from the stage at shared address st
                 auto issue = [&](auto qc, uint32_t st, int kb) {
                     constexpr int q = decltype(qc)::value;
                     constexpr Term tm = Sc::term(q);
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     const uint64_t bd = sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
 #pragma unroll
                     for (int kk = 0; kk < BK / 32; ++kk) {
-                        const uint32_t accum = (kb > 0 || kk > 0 || !first) ? 1u : 0u;
+                        const uint32_t accum = (kb > kc || kk > 0 || !first) ? 1u : 0u;
                         // +32 bytes along K inside the swizzle row = +2 in the 16-byte address field
                         if constexpr (PAIR)
                             sm100::mma_i8_pair(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         ph ^= 1;
                     }
                 };
-                int kb0 = 0;
+                int kb0 = kc;
                 if constexpr (C::STAGGER) {
                     // The epilogue frees the accumulators one by one (0 first).  The terms of every
                     // accumulator but the last start as soon as theirs is free, for as many K-blocks
@@ -292,17 +296,17 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     // it is free (per accumulator the sums run in the same K order, so the int32
                     // results are the same).  The tensor pipe thus works while the epilogue drains.
                     constexpr int LAST = C::NACC - 1;
-                    const int L = g.k_blocks < STAGES ? g.k_blocks : STAGES;
+                    const int L = kend - kc < STAGES ? kend - kc : STAGES;
                     int s1 = stage;
                     uint32_t ph1 = phase;
-                    for (int kb = 0; kb < L; ++kb) {
+                    for (int kb = kc; kb < kc + L; ++kb) {
                         sm100::mbar_wait(&full[s1], ph1);
                         sm100::tc_fence_after();
                         const uint32_t st = sm100::smem_u32(smem + s1 * C::STAGE_BYTES);
                         static_for<Sc::NT>([&](auto qc) {
                             constexpr Term tm = Sc::term(decltype(qc)::value);
                             if constexpr (tm.acc != LAST) {
-                                if (kb == 0 && first_term<S>(tm.acc) == decltype(qc)::value) {
+                                if (kb == kc && first_term<S>(tm.acc) == decltype(qc)::value) {
                                     sm100::mbar_wait(&acc_empty[tm.acc], (use & 1) ^ 1);
                                     sm100::tc_fence_after();
                                 }
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     }
                     sm100::mbar_wait(&acc_empty[LAST], (use & 1) ^ 1);
                     sm100::tc_fence_after();
-                    for (int kb = 0; kb < L; ++kb) {
+                    for (int kb = kc; kb < kc + L; ++kb) {
                         const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
                         static_for<Sc::NT>([&](auto qc) {
                             if constexpr (Sc::term(decltype(qc)::value).acc == LAST) issue(qc, st, kb);
@@ -321,9 +325,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         sm100::tc_commit(&empty[stage]);
                         advance(stage, phase);
                     }
-                    kb0 = L;
+                    kb0 = kc + L;
                 }
-                for (int kb = kb0; kb < g.k_blocks; ++kb) {
+                for (int kb = kb0; kb < kend; ++kb) {
                     sm100::mbar_wait(&full[stage], phase);
                     sm100::tc_fence_after();
                     const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
@@ -339,6 +343,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 else
                     sm100::tc_commit(&tmem_full[buf]);
                 KTRACE(it, 2);
+              }
             }
         }
     } else {
@@ -366,9 +371,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             report_round = -1;
         };
         uint32_t it = 0;
-        for (int t = unit; t < args.ntiles; t += nunits, ++it) {
-            const int4 tile = args.tiles[t];
-            const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
+        for (int t = unit; t < args.ntiles; t += nunits) {
+          const int4 tile = args.tiles[t];
+          const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
+          const int nchunks = (g.k_blocks + g.chunk_blocks - 1) / g.chunk_blocks;
+          for (int kc = 0; kc < nchunks; ++kc, ++it) {
             const int buf = C::NBUF == 2 ? (int)(it & 1) : 0;
             const uint32_t use = C::NBUF == 2 ? it >> 1 : it;
             const uint32_t lane_base = tmem + buf * C::BUF_COLS + ((uint32_t)(quad * 32) << 16);
@@ -477,7 +484,40 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
 #endif
             const bool staged = C::TSTORE && g.tma_ok;
             uint32_t ra[C::NACC][16];
-            if constexpr (C::STAGGER) {
+            if (nchunks > 1) {
+                // K-chunked tile (K beyond the int32 exactness bound): every chunk's accumulators
+                // are folded to residues and added mod p into the output rows (read-modify-write by
+                // the lane that owns the row, so program order makes its own earlier writes
+                // visible); the accumulators are released (either protocol) once drained
+#pragma unroll
+                for (int j = 0; j < C::NCW; ++j) {
+                    if (j < nch) {
+                        load(ra, col_of(j));
+                        ready(ra);
+                        uint32_t res[16];
+                        fold(ra, res);
+                        const long long gc0 = (long long)tile.w * BN + col_of(j);
+                        if (row_ok) {
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) {
+                                const long long gc = gc0 + c;
+                                if (gc < g.N && (!g.syrk || gc <= grow)) {
+                                    const uint32_t s2 = (kc == 0 ? 0u : out[gc]) + res[c];
+                                    out[gc] = s2 >= m.p ? s2 - m.p : s2;
+                                }
+                            }
+                        }
+                    }
+                }
+                if constexpr (C::STAGGER) {
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int s = 0; s < C::NACC; ++s) sm100::mbar_arrive(&acc_empty[s]);
+                } else {
+                    release();
+                }
+            } else if constexpr (C::STAGGER) {
                 using V = typename SplitFold<S>::V;
                 const bool short_k = g.k_blocks * BK <= 2048;
                 V v[C::NCW][16];
@@ -561,8 +601,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     }
                 }
             }
-            if (args.round_done) report_round = tile.x >> kTileGroupBits;  // reported when the warp next idles
+            if (args.round_done && kc + 1 == nchunks) report_round = tile.x >> kTileGroupBits;  // reported when the warp next idles
             if (lane == 0 && warp == 2) KTRACE(it, 6);
+          }
         }
         report();
         if (stores_pending && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

@@ -69,7 +69,12 @@ def test_config_digest_through_host_api(gpu, cfg_name):
     _check(cfg_name, c)
 
 
-@pytest.mark.parametrize("cfg_name,threshold,levels", [("cfg2", 2, 1), ("cfg3", 512, 3), ("cfg5", 2, 2)])
+@pytest.mark.parametrize("cfg_name,threshold,levels", [("cfg2", 2, 1), ("cfg3", 512, 3), ("cfg5", 2, 2),
+                                                       # depth 0: one classical leaf over the whole
+                                                       # problem (cfg4: k = 16384 > the M31 K bound,
+                                                       # two exact K chunks per tile)
+                                                       ("cfg1", 2, 0), ("cfg2", 2, 0), ("cfg3", 2, 0),
+                                                       ("cfg4", 2, 0), ("cfg5", 2, 0)])
 def test_config_digest_independent_of_recursion(gpu, cfg_name, threshold, levels):
     fs = gpu
     cfg = _bench().CONFIGS[cfg_name]

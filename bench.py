@@ -383,19 +383,30 @@ def main():
     # parity self-check of the device output against the reference's digest of the config
     parity = None
     ref_json = os.path.join(REPO, "tests", "golden", "configs", f"{args.config}.json")
-    if os.path.exists(ref_json) and (not part or c_init is None):
+    ref_digest = json.loads(open(ref_json).read())["digest"] if os.path.exists(ref_json) else None
+    comm = None
+    if part:  # the library's multi-GPU call: NCCL communicator from a unique id made on rank 0
+        obj = [fs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = fs.Communicator(obj[0], rank, world)
+    if ref_digest and not part:
         try:
-            ref = json.loads(open(ref_json).read())
             reset_c()
             step()
             torch.cuda.synchronize()
-            if part:  # disjoint shares over zeroed buffers: the sum over ranks is the full result
-                dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
-            if rank == 0:
-                parity = "digest-match" if lower_digest(c_dev.cpu().numpy().view(np.uint64)) == ref["digest"] \
-                    else "DIGEST-MISMATCH"
+            parity = "digest-match" if lower_digest(c_dev.cpu().numpy().view(np.uint64)) == ref_digest \
+                else "DIGEST-MISMATCH"
         except Exception as ex:  # noqa: BLE001
             parity = f"unchecked ({type(ex).__name__})"
+    elif ref_digest:  # partitioned: the whole multi-GPU call (shares gathered to rank 0) on the host C
+        try:
+            c_chk = c0_host.copy() if c0_host is not None else np.zeros((n, n), dtype=np.uint64)
+            plan_chk = fs.make_syrk_plan(f, policy)
+            comm.syrk(f, a_host if rank == 0 else None, c_chk if rank == 0 else None, n, k, plan_chk, alpha, beta, d)
+            if rank == 0:
+                parity = "digest-match" if lower_digest(c_chk) == ref_digest else "DIGEST-MISMATCH"
+        except Exception as ex:  # noqa: BLE001
+            parity = f"unchecked ({type(ex).__name__}: {ex})"
 
     # per-phase device times (phase events inside the library, same stream) for the roofline
     fs.set_phase_timing(True)
@@ -414,29 +425,17 @@ def main():
     # numpy buffers, the memory a drop-in caller hands in (the reference's Matrix is a
     # std::vector, matrix.hpp:122-126); the same from pinned buffers is reported beside it.
     e2e = e2e_pinned = None
-    if not args.no_e2e and (not part or cfg["mode"] == "plain"):
+    if not args.no_e2e:
         plan_obj = fs.make_syrk_plan(f, policy)
 
         def measure(a_np, c_np):
-            up_bytes = [0, 0]
             if cfg["mode"] != "plain":
                 c_np[:] = c0_host
 
             def host_step():
-                if part:  # rank 0 uploads A, NCCL broadcast, per-rank shares, NCCL reduce of C, rank 0 downloads
-                    # rank 0's host copies go through the library's staging path (bit-packed residues,
-                    # fsyrk_b200_upload / _download: Low(C) only), like the single-GPU host entry points
-                    if rank == 0:
-                        fs.upload(p, a_np, a_dev.data_ptr(), k, stream=sh)
-                        up_bytes[0] = fs.last_transfer_bytes()[0]
-                    dist.broadcast(a_dev, src=0)
-                    c_dev.zero_()
-                    step()
-                    dist.reduce(c_dev, dst=0, op=dist.ReduceOp.SUM)
-                    if rank == 0:
-                        fs.download(p, c_dev.data_ptr(), n, c_np, lower=True, stream=sh)
-                        up_bytes[1] = fs.last_transfer_bytes()[1]
-                    torch.cuda.synchronize()
+                if part:  # the library's collective multi-GPU call: rank 0 holds the host A and C
+                    comm.syrk(f, a_np if rank == 0 else None, c_np if rank == 0 else None, n, k, plan_obj, alpha,
+                              beta, d)
                 elif cfg["mode"] == "plain":
                     fs.syrk_fast_into(f, a_np, c_np, plan_obj)
                 elif cfg["mode"] == "acc":  # C accumulates across steps (any C_in is a valid input)
@@ -459,10 +458,10 @@ def main():
                 t1 = time.perf_counter()
                 round_secs.append(max_over_ranks(t1 - t0, world))
             secs = statistics.median(round_secs)
-            if part:  # rank 0's staged copies around the NCCL broadcast / reduce
-                h2d, d2h = up_bytes
-            else:     # what the host API moved (A, and the lower-triangle row blocks of C)
-                h2d, d2h = fs.last_transfer_bytes()
+            # what the host API moved (A, and the lower-triangle row blocks of C); partitioned: rank
+            # 0's PCIe traffic (the NVLink broadcast / share gather are device-to-device)
+            h2d, d2h = fs.last_transfer_bytes()
+            if not part:
                 h2d, d2h = h2d * world, d2h * world
             return {"value": round(E * e2e_steps * problems / secs / 1e9, 3), "unit": "GOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
@@ -475,6 +474,8 @@ def main():
         e2e_pinned = measure(a_pin.numpy().view(np.uint64), c_pin.numpy().view(np.uint64))
         e2e_pinned["host_memory"] = "pinned"
 
+    if comm is not None:
+        comm.close()
     if rank != 0:
         if world > 1 or part:
             dist.destroy_process_group()

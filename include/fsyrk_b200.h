@@ -200,6 +200,41 @@ int fsyrk_b200_download(uint64_t p, const uint64_t* d_dev, size_t rows, size_t c
 int fsyrk_b200_partition_owners(uint64_t p, size_t h, int nranks, int* owners, size_t owners_len, size_t* nblocks,
                                 size_t* block);
 
+/* ------------------------------------------------------------- multi-GPU */
+
+/* Multi-GPU syrk_fast_into / syrk_fast_acc / syrkd over `ngpus` devices of this process
+ * (replaces the same reference entry points as the host API above,
+ * include/fsyrk/fast_syrk.hpp:274-303 and scaled_syrk.hpp:58-104, for callers that want
+ * several GPUs).  Host A / C as in the host API; d: syrkd diagonal (k entries) or NULL;
+ *   Low(C) <- Low(alpha * A * Diag(d) * A^T + beta * C).
+ * A crosses PCIe once into devices[0], is broadcast as uint32 residues over NVLink by an
+ * internal NCCL communicator (ncclCommInitAll, cached per device list), every device computes
+ * the top-level tile pairs it owns (fsyrk_b200_share_pairs), and the owned tiles of Low(C)
+ * return to devices[0] as packed uint32 shares (ncclSend / ncclRecv) before crossing PCIe.
+ * Shapes whose top level is not partitionable run on devices[0] alone.  A device listed more
+ * than once makes the ranks on it exchange by device copies instead of NCCL (a test mode). */
+int fsyrk_b200_syrk_mgpu(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                         const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy,
+                         int mirror_output, const int* devices, int ngpus, fsyrk_b200_opcount* ops);
+
+/* The same call with one process per GPU (e.g. under torchrun): rank 0 creates an NCCL unique
+ * id and hands it to the other ranks out of band; every rank creates its communicator on its
+ * current device and makes the same collective call.  Only rank 0 reads `a` and reads / writes
+ * `c` (the other ranks may pass NULL); d, alpha, beta, policy must agree on every rank. */
+int fsyrk_b200_nccl_unique_id(uint8_t id[128]);
+int fsyrk_b200_comm_init_rank(const uint8_t id[128], int rank, int nranks, void** comm);
+int fsyrk_b200_comm_destroy(void* comm);
+int fsyrk_b200_syrk_mgpu_rank(void* comm, uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
+                              size_t lda, const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc,
+                              fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops);
+
+/* The 32 x 32 tile pairs (I >= J, as int pairs I, J) of the h x h top-level quadrants owned
+ * by `rank` of `nranks`: its share of Low(C) is tile (I, J) of C11, C21 and C22 and tile
+ * (J, I) of C21 for each pair, moved as 4 x 1024 uint32 words per pair (slot order C11(I,J),
+ * C21(I,J), C22(I,J), C21(J,I); entries outside Low(C) or beyond h are zero).  Host-only.
+ * pairs may be NULL (count only); *count = number of pairs. */
+int fsyrk_b200_share_pairs(uint64_t p, size_t h, int rank, int nranks, int* pairs, size_t cap, size_t* count);
+
 /* Drop cached plans and device arenas (tests, memory pressure). */
 void fsyrk_b200_release_cache(void);
 

@@ -15,6 +15,8 @@
 // (p, n, k, policy) so repeated calls only launch kernels.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -29,6 +31,7 @@
 #include <string>
 #include <thread>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fsyrk_b200.h"
@@ -36,6 +39,7 @@
 #include "field_host.h"
 #include "host_io.h"
 #include "modp.cuh"
+#include "per_device.h"
 #include "tc_modmm.h"
 
 namespace fsyrk_b200 {
@@ -84,19 +88,26 @@ int guarded(F&& f) {
 }
 
 // ------------------------------------------------------------------ device
+struct DeviceProbe {
+    std::once_flag flag;
+    int ok = 0;
+};
 int device_ok() {
-    static int cached = -1;
-    if (cached >= 0) return cached;
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
         cudaGetLastError();
-        return cached = 0;
+        return 0;
     }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceProp prop{};
-    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cached = 0;
-    return cached = (prop.major == 10) ? 1 : 0;
+    DeviceProbe& pr = per_device<DeviceProbe>();  // cached per device (a process may use several)
+    std::call_once(pr.flag, [&] {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, current_device()) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        pr.ok = prop.major == 10 ? 1 : 0;
+    });
+    return pr.ok;
 }
 
 void require_device() {
@@ -924,6 +935,10 @@ struct Plan {
                    "upload add table");
             }
         }
+        // the arena clear and the table uploads above ran on the legacy stream with pageable
+        // sources (the DMA may still be in flight when cudaMemcpy returns); the calls run on
+        // non-blocking streams, so finish them here
+        ck(cudaDeviceSynchronize(), "plan upload");
         // op tallies
         tensor_macs = int8_macs = ew_adds = 0;
         for (auto& lg : leaves) {
@@ -1409,8 +1424,9 @@ struct DevBuf {
     }
 };
 
+// The host entry points' staging (device buffers, pinned slots, the host worker pool) is one
+// resource: one host call at a time.  The device-side buffers and streams are per device.
 std::mutex g_stage_mu;
-DevBuf g_stage_a, g_stage_c;
 
 void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
     if (!ops) return;
@@ -1439,10 +1455,14 @@ void gemm_batch_dev(uint64_t p, size_t m, size_t n, size_t k, const std::vector<
     if (m == 0 || n == 0 || batch == 0) return;
     const long long kpad = round_up((long long)std::max<size_t>(k, 1), 128);
     const long long mpad = round_up((long long)m, 128), npad = round_up((long long)n, 128);
-    // scratch kept across calls (grows to the largest product seen); one product at a time
-    static std::mutex mu;
-    static DevBuf pa, pb, dtiles;
-    std::lock_guard<std::mutex> lk(mu);
+    // scratch kept across calls (grows to the largest product seen); one product at a time per device
+    struct Scratch {
+        std::mutex mu;
+        DevBuf pa, pb, dtiles;
+    };
+    Scratch& sc = per_device<Scratch>();
+    std::lock_guard<std::mutex> lk(sc.mu);
+    DevBuf &pa = sc.pa, &pb = sc.pb, &dtiles = sc.dtiles;
     pa.ensure((size_t)(mpad * kpad * L * batch));
     pb.ensure((size_t)(npad * kpad * L * batch));
     ck(cudaMemsetAsync(pa.ptr, 0, (size_t)(mpad * kpad * L * batch), s), "memset");
@@ -1518,9 +1538,13 @@ void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const
         long long hm, hn;
     };
     std::vector<Level> levels;
-    static std::mutex mu;  // per-level scratch kept across calls
-    static std::vector<std::unique_ptr<DevBuf>> pool;
-    std::lock_guard<std::mutex> lk(mu);
+    struct Pool {  // per-level scratch kept across calls, per device
+        std::mutex mu;
+        std::vector<std::unique_ptr<DevBuf>> bufs;
+    };
+    Pool& pl = per_device<Pool>();
+    std::lock_guard<std::mutex> lk(pl.mu);
+    std::vector<std::unique_ptr<DevBuf>>& pool = pl.bufs;
     size_t cm = m, cn = n, ck_ = k;
     const uint32_t pp = (uint32_t)p;
     for (uint64_t lev = 0; lev < pol.max_levels; ++lev) {
@@ -1671,8 +1695,12 @@ struct IoStreams {
         }
     }
 };
-IoStreams g_io;
-DevBuf g_stage_x;
+struct DevStage {
+    DevBuf a, c, x;        // caller's A / C (uint64 rows), alpha X of the duplex path
+    DevBuf a32, sendb, recvb, pairs;  // multi-GPU: A residues, packed shares, pair lists
+    IoStreams io;
+};
+DevStage& stage() { return per_device<DevStage>(); }
 
 void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda, const ColXform* xf,
               uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy pol, bool mirror, fsyrk_b200_opcount* ops) {
@@ -1687,12 +1715,14 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     if ((k > 0 && hio::is_device(a)) || hio::is_device(c))
         fail(FSYRK_B200_EINVAL, "host entry point called with device memory (use fsyrk_b200_syrk_dev)");
     std::lock_guard<std::mutex> lk(g_stage_mu);
+    DevStage& st = stage();
+    IoStreams& g_io = st.io;
     g_io.init();
     const size_t abytes = n * std::max<size_t>(k, 1) * 8, cbytes = n * n * 8;
-    g_stage_a.ensure(abytes);
-    g_stage_c.ensure(cbytes);
-    uint64_t* da = static_cast<uint64_t*>(g_stage_a.ptr);
-    uint64_t* dc = static_cast<uint64_t*>(g_stage_c.ptr);
+    st.a.ensure(abytes);
+    st.c.ensure(cbytes);
+    uint64_t* da = static_cast<uint64_t*>(st.a.ptr);
+    uint64_t* dc = static_cast<uint64_t*>(st.c.ptr);
     cudaStream_t s = g_io.main;
     uint64_t h2d = 0, d2h = 0;
     static const bool io_trace = getenv("FSYRK_B200_IO_TRACE") != nullptr;
@@ -1762,8 +1792,8 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
         ck(hio::download(dc, n, hio::Region{n, n, !mirror}, c, ldc, (need_c || mirror) ? 0 : kTriRows, bits, s, &d2h),
            "D2H C");
     } else {
-        g_stage_x.ensure(cbytes);
-        uint64_t* dx = static_cast<uint64_t*>(g_stage_x.ptr);
+        st.x.ensure(cbytes);
+        uint64_t* dx = static_cast<uint64_t*>(st.x.ptr);
         if (!cin_early) {
             ck(cudaEventRecord(g_io.a_done, s), "event");
             ck(cudaStreamWaitEvent(g_io.cin, g_io.a_done, 0), "wait");
@@ -1856,6 +1886,346 @@ void run_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint
        "fp2 combine");
     ck(cudaMemcpy2DAsync(c, 2 * ldc * 8, dC.ptr, 2 * n * 8, 2 * n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
     ck(cudaStreamSynchronize(s), "sync");
+}
+
+
+// ------------------------------------------------------------- multi-GPU
+// one problem over several GPUs.  Rank 0 holds the caller's host A (and C);
+// A crosses PCIe once (bit-packed, host_io) into rank 0, is reduced to uint32 residues and
+// broadcast over NVLink by NCCL; every rank computes the top-level tile pairs it owns
+// (partition_owners, Plan::create) with no data-path exchange; the owned 32 x 32 tiles of
+// Low(C) come back to rank 0 as packed uint32 shares (ncclSend / ncclRecv, 4 bytes per entry
+// instead of a reduce over the full uint64 C) and cross PCIe once.  Accumulating calls scatter
+// the owned tiles of Low(C_in) the same way before the compute.
+//
+// NCCL is loaded at first use (dlopen of libnccl.so.2: the copy a host process such as
+// PyTorch already loaded, else the system one), so the library itself has no link-time NCCL
+// dependency and its version never conflicts with the caller's.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) init_rank = nullptr;
+    decltype(&ncclCommInitAll) init_all = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    std::string error;
+};
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.error = e ? e : "dlopen(libnccl.so.2) failed";
+            return a;
+        }
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (!fn && a.error.empty()) a.error = std::string("symbol ") + name + " missing";
+        };
+        sym(a.get_unique_id, "ncclGetUniqueId");
+        sym(a.init_rank, "ncclCommInitRank");
+        sym(a.init_all, "ncclCommInitAll");
+        sym(a.destroy, "ncclCommDestroy");
+        sym(a.broadcast, "ncclBroadcast");
+        sym(a.send, "ncclSend");
+        sym(a.recv, "ncclRecv");
+        sym(a.group_start, "ncclGroupStart");
+        sym(a.group_end, "ncclGroupEnd");
+        sym(a.error_string, "ncclGetErrorString");
+        return a;
+    }();
+    if (!api.error.empty()) fail(FSYRK_B200_ENCCL, "NCCL unavailable: " + api.error);
+    return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(FSYRK_B200_ENCCL, std::string(what) + ": " + nccl().error_string(r));
+}
+
+// A communicator handle of the C ABI (fsyrk_b200_comm_init_rank).
+struct Comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1, dev = 0;
+};
+
+// One rank driven by this process.  comm == nullptr: loopback transport (several ranks of a
+// single-process call on one device -- a test configuration: the shares move by device copies).
+struct LocalRank {
+    int dev = 0, rank = 0;
+    ncclComm_t comm = nullptr;
+};
+
+// Device buffers of one rank (several loopback ranks may share a device).
+struct RankBufs {
+    DevBuf a64, a32, c64, sendb, recvb, pairs;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev = nullptr;
+};
+RankBufs& rank_bufs(int rank) {
+    struct M {
+        std::mutex mu;
+        std::map<int, std::unique_ptr<RankBufs>> m;
+    };
+    M& mm = per_device<M>();
+    std::lock_guard<std::mutex> lk(mm.mu);
+    std::unique_ptr<RankBufs>& b = mm.m[rank];
+    if (!b) {
+        b.reset(new RankBufs);
+        ck(cudaStreamCreateWithFlags(&b->s, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&b->ev, cudaEventDisableTiming), "event");
+    }
+    return *b;
+}
+
+// The 32 x 32 tile pairs of the root post-addition owned by `rank` (Plan::create root_pairs).
+std::vector<int2> owned_pairs(const Plan& pl, int rank) {
+    std::vector<int2> out;
+    const int h = pl.nodes[0].h, T = (h + 31) / 32;
+    for (int I = 0; I < T; ++I)
+        for (int J = 0; J <= I; ++J) {
+            const int bi = I * 32 / pl.kPartBlock, bj = J * 32 / pl.kPartBlock;
+            if (pl.owner[(size_t)bi * pl.part_nb + bj] == rank) out.push_back(make_int2(I, J));
+        }
+    return out;
+}
+
+constexpr size_t kShareWords = 4 * 1024;  // uint32 words of one tile pair's share
+
+void mgpu_run(const std::vector<LocalRank>& loc, int nranks, uint64_t p, uint64_t alpha, const uint64_t* a, size_t n,
+              size_t k, size_t lda, const ColXform* xf, uint64_t beta, uint64_t* c, size_t ldc,
+              fsyrk_b200_policy pol, bool mirror, fsyrk_b200_opcount* ops) {
+    validate_field(p);
+    validate_policy(pol);
+    validate_shapes(n, k, lda, ldc);
+    const LocalRank* r0 = nullptr;
+    for (const LocalRank& lr : loc)
+        if (lr.rank == 0) r0 = &lr;
+    if (r0) {
+        if (ranges_overlap(a, span_bytes(n, k, lda), c, span_bytes(n, n, ldc)))
+            fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
+        if ((n > 0 && k > 0 && !a) || (n > 0 && !c)) fail(FSYRK_B200_EINVAL, "syrk_mgpu: rank 0 needs host A and C");
+    }
+    const int saved = current_device();
+    struct DevGuard {
+        int d;
+        ~DevGuard() { cudaSetDevice(d); }
+    } guard{saved};
+    if (n == 0) return;
+    const int kbar = xf ? (int)xf->map.size() : (int)k;
+    const bool need_c = (beta % p) != 0;
+    // plans first: every rank's plan is built from the same deterministic partition
+    struct R {
+        LocalRank lr;
+        RankBufs* b;
+        std::shared_ptr<Plan> plan;
+    };
+    std::vector<R> rs;
+    for (const LocalRank& lr : loc) {
+        ck(cudaSetDevice(lr.dev), "cudaSetDevice");
+        require_device();
+        rs.push_back(R{lr, &rank_bufs(lr.rank), k > 0 ? get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, lr.rank,
+                                                                 nranks)
+                                                      : nullptr});
+    }
+    const bool part = k > 0 && nranks > 1 && rs[0].plan->partitioned;
+    if (!part) {  // not partitionable (or one rank): rank 0 runs the single-GPU host path
+        if (r0) {
+            ck(cudaSetDevice(r0->dev), "cudaSetDevice");
+            run_host(p, alpha, a, n, k, lda, xf, beta, c, ldc, pol, mirror, ops);
+        }
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_stage_mu);  // rank 0's host staging
+    g_transfer[0] = g_transfer[1] = 0;
+    if (r0 && ((k > 0 && hio::is_device(a)) || hio::is_device(c)))
+        fail(FSYRK_B200_EINVAL, "host entry point called with device memory (use fsyrk_b200_syrk_part_dev)");
+    const Plan& pl0 = *rs[0].plan;
+    const int h = pl0.nodes[0].h;
+    std::vector<std::vector<int2>> pairs(nranks);
+    for (int r = 0; r < nranks; ++r) pairs[r] = owned_pairs(pl0, r);
+    std::vector<size_t> roff(nranks + 1, 0);  // rank 0's receive offsets (words)
+    for (int r = 0; r < nranks; ++r) roff[r + 1] = roff[r] + (r == 0 ? 0 : pairs[r].size() * kShareWords);
+    const int bits = hio::transfer_bits(p);
+    const bool loopback = loc.front().comm == nullptr;
+    // ---- buffers; pair lists on the devices (rank 0: every rank's, concatenated)
+    std::vector<int2> all_pairs;
+    std::vector<size_t> poff(nranks + 1, 0);
+    for (int r = 0; r < nranks; ++r) {
+        all_pairs.insert(all_pairs.end(), pairs[r].begin(), pairs[r].end());
+        poff[r + 1] = all_pairs.size();
+    }
+    for (R& x : rs) {
+        ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+        RankBufs& b = *x.b;
+        b.a64.ensure(n * k * 8);
+        b.a32.ensure(n * k * 4);
+        b.c64.ensure(n * n * 8);
+        b.sendb.ensure(std::max<size_t>(1, pairs[x.lr.rank].size()) * kShareWords * 4);
+        if (x.lr.rank == 0) b.recvb.ensure(std::max<size_t>(1, roff[nranks]) * 4);
+        b.pairs.ensure(std::max<size_t>(1, all_pairs.size()) * sizeof(int2));
+        ck(cudaMemcpyAsync(b.pairs.ptr, all_pairs.data(), all_pairs.size() * sizeof(int2), cudaMemcpyHostToDevice, b.s),
+           "upload pair lists");
+    }
+    auto pairs_dev = [&](const R& x, int r) { return static_cast<int2*>(x.b->pairs.ptr) + poff[r]; };
+    auto u64 = [](DevBuf& d) { return static_cast<uint64_t*>(d.ptr); };
+    auto u32 = [](DevBuf& d) { return static_cast<uint32_t*>(d.ptr); };
+    R* x0 = nullptr;
+    for (R& x : rs)
+        if (x.lr.rank == 0) x0 = &x;
+    // loopback transport: copies between the ranks' buffers, ordered by events
+    auto copy_from = [&](R& dst, void* to, R& src, const void* from, size_t bytes) {
+        ck(cudaSetDevice(src.lr.dev), "cudaSetDevice");
+        ck(cudaEventRecord(src.b->ev, src.b->s), "event");
+        ck(cudaSetDevice(dst.lr.dev), "cudaSetDevice");
+        ck(cudaStreamWaitEvent(dst.b->s, src.b->ev, 0), "wait");
+        ck(cudaMemcpyAsync(to, from, bytes, cudaMemcpyDefault, dst.b->s), "loopback copy");
+    };
+    uint64_t h2d = 0, d2h = 0;
+    // 1. rank 0: A (and Low(C_in)) from the host; A reduced to uint32 residues for the broadcast
+    if (x0) {
+        ck(cudaSetDevice(x0->lr.dev), "cudaSetDevice");
+        ck(hio::upload(a, lda, hio::Region{n, k, false}, u64(x0->b->a64), k, bits, x0->b->s, &h2d), "H2D A");
+        ck(launch_convert_in(u64(x0->b->a64), (long long)k, (int)n, (int)k, (int)k, nullptr, (uint32_t)p,
+                             u32(x0->b->a32), (long long)k, x0->b->s),
+           "narrow A");
+        if (need_c) ck(hio::upload(c, ldc, hio::Region{n, n, true}, u64(x0->b->c64), n, bits, x0->b->s, &h2d), "H2D C");
+    }
+    // 2. broadcast A; the other ranks widen it back to the uint64 layout the plan reads
+    if (loopback) {
+        for (R& x : rs)
+            if (x.lr.rank != 0) copy_from(x, x.b->a32.ptr, *x0, x0->b->a32.ptr, n * k * 4);
+    } else {
+        const NcclApi& nc = nccl();
+        nck(nc.group_start(), "ncclGroupStart");
+        for (R& x : rs) {
+            ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+            nck(nc.broadcast(x.b->a32.ptr, x.b->a32.ptr, n * k, ncclUint32, 0, x.lr.comm, x.b->s), "ncclBroadcast(A)");
+        }
+        nck(nc.group_end(), "ncclGroupEnd");
+    }
+    for (R& x : rs) {
+        if (x.lr.rank == 0) continue;
+        ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+        ck(launch_u32_to_u64(u32(x.b->a32), (long long)k, (int)n, (int)k, u64(x.b->a64), (long long)k, x.b->s),
+           "widen A");
+    }
+    // 2b. accumulate: rank 0 scatters the owned tiles of Low(C_in)
+    if (need_c) {
+        if (x0) {
+            ck(cudaSetDevice(x0->lr.dev), "cudaSetDevice");
+            for (int r = 1; r < nranks; ++r)
+                ck(launch_share_pack(u64(x0->b->c64), (long long)n, h, pairs_dev(*x0, r), (int)pairs[r].size(),
+                                     u32(x0->b->recvb) + roff[r], x0->b->s),
+                   "pack C_in share");
+        }
+        if (loopback) {
+            for (R& x : rs)
+                if (x.lr.rank != 0)
+                    copy_from(x, x.b->sendb.ptr, *x0, u32(x0->b->recvb) + roff[x.lr.rank],
+                              pairs[x.lr.rank].size() * kShareWords * 4);
+        } else {
+            const NcclApi& nc = nccl();
+            nck(nc.group_start(), "ncclGroupStart");
+            for (R& x : rs) {
+                ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+                if (x.lr.rank == 0) {
+                    for (int r = 1; r < nranks; ++r)
+                        if (!pairs[r].empty())
+                            nck(nc.send(u32(x.b->recvb) + roff[r], pairs[r].size() * kShareWords, ncclUint32, r,
+                                        x.lr.comm, x.b->s),
+                                "ncclSend(C_in)");
+                } else if (!pairs[x.lr.rank].empty()) {
+                    nck(nc.recv(x.b->sendb.ptr, pairs[x.lr.rank].size() * kShareWords, ncclUint32, 0, x.lr.comm,
+                                x.b->s),
+                        "ncclRecv(C_in)");
+                }
+            }
+            nck(nc.group_end(), "ncclGroupEnd");
+        }
+        for (R& x : rs) {
+            if (x.lr.rank == 0) continue;
+            ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+            ck(launch_share_unpack(u32(x.b->sendb), h, pairs_dev(x, x.lr.rank), (int)pairs[x.lr.rank].size(),
+                                   u64(x.b->c64), (long long)n, x.b->s),
+               "unpack C_in share");
+        }
+    }
+    // 3. every rank computes its share (no data-path exchange)
+    for (R& x : rs) {
+        ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+        run_dev(p, (uint32_t)(alpha % p), u64(x.b->a64), n, k, k, xf, (uint32_t)(beta % p), u64(x.b->c64), n, pol,
+                false, x.b->s, x.lr.rank == 0 ? ops : nullptr, x.lr.rank, nranks);
+    }
+    // 4. gather the shares into rank 0's C
+    for (R& x : rs) {
+        if (x.lr.rank == 0) continue;
+        ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+        ck(launch_share_pack(u64(x.b->c64), (long long)n, h, pairs_dev(x, x.lr.rank), (int)pairs[x.lr.rank].size(),
+                             u32(x.b->sendb), x.b->s),
+           "pack share");
+    }
+    if (loopback) {
+        for (R& x : rs)
+            if (x.lr.rank != 0)
+                copy_from(*x0, u32(x0->b->recvb) + roff[x.lr.rank], x, x.b->sendb.ptr,
+                          pairs[x.lr.rank].size() * kShareWords * 4);
+    } else {
+        const NcclApi& nc = nccl();
+        nck(nc.group_start(), "ncclGroupStart");
+        for (R& x : rs) {
+            ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+            if (x.lr.rank == 0) {
+                for (int r = 1; r < nranks; ++r)
+                    if (!pairs[r].empty())
+                        nck(nc.recv(u32(x.b->recvb) + roff[r], pairs[r].size() * kShareWords, ncclUint32, r, x.lr.comm,
+                                    x.b->s),
+                            "ncclRecv(share)");
+            } else if (!pairs[x.lr.rank].empty()) {
+                nck(nc.send(x.b->sendb.ptr, pairs[x.lr.rank].size() * kShareWords, ncclUint32, 0, x.lr.comm, x.b->s),
+                    "ncclSend(share)");
+            }
+        }
+        nck(nc.group_end(), "ncclGroupEnd");
+    }
+    // 5. rank 0: unpack, optional mirror, Low(C) (or all of C) back to the host
+    if (x0) {
+        ck(cudaSetDevice(x0->lr.dev), "cudaSetDevice");
+        for (int r = 1; r < nranks; ++r)
+            ck(launch_share_unpack(u32(x0->b->recvb) + roff[r], h, pairs_dev(*x0, r), (int)pairs[r].size(),
+                                   u64(x0->b->c64), (long long)n, x0->b->s),
+               "unpack share");
+        if (mirror) ck(launch_mirror(u64(x0->b->c64), (long long)n, (int)n, x0->b->s), "mirror");
+        ck(hio::download(u64(x0->b->c64), n, hio::Region{n, n, !mirror}, c, ldc, (need_c || mirror) ? 0 : kTriRows,
+                         bits, x0->b->s, &d2h),
+           "D2H C");
+    }
+    for (R& x : rs) {
+        ck(cudaSetDevice(x.lr.dev), "cudaSetDevice");
+        ck(cudaStreamSynchronize(x.b->s), "sync");
+    }
+    g_transfer[0] = h2d;
+    g_transfer[1] = d2h;
+}
+
+// Single-process communicators over distinct devices (ncclCommInitAll), cached per device list.
+std::vector<ncclComm_t> comms_for(const std::vector<int>& devs) {
+    static std::mutex mu;
+    static std::map<std::vector<int>, std::vector<ncclComm_t>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(devs);
+    if (it != cache.end()) return it->second;
+    std::vector<ncclComm_t> comms(devs.size(), nullptr);
+    nck(nccl().init_all(comms.data(), (int)devs.size(), devs.data()), "ncclCommInitAll");
+    cache[devs] = comms;
+    return comms;
 }
 
 }  // namespace
@@ -2219,9 +2589,13 @@ int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m,
         if (m == 0 || n == 0) return;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t kk = std::max<size_t>(k, 1);
-        static std::mutex mu;
-        static DevBuf ra, rb, rc;
-        std::lock_guard<std::mutex> lk(mu);
+        struct Io {  // residue copies of A, B, C kept across calls, per device
+            std::mutex mu;
+            DevBuf ra, rb, rc;
+        };
+        Io& io = per_device<Io>();
+        std::lock_guard<std::mutex> lk(io.mu);
+        DevBuf &ra = io.ra, &rb = io.rb, &rc = io.rc;
         ra.ensure(m * kk * 4);
         rb.ensure(n * kk * 4);
         rc.ensure(m * n * 4);
@@ -2250,6 +2624,103 @@ int fsyrk_b200_herk_fast_into(uint64_t p, const uint64_t* a, size_t n, size_t k,
 int fsyrk_b200_syrk_fast_into_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint64_t* c,
                                   size_t ldc, fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
     return guarded([&] { run_fp2(p, a, n, k, lda, c, ldc, policy, mirror_output != 0, false, ops); });
+}
+
+
+int fsyrk_b200_syrk_mgpu(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k, size_t lda,
+                         const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc, fsyrk_b200_policy policy,
+                         int mirror_output, const int* devices, int ngpus, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        if (ngpus < 1 || !devices) fail(FSYRK_B200_EINVAL, "syrk_mgpu: need at least one device");
+        validate_field(p);
+        ColXform xf;
+        if (d) xf = xform_diag(p, d, k);
+        std::vector<int> devs(devices, devices + ngpus);
+        std::vector<int> sorted = devs;
+        std::sort(sorted.begin(), sorted.end());
+        const bool distinct = std::unique(sorted.begin(), sorted.end()) == sorted.end();
+        std::vector<LocalRank> loc(ngpus);
+        std::vector<ncclComm_t> comms;
+        if (distinct && ngpus > 1) comms = comms_for(devs);
+        for (int r = 0; r < ngpus; ++r) loc[r] = LocalRank{devs[r], r, comms.empty() ? nullptr : comms[r]};
+        mgpu_run(loc, ngpus, p, alpha, a, n, k, lda, d ? &xf : nullptr, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_nccl_unique_id(uint8_t id[128]) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+        ncclUniqueId u;
+        nck(nccl().get_unique_id(&u), "ncclGetUniqueId");
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int fsyrk_b200_comm_init_rank(const uint8_t id[128], int rank, int nranks, void** comm) {
+    return guarded([&] {
+        if (!comm || nranks < 1 || rank < 0 || rank >= nranks) fail(FSYRK_B200_EINVAL, "comm_init_rank: bad rank");
+        require_device();
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        auto* cm = new Comm;
+        cm->rank = rank;
+        cm->nranks = nranks;
+        cm->dev = current_device();
+        const ncclResult_t r = nccl().init_rank(&cm->comm, nranks, u, rank);
+        if (r != ncclSuccess) {
+            delete cm;
+            nck(r, "ncclCommInitRank");
+        }
+        *comm = cm;
+    });
+}
+
+int fsyrk_b200_comm_destroy(void* comm) {
+    return guarded([&] {
+        if (!comm) return;
+        auto* cm = static_cast<Comm*>(comm);
+        if (cm->comm) nck(nccl().destroy(cm->comm), "ncclCommDestroy");
+        delete cm;
+    });
+}
+
+int fsyrk_b200_syrk_mgpu_rank(void* comm, uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
+                              size_t lda, const uint64_t* d, uint64_t beta, uint64_t* c, size_t ldc,
+                              fsyrk_b200_policy policy, int mirror_output, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        if (!comm) fail(FSYRK_B200_EINVAL, "syrk_mgpu_rank: null communicator");
+        const Comm& cm = *static_cast<const Comm*>(comm);
+        validate_field(p);
+        ColXform xf;
+        if (d) xf = xform_diag(p, d, k);
+        std::vector<LocalRank> loc{LocalRank{cm.dev, cm.rank, cm.comm}};
+        mgpu_run(loc, cm.nranks, p, alpha, a, n, k, lda, d ? &xf : nullptr, beta, c, ldc, policy, mirror_output != 0,
+                 ops);
+    });
+}
+
+
+int fsyrk_b200_share_pairs(uint64_t p, size_t h, int rank, int nranks, int* pairs, size_t cap, size_t* count) {
+    return guarded([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(FSYRK_B200_EINVAL, "rank out of range");
+        validate_field(p);
+        const SchemeInfo si = scheme_for(p, nranks);
+        const int blk = part_block_for(si.bm, si.bn);
+        const std::vector<int> own = partition_owners((int)h, nranks, blk);
+        const int nb = ((int)h + blk - 1) / blk, T = ((int)h + 31) / 32;
+        size_t cnt = 0;
+        for (int I = 0; I < T; ++I)
+            for (int J = 0; J <= I; ++J)
+                if (own[(size_t)(I * 32 / blk) * nb + J * 32 / blk] == rank) {
+                    if (pairs) {
+                        if (cnt >= cap) fail(FSYRK_B200_EDIMENSION, "share_pairs: buffer too small");
+                        pairs[2 * cnt] = I;
+                        pairs[2 * cnt + 1] = J;
+                    }
+                    ++cnt;
+                }
+        if (count) *count = cnt;
+    });
 }
 
 }  // extern "C"

@@ -695,11 +695,52 @@ __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ x, long long ldx,
                                   uint64_t* __restrict__ out, long long ldo) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
-    const long long total = (long long)rows * cols;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / cols), j = (int)(idx % cols);
-        out[(long long)i * ldo + j] = x[(long long)i * ldx + j];
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;  // 2-D grid: no 64-bit division per element
+    if (j >= cols) return;
+    for (int i = blockIdx.y; i < rows; i += gridDim.y) out[(long long)i * ldo + j] = x[(long long)i * ldx + j];
+}
+
+// Multi-GPU shares (driver.cu, mgpu): the root post-addition of a partitioned plan writes, for
+// each owned 32 x 32 tile pair (I >= J) of the h x h quadrants, tile (I, J) of C11, C21 and
+// C22 and tile (J, I) of C21 (elementwise.cu post_vec_pair).  A share is those tiles packed as
+// uint32 residues, 4 x 1024 words per pair (slot t: 0 C11(I,J), 1 C21(I,J), 2 C22(I,J),
+// 3 C21(J,I)); entries outside Low(C) or beyond h are skipped (pack writes 0 there).
+__device__ __forceinline__ bool share_entry(int t, int I, int J, int r, int cl, int h, long long& gi,
+                                            long long& gj) {
+    if (t == 3 && I == J) return false;
+    const int bi = t == 3 ? J : I, bj = t == 3 ? I : J;
+    const int li = bi * 32 + r, lj = bj * 32 + cl;
+    if (li >= h || lj >= h) return false;
+    if ((t == 0 || t == 2) && I == J && cl > r) return false;  // diagonal tiles of C11 / C22: lower only
+    gi = li + (t == 0 ? 0 : h);
+    gj = lj + (t == 2 ? h : 0);
+    return true;
+}
+
+__global__ void share_pack_kernel(const uint64_t* __restrict__ c, long long ldc, int h, const int2* __restrict__ pairs,
+                                  uint32_t* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int2 pr = pairs[blockIdx.x];
+    const int t = blockIdx.y;
+    uint32_t* o = out + ((long long)blockIdx.x * 4 + t) * 1024;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        long long gi, gj;
+        const bool ok = share_entry(t, pr.x, pr.y, r, threadIdx.x, h, gi, gj);
+        o[r * 32 + threadIdx.x] = ok ? (uint32_t)c[gi * ldc + gj] : 0u;
+    }
+}
+
+__global__ void share_unpack_kernel(const uint32_t* __restrict__ in, int h, const int2* __restrict__ pairs,
+                                    uint64_t* __restrict__ c, long long ldc) {
+    pdl_wait();
+    pdl_trigger();
+    const int2 pr = pairs[blockIdx.x];
+    const int t = blockIdx.y;
+    const uint32_t* src = in + ((long long)blockIdx.x * 4 + t) * 1024;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        long long gi, gj;
+        if (share_entry(t, pr.x, pr.y, r, threadIdx.x, h, gi, gj)) c[gi * ldc + gj] = src[r * 32 + threadIdx.x];
     }
 }
 
@@ -930,9 +971,21 @@ cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStr
 
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s) {
-    const long long total = (long long)rows * cols;
-    if (total == 0) return cudaSuccess;
-    return launch_pdl(u32_to_u64_kernel, dim3(grid_for(total, 256)), dim3(256), 0, s, x, ldx, rows, cols, out, ldo);
+    if ((long long)rows * cols == 0) return cudaSuccess;
+    const int gx = (cols + 255) / 256;
+    return launch_pdl(u32_to_u64_kernel, dim3(gx, rows_grid(rows, gx)), dim3(256), 0, s, x, ldx, rows, cols, out, ldo);
+}
+
+cudaError_t launch_share_pack(const uint64_t* c, long long ldc, int h, const int2* pairs, int npairs, uint32_t* out,
+                              cudaStream_t s) {
+    if (npairs == 0) return cudaSuccess;
+    return launch_pdl(share_pack_kernel, dim3(npairs, 4), dim3(32, 8), 0, s, c, ldc, h, pairs, out);
+}
+
+cudaError_t launch_share_unpack(const uint32_t* in, int h, const int2* pairs, int npairs, uint64_t* c, long long ldc,
+                                cudaStream_t s) {
+    if (npairs == 0) return cudaSuccess;
+    return launch_pdl(share_unpack_kernel, dim3(npairs, 4), dim3(32, 8), 0, s, in, h, pairs, c, ldc);
 }
 
 cudaError_t launch_wino_pre(const uint32_t* x11, const uint32_t* x12, const uint32_t* x21, const uint32_t* x22,

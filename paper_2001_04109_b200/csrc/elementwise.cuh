@@ -125,6 +125,12 @@ cudaError_t launch_deinterleave(const uint64_t* a, long long ldp, int n, int k, 
 cudaError_t launch_fp2_combine(const uint64_t* r, long long ldr, const uint32_t* g, long long ldg, int n, uint32_t p,
                                int conj, int mirror, uint64_t* c, long long ldcp, cudaStream_t s);
 cudaError_t launch_zero_upper(uint64_t* c, long long ldc, int n, int rb, cudaStream_t s);
+// Multi-GPU shares: the 32 x 32 tiles of Low(C) a partitioned rank's root post writes for its
+// tile pairs, packed as uint32 (4 x 1024 words per pair), and back into a uint64 C
+cudaError_t launch_share_pack(const uint64_t* c, long long ldc, int h, const int2* pairs, int npairs, uint32_t* out,
+                              cudaStream_t s);
+cudaError_t launch_share_unpack(const uint32_t* in, int h, const int2* pairs, int npairs, uint64_t* c, long long ldc,
+                                cudaStream_t s);
 cudaError_t launch_u32_to_u64(const uint32_t* x, long long ldx, int rows, int cols, uint64_t* out, long long ldo,
                               cudaStream_t s);
 

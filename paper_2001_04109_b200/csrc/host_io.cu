@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -30,6 +31,7 @@
 #include <vector>
 
 #include "elementwise.cuh"
+#include "per_device.h"
 
 namespace fsyrk_b200 {
 namespace hio {
@@ -309,23 +311,31 @@ struct Slot {
     cudaEvent_t ev = nullptr;
     bool pending = false;  // a copy from / into buf may still be in flight
 };
-Slot g_slot[kSlots];
-cudaStream_t g_raw = nullptr;  // second copy stream for the unnarrowed share
-cudaEvent_t g_raw_done = nullptr, g_fork = nullptr;
-
 struct Staging {
     uint32_t* ptr = nullptr;
     size_t n = 0;
-} g_dev32;  // packed uint32 rows on the device
+};
 
-cudaError_t ensure_slots(size_t cap) {
-    if (!g_raw) {
-        cudaError_t e = cudaStreamCreateWithFlags(&g_raw, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_raw_done, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming);
+// Staging state of one device (streams, events and device buffers belong to the device that was
+// current when they were made; a process may drive several GPUs): pinned slots with their copy
+// events, the second copy stream for the unnarrowed share, packed words / uint32 rows.
+struct DevIo {
+    Slot slot[kSlots];
+    cudaStream_t raw = nullptr;
+    cudaEvent_t raw_done = nullptr, fork = nullptr;
+    Staging dev32, devw;
+};
+
+DevIo& dev_io() { return per_device<DevIo>(); }
+
+cudaError_t ensure_slots(DevIo& io, size_t cap) {
+    if (!io.raw) {
+        cudaError_t e = cudaStreamCreateWithFlags(&io.raw, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.raw_done, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&io.fork, cudaEventDisableTiming);
         if (e != cudaSuccess) return e;
     }
-    for (auto& s : g_slot) {
+    for (auto& s : io.slot) {
         if (!s.ev) {
             cudaError_t e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming);
             if (e != cudaSuccess) return e;
@@ -355,25 +365,23 @@ cudaError_t acquire(Slot& s) {
     return e;
 }
 
-struct Staging g_devw;  // packed words on the device
-
-cudaError_t ensure_devw(size_t n) {
-    if (g_devw.n >= n) return cudaSuccess;
-    if (g_devw.ptr) cudaFree(g_devw.ptr);
-    g_devw.ptr = nullptr;
-    g_devw.n = 0;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&g_devw.ptr), n * 4);
-    if (e == cudaSuccess) g_devw.n = n;
+cudaError_t ensure_devw(DevIo& io, size_t n) {
+    if (io.devw.n >= n) return cudaSuccess;
+    if (io.devw.ptr) cudaFree(io.devw.ptr);
+    io.devw.ptr = nullptr;
+    io.devw.n = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&io.devw.ptr), n * 4);
+    if (e == cudaSuccess) io.devw.n = n;
     return e;
 }
 
-cudaError_t ensure_dev32(size_t n) {
-    if (g_dev32.n >= n) return cudaSuccess;
-    if (g_dev32.ptr) cudaFree(g_dev32.ptr);
-    g_dev32.ptr = nullptr;
-    g_dev32.n = 0;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&g_dev32.ptr), n * 4);
-    if (e == cudaSuccess) g_dev32.n = n;
+cudaError_t ensure_dev32(DevIo& io, size_t n) {
+    if (io.dev32.n >= n) return cudaSuccess;
+    if (io.dev32.ptr) cudaFree(io.dev32.ptr);
+    io.dev32.ptr = nullptr;
+    io.dev32.n = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&io.dev32.ptr), n * 4);
+    if (e == cudaSuccess) io.dev32.n = n;
     return e;
 }
 
@@ -605,7 +613,9 @@ int host_threads() {
             if (v > 0) return std::min(v, 256);
         }
         const int hw = (int)std::thread::hardware_concurrency();
-        return std::max(2, std::min(hw, 32));
+        // a library should not claim a whole large host by default: at most 16 worker threads
+        // (the B200 box has 16 cores; FSYRK_B200_HOST_THREADS raises or lowers it)
+        return std::max(2, std::min(hw, 16));
     }();
     return n;
 }
@@ -640,35 +650,36 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
                    uint64_t* bytes) {
     const size_t total = r.offset(r.rows);
     if (total == 0) return cudaSuccess;
+    DevIo& io = dev_io();
     if (bits < 32 && (bits < kMinBits || bits > kMaxBits)) bits = 32;
     const size_t cap = std::max(kChunk, r.lower ? r.rows : r.cols);
     cudaError_t e;
-    if ((e = ensure_slots(cap)) != cudaSuccess) return e;
-    if ((e = ensure_dev32(total)) != cudaSuccess) return e;
+    if ((e = ensure_slots(io, cap)) != cudaSuccess) return e;
+    if ((e = ensure_dev32(io, total)) != cudaSuccess) return e;
     // pinned caller: the tail rows go unnarrowed on the second copy stream, queued first
     const size_t split = is_pinned(h) ? raw_split(r, env_frac("FSYRK_B200_RAW_UP", 0.12)) : r.rows;
     if (split < r.rows) {
-        if ((e = cudaEventRecord(g_fork, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(g_raw, g_fork, 0)) != cudaSuccess) return e;
-        if ((e = raw_copy(r, split, d, ldd, h, ldh, cudaMemcpyHostToDevice, g_raw, bytes)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(g_raw_done, g_raw)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(io.fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(io.raw, io.fork, 0)) != cudaSuccess) return e;
+        if ((e = raw_copy(r, split, d, ldd, h, ldh, cudaMemcpyHostToDevice, io.raw, bytes)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(io.raw_done, io.raw)) != cudaSuccess) return e;
     }
     const std::vector<Chunk> chunks = make_chunks(r, split, cap);
     std::vector<size_t> wofs(chunks.size() + 1, 0);  // packed words of each chunk in the device word buffer
     for (size_t c = 0; c < chunks.size(); ++c) wofs[c + 1] = wofs[c] + packed_words(chunks[c].len, bits);
-    if (bits < 32 && (e = ensure_devw(wofs.back())) != cudaSuccess) return e;
+    if (bits < 32 && (e = ensure_devw(io, wofs.back())) != cudaSuccess) return e;
     const PackFn packer = bits < 32 ? Tab::pack[bits - kMinBits] : nullptr;
     const size_t nw = (size_t)workers().size();
     std::vector<uint64_t> high(chunks.size() * nw, 0);  // out-of-range bits seen, per chunk and worker
     e = run_chunks(
-        chunks.size(), kSlots - 1, [&](size_t c) { return acquire(g_slot[c % kSlots]); },
+        chunks.size(), kSlots - 1, [&](size_t c) { return acquire(io.slot[c % kSlots]); },
         [&](size_t c, int w, int nwk) {
             const Chunk& ch = chunks[c];
             uint64_t hi = 0;
             if (packer) {
-                hi = packer(r, ch, w, nwk, h, ldh, g_slot[c % kSlots].buf);
+                hi = packer(r, ch, w, nwk, h, ldh, io.slot[c % kSlots].buf);
             } else {
-                uint32_t* dst = g_slot[c % kSlots].buf - ch.off;
+                uint32_t* dst = io.slot[c % kSlots].buf - ch.off;
                 slice(r, ch, w, nwk, [&](size_t i, size_t c0, size_t c1, size_t pos) {
                     hi |= narrow_run(h + i * ldh + c0, dst + pos, c1 - c0);
                 });
@@ -686,10 +697,10 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
                 return cudaMemcpy2DAsync(d + ch.r0 * ldd, ldd * 8, h + ch.r0 * ldh, ldh * 8, wd * 8, ch.r1 - ch.r0,
                                          cudaMemcpyHostToDevice, s);
             }
-            Slot& sl = g_slot[c % kSlots];
-            uint32_t* d32 = g_dev32.ptr + ch.off;
+            Slot& sl = io.slot[c % kSlots];
+            uint32_t* d32 = io.dev32.ptr + ch.off;
             const size_t nwords = wofs[c + 1] - wofs[c];
-            uint32_t* dst = bits < 32 ? g_devw.ptr + wofs[c] : d32;
+            uint32_t* dst = bits < 32 ? io.devw.ptr + wofs[c] : d32;
             if ((e2 = cudaMemcpyAsync(dst, sl.buf, nwords * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e2;
             if ((e2 = cudaEventRecord(sl.ev, s)) != cudaSuccess) return e2;
             sl.pending = true;
@@ -704,7 +715,7 @@ cudaError_t upload(const uint64_t* h, size_t ldh, Region r, uint64_t* d, size_t 
             return cudaGetLastError();
         });
     if (e != cudaSuccess) return e;
-    if (split < r.rows) e = cudaStreamWaitEvent(s, g_raw_done, 0);
+    if (split < r.rows) e = cudaStreamWaitEvent(s, io.raw_done, 0);
     return e;
 }
 
@@ -712,11 +723,12 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
                      cudaStream_t s, uint64_t* bytes) {
     const size_t total = r.offset(r.rows);
     if (total == 0) return cudaSuccess;
+    DevIo& io = dev_io();
     if (bits < 32 && (bits < kMinBits || bits > kMaxBits)) bits = 32;
     const size_t cap = std::max(kChunk, r.lower ? r.rows : r.cols);
     cudaError_t e;
-    if ((e = ensure_slots(cap)) != cudaSuccess) return e;
-    if ((e = ensure_dev32(total)) != cudaSuccess) return e;
+    if ((e = ensure_slots(io, cap)) != cudaSuccess) return e;
+    if ((e = ensure_dev32(io, total)) != cudaSuccess) return e;
     const size_t split = is_pinned(h) ? raw_split(r, env_frac("FSYRK_B200_RAW_DOWN", 0.0)) : r.rows;
     if (split < r.rows) {
         // the unnarrowed row blocks carry their diagonal blocks' strict upper parts: clear them on
@@ -725,33 +737,33 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
             (e = launch_zero_upper(const_cast<uint64_t*>(d), (long long)ldd, (int)r.rows, (int)zero_rb, s)) !=
                 cudaSuccess)
             return e;
-        if ((e = cudaEventRecord(g_fork, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(g_raw, g_fork, 0)) != cudaSuccess) return e;
-        if ((e = raw_copy(r, split, h, ldh, d, ldd, cudaMemcpyDeviceToHost, g_raw, bytes)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(g_raw_done, g_raw)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(io.fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(io.raw, io.fork, 0)) != cudaSuccess) return e;
+        if ((e = raw_copy(r, split, h, ldh, d, ldd, cudaMemcpyDeviceToHost, io.raw, bytes)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(io.raw_done, io.raw)) != cudaSuccess) return e;
     }
     const std::vector<Chunk> chunks = make_chunks(r, split, cap);
     std::vector<size_t> wofs(chunks.size() + 1, 0);
     for (size_t c = 0; c < chunks.size(); ++c) wofs[c + 1] = wofs[c] + packed_words(chunks[c].len, bits);
-    if (bits < 32 && (e = ensure_devw(wofs.back())) != cudaSuccess) return e;
+    if (bits < 32 && (e = ensure_devw(io, wofs.back())) != cudaSuccess) return e;
     if (!chunks.empty()) {
         narrow_kernel<<<rows_grid(split, r.lower ? split : r.cols), 256, 0, s>>>(
-            d, (long long)ldd, (int)split, (int)r.cols, r.lower ? 1 : 0, g_dev32.ptr);
+            d, (long long)ldd, (int)split, (int)r.cols, r.lower ? 1 : 0, io.dev32.ptr);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (bits < 32)
             for (size_t c = 0; c < chunks.size(); ++c) {
                 const size_t nwords = wofs[c + 1] - wofs[c];
                 pack_kernel<<<(unsigned)std::min<size_t>(4096, (nwords + 255) / 256), 256, 0, s>>>(
-                    g_dev32.ptr + chunks[c].off, chunks[c].len, bits, g_devw.ptr + wofs[c], nwords);
+                    io.dev32.ptr + chunks[c].off, chunks[c].len, bits, io.devw.ptr + wofs[c], nwords);
             }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     auto issue = [&](size_t c) -> cudaError_t {
-        Slot& sl = g_slot[c % kSlots];
+        Slot& sl = io.slot[c % kSlots];
         cudaError_t e2 = acquire(sl);
         if (e2 != cudaSuccess) return e2;
         const size_t nwords = wofs[c + 1] - wofs[c];
-        const uint32_t* src = bits < 32 ? g_devw.ptr + wofs[c] : g_dev32.ptr + chunks[c].off;
+        const uint32_t* src = bits < 32 ? io.devw.ptr + wofs[c] : io.dev32.ptr + chunks[c].off;
         e2 = cudaMemcpyAsync(sl.buf, src, nwords * 4, cudaMemcpyDeviceToHost, s);
         if (e2 != cudaSuccess) return e2;
         e2 = cudaEventRecord(sl.ev, s);
@@ -763,14 +775,14 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
         if ((e = issue(c)) != cudaSuccess) return e;
     const UnpackFn unpacker = bits < 32 ? Tab::unpack[bits - kMinBits] : nullptr;
     e = run_chunks(
-        chunks.size(), 1, [&](size_t c) { return acquire(g_slot[c % kSlots]); },
+        chunks.size(), 1, [&](size_t c) { return acquire(io.slot[c % kSlots]); },
         [&](size_t c, int w, int nw) {
             const Chunk& ch = chunks[c];
             if (unpacker) {
-                unpacker(r, ch, w, nw, g_slot[c % kSlots].buf, h, ldh, zero_rb);
+                unpacker(r, ch, w, nw, io.slot[c % kSlots].buf, h, ldh, zero_rb);
                 return;
             }
-            const uint32_t* src = g_slot[c % kSlots].buf - ch.off;
+            const uint32_t* src = io.slot[c % kSlots].buf - ch.off;
             slice(r, ch, w, nw, [&](size_t i, size_t c0, size_t c1, size_t pos) {
                 uint64_t* o = h + i * ldh;
                 widen_run(src + pos, o + c0, c1 - c0);
@@ -782,7 +794,7 @@ cudaError_t download(const uint64_t* d, size_t ldd, Region r, uint64_t* h, size_
         },
         [&](size_t c) { return c + kSlots < chunks.size() ? issue(c + kSlots) : cudaSuccess; });
     if (e != cudaSuccess) return e;
-    if (split < r.rows) e = cudaEventSynchronize(g_raw_done);
+    if (split < r.rows) e = cudaEventSynchronize(io.raw_done);
     return e;
 }
 

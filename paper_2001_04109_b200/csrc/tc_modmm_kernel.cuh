@@ -27,6 +27,7 @@
 
 #include "modp.cuh"
 #include "pdl.cuh"
+#include "per_device.h"
 #include "schemes.cuh"
 #include "sm100.cuh"
 #include "tc_modmm.h"
@@ -646,13 +647,19 @@ cudaLaunchConfig_t launch_config(int grid, cudaStream_t stream, cudaLaunchAttrib
     return cfg;
 }
 
+template <int S, int EPI>
+struct SmemAttrOnce : DeviceOnce {};
+
 template <int S, int EPI = kEpiWarpsDefault>
 cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<S>;
     auto kern = modmm_kernel<S, EPI>;
-    static const cudaError_t smem_attr =  // thread-safe one-time setup
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (smem_attr != cudaSuccess) return smem_attr;
+    // thread-safe one-time setup per device (the attribute applies to the current device only)
+    DeviceOnce& once = per_device<SmemAttrOnce<S, EPI>>();
+    std::call_once(once.flag, [&] {
+        once.result = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    });
+    if (once.result != cudaSuccess) return once.result;
     if (args.ntiles == 0) return cudaSuccess;
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);

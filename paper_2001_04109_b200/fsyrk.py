@@ -95,6 +95,8 @@ EXPORTS = (
     "fsyrk_b200_last_transfer_bytes", "fsyrk_b200_sum_of_squares", "fsyrk_b200_nrsyf",
     "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2", "fsyrk_b200_gemm_winograd_nt",
     "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip", "fsyrk_b200_upload", "fsyrk_b200_download",
+    "fsyrk_b200_syrk_mgpu", "fsyrk_b200_nccl_unique_id", "fsyrk_b200_comm_init_rank", "fsyrk_b200_comm_destroy",
+    "fsyrk_b200_syrk_mgpu_rank", "fsyrk_b200_share_pairs",
 )
 
 
@@ -141,6 +143,20 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_last_transfer_bytes.argtypes = [_u64p, _u64p]
+    L.fsyrk_b200_syrk_mgpu.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
+                                       ctypes.c_size_t, _u64p, ctypes.c_uint64, _u64p, ctypes.c_size_t, _Policy,
+                                       ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                       ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.fsyrk_b200_comm_init_rank.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_void_p)]
+    L.fsyrk_b200_comm_destroy.argtypes = [ctypes.c_void_p]
+    L.fsyrk_b200_syrk_mgpu_rank.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, _u64p, ctypes.c_size_t,
+                                            ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64, _u64p,
+                                            ctypes.c_size_t, _Policy, ctypes.c_int, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_share_pairs.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int), ctypes.c_size_t,
+                                         ctypes.POINTER(ctypes.c_size_t)]
     L.fsyrk_b200_upload.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     L.fsyrk_b200_download.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
@@ -673,3 +689,84 @@ def last_phase_ms() -> dict:
 
 def release_cache() -> None:
     lib().fsyrk_b200_release_cache()
+
+
+# -------------------------------------------------------------- multi-GPU
+def _mgpu_args(f: PrimeField, a: np.ndarray, c: np.ndarray, d):
+    pa, n, k, lda = _view(a, "a")
+    pc, cn, cm, ldc = _view(c, "c")
+    if cn != cm or cn != n:
+        raise DimensionError("syrk_fast: dimension mismatch")
+    dptr, keep = None, None
+    if d is not None:
+        keep = np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+        if keep.ndim != 1 or keep.shape[0] != k:
+            raise DimensionError("syrkd: diagonal length must match column count")
+        dptr = keep.ctypes.data_as(_u64p) if k > 0 else None
+    return pa, n, k, lda, pc, ldc, dptr, keep
+
+
+def syrk_mgpu(f: PrimeField, a: np.ndarray, c: np.ndarray, plan: SyrkPlan, devices: Sequence[int], alpha: int = 1,
+              beta: int = 0, d: Optional[np.ndarray] = None, ops: Optional[OpCount] = None) -> np.ndarray:
+    """Multi-GPU Low(C) <- Low(alpha A Diag(d) A^T + beta C) over `devices` of this process
+    (fsyrk_b200_syrk_mgpu: NCCL broadcast of A, owned tile pairs per device, uint32 share gather)."""
+    plan.policy.validate()
+    pa, n, k, lda, pc, ldc, dptr, _keep = _mgpu_args(f, a, c, d)
+    devs = (ctypes.c_int * max(1, len(devices)))(*[int(x) for x in devices])
+    co = _OpCount()
+    _check(lib().fsyrk_b200_syrk_mgpu(f.p, int(alpha) % f.p, pa, n, k, lda, dptr, int(beta) % f.p, pc, ldc,
+                                      plan.policy._c(), int(plan.mirror_output), devs, len(devices), ctypes.byref(co)))
+    _ops_out(ops, co)
+    return c
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fsyrk_b200_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Communicator:
+    """One rank of a multi-process (one process per GPU) library call: the NCCL communicator
+    on the current device (fsyrk_b200_comm_init_rank)."""
+
+    def __init__(self, uid: bytes, rank: int, nranks: int):
+        h = ctypes.c_void_p()
+        _check(lib().fsyrk_b200_comm_init_rank(bytes(uid), int(rank), int(nranks), ctypes.byref(h)))
+        self.handle, self.rank, self.nranks = h, int(rank), int(nranks)
+
+    def close(self) -> None:
+        if self.handle:
+            _check(lib().fsyrk_b200_comm_destroy(self.handle))
+            self.handle = None
+
+    def syrk(self, f: PrimeField, a: Optional[np.ndarray], c: Optional[np.ndarray], n: int, k: int, plan: SyrkPlan,
+             alpha: int = 1, beta: int = 0, d: Optional[np.ndarray] = None, ops: Optional[OpCount] = None) -> None:
+        """Collective fsyrk_b200_syrk_mgpu_rank: rank 0 passes host a (n x k) and c (n x n);
+        the other ranks pass None."""
+        plan.policy.validate()
+        if self.rank == 0:
+            pa, n2, k2, lda, pc, ldc, dptr, _keep = _mgpu_args(f, a, c, d)
+            if (n2, k2) != (int(n), int(k)):
+                raise DimensionError("syrk_mgpu: dimension mismatch")
+        else:
+            pa = pc = None
+            lda, ldc = max(int(k), 1), max(int(n), 1)
+            _keep = None if d is None else np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+            dptr = _keep.ctypes.data_as(_u64p) if _keep is not None and int(k) > 0 else None
+        co = _OpCount()
+        _check(lib().fsyrk_b200_syrk_mgpu_rank(self.handle, f.p, int(alpha) % f.p, pa, int(n), int(k), lda, dptr,
+                                               int(beta) % f.p, pc, ldc, plan.policy._c(), int(plan.mirror_output),
+                                               ctypes.byref(co)))
+        _ops_out(ops, co)
+
+
+def share_pairs(p: int, h: int, rank: int, nranks: int) -> np.ndarray:
+    """Tile pairs (I, J) of rank's share of Low(C) (fsyrk_b200_share_pairs), shape (count, 2)."""
+    cnt = ctypes.c_size_t(0)
+    _check(lib().fsyrk_b200_share_pairs(int(p), int(h), int(rank), int(nranks), None, 0, ctypes.byref(cnt)))
+    out = np.zeros((cnt.value, 2), dtype=np.int32)
+    _check(lib().fsyrk_b200_share_pairs(int(p), int(h), int(rank), int(nranks),
+                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), cnt.value,
+                                        ctypes.byref(cnt)))
+    return out

@@ -1,10 +1,13 @@
 """Multi-GPU partition of the top level.
 
-CPU: the block-pair ownership is complete, disjoint and balanced, and the
-multi-rank composition used by bench.py (disjoint shares summed over ranks,
-max-over-ranks timing) is exercised with world_size 2 over gloo.
+CPU: the block-pair ownership is complete, disjoint and balanced; the library's share tile
+pairs cover Low(C) exactly once; and the data flow of the library's multi-GPU call
+(fsyrk_b200_syrk_mgpu_rank: broadcast A, per-rank shares in the packed uint32 layout for the
+library's tile pairs, gather to rank 0) runs with world_size 2 over gloo.
 GPU: every rank's share computed on one device (ranks are independent: no rank
-waits on another) reassembles bit-exactly into the single-GPU result."""
+waits on another) reassembles bit-exactly into the single-GPU result, and the library's
+multi-GPU entry point (loopback ranks on one device; a 1-rank NCCL communicator) matches
+the oracle."""
 import os
 import socket
 import sys
@@ -57,7 +60,35 @@ def test_partition_owners_complete_and_balanced(fsyrk, p, h, nranks):
         assert load.max() / load.mean() < 1.2
 
 
+def share_entries(pairs, h):
+    """(slot, r, col) -> (row, col) of C for a share in the library's layout
+    (include/fsyrk_b200.h fsyrk_b200_share_pairs): per pair (I, J), slots C11(I,J), C21(I,J),
+    C22(I,J), C21(J,I) of 32 x 32 words; entries outside Low(C) or beyond h are unused."""
+    idx_pos, idx_rc = [], []
+    r, cl = np.meshgrid(np.arange(32), np.arange(32), indexing="ij")
+    for q, (I, J) in enumerate(pairs):
+        for t in range(4):
+            if t == 3 and I == J:
+                continue
+            bi, bj = (J, I) if t == 3 else (I, J)
+            li, lj = bi * 32 + r, bj * 32 + cl
+            ok = (li < h) & (lj < h)
+            if t in (0, 2) and I == J:
+                ok &= cl <= r
+            gi = li + (0 if t == 0 else h)
+            gj = lj + (h if t == 2 else 0)
+            pos = (q * 4 + t) * 1024 + r * 32 + cl
+            idx_pos.append(pos[ok])
+            idx_rc.append((gi[ok], gj[ok]))
+    if not idx_pos:
+        return np.zeros(0, np.int64), (np.zeros(0, np.int64), np.zeros(0, np.int64))
+    return (np.concatenate(idx_pos), (np.concatenate([x[0] for x in idx_rc]), np.concatenate([x[1] for x in idx_rc])))
+
+
 def _gloo_worker(rank, world, port, n, p, result_q):
+    # the multi-GPU data flow of fsyrk_b200_syrk_mgpu_rank with gloo standing in for NCCL:
+    # broadcast A (uint32 residues), each rank's share of Low(C) in the library's packed layout
+    # for the tile pairs the library assigns it, gathered to rank 0 and unpacked
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -66,34 +97,55 @@ def _gloo_worker(rank, world, port, n, p, result_q):
     import oracle_py as o
     import paper_2001_04109_b200 as fs
     import bench
-    a = o.random_matrix(p, n, n, 42)
-    full = o.syrk_classical(p, a)
-    owners, blk = fs.partition_owners(p, n // 2, world)
-    mask = owner_mask(n, owners, rank, blk)
-    share = np.where(mask, full, 0).astype(np.int64)  # what this rank's device C holds (beta = 0)
+    h = n // 2
+    a32 = torch.zeros((n, n), dtype=torch.int32)
+    if rank == 0:
+        a32 = torch.from_numpy(o.random_matrix(p, n, n, 42).astype(np.int32))
+    dist.broadcast(a32, src=0)
+    a = a32.numpy().astype(np.uint64)
+    full = o.syrk_classical(p, a)              # what every rank's device C would hold on its tiles
+    pairs = [fs.share_pairs(p, h, r, world) for r in range(world)]
+    pos, (gi, gj) = share_entries(pairs[rank], h)
+    share = np.zeros(len(pairs[rank]) * 4096, dtype=np.int32)
+    share[pos] = full[gi, gj].astype(np.int32)
     t = torch.from_numpy(share)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)           # bench.py's gather of disjoint shares
+    if rank == 0:
+        got = np.zeros((n, n), dtype=np.uint64)
+        covered = np.zeros((n, n), dtype=np.int32)
+        for r in range(world):
+            buf = t if r == 0 else torch.zeros(len(pairs[r]) * 4096, dtype=torch.int32)
+            if r:
+                dist.recv(buf, src=r)
+            pr, (ri, rj) = share_entries(pairs[r], h)
+            got[ri, rj] = buf.numpy()[pr].astype(np.uint64)
+            np.add.at(covered, (ri, rj), 1)
+        ok = orc_lower_equal(got, full) and (covered[np.tril_indices(n)] == 1).all() and \
+            not covered[np.triu_indices(n, 1)].any()
+    else:
+        dist.send(t, dst=0)
+        ok = True
     ms = bench.max_over_ranks(float(rank + 1), world)  # bench.py's timing reduction
-    ok = np.array_equal(np.tril(t.numpy().astype(np.uint64)), np.tril(full)) and ms == float(world)
-    result_q.put((rank, ok, int(mask.sum())))
+    result_q.put((rank, bool(ok) and ms == float(world), int(len(pos))))
     dist.destroy_process_group()
 
 
-def test_two_rank_composition_over_gloo(fsyrk):
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    n, p, world = 1536, 131071, 2
-    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, p, q)) for r in range(world)]
-    for pr in procs:
-        pr.start()
-    res = [q.get(timeout=300) for _ in range(world)]
-    for pr in procs:
-        pr.join(timeout=60)
-    assert all(ok for _, ok, _ in res), res
-    assert sum(c for _, _, c in res) == n * (n + 1) // 2  # every lower entry owned exactly once
+def orc_lower_equal(x, y):
+    i = np.tril_indices(x.shape[0])
+    return np.array_equal(x[i], y[i])
+
+
+def test_share_pairs_partition_every_tile_once(fsyrk):
+    # the owned tile pairs of all ranks cover the 32 x 32 tile pairs of the quadrants exactly once
+    # and agree with partition_owners' block-pair owners
+    for p, h, world in ((131071, 2048, 3), (2147483647, 1000, 4), (65521, 4096, 8)):
+        own, blk = fsyrk.partition_owners(p, h, world)
+        T = (h + 31) // 32
+        seen = np.zeros((T, T), dtype=np.int32)
+        for r in range(world):
+            for I, J in fsyrk.share_pairs(p, h, r, world):
+                assert I >= J and own[I * 32 // blk, J * 32 // blk] == r
+                seen[I, J] += 1
+        assert (seen[np.tril_indices(T)] == 1).all() and not seen[np.triu_indices(T, 1)].any()
 
 
 @pytest.mark.gpu
@@ -127,3 +179,65 @@ def test_partition_shares_reassemble(gpu, nranks, mode):
     torch.cuda.synchronize()
     written = np.tril(c1.cpu().numpy()) != 0
     assert not (written & ~owner_mask(n, owners, 1, blk)).any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+@pytest.mark.parametrize("mode", ["plain", "acc", "schur", "mirror"])
+def test_syrk_mgpu_entry(gpu, devices, mode):
+    # fsyrk_b200_syrk_mgpu: one GPU on this box, so >1 ranks are loopback ranks on device 0
+    # (same partition, share packing, scatter of C_in and gather as over NCCL; the exchange is
+    # device copies) -- bit-exact against the oracle
+    fs = gpu
+    p, n, k = 131071, 1600, 640
+    f = fs.PrimeField(p)
+    a = orc.random_matrix(p, n, k, 71)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(2, 1), mirror_output=(mode == "mirror"))
+    want = orc.syrk_classical(p, a)
+    c0 = orc.random_matrix(p, n, n, 72)
+    c = c0.copy()
+    idx = np.tril_indices(n)
+    if mode in ("plain", "mirror"):
+        fs.syrk_mgpu(f, a, c, plan, devices)
+        assert orc.lower_equal(c, want)
+        if mode == "mirror":
+            assert np.array_equal(c, c.T)
+    elif mode == "acc":
+        fs.syrk_mgpu(f, a, c, plan, devices, alpha=5, beta=7)
+        assert np.array_equal(c[idx], (want[idx] * np.uint64(5) + c0[idx] * np.uint64(7)) % np.uint64(p))
+        assert np.array_equal(c[np.triu_indices(n, 1)], c0[np.triu_indices(n, 1)])
+    else:
+        d = orc.random_nonzero(p, k, 73)
+        fs.syrk_mgpu(f, a, c, plan, devices, alpha=p - 1, beta=1, d=d)
+        sd = orc.syrkd(p, a, d, 2)
+        assert np.array_equal(c[idx], (c0[idx] + np.uint64(p) - sd[idx]) % np.uint64(p))
+
+
+@pytest.mark.gpu
+def test_syrk_mgpu_unpartitionable_and_odd_shapes(gpu):
+    # shapes whose top level does not recurse (odd n) run on the first device alone; k = 0
+    fs = gpu
+    p = 2147483647
+    f = fs.PrimeField(p)
+    plan = fs.make_syrk_plan(f, fs.RecursionPolicy(2, 1))
+    for n, k in ((301, 200), (256, 0), (640, 700)):
+        a = orc.random_matrix(p, n, k, 74) if k else np.zeros((n, 0), np.uint64)
+        c = np.full((n, n), 3, dtype=np.uint64)
+        fs.syrk_mgpu(f, a, c, plan, [0, 0])
+        assert orc.lower_equal(c, orc.syrk_classical(p, a) if k else np.zeros((n, n), np.uint64)), (n, k)
+
+
+@pytest.mark.gpu
+def test_communicator_single_rank(gpu):
+    # the multi-process entry with a real NCCL communicator of one rank (the box has one GPU)
+    fs = gpu
+    p, n, k = 65521, 700, 500
+    f = fs.PrimeField(p)
+    comm = fs.Communicator(fs.nccl_unique_id(), 0, 1)
+    try:
+        a = orc.random_matrix(p, n, k, 75)
+        c = np.zeros((n, n), dtype=np.uint64)
+        comm.syrk(f, a, c, n, k, fs.make_syrk_plan(f, fs.RecursionPolicy(8)))
+        assert orc.lower_equal(c, orc.syrk_classical(p, a))
+    finally:
+        comm.close()

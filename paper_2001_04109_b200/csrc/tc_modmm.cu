@@ -11,10 +11,14 @@
 // tcgen05.mma.kind::i8 and the epilogue folds its NACC accumulators mod p.
 // Scheme choice (scheme_for):
 //   p = 2^17 - 1 : M17  (9 MMAs, 3 accumulators, 128 x 160 tiles)
-//   p = 2^31 - 1 : M31  (16 MMAs, 5 accumulators, 128 x 96 tiles)
+//   p = 2^31 - 1 : M31  (default ACC4: 17 MMAs -- d2 e2 issued twice -- into
+//                        4 accumulators, 128 x 128 tiles; without ACC4:
+//                        16 MMAs, 5 accumulators, 128 x 96)
 //   p <= 2^16    : LIMB2 (4 MMAs, 3 accumulators, 128 x 128)
 //   p <= 2^24    : LIMB3 (9 MMAs, 5 accumulators, 128 x 96)
 //   otherwise    : LIMB4 (16 MMAs, 7 accumulators, 128 x 64)
+// Above modmm_k_limit the kernel drains its int32 accumulators mod p every
+// K chunk, so any inner dimension is exact.
 // The tile N is as large as TMEM allows for the accumulators: the
 // microbenchmark in profiles/ubench shows the int8 MMA rate falls with N
 // (shared-memory operand bandwidth), so the accumulators are not double

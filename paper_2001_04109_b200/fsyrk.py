@@ -324,8 +324,12 @@ def _view(m: np.ndarray, name: str):
         raise DimensionError(f"{name} must be a 2-D numpy uint64 array")
     if m.size > 0 and m.shape[1] > 1 and m.strides[1] != 8:
         raise DimensionError(f"{name} rows must be contiguous")
+    if m.size > 0 and m.shape[0] > 1 and (m.strides[0] % 8 != 0 or m.strides[0] < 8 * m.shape[1]):
+        # negative, overlapping or misaligned row strides cannot be expressed as a (data, ld)
+        # view: the library would walk forward from the first row's address
+        raise DimensionError(f"{name} row stride must be a positive multiple of 8 bytes >= 8*cols")
     ld = m.strides[0] // 8 if m.shape[0] > 1 and m.size > 0 else max(m.shape[1], 1)
-    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(max(ld, m.shape[1]))
+    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(ld)
 
 
 def random_matrix(f: PrimeField, rows: int, cols: int, seed: int) -> np.ndarray:
@@ -491,8 +495,10 @@ def _view_fp2(m: np.ndarray, name: str):
         raise DimensionError(f"{name} must be a (rows, cols, 2) numpy uint64 array of (a, b) pairs")
     if m.size > 0 and (m.strides[2] != 8 or (m.shape[1] > 1 and m.strides[1] != 16)):
         raise DimensionError(f"{name} rows must be contiguous pairs")
+    if m.size > 0 and m.shape[0] > 1 and (m.strides[0] % 16 != 0 or m.strides[0] < 16 * m.shape[1]):
+        raise DimensionError(f"{name} row stride must be a positive multiple of 16 bytes >= 16*cols")
     ld = m.strides[0] // 16 if m.shape[0] > 1 and m.size > 0 else max(m.shape[1], 1)
-    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(max(ld, m.shape[1]))
+    return m.ctypes.data_as(_u64p), int(m.shape[0]), int(m.shape[1]), int(ld)
 
 
 def make_herk_plan(f: QuadExtField, policy: Optional[RecursionPolicy] = None, mirror_output: bool = False) -> SyrkPlan:

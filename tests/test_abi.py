@@ -88,3 +88,22 @@ def test_python_mirror_shape_errors(fsyrk):
         fsyrk.syrkd(f, np.zeros((2, 2), np.uint64), [1], plan)
     with pytest.raises(ValueError):
         fsyrk.syrkd(fsyrk.PrimeField(2), np.ones((2, 2), np.uint64), [1, 1], plan)
+
+
+def test_python_mirror_rejects_reversed_or_overlapping_rows(fsyrk):
+    # a[::-1] has a negative row stride; an as_strided overlap has stride < 8*cols: neither is a
+    # (data, rows, cols, ld) view, so both are refused before any library call
+    f = fsyrk.PrimeField(7)
+    plan = fsyrk.make_syrk_plan(f, fsyrk.RecursionPolicy(2))
+    a = np.ones((6, 4), np.uint64)
+    with pytest.raises(fsyrk.DimensionError):
+        fsyrk.syrk_fast(f, a[::-1], plan)
+    c = np.zeros((6, 6), np.uint64)
+    with pytest.raises(fsyrk.DimensionError):
+        fsyrk.syrk_fast_into(f, a, c[::-1], plan)
+    over = np.lib.stride_tricks.as_strided(np.zeros(40, np.uint64), shape=(6, 6), strides=(16, 8))
+    with pytest.raises(fsyrk.DimensionError):
+        fsyrk.syrk_fast_into(f, a, over, plan)
+    a2 = np.ones((4, 3, 2), np.uint64)
+    with pytest.raises(fsyrk.DimensionError):
+        fsyrk.herk_fast(fsyrk.QuadExtField(7), a2[::-1], fsyrk.make_herk_plan(fsyrk.QuadExtField(7), fsyrk.RecursionPolicy(2)))

@@ -60,8 +60,12 @@ typedef struct fsyrk_b200_policy {
 } fsyrk_b200_policy;
 
 /* Operation tally: replaces fsyrk::OpCount (include/fsyrk/opcount.hpp:10-25).
- * The device path reports the modular multiply-accumulates it issued on the
- * tensor cores in `mults` and its elementwise field additions in `adds`. */
+ * Every entry point adds what the reference would have counted for the same call
+ * (its per-routine tallies of syrk_classical, the Winograd engine, the level
+ * additions, the skew and the syrkd / syrkbd column transforms; a host dry-run of
+ * its recursion, csrc/ref_opcount.h), so the reference's reconciliations with its
+ * count model (tests/test_fast_syrk.cpp:202-238, tools/fsyrk.cpp:215-242) hold.
+ * The device's own work (tensor MACs, elementwise bytes) is in fsyrk_b200_last_plan_json. */
 typedef struct fsyrk_b200_opcount {
     uint64_t mults;
     uint64_t adds;
@@ -291,6 +295,21 @@ int fsyrk_b200_gemm_winograd_nt(uint64_t p, const uint64_t* a, size_t m, size_t 
 int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m, size_t k, size_t lda,
                                     const uint64_t* b_dev, size_t n, size_t ldb, uint64_t* c_dev, size_t ldc,
                                     fsyrk_b200_policy policy, void* stream);
+
+/* ------------------------------------------------ reference op tallies (host only) */
+
+/* The OpCount the reference's entry point adds for one call, without running it
+ * (no device needed): syrk_fast_into (alpha = 1, beta = 0) / syrk_fast_acc
+ * (fast_syrk.hpp:274-303); syrkd (scaled_syrk.hpp:58-104, d has k entries) and syrkbd
+ * (:117-159) with this library's alpha / beta extension (alpha = 1, beta = 0 is the
+ * reference's call); herk_fast / syrk_fast over F_{p^2} (fast_syrk.hpp:305-320). */
+int fsyrk_b200_opcount_syrk(uint64_t p, size_t n, size_t k, uint64_t alpha, uint64_t beta,
+                            fsyrk_b200_policy policy, fsyrk_b200_opcount* ops);
+int fsyrk_b200_opcount_syrkd(uint64_t p, size_t n, size_t k, const uint64_t* d, uint64_t alpha, uint64_t beta,
+                             fsyrk_b200_policy policy, fsyrk_b200_opcount* ops);
+int fsyrk_b200_opcount_syrkbd(uint64_t p, size_t n, const fsyrk_b200_block* blocks, size_t nblocks,
+                              uint64_t alpha, uint64_t beta, fsyrk_b200_policy policy, fsyrk_b200_opcount* ops);
+int fsyrk_b200_opcount_fp2(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, fsyrk_b200_opcount* ops);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,7 @@ struct Instance {
     std::vector<std::uint64_t> d;  // schur: D; syrkbd: blocks as (two, d, beta, gamma) quadruples
     BlockDiagonal<PrimeField> b;
     std::uint64_t alpha = 1, beta = 0;
+    OpCount ops;  // the reference's own tally of the last call (opcount.hpp)
 };
 
 Instance make_instance(const PrimeField& f, const Args& g) {
@@ -184,6 +185,7 @@ double run_instance(const PrimeField& f, const Args& g, Instance& in) {
         usage();
     }
     auto t1 = std::chrono::steady_clock::now();
+    in.ops = ops;
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
@@ -207,8 +209,9 @@ int main_fp2(const Args& g) {
     dump(g.out_a, a.data().data(), a.data().size() * sizeof(QuadExtElement));
     dump(g.out_c, c.data().data(), c.data().size() * sizeof(QuadExtElement));
     std::printf("{\"p\": %" PRIu64 ", \"n\": %zu, \"k\": %zu, \"mode\": \"%s\", \"seed\": %" PRIu64
-                ", \"non_residue\": %" PRIu64 ", \"alpha\": 1, \"beta\": 0, \"digest\": \"\"}\n",
-                g.p, g.n, g.k, g.mode.c_str(), g.seed, f.non_residue());
+                ", \"non_residue\": %" PRIu64 ", \"alpha\": 1, \"beta\": 0, \"digest\": \"\""
+                ", \"ops_mults\": %" PRIu64 ", \"ops_adds\": %" PRIu64 "}\n",
+                g.p, g.n, g.k, g.mode.c_str(), g.seed, f.non_residue(), ops.mults, ops.adds);
     return 0;
 }
 
@@ -251,12 +254,13 @@ int main(int argc, char** argv) {
                 ", \"threshold\": %zu, \"levels\": %s, \"threads\": %d, \"reps\": %d"
                 ", \"alpha\": %" PRIu64 ", \"beta\": %" PRIu64
                 ", \"skew_form\": \"%s\", \"skew_a\": %" PRIu64 ", \"skew_b\": %" PRIu64
-                ", \"seconds_per_call\": %.6f, \"wall_seconds\": %.6f, \"digest\": \"%s\"",
+                ", \"seconds_per_call\": %.6f, \"wall_seconds\": %.6f, \"digest\": \"%s\""
+                ", \"ops_mults\": %" PRIu64 ", \"ops_adds\": %" PRIu64,
                 g.p, g.n, g.k, g.mode.c_str(), g.seed, g.threshold,
                 g.levels == kUnlimitedLevels ? "\"inf\"" : std::to_string(g.levels).c_str(),
                 g.threads, g.reps, r0.alpha, r0.beta,
                 y.form == SkewOrthogonal<PrimeField>::Form::Pair ? "pair" : "scalar", y.a, y.b,
-                sum_s / (g.threads * g.reps), wall, hex);
+                sum_s / (g.threads * g.reps), wall, hex, r0.ops.mults, r0.ops.adds);
     if (g.sample > 0) {
         // deterministic sample positions in the lower triangle
         std::mt19937_64 rng(12345);

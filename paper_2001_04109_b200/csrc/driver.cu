@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <exception>
 #include <array>
 #include <cstdio>
 #include <cstring>
@@ -37,6 +38,7 @@
 #include "../../include/fsyrk_b200.h"
 #include "elementwise.cuh"
 #include "field_host.h"
+#include "ref_opcount.h"
 #include "host_io.h"
 #include "modp.cuh"
 #include "per_device.h"
@@ -1280,6 +1282,9 @@ size_t span_bytes(size_t rows, size_t cols, size_t ld) { return rows == 0 || col
 // transformed matrix is sum_t c[t] * A[:, src[t]].
 struct ColXform {
     std::vector<ColMap> map;
+    // the reference's own tallies of the column transform, per row of A (scaled_syrk.hpp:42-48,
+    // 91-100, 146-153): columns scaled by sqrt(d) != 1, nrsyf pairs, syrkbd 2x2 blocks
+    uint64_t scaled_cols = 0, nr_pairs = 0, blocks2 = 0;
 };
 
 ColMap col_identity(int j) { return ColMap{{j, -1, -1, -1}, {1, 0, 0, 0}}; }
@@ -1323,7 +1328,7 @@ void parallel_for(size_t n, Fn fn) {
     for (auto& th : pool) th.join();
 }
 
-void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& map) {
+void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& map, ColXform* tally = nullptr) {
     host::Field f{p};
     if (p == 2) fail(FSYRK_B200_EINVAL, "syrkd requires an odd prime field");
     const size_t k = dbar.size();
@@ -1339,9 +1344,11 @@ void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& 
         nr.push_back(k);
         map.push_back(ColMap{{-1, -1, -1, -1}, {0, 0, 0, 0}});  // the appended zero column
     }
+    std::vector<char> scaled(dbar.size(), 0);
     parallel_for(dbar.size(), [&](size_t j) {
         if (leg[j] < 0) return;
         const uint64_t sq = f.sqrt(dbar[j]);
+        scaled[j] = sq != 1;  // scale_column skips s = 1 (scaled_syrk.hpp:45)
         for (int q = 0; q < 4; ++q)
             if (map[j].src[q] >= 0) map[j].c[q] = (uint32_t)f.mul(map[j].c[q], sq);
     });
@@ -1367,12 +1374,16 @@ void fold_diagonal(uint64_t p, std::vector<uint64_t> dbar, std::vector<ColMap>& 
         if (b == 1) fail(FSYRK_B200_ENONRES, "nrsyf: argument is not a non-residue");
         if (b == 2) fail(FSYRK_B200_EINVAL, "column transform exceeds 4 source columns");
     }
+    if (tally) {
+        for (char c : scaled) tally->scaled_cols += (uint64_t)c;
+        tally->nr_pairs += npairs;
+    }
 }
 
 ColXform xform_diag(uint64_t p, const uint64_t* d, size_t k) {
     ColXform x;
     for (size_t j = 0; j < k; ++j) x.map.push_back(col_identity((int)j));
-    fold_diagonal(p, std::vector<uint64_t>(d, d + k), x.map);
+    fold_diagonal(p, std::vector<uint64_t>(d, d + k), x.map, &x);
     return x;
 }
 
@@ -1403,8 +1414,9 @@ ColXform xform_blocks(uint64_t p, const fsyrk_b200_block* b, size_t nblocks, siz
         x.map.push_back(ColMap{{(int)j, (int)j + 1, -1, -1}, {1, 1, 0, 0}});
         x.map.push_back(ColMap{{(int)j, (int)j + 1, -1, -1}, {1, (uint32_t)(p - 1), 0, 0}});
         j += 2;
+        x.blocks2++;
     }
-    fold_diagonal(p, std::move(dbar), x.map);
+    fold_diagonal(p, std::move(dbar), x.map, &x);
     return x;
 }
 
@@ -1428,11 +1440,69 @@ struct DevBuf {
 // resource: one host call at a time.  The device-side buffers and streams are per device.
 std::mutex g_stage_mu;
 
-void fill_ops(fsyrk_b200_opcount* ops, const Plan* plan) {
-    if (!ops) return;
-    ops->mults += plan->tensor_macs;
-    ops->adds += plan->ew_adds;
+// OpCount as the reference counts it (ref_opcount.h): a host dry-run of the reference's
+// recursion for this call.  syrk_fast_into is syrk_fast_acc with (1, 0), which the reference
+// tallies identically.  With a column transform the call is the reference's syrkd / syrkbd
+// (transform + plain syrk_fast over the transformed A) followed by this library's alpha / beta
+// extension, tallied like syrk_classical's scaling: tri mults per alpha != 1 and per
+// beta not in {0, 1}, tri adds for beta != 0.
+refops::Model ref_model(uint64_t p, const fsyrk_b200_policy& pol) {
+    refops::Model md;
+    md.threshold = pol.threshold;
+    md.max_levels = pol.max_levels;
+    const host::Skew y = host::skew_orthogonal(host::Field{p});
+    md.skew_form = y.form;
+    md.skew_a_one = y.a == 1;
+    return md;
 }
+
+refops::Tally ref_tally(uint64_t p, size_t n, size_t kbar, const fsyrk_b200_policy& pol, uint64_t alpha, uint64_t beta,
+                        const ColXform* xf) {
+    refops::Model md = ref_model(p, pol);
+    alpha %= p;
+    beta %= p;
+    if (!xf) {
+        const bool acc = !(alpha == 1 && beta == 0);
+        return md.syrk(n, kbar, pol.max_levels, acc, refops::Scalar::of(alpha), refops::Scalar::of(beta));
+    }
+    refops::Tally t;
+    t.mults = n * (xf->scaled_cols + 4 * xf->nr_pairs);
+    t.adds = n * (2 * xf->nr_pairs + 2 * xf->blocks2);
+    t += md.syrk(n, kbar, pol.max_levels, false, refops::Scalar::unit(), refops::Scalar::nil());
+    const uint64_t tri = refops::Model::tri(n);
+    if (alpha != 1) t.mults += tri;
+    if (beta != 0 && beta != 1) t.mults += tri;
+    if (beta != 0) t.adds += tri;
+    return t;
+}
+
+// F_{p^2}: the reference's syrk_fast / herk_fast recursion over QuadExtField (scalar skew root
+// sqrt(-1) or the skew-unitary z, never 1 for odd p; skew.hpp:76-100), one tally per
+// extension-field operation.
+refops::Tally ref_tally_fp2(size_t n, size_t k, const fsyrk_b200_policy& pol) {
+    refops::Model md;
+    md.threshold = pol.threshold;
+    md.max_levels = pol.max_levels;
+    md.skew_form = 0;
+    md.skew_a_one = false;
+    return md.syrk(n, k, pol.max_levels, false, refops::Scalar::unit(), refops::Scalar::nil());
+}
+
+void add_tally(fsyrk_b200_opcount* ops, const refops::Tally& t) {
+    if (!ops) return;
+    ops->mults += t.mults;
+    ops->adds += t.adds;
+}
+
+// Adds a call's tally when the call returns normally (not when it throws).
+struct TallyOnSuccess {
+    fsyrk_b200_opcount* ops;
+    refops::Tally t;
+    int exc = std::uncaught_exceptions();
+    ~TallyOnSuccess() {
+        if (std::uncaught_exceptions() == exc) add_tally(ops, t);
+    }
+};
 
 // One operand of a batched product: a uint32 residue view, or a window of a uint64 matrix.
 struct GemmOperand {
@@ -1649,7 +1719,7 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     }
     plan->execute(a_dev, (long long)lda, c_dev, (long long)ldc, alpha, beta, mirror, s);
     ck(cudaEventRecord(plan->ev_done, s), "event record");
-    fill_ops(ops, plan);
+    if (ops && rank == 0) add_tally(ops, ref_tally(p, n, (size_t)kbar, pol, alpha, beta, xf));
 }
 
 // Host call: the caller's A (and Low(C_in) when accumulating) cross PCIe through host_io
@@ -1712,6 +1782,7 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
         fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
     require_device();
     if (n == 0) return;
+    TallyOnSuccess tally{ops, ops ? ref_tally(p, n, xf ? xf->map.size() : k, pol, alpha, beta, xf) : refops::Tally{}};
     if ((k > 0 && hio::is_device(a)) || hio::is_device(c))
         fail(FSYRK_B200_EINVAL, "host entry point called with device memory (use fsyrk_b200_syrk_dev)");
     std::lock_guard<std::mutex> lk(g_stage_mu);
@@ -1784,7 +1855,7 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
     }
     if (!duplex) {
         if (need_c) ck(hio::upload(c, ldc, hio::Region{n, n, true}, dc, n, bits, s, &h2d), "H2D C");
-        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, ops);
+        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, (uint32_t)(beta % p), dc, n, pol, mirror, s, nullptr);
         if (io_trace) {
             ck(cudaStreamSynchronize(s), "sync");
             tr[2] = tnow();
@@ -1799,7 +1870,7 @@ void run_host(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, size_t k,
             ck(cudaStreamWaitEvent(g_io.cin, g_io.a_done, 0), "wait");
             queue_cin();
         }
-        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, 0, dx, n, pol, false, s, ops);
+        run_dev(p, (uint32_t)(alpha % p), da, n, k, lda_dev, xf, 0, dx, n, pol, false, s, nullptr);
         if (io_trace) {
             ck(cudaStreamSynchronize(s), "sync");
             tr[2] = tnow();
@@ -1846,6 +1917,7 @@ void run_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint
         fail(FSYRK_B200_EINVAL, "syrk_fast: C must not alias A");
     require_device();
     if (n == 0) return;
+    TallyOnSuccess tally{ops, ops ? ref_tally_fp2(n, k, pol) : refops::Tally{}};
     host::Field f{p};
     const uint64_t ns = f.lqnr();
     std::lock_guard<std::mutex> lk(g_stage_mu);
@@ -1873,7 +1945,7 @@ void run_fp2(uint64_t p, const uint64_t* a, size_t n, size_t k, size_t lda, uint
         std::vector<uint64_t> dbar(2 * k, 1);
         for (size_t j = k; j < 2 * k; ++j) dbar[j] = conj ? p - ns : ns;
         fold_diagonal(p, std::move(dbar), xf.map);
-        run_dev(p, 1, A, n, 2 * k, 2 * k, &xf, 0, R, n, pol, false, s, ops);
+        run_dev(p, 1, A, n, 2 * k, 2 * k, &xf, 0, R, n, pol, false, s, nullptr);
         // imaginary part: G = Y X^T
         ck(launch_deinterleave(A, (long long)k, (int)n, (int)k, static_cast<uint64_t*>(dX.ptr),
                                static_cast<uint64_t*>(dY.ptr), s),
@@ -2311,6 +2383,52 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
         validate_field(p);
         const ColXform xf = xform_diag(p, d, d ? k : 0);
         run_host(p, alpha, a, n, k, lda, &xf, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_opcount_syrk(uint64_t p, size_t n, size_t k, uint64_t alpha, uint64_t beta, fsyrk_b200_policy policy,
+                            fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (!ops) fail(FSYRK_B200_EINVAL, "null opcount");
+        add_tally(ops, ref_tally(p, n, k, policy, alpha, beta, nullptr));
+    });
+}
+
+int fsyrk_b200_opcount_syrkd(uint64_t p, size_t n, size_t k, const uint64_t* d, uint64_t alpha, uint64_t beta,
+                             fsyrk_b200_policy policy, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (!ops) fail(FSYRK_B200_EINVAL, "null opcount");
+        if (!d && k > 0) fail(FSYRK_B200_EDIMENSION, "syrkd: diagonal length must match column count");
+        const ColXform xf = xform_diag(p, d, d ? k : 0);
+        add_tally(ops, ref_tally(p, n, xf.map.size(), policy, alpha, beta, &xf));
+    });
+}
+
+int fsyrk_b200_opcount_syrkbd(uint64_t p, size_t n, const fsyrk_b200_block* blocks, size_t nblocks, uint64_t alpha,
+                              uint64_t beta, fsyrk_b200_policy policy, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (!ops) fail(FSYRK_B200_EINVAL, "null opcount");
+        if (!blocks && nblocks) fail(FSYRK_B200_EINVAL, "syrkbd: null block list");
+        size_t k = 0;
+        for (size_t i = 0; i < nblocks; ++i) k += blocks[i].two ? 2 : 1;
+        const ColXform xf = xform_blocks(p, blocks, nblocks, k);
+        add_tally(ops, ref_tally(p, n, xf.map.size(), policy, alpha, beta, &xf));
+    });
+}
+
+int fsyrk_b200_opcount_fp2(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, fsyrk_b200_opcount* ops) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        if (p == 2) fail(FSYRK_B200_EINVAL, "QuadExtField requires an odd prime");
+        if (!ops) fail(FSYRK_B200_EINVAL, "null opcount");
+        add_tally(ops, ref_tally_fp2(n, k, policy));
     });
 }
 

@@ -96,7 +96,8 @@ EXPORTS = (
     "fsyrk_b200_herk_fast_into", "fsyrk_b200_syrk_fast_into_fp2", "fsyrk_b200_gemm_winograd_nt",
     "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip", "fsyrk_b200_upload", "fsyrk_b200_download",
     "fsyrk_b200_syrk_mgpu", "fsyrk_b200_nccl_unique_id", "fsyrk_b200_comm_init_rank", "fsyrk_b200_comm_destroy",
-    "fsyrk_b200_syrk_mgpu_rank", "fsyrk_b200_share_pairs",
+    "fsyrk_b200_syrk_mgpu_rank", "fsyrk_b200_share_pairs", "fsyrk_b200_opcount_syrk", "fsyrk_b200_opcount_syrkd",
+    "fsyrk_b200_opcount_syrkbd", "fsyrk_b200_opcount_fp2",
 )
 
 
@@ -115,6 +116,14 @@ def lib() -> ctypes.CDLL:
     L.fsyrk_b200_skew_orthogonal.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.POINTER(_Skew)]
     L.fsyrk_b200_random_matrix.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                            _u64p, ctypes.c_size_t]
+    L.fsyrk_b200_opcount_syrk.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
+                                          ctypes.c_uint64, _Policy, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_opcount_syrkd.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64,
+                                           ctypes.c_uint64, _Policy, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_opcount_syrkbd.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.POINTER(_Block), ctypes.c_size_t,
+                                            ctypes.c_uint64, ctypes.c_uint64, _Policy, ctypes.POINTER(_OpCount)]
+    L.fsyrk_b200_opcount_fp2.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _Policy,
+                                         ctypes.POINTER(_OpCount)]
     L.fsyrk_b200_syrk_fast_into.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_size_t, ctypes.c_size_t,
                                             ctypes.c_size_t, _u64p, ctypes.c_size_t, _Policy, ctypes.c_int,
                                             ctypes.POINTER(_OpCount)]
@@ -630,6 +639,30 @@ def level_blocks(f: PrimeField, a: np.ndarray):
     S = [np.ascontiguousarray(s.reshape(-1)[: h * kw].reshape(h, kw)) for s in S]
     return {"S1": S[0], "S2": S[1], "S3": S[2], "S4": S[3],
             "P1": P[0], "P2": P[1], "P3": P[2], "P4": P[3], "P5": P[4], "kw": kw}
+
+
+def reference_opcount(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None, alpha: int = 1, beta: int = 0,
+                      d: Optional[Sequence[int]] = None, blocks: Optional[BlockDiagonal] = None,
+                      fp2: bool = False) -> OpCount:
+    """The OpCount the reference adds for one call (host only, no device): syrk_fast_into /
+    syrk_fast_acc (fast_syrk.hpp:274-303), syrkd with `d` (scaled_syrk.hpp:58-104), syrkbd with
+    `blocks` (:117-159), or herk/syrk over F_{p^2} with fp2=True (fast_syrk.hpp:305-320).
+    The library's entry points fill their `ops` argument with exactly this."""
+    pol = (policy or RecursionPolicy())._c()
+    c = _OpCount()
+    if fp2:
+        _check(lib().fsyrk_b200_opcount_fp2(int(p), int(n), int(k), pol, ctypes.byref(c)))
+    elif blocks is not None:
+        arr = blocks._c()
+        _check(lib().fsyrk_b200_opcount_syrkbd(int(p), int(n), arr, len(blocks.blocks), int(alpha), int(beta), pol,
+                                               ctypes.byref(c)))
+    elif d is not None:
+        dv = np.ascontiguousarray(np.asarray(d, dtype=np.uint64))
+        _check(lib().fsyrk_b200_opcount_syrkd(int(p), int(n), len(dv), dv.ctypes.data_as(_u64p), int(alpha),
+                                              int(beta), pol, ctypes.byref(c)))
+    else:
+        _check(lib().fsyrk_b200_opcount_syrk(int(p), int(n), int(k), int(alpha), int(beta), pol, ctypes.byref(c)))
+    return OpCount(int(c.mults), int(c.adds))
 
 
 def last_launch_counts() -> dict:

@@ -12,6 +12,7 @@
 #include <random>
 #include <stdexcept>
 
+#include "fsyrk/count_model.hpp"
 #include "fsyrk/fast_syrk.hpp"
 #include "fsyrk/scaled_syrk.hpp"
 #define FSYRK_B200_OVERRIDE
@@ -45,6 +46,9 @@ int main() {
             auto dev = syrk_fast(f, a.view(), plan, o1);                 // resolves to the B200 overload
             auto ref = syrk_fast<PrimeField>(f, a.view(), plan, o2);     // the reference template
             CHECK(lower_equal(f, dev.view(), ref.view()), "syrk_fast p=%llu n=%zu k=%zu", (unsigned long long)p, n, k);
+            CHECK(o1 == o2, "syrk_fast OpCount p=%llu n=%zu k=%zu: %llu/%llu vs %llu/%llu", (unsigned long long)p, n, k,
+                  (unsigned long long)o1.mults, (unsigned long long)o1.adds, (unsigned long long)o2.mults,
+                  (unsigned long long)o2.adds);
         }
     }
     // 2. accumulating form with random alpha, beta
@@ -58,10 +62,11 @@ int main() {
             auto c0 = random_matrix(f, n, n, r2());
             auto c1 = c0, c2 = c0;
             auto plan = make_syrk_plan(f, {2, kUnlimitedLevels});
-            OpCount ops;
-            syrk_fast_acc(f, alpha, a.view(), beta, c1.view(), plan, ops);
-            syrk_fast_acc<PrimeField>(f, alpha, a.view(), beta, c2.view(), plan, ops);
+            OpCount o1, o2;
+            syrk_fast_acc(f, alpha, a.view(), beta, c1.view(), plan, o1);
+            syrk_fast_acc<PrimeField>(f, alpha, a.view(), beta, c2.view(), plan, o2);
             CHECK(lower_equal(f, c1.view(), c2.view()), "syrk_fast_acc n=%zu k=%zu", n, k);
+            CHECK(o1 == o2, "syrk_fast_acc OpCount n=%zu k=%zu", n, k);
         }
     }
     // 3. syrkd through the shim vs the reference's syrkd
@@ -74,10 +79,11 @@ int main() {
             auto a = random_matrix(f, m, n, r3());
             std::vector<PrimeField::Element> d(n);
             for (auto& v : d) v = f.random_element(r3);
-            OpCount ops;
-            auto dev = fsyrk_b200::syrkd(f, a.view(), d, plan, ops);
-            auto ref = syrkd<PrimeField>(f, a.view(), d, plan, ops);
+            OpCount o1, o2;
+            auto dev = fsyrk_b200::syrkd(f, a.view(), d, plan, o1);
+            auto ref = syrkd<PrimeField>(f, a.view(), d, plan, o2);
             CHECK(lower_equal(f, dev.view(), ref.view()), "syrkd p=%llu m=%zu n=%zu", (unsigned long long)p, m, n);
+            CHECK(o1 == o2, "syrkd OpCount p=%llu m=%zu n=%zu", (unsigned long long)p, m, n);
         }
     }
     // 3b. syrkbd through the shim vs the reference's syrkbd (random block structures,
@@ -100,10 +106,11 @@ int main() {
                 }
             }
             auto a = random_matrix(f, m, dim, r4());
-            OpCount ops;
-            auto dev = fsyrk_b200::syrkbd(f, a.view(), b, plan, ops);
-            auto ref = syrkbd<PrimeField>(f, a.view(), b, plan, ops);
+            OpCount o1, o2;
+            auto dev = fsyrk_b200::syrkbd(f, a.view(), b, plan, o1);
+            auto ref = syrkbd<PrimeField>(f, a.view(), b, plan, o2);
             CHECK(lower_equal(f, dev.view(), ref.view()), "syrkbd p=%llu m=%zu k=%zu", (unsigned long long)p, m, dim);
+            CHECK(o1 == o2, "syrkbd OpCount p=%llu m=%zu k=%zu", (unsigned long long)p, m, dim);
         }
         BlockDiagonal<PrimeField> bad;
         bad.blocks.push_back(BlockDiagonal<PrimeField>::two_by_two(1, 1));
@@ -125,11 +132,36 @@ int main() {
             const std::size_t n = 1 + r5() % 70, k = 1 + r5() % 50;
             auto a = random_matrix(f, n, k, r5());
             auto plan = make_herk_plan(f, {4, kUnlimitedLevels}, t % 2 == 1);
-            OpCount ops;
-            auto dev = fsyrk_b200::herk_fast(f, a.view(), plan, ops);
-            auto ref = herk_fast(f, a.view(), plan, ops);
+            OpCount o1, o2;
+            auto dev = fsyrk_b200::herk_fast(f, a.view(), plan, o1);
+            auto ref = herk_fast(f, a.view(), plan, o2);
             CHECK(lower_equal(f, dev.view(), ref.view()), "herk_fast p=%llu n=%zu k=%zu", (unsigned long long)p, n, k);
+            CHECK(o1 == o2, "herk_fast OpCount p=%llu n=%zu k=%zu", (unsigned long long)p, n, k);
         }
+    }
+    // 3d. the reference's count-model reconciliation through the drop-in
+    //     (test_fast_syrk.cpp:202-238, the `count` command of tools/fsyrk.cpp:215-242)
+    for (std::uint64_t p : {5ull, 13ull, 11ull, 19ull, 7ull, 23ull}) {
+        PrimeField f(p);
+        const int y = skew_orthogonal(f, 0).ycost;
+        for (std::size_t n : {4u, 8u, 16u, 32u})
+            for (unsigned rec : {1u, 2u}) {
+                if (n < (std::size_t{2} << rec)) continue;
+                auto a = random_matrix(f, n, n, n * 10 + rec);
+                OpCount ops;
+                auto c = syrk_fast(f, a.view(), make_syrk_plan(f, {2, rec}), ops);  // the B200 overload
+                (void)c;
+                const std::uint64_t expect = count({CountAlg::FastSyrk, n, rec, y, HalfAddConvention::Triangular});
+                CHECK(ops.total() == expect, "count model p=%llu n=%zu rec=%u: %llu vs %llu", (unsigned long long)p, n,
+                      rec, (unsigned long long)ops.total(), (unsigned long long)expect);
+            }
+    }
+    {
+        PrimeField f(5);
+        auto a = random_matrix(f, 4, 4, 1);
+        OpCount ops;
+        syrk_fast(f, a.view(), make_syrk_plan(f, {2, 1}), ops);
+        CHECK(ops.total() == 92, "hand-counted cell: %llu", (unsigned long long)ops.total());
     }
     // 4. error convention: aliased output and bad policy throw std::invalid_argument
     {

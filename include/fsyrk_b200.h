@@ -296,6 +296,14 @@ int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m,
                                     const uint64_t* b_dev, size_t n, size_t ldb, uint64_t* c_dev, size_t ldc,
                                     fsyrk_b200_policy policy, void* stream);
 
+/* Device memory a call needs, without allocating it (host only): the plan's workspace
+ * (`arena`: digit-plane operands, product outputs, node outputs; cached per shape) and, for
+ * the host entry points, the workspace plus the device staging of A and C
+ * (`host_call`).  Either output may be NULL.  A workspace the device cannot hold makes the
+ * call fail with FSYRK_B200_ECUDA and the byte count in fsyrk_b200_last_error(). */
+int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, uint64_t* arena,
+                               uint64_t* host_call);
+
 /* ------------------------------------------------ reference op tallies (host only) */
 
 /* The OpCount the reference's entry point adds for one call, without running it

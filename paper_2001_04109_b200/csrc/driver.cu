@@ -345,6 +345,12 @@ struct Plan {
     uint64_t ew_adds = 0;
     uint64_t prep_bytes = 0, post_bytes = 0, post_cin_bytes = 0, convert_bytes = 0;  // algorithmic HBM bytes
 
+    // fused subtree pre-additions (prep_tree_kernel): depth of the complete uniform tree read in
+    // one launch from the caller's A (0: per-depth launches)
+    int tree_depth = 0;
+    PrepTreeArgs tree_args{};
+    PrepNode* tree_dev = nullptr;  // depth-ordered PrepNode tables in tree order
+
     // side stream + events: the top level's general products overlap the deeper pre/post-additions
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -370,6 +376,7 @@ struct Plan {
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (tree_dev) cudaFree(tree_dev);
     }
 
     int build(int n_, int k_, uint64_t levels, int depth, int parent, int role) {
@@ -437,8 +444,9 @@ struct Plan {
         return (int)gemms.size() - 1;
     }
 
+    // dry: lay out the plan and its arena (arena_bytes) without touching the device
     void create(uint64_t p_, int n_, int kin_, int k_, fsyrk_b200_policy pol, bool colmap_, int rank_ = 0,
-                int nranks_ = 1) {
+                int nranks_ = 1, bool dry = false) {
         p = p_;
         n = n_;
         kin = kin_;
@@ -642,7 +650,8 @@ struct Plan {
         std::vector<size_t> off_x(nodes.size(), 0), off_s3(nodes.size(), 0);
         for (size_t i = 0; i < nodes.size(); ++i) {
             Node& nd = nodes[i];
-            if (nd.kind != LEAF) off_x[i] = ar.take((size_t)nd.n * nd.n * 4);
+            // node outputs X; a LEVEL root's post-addition writes the caller's C directly (no X)
+            if (nd.kind != LEAF && !(i == 0 && nd.kind == LEVEL)) off_x[i] = ar.take((size_t)nd.n * nd.n * 4);
             if (nd.kind == LEVEL && nodes[nd.ch[2]].kind != LEAF) off_s3[i] = ar.take((size_t)nd.h * nd.kw * 4);
         }
         // prep / post groups
@@ -698,7 +707,13 @@ struct Plan {
 
         // ---- allocate and clear (the zero padding of every operand plane is never rewritten)
         arena_bytes = ar.size;
-        ck(cudaMalloc(&arena, arena_bytes), "cudaMalloc(plan arena)");
+        if (dry) return;
+        if (cudaMalloc(&arena, arena_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            arena = nullptr;
+            fail(FSYRK_B200_ECUDA, "cudaMalloc(plan arena of " + std::to_string(arena_bytes) +
+                                       " bytes) failed: out of device memory (fsyrk_b200_workspace_bytes reports it)");
+        }
         ck(cudaMemset(arena, 0, arena_bytes), "cudaMemset(plan arena)");
         if (colmap) {
             root_in = reinterpret_cast<uint32_t*>(arena + off_root_in);
@@ -786,6 +801,9 @@ struct Plan {
                 LeafGroup& lg = leaves[nd.lgroup];
                 nd.x = lg.xout + (long long)nd.lslot * nd.n * nd.n;
                 nd.ldx = nd.n;
+            } else if (i == 0 && nd.kind == LEVEL) {
+                nd.x = nullptr;  // the root post writes the caller's C
+                nd.ldx = 0;
             } else {
                 nd.x = reinterpret_cast<uint32_t*>(arena + off_x[i]);
                 nd.ldx = nd.n;
@@ -816,6 +834,7 @@ struct Plan {
             }
         }
         // prep node tables
+        std::vector<PrepNode> host_prep(nodes.size());
         for (auto& pg : preps) {
             const Node& n0 = nodes[pg.nodes[0]];
             GemmGroup& gg = gemms[n0.ggroup];
@@ -883,6 +902,7 @@ struct Plan {
                 pn.r_s3 = nd.s3res;
                 pn.ld_s3 = nd.lds3;
                 tab.push_back(pn);
+                host_prep[ni] = pn;
             }
             pg.dev_nodes = reinterpret_cast<PrepNode*>(arena + pg.off_nodes);
             a.nodes = pg.dev_nodes;
@@ -890,6 +910,7 @@ struct Plan {
             ck(cudaMemcpy(pg.dev_nodes, tab.data(), tab.size() * sizeof(PrepNode), cudaMemcpyHostToDevice),
                "upload prep table");
         }
+        setup_tree_prep(host_prep);
         for (auto& pg : posts) {
             if (pg.kind == LEVEL) {
                 std::vector<PostNode> tab;
@@ -962,12 +983,13 @@ struct Plan {
         for (const Node& nd : nodes) {
             if (nd.kind == LEVEL) {
                 const uint64_t h = nd.h, kh = nd.kh, kw = nd.kw;
-                prep_bytes += (uint64_t)nd.n * nd.k * (nd.in64 ? 8 : 4);        // the four quadrants
+                // the four quadrants (the fused subtree prep reads only the root's, from the caller)
+                if (!tree_depth || nd.parent < 0) prep_bytes += (uint64_t)nd.n * nd.k * (nd.in64 ? 8 : 4);
                 prep_bytes += 2 * h * kw * (uint64_t)(sch.pa + sch.pb);          // S1, A22 / S2, S4 planes
                 for (int c = 0; c < 3; ++c) {
                     const Node& ch = nodes[nd.ch[c]];
                     if (ch.kind == LEAF) prep_bytes += h * (uint64_t)ch.k * L;   // leaf operand planes
-                    else if (c == 2) prep_bytes += h * kw * 4;                    // S3 residues
+                    else if (c == 2 && !tree_depth) prep_bytes += h * kw * 4;     // S3 residues
                 }
                 post_bytes += 3 * lower(h) * 4 + 2 * h * h * 4;                  // P1, P2, P5 (lower), P3, P4
             } else if (nd.kind == SPLITK) {
@@ -1003,6 +1025,74 @@ struct Plan {
               << ", \"count\": " << gemms[i].count << "}";
         o << "], \"prep_groups\": " << preps.size() << ", \"post_groups\": " << posts.size() << "}";
         return o.str();
+    }
+
+    // One launch for all pre-additions when the tree is complete and uniform below the root
+    // (every node at depth d < D a LEVEL node of the same shape, unpadded; all depth-D nodes
+    // leaves) and the root reads the caller's A; D = 2 or 3 (registers: 4^D fine blocks per
+    // thread).  FSYRK_B200_TREE_PREP=0 keeps the per-depth launches.
+    void setup_tree_prep(const std::vector<PrepNode>& host_prep) {
+        static const bool want = [] {
+            const char* e = getenv("FSYRK_B200_TREE_PREP");
+            return !(e && atoi(e) == 0);
+        }();
+        tree_depth = 0;
+        if (!want || colmap || partitioned || idle || nodes.empty() || nodes[0].kind != LEVEL || !nodes[0].in64 ||
+            !split_leaves.empty())
+            return;
+        std::vector<std::vector<int>> lv(1, std::vector<int>{0});
+        int D = 0;
+        for (;;) {
+            const std::vector<int>& cur = lv.back();
+            const Node& f0 = nodes[cur[0]];
+            bool all_level = true, all_leaf = true;
+            for (int i : cur) {
+                const Node& nd = nodes[i];
+                all_level &= nd.kind == LEVEL && !nd.padded && nd.n == f0.n && nd.k == f0.k;
+                all_leaf &= nd.kind == LEAF && nd.n == f0.n && nd.k == f0.k;
+            }
+            if (all_leaf) break;
+            if (!all_level || lv.size() > 3) return;
+            std::vector<int> next;
+            for (int i : cur)
+                for (int r = 0; r < 3; ++r) next.push_back(nodes[i].ch[r]);
+            lv.push_back(next);
+            ++D;
+        }
+        if (D < 2 || D > 3) return;
+        const Node& leaf = nodes[lv[D][0]];
+        if (leaf.n != (n >> D) || leaf.k != (k >> D) || leaf.n * (1 << D) != n || leaf.k * (1 << D) != k) return;
+        const int ncol = y.form == 1 ? leaf.k / 2 : leaf.k;  // columns (pairs) of the fine block
+        if ((y.form == 1 && leaf.k % 2 != 0) || ncol % 4 != 0) return;
+        int cp = 32;  // kTreeCP (elementwise.cu)
+        while (ncol % cp) cp /= 2;
+        PrepTreeArgs& a = tree_args;
+        a = PrepTreeArgs{};
+        a.m = m;
+        a.L = sch.id;
+        a.depth = D;
+        a.rows = leaf.n;
+        a.w = leaf.k;
+        a.cp = cp;
+        a.pair = y.form == 1;
+        a.cya = make_mulconst((uint32_t)y.a, (uint32_t)p);
+        a.cyb = make_mulconst((uint32_t)y.b, (uint32_t)p);
+        a.c_plane = leaves[leaf.lgroup].plane;
+        a.c_row = leaves[leaf.lgroup].kpad;
+        std::vector<PrepNode> tab;
+        std::vector<size_t> start;
+        for (int d = 0; d < D; ++d) {
+            const GemmGroup& gg = gemms[nodes[lv[d][0]].ggroup];
+            a.g_plane[d] = gg.plane;
+            a.g_row[d] = gg.kpad;
+            start.push_back(tab.size());
+            for (int i : lv[d]) tab.push_back(host_prep[i]);
+        }
+        ck(cudaMalloc(&tree_dev, tab.size() * sizeof(PrepNode)), "cudaMalloc(tree prep table)");
+        ck(cudaMemcpy(tree_dev, tab.data(), tab.size() * sizeof(PrepNode), cudaMemcpyHostToDevice),
+           "upload tree prep table");
+        for (int d = 0; d < D; ++d) a.nodes[d] = tree_dev + start[d];
+        tree_depth = D;
     }
 
     void execute(const uint64_t* a_dev, long long lda, uint64_t* c_dev, long long ldc, uint32_t alpha,
@@ -1144,7 +1234,15 @@ struct Plan {
             mark(4);
         } else if (!overlap) {
             // 3. fused pre-additions, top-down; 4. products; 5. post-additions, bottom-up
-            for (auto& pg : preps) run_prep(pg, s);
+            if (tree_depth) {
+                PrepTreeArgs a = tree_args;
+                a.a64 = a_dev;
+                a.ld64 = lda;
+                traced("prep tree", s, [&] { ck(launch_prep_tree(a, nsm, s), "prep tree"); });
+                counts[1]++;
+            } else {
+                for (auto& pg : preps) run_prep(pg, s);
+            }
             mark(2);
             for (auto& pl : prods) run_prod(pl, s);
             mark(3);
@@ -2383,6 +2481,24 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
         validate_field(p);
         const ColXform xf = xform_diag(p, d, d ? k : 0);
         run_host(p, alpha, a, n, k, lda, &xf, beta, c, ldc, policy, mirror_output != 0, ops);
+    });
+}
+
+int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, uint64_t* arena,
+                               uint64_t* host_call) {
+    return guarded([&] {
+        validate_field(p);
+        validate_policy(policy);
+        validate_shapes(n, k, k, n);
+        uint64_t bytes = 0;
+        if (n > 0 && k > 0) {
+            Plan plan;
+            plan.create(p, (int)n, (int)k, (int)k, policy, false, 0, 1, true);
+            bytes = plan.arena_bytes;
+        }
+        if (arena) *arena = bytes;
+        // host entry points also stage A and C on the device as uint64 rows
+        if (host_call) *host_call = bytes + (uint64_t)n * k * 8 + (uint64_t)n * n * 8;
     });
 }
 

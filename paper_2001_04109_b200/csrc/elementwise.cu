@@ -28,10 +28,12 @@
 // 4-byte packed limb stores); scalar variants cover unaligned shapes.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "elementwise.cuh"
 #include "pdl.cuh"
+#include "per_device.h"
 
 namespace fsyrk_b200 {
 
@@ -40,6 +42,9 @@ namespace fsyrk_b200 {
 #endif
 #ifndef FSYRK_CONVERT_ROWS
 #define FSYRK_CONVERT_ROWS 1  // rows per iteration of the conversion (4: 0.161 vs 0.149 ms on cfg5)
+#endif
+#ifndef FSYRK_TREE_MINB
+#define FSYRK_TREE_MINB 5  // fused subtree prep: blocks per SM the registers must allow
 #endif
 #ifndef FSYRK_POST_MINB
 #define FSYRK_POST_MINB 6  // measured: cfg2 post 60 -> 55 us, cfg5 2.53 -> 2.13 ms
@@ -389,6 +394,186 @@ __global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const Pr
     const PrepNode local = nd;
     if (local.in.in64) prep_vec_body<S, PAIR, true>(args, local, i, g);
     else prep_vec_body<S, PAIR, false>(args, local, i, g);
+}
+
+// ------------------------------------------------------------ prep (fused subtree)
+// All D levels of a complete uniform subtree in one pass over the caller's uint64 A
+// (fast_syrk.hpp:100-115 at every node).  A CTA owns CP consecutive columns c0 .. c0 + CP of
+// one row r of the leaf-sized fine block (in Pair form also their partners c + w/2: Y pairs
+// columns half a quadrant apart at every level, so the partners of a CTA's columns are again
+// its own columns) and stages their values in all 4^D fine blocks of A in shared memory.  Each
+// level then forms S1..S4 of all its nodes from shared memory, writes the GEMM operands as
+// digit planes (4 columns per thread, packed 4-byte stores) and hands A11, A12, S3 to the
+// children in shared memory; the deepest level writes the leaf operands.  Compared with one
+// launch per depth this drops the uint32 S3 residues of every non-leaf child (written once,
+// read once) and the small latency-bound launches of the deep levels.
+//
+// Shared layout of level d (node t of 3^d, B = 2^(D-d) fine blocks per side, NC = 2 in Pair
+// form): buf[((t * B + bi) * (B * NC) + v) * CP + cp], v = bj * NC + e the "virtual column"
+// (fine block column bj, half e).  A quadrant is a half in each direction; the Pair partner of
+// virtual column v (< V/2) of a V-wide quadrant is v + V/2.  Levels alternate between two
+// buffers (level 0 and 2 in one, level 1 in the other).
+constexpr int kTreeCP = 32;       // columns (column pairs) per CTA (at most)
+constexpr int kTreeThreads = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+
+// One level d of the fused subtree: every node's S1..S4 from shared memory (level 0: the raw
+// uint64 input), GEMM operand planes to HBM, children's inputs (or leaf operand planes) out.
+// Everything but the column-group count is compile-time (powers of two: shifts and masks).
+template <int S, bool PAIR, int D, int d>
+__device__ __forceinline__ void tree_level(const PrepTreeArgs& a, const uint64_t* raw, const uint32_t* in,
+                                           uint32_t* out, int r, int c0, int CP, int lgG) {
+    constexpr int NC = PAIR ? 2 : 1, NU = PAIR ? 2 : 1;
+    constexpr int PA = Scheme<S>::PA, PB = Scheme<S>::PB;
+    constexpr int Bq = 1 << (D - d - 1), B = 2 * Bq;  // quadrant / node size in fine blocks
+    constexpr int V = Bq * NC, W2 = 2 * V;            // virtual columns of a quadrant / of the node
+    constexpr int U = PAIR ? V / 2 : V;               // work columns per quadrant row
+    constexpr int NODES = d == 0 ? 1 : d == 1 ? 3 : 9;
+    constexpr bool last = d == D - 1;
+    const uint32_t p = a.m.p;
+    const ModP m = a.m;
+    const int half = a.w / 2, G = 1 << lgG;
+    const long long gp = a.g_plane[d], gr = a.g_row[d];
+    const int items = NODES * Bq * U << lgG;
+    for (int it = threadIdx.x; it < items; it += kTreeThreads) {
+        const int g = it & (G - 1);
+        const int rest = it >> lgG;
+        const int u = rest % U, qi = (rest / U) % Bq, t = rest / (U * Bq);
+        const PrepNode& nd = a.nodes[d][t];
+        uint4 a11[NU], a12[NU], a21[NU], a22[NU], s1[NU], ay[NU];
+        auto at = [&](int bi, int v) -> uint4 {
+            const int o = ((t * B + bi) * W2 + v) * CP + 4 * g;
+            if constexpr (d > 0) {
+                return *reinterpret_cast<const uint4*>(in + o);
+            } else {
+                // the caller's uint64 values: canonical residues are the contract (fields.hpp:32-36);
+                // reduce only the ones that are not
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(raw + o);
+                const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(raw + o + 2);
+                if ((x.x | x.y | y.x | y.y) >> 31 || x.x >= p || x.y >= p || y.x >= p || y.y >= p)
+                    return make_uint4(mod_u64(x.x, m), mod_u64(x.y, m), mod_u64(y.x, m), mod_u64(y.y, m));
+                return make_uint4((uint32_t)x.x, (uint32_t)x.y, (uint32_t)y.x, (uint32_t)y.y);
+            }
+        };
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            const int ue = u + e * (V / 2);
+            a11[e] = at(qi, ue);
+            a12[e] = at(qi, V + ue);
+            a21[e] = at(Bq + qi, ue);
+            a22[e] = at(Bq + qi, V + ue);
+        }
+        if constexpr (PAIR) {
+            pair_y4(sub4(a21[0], a11[0], p), sub4(a21[1], a11[1], p), a.cya, a.cyb, p, s1[0], s1[1]);
+            pair_y4(a21[0], a21[1], a.cya, a.cyb, p, ay[0], ay[1]);
+        } else {
+            s1[0] = mulc4(sub4(a21[0], a11[0], p), a.cya, p);
+            ay[0] = mulc4(a21[0], a.cya, p);
+        }
+        const long long row = (long long)qi * a.rows + r;
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            const int uu = u + e * (V / 2);
+            const uint4 s2 = sub4(a22[e], ay[e], p);
+            const uint4 s3 = sub4(s1[e], a22[e], p);
+            const uint4 s4 = add4(s3, a12[e], p);
+            const int cin = c0 + 4 * g + (uu % NC) * half;  // column inside the fine block
+            const long long go = row * gr + (long long)(uu / NC) * a.w + cin;
+            put_planes4<S, PA>(nd.s1, gp, go, s1[e], p);  // A-role: first PA planes
+            put_planes4<S, PA>(nd.a22, gp, go, a22[e], p);
+            put_planes4<S, PB>(nd.s2, gp, go, s2, p);  // B-role: first PB planes
+            put_planes4<S, PB>(nd.s4, gp, go, s4, p);
+            if constexpr (last) {  // children are leaves: all planes
+                const long long lo = (long long)r * a.c_row + cin;
+                put_planes4<S>(nd.c_a11, a.c_plane, lo, a11[e], p);
+                put_planes4<S>(nd.c_a12, a.c_plane, lo, a12[e], p);
+                put_planes4<S>(nd.c_s3, a.c_plane, lo, s3, p);
+            } else {  // child 3t + role (Bq x Bq blocks): virtual column uu of block row qi
+                const int o = (qi * V + uu) * CP + 4 * g;
+                const int cs = Bq * V * CP;  // one child's input
+                *reinterpret_cast<uint4*>(out + (3 * t + 0) * cs + o) = a11[e];
+                *reinterpret_cast<uint4*>(out + (3 * t + 1) * cs + o) = a12[e];
+                *reinterpret_cast<uint4*>(out + (3 * t + 2) * cs + o) = s3;
+            }
+        }
+    }
+}
+
+template <int S, bool PAIR, int D>
+__global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kernel(const PrepTreeArgs a) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
+    extern __shared__ __align__(16) uint32_t tsm[];
+    constexpr int NC = PAIR ? 2 : 1, B = 1 << D;
+    const int CP = a.cp, lgCP = 31 - __clz(CP);
+    const int r = blockIdx.y, c0 = blockIdx.x * CP;
+    const int half = a.w / 2;
+    // buffer 0: the root's raw uint64 input, later level 2; buffer 1: level 1
+    constexpr int kSegs = B * B * NC;
+    uint64_t* raw = reinterpret_cast<uint64_t*>(tsm);
+    uint32_t* buf1 = tsm + 2 * (kSegs << lgCP);
+    {
+        // every 16-byte chunk of the CTA's 4^D x NC segments of CP columns in flight at once
+        const int chunks = (kSegs << lgCP) / 2;
+        for (int ch = threadIdx.x; ch < chunks; ch += kTreeThreads) {
+            const int idx = 2 * ch, cp = idx & (CP - 1), seg = idx >> lgCP;
+            const int v = seg % (B * NC), bi = seg / (B * NC);
+            const long long row = (long long)bi * a.rows + r;
+            const long long col = (long long)(v / NC) * a.w + c0 + cp + (v % NC) * half;
+            cp_async16(raw + idx, a.a64 + row * a.ld64 + col);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    const int lgG = lgCP - 2;
+    tree_level<S, PAIR, D, 0>(a, raw, nullptr, D > 1 ? buf1 : nullptr, r, c0, CP, lgG);
+    if constexpr (D > 1) {
+        __syncthreads();
+        tree_level<S, PAIR, D, (D > 1 ? 1 : 0)>(a, nullptr, buf1, tsm, r, c0, CP, lgG);
+    }
+    if constexpr (D > 2) {
+        __syncthreads();
+        tree_level<S, PAIR, D, (D > 2 ? 2 : 0)>(a, nullptr, tsm, nullptr, r, c0, CP, lgG);
+    }
+}
+
+size_t prep_tree_smem(int D, bool pair, int cp) {
+    const size_t nc = pair ? 2 : 1;
+    // buffer 0: the root's uint64 input (4^D blocks; level 2's 9 x 4^(D-2) uint32 blocks fit in
+    // it); buffer 1: level 1 = 3 * 4^(D-1) blocks of uint32
+    return ((size_t)1 << (2 * D)) * nc * cp * 8 + 3 * ((size_t)1 << (2 * (D - 1))) * nc * cp * 4;
+}
+
+template <int S, bool PAIR, int D>
+struct TreeAttrOnce : DeviceOnce {};
+
+template <int S>
+cudaError_t prep_tree_dispatch(const PrepTreeArgs& a, int nsm, cudaStream_t s) {
+    (void)nsm;
+    const bool pair = a.pair != 0;
+    const int nc = pair ? 2 : 1;
+    if (a.cp < 4 || a.cp > kTreeCP || (a.cp & (a.cp - 1)) || (a.w / nc) % a.cp || (pair && a.w % 2) ||
+        a.depth < 2 || a.depth > 3)
+        return cudaErrorInvalidValue;
+    const size_t smem = prep_tree_smem(a.depth, pair, a.cp);
+    dim3 grid(a.w / nc / a.cp, a.rows);
+    auto kern = a.depth == 3 ? (pair ? prep_tree_kernel<S, true, 3> : prep_tree_kernel<S, false, 3>)
+                             : (pair ? prep_tree_kernel<S, true, 2> : prep_tree_kernel<S, false, 2>);
+    // thread-safe one-time setup per device (the attribute applies to the current device only)
+    DeviceOnce& once = a.depth == 3 ? (pair ? static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, true, 3>>())
+                                            : static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, false, 3>>()))
+                                     : (pair ? static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, true, 2>>())
+                                             : static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, false, 2>>()));
+    std::call_once(once.flag, [&] {
+        once.result = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_tree_smem(3, true, kTreeCP));
+    });
+    if (once.result != cudaSuccess) return once.result;
+    return launch_pdl(kern, grid, dim3(kTreeThreads), smem, s, a);
 }
 
 // ------------------------------------------------------------------ post
@@ -923,6 +1108,19 @@ cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s) {
         case SCHEME_M17: return prep_dispatch<SCHEME_M17>(args, s);
         case SCHEME_M17N: return prep_dispatch<SCHEME_M17N>(args, s);
         case SCHEME_M31: return prep_dispatch<SCHEME_M31>(args, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_prep_tree(const PrepTreeArgs& a, int nsm, cudaStream_t s) {
+    if (a.rows == 0 || a.w == 0) return cudaSuccess;
+    switch (a.L) {
+        case SCHEME_LIMB2: return prep_tree_dispatch<SCHEME_LIMB2>(a, nsm, s);
+        case SCHEME_LIMB3: return prep_tree_dispatch<SCHEME_LIMB3>(a, nsm, s);
+        case SCHEME_LIMB4: return prep_tree_dispatch<SCHEME_LIMB4>(a, nsm, s);
+        case SCHEME_M17: return prep_tree_dispatch<SCHEME_M17>(a, nsm, s);
+        case SCHEME_M17N: return prep_tree_dispatch<SCHEME_M17N>(a, nsm, s);
+        case SCHEME_M31: return prep_tree_dispatch<SCHEME_M31>(a, nsm, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -65,6 +65,25 @@ struct PrepArgs {
     unsigned long long need_mask;
 };
 
+// Fused pre-additions of a complete uniform subtree of D levels (D = 2, 3) read straight from
+// the caller's uint64 A: every LEVEL node at depth d < D has the same (h, kh), no padding, and
+// all nodes at depth D are leaves.  nodes[d] holds the depth-d PrepNode tables in tree order
+// (node t's children P1, P2, P5 are 3t, 3t + 1, 3t + 2 at depth d + 1).
+struct PrepTreeArgs {
+    ModP m;
+    int L;  // digit scheme
+    int depth;
+    const uint64_t* a64;  // caller's input (per call)
+    long long ld64;
+    int rows, w;  // fine block (the leaf operand): rows = n >> D, w = k >> D
+    int cp;       // columns (Pair: column pairs) per CTA: a multiple of 4 dividing w / NC, <= 64
+    int pair;
+    MulConst cya, cyb;
+    long long g_plane[4], g_row[4];  // GEMM operand plane / row stride per depth
+    long long c_plane, c_row;        // leaf operand planes (depth D)
+    const PrepNode* nodes[4];
+};
+
 struct PostNode {
     const uint32_t *p1, *p2, *p5, *p3, *p4;
     long long ld1, ld2, ld5, ld3, ld4;
@@ -106,6 +125,7 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
                                 uint32_t p, int8_t* planes, long long plane_stride, long long row_stride,
                                 cudaStream_t s);
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s);
+cudaError_t launch_prep_tree(const PrepTreeArgs& args, int nsm, cudaStream_t s);
 cudaError_t launch_post(const PostArgs& args, cudaStream_t s);
 cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p, cudaStream_t s);
 // C (uint64) <- alpha * X + beta * C on the lower triangle (X == nullptr: X = 0).

@@ -97,7 +97,7 @@ EXPORTS = (
     "fsyrk_b200_gemm_winograd_nt_dev", "fsyrk_b200_hostio_roundtrip", "fsyrk_b200_upload", "fsyrk_b200_download",
     "fsyrk_b200_syrk_mgpu", "fsyrk_b200_nccl_unique_id", "fsyrk_b200_comm_init_rank", "fsyrk_b200_comm_destroy",
     "fsyrk_b200_syrk_mgpu_rank", "fsyrk_b200_share_pairs", "fsyrk_b200_opcount_syrk", "fsyrk_b200_opcount_syrkd",
-    "fsyrk_b200_opcount_syrkbd", "fsyrk_b200_opcount_fp2",
+    "fsyrk_b200_opcount_syrkbd", "fsyrk_b200_opcount_fp2", "fsyrk_b200_workspace_bytes",
 )
 
 
@@ -116,6 +116,8 @@ def lib() -> ctypes.CDLL:
     L.fsyrk_b200_skew_orthogonal.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.POINTER(_Skew)]
     L.fsyrk_b200_random_matrix.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                            _u64p, ctypes.c_size_t]
+    L.fsyrk_b200_workspace_bytes.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _Policy,
+                                             ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     L.fsyrk_b200_opcount_syrk.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                           ctypes.c_uint64, _Policy, ctypes.POINTER(_OpCount)]
     L.fsyrk_b200_opcount_syrkd.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64,
@@ -639,6 +641,15 @@ def level_blocks(f: PrimeField, a: np.ndarray):
     S = [np.ascontiguousarray(s.reshape(-1)[: h * kw].reshape(h, kw)) for s in S]
     return {"S1": S[0], "S2": S[1], "S3": S[2], "S4": S[3],
             "P1": P[0], "P2": P[1], "P3": P[2], "P4": P[3], "P5": P[4], "kw": kw}
+
+
+def workspace_bytes(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None) -> dict:
+    """Device memory of a call without allocating it (host only): the plan's workspace and, for
+    the host entry points, workspace + device staging of A and C."""
+    ar, hc = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check(lib().fsyrk_b200_workspace_bytes(int(p), int(n), int(k), (policy or RecursionPolicy())._c(),
+                                            ctypes.byref(ar), ctypes.byref(hc)))
+    return {"arena": int(ar.value), "host_call": int(hc.value)}
 
 
 def reference_opcount(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None, alpha: int = 1, beta: int = 0,

@@ -1,0 +1,10 @@
+# fused subtree prep: tests, then cfg2 with and without it
+mkdir -p gpurun_out/r02
+timeout 300 python -m pytest tests/test_gpu_tree.py -x -q > gpurun_out/r02/tree_tests.log 2>&1; echo tree tests rc=$?; tail -3 gpurun_out/r02/tree_tests.log
+for t in 1 0; do
+  FSYRK_B200_TREE_PREP=$t timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02/bench_tree$t.json 2>gpurun_out/r02/bench_tree$t.err; echo bench tree=$t rc=$?
+  python -c "
+import json; d=json.load(open('gpurun_out/r02/bench_tree$t.json'))
+print('tree=$t', d['ms_per_step'], d['value'], d['parity'], d['roofline']['phase_ms'], d['roofline']['elementwise_hbm']['pre'])"
+done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02/pytest_gpu_tree.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/r02/pytest_gpu_tree.log

@@ -539,7 +539,8 @@ def main():
                              "reference_sample": cpu and cpu.get("sample")},
             "e2e": e2e, "e2e_pinned": e2e_pinned,
             "clocks": clocks, "plan": {k2: plan.get(k2) for k2 in ("scheme", "terms", "block_n", "nodes", "leaf_groups",
-                                                                     "gemm_groups", "arena_bytes")}}
+                                                                     "gemm_groups", "arena_bytes", "schedule", "tree_prep",
+                                                                     "winograd_groups")}}
     print(json.dumps(line))
     if world > 1 or part:
         dist.destroy_process_group()

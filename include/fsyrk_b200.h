@@ -297,12 +297,34 @@ int fsyrk_b200_gemm_winograd_nt_dev(uint64_t p, const uint64_t* a_dev, size_t m,
                                     fsyrk_b200_policy policy, void* stream);
 
 /* Device memory a call needs, without allocating it (host only): the plan's workspace
- * (`arena`: digit-plane operands, product outputs, node outputs; cached per shape) and, for
- * the host entry points, the workspace plus the device staging of A and C
- * (`host_call`).  Either output may be NULL.  A workspace the device cannot hold makes the
- * call fail with FSYRK_B200_ECUDA and the byte count in fsyrk_b200_last_error(). */
-int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, uint64_t* arena,
-                               uint64_t* host_call);
+ * (`arena`: digit-plane operands, product outputs, node outputs; cached per shape) under the
+ * wide (lowmem = 0) or the low-memory (lowmem = 1) schedule and, for the host entry points,
+ * the workspace plus the device staging of A and C (`host_call`).  Either output may be
+ * NULL.  A workspace the device cannot hold makes the call fail with FSYRK_B200_ECUDA and
+ * the byte count in fsyrk_b200_last_error(). */
+int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, int lowmem,
+                               uint64_t* arena, uint64_t* host_call);
+
+/* Process-wide workspace limit in bytes (0 = none, the default).  A call whose wide
+ * workspace exceeds it runs the low-memory schedule -- the reference's placement of the
+ * top level's general products in the scratch quadrant C12 of C (fast_syrk.hpp:96-98,
+ * 271-273): P4 and P3 go to the strict upper triangle of the caller's C (device C needs an
+ * even row stride and 16-byte alignment) instead of the workspace -- and one whose
+ * low-memory workspace still exceeds it fails with FSYRK_B200_EINVAL.  Results are
+ * identical; only the strict upper triangle of C (scratch, fast_syrk.hpp:271-273) differs. */
+int fsyrk_b200_set_workspace_limit(uint64_t bytes);
+
+/* Process-wide: enable = 1 runs every plan created afterwards (where a 2 x 2 top level
+ * exists) with the low-memory schedule regardless of the limit; 0 restores the default. */
+int fsyrk_b200_set_low_memory(int enable);
+
+/* Process-wide: the top level's two general products P4, P3 run Strassen-Winograd levels
+ * (the reference's gemm_winograd_nt_into inside the level, winograd.hpp:118-169, 195-202;
+ * levels while every dimension is even and at least max(threshold, min_dim, 256)) when
+ * min(h, kw) >= min_dim; below it they are direct tensor-core products (exact either way).
+ * Default 16384, the measured crossover on B200; 0 = never.  Applies to plans created
+ * afterwards (fsyrk_b200_release_cache drops cached ones). */
+int fsyrk_b200_set_winograd_min(uint64_t min_dim);
 
 /* ------------------------------------------------ reference op tallies (host only) */
 

@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <exception>
 #include <array>
@@ -216,6 +217,26 @@ std::vector<int> partition_owners(int h, int nranks, int kPartBlock) {
 // ------------------------------------------------------------------- plan
 enum Kind { LEAF = 0, LEVEL = 1, SPLITK = 2 };
 
+// One problem C = A B^T of the Strassen-Winograd engine (uint32 residue operands).
+struct WinoProblem {
+    const uint32_t* a;
+    long long lda;
+    const uint32_t* b;
+    long long ldb;
+    uint32_t* c;
+    long long ldc;
+};
+void wino_gemm_multi(uint64_t p, const std::vector<WinoProblem>& probs, size_t m, size_t n, size_t k,
+                     fsyrk_b200_policy pol, cudaStream_t s);
+
+// Smallest general product (min(h, kw)) of the top level that runs Strassen-Winograd levels
+// (fsyrk_b200_set_winograd_min; 0 = never).  Default 16384: the measured crossover on B200
+// (profiles/r01/winograd_ablation.txt); FSYRK_B200_WINOGRAD_MIN overrides it at load time.
+std::atomic<uint64_t> g_wino_min{[] {
+    const char* e = getenv("FSYRK_B200_WINOGRAD_MIN");
+    return e ? (uint64_t)atoll(e) : (uint64_t)16384;
+}()};
+
 struct Node {
     int kind = LEAF;
     int n = 0, k = 0, depth = 0;
@@ -258,6 +279,13 @@ struct GemmGroup {
     uint32_t* out = nullptr;
     CUtensorMap tA, tB;
     size_t off_ga = 0, off_gb = 0, off_out = 0;
+    // Strassen-Winograd general products (the reference's gemm_winograd_nt_into inside the
+    // level, winograd.hpp:118-169): operands as uint32 residues S1 | S2 | A22 | S4 (h x kw each)
+    // and the Winograd engine instead of the grouped product launch; wino = levels it may use
+    int wino = 0;
+    fsyrk_b200_policy wino_pol{0, 0};
+    uint32_t* res = nullptr;
+    size_t off_res = 0;
 };
 
 // One persistent grouped launch of the product kernel.
@@ -345,6 +373,13 @@ struct Plan {
     uint64_t ew_adds = 0;
     uint64_t prep_bytes = 0, post_bytes = 0, post_cin_bytes = 0, convert_bytes = 0;  // algorithmic HBM bytes
 
+    // low-memory schedule (fsyrk_b200_set_workspace_limit): the top level's two general products
+    // P4, P3 are written into the caller's C12 quadrant -- strict upper triangle, scratch in the
+    // reference too (fast_syrk.hpp:271-273), which also keeps its S blocks there (:96-98) --
+    // instead of the arena; the root post-addition reads them from there
+    bool lowmem = false;
+    const uint64_t* lm_c = nullptr;  // C the root group's output map was last encoded for
+    long long lm_ldc = 0;
     // fused subtree pre-additions (prep_tree_kernel): depth of the complete uniform tree read in
     // one launch from the caller's A (0: per-depth launches)
     int tree_depth = 0;
@@ -446,7 +481,7 @@ struct Plan {
 
     // dry: lay out the plan and its arena (arena_bytes) without touching the device
     void create(uint64_t p_, int n_, int kin_, int k_, fsyrk_b200_policy pol, bool colmap_, int rank_ = 0,
-                int nranks_ = 1, bool dry = false) {
+                int nranks_ = 1, bool dry = false, bool lowmem_ = false) {
         p = p_;
         n = n_;
         kin = kin_;
@@ -479,6 +514,8 @@ struct Plan {
                 idle = prank != 0;  // not partitionable: rank 0 computes everything
             }
         }
+        // the low-memory schedule applies to a single-rank plan whose top level is a 2 x 2 level
+        lowmem = lowmem_ && pnranks == 1 && nodes[0].kind == LEVEL && nodes[0].h % 4 == 0;
         // any K is exact: the product kernel drains its int32 accumulators mod p every
         // modmm_k_limit(sch, p) of K (chunk_blocks), like the reference's __int128 dot
         // products accept any k (matrix.hpp:144-160)
@@ -535,7 +572,31 @@ struct Plan {
             for (int tm = 0; tm * BMt < lg.n; ++tm)
                 for (int tn = 0; tn * BN < lg.n && tn * BN <= tm * BMt + BMt - 1; ++tn) ++lg.ntiles;
         }
+        // Winograd levels for the top level's general products where they pay: min(h, kw) of at
+        // least FSYRK_B200_WINOGRAD_MIN (default 16384, the measured crossover,
+        // profiles/r01/winograd_ablation.txt; 0 = wherever the reference's policy recurses)
+        {
+            const uint64_t wmin = g_wino_min.load();
+            const uint64_t next = pol.max_levels == UINT64_MAX ? UINT64_MAX : pol.max_levels - 1;
+            for (auto& gg : gemms) {
+                if (!gg.root || pnranks > 1 || next == 0 || wmin == 0) continue;
+                // base products of at least 128 (one tensor tile) below the last level
+                const uint64_t thr = std::max<uint64_t>({pol.threshold, wmin, 256});
+                if (gg.h % 2 == 0 && gg.kw % 2 == 0 && (uint64_t)std::min(gg.h, gg.kw) >= thr) {
+                    gg.wino = 1;
+                    gg.wino_pol = fsyrk_b200_policy{thr, next};
+                }
+            }
+        }
         for (auto& gg : gemms) {
+            if (gg.wino) {  // residue operands only; the engine keeps its own scratch
+                gg.hpad = gg.h;
+                gg.kpad = gg.kw;
+                gg.plane = gg.slot = gg.slot_b = 0;
+                gg.off_res = ar.take((size_t)4 * gg.count * gg.h * gg.kw * 4);
+                if (!(lowmem && gg.root)) gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
+                continue;
+            }
             gg.hpad = (int)round_up(gg.h, 128);
             gg.kpad = (int)round_up(gg.kw, 128);
             gg.plane = (long long)gg.hpad * gg.kpad;
@@ -543,7 +604,7 @@ struct Plan {
             gg.off_ga = ar.take((size_t)gg.slot * 2 * gg.count, 1024);
             gg.slot_b = gg.plane * sch.pb;
             gg.off_gb = ar.take((size_t)gg.slot_b * 2 * gg.count, 1024);
-            gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
+            if (!(lowmem && gg.root)) gg.off_out = ar.take((size_t)2 * gg.count * gg.h * gg.h * 4);
         }
         // product launches: every GEMM group and leaf group, kMaxGroups per persistent launch,
         // tiles (group, batch, tm, tn) ordered longest-K first
@@ -553,9 +614,9 @@ struct Plan {
             // FSYRK_B200_OVERLAP=1: launch the top level's products on their own, overlapped with
             // the deeper pre/post-additions (measured slower on cfg2: the elementwise kernels get
             // only the SM resources the persistent kernel leaves); default: one launch
-            static const bool split_root = getenv("FSYRK_B200_OVERLAP") != nullptr;
+            const bool split_root = getenv("FSYRK_B200_OVERLAP") != nullptr && !lowmem_;
             for (int i = 0; i < (int)gemms.size(); ++i)
-                pgs.push_back({false, i, gemms[i].kpad, gemms[i].root && split_root ? 0 : 1});
+                if (!gemms[i].wino) pgs.push_back({false, i, gemms[i].kpad, gemms[i].root && split_root ? 0 : 1});
             for (int i = 0; i < (int)leaves.size(); ++i) pgs.push_back({true, i, leaves[i].kpad, 1});
             std::stable_sort(pgs.begin(), pgs.end(), [](const PG& a, const PG& b) {
                 return a.phase != b.phase ? a.phase < b.phase : a.kpad > b.kpad;
@@ -605,7 +666,8 @@ struct Plan {
                 return e ? atoi(e) : 0;  // measured slower (profiles/r01/variants.txt): off
             }();
             const Node& r0 = nodes[0];
-            if (want > 1 && !partitioned && !idle && r0.kind == LEVEL && nodes[r0.ch[0]].kind == LEAF &&
+            const bool any_wino = std::any_of(gemms.begin(), gemms.end(), [](const GemmGroup& g) { return g.wino; });
+            if (want > 1 && !partitioned && !idle && !lowmem && !any_wino && r0.kind == LEVEL && nodes[r0.ch[0]].kind == LEAF &&
                 nodes[r0.ch[1]].kind == LEAF && nodes[r0.ch[2]].kind == LEAF && prods.size() == 1 &&
                 r0.h >= 2048) {
                 const ProdLaunch& pl = prods[0];
@@ -728,7 +790,12 @@ struct Plan {
         for (auto& gg : gemms) {
             gg.ga = reinterpret_cast<int8_t*>(arena + gg.off_ga);
             gg.gb = reinterpret_cast<int8_t*>(arena + gg.off_gb);
-            gg.out = reinterpret_cast<uint32_t*>(arena + gg.off_out);
+            gg.out = lowmem && gg.root ? nullptr : reinterpret_cast<uint32_t*>(arena + gg.off_out);
+            if (gg.wino) {
+                gg.res = reinterpret_cast<uint32_t*>(arena + gg.off_res);
+                gg.ga = gg.gb = nullptr;
+                continue;  // no digit-plane operand maps
+            }
             gg.tA = make_plane_map(gg.ga, gg.kpad, gg.hpad, sch.pa, 2 * gg.count, 128, BK);
             gg.tB = make_plane_map(gg.gb, gg.kpad, gg.hpad, sch.pb, 2 * gg.count, sch.b_box, BK);
         }
@@ -889,10 +956,18 @@ struct Plan {
                             : nd.ldin % 4 != 0 || reinterpret_cast<uintptr_t>(nd.in) % 16 != 0)
                     a.aligned = 0;
                 if (nd.s3res && (nd.lds3 % 4 != 0 || reinterpret_cast<uintptr_t>(nd.s3res) % 16 != 0)) a.aligned = 0;
-                pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
-                pn.s2 = g.gb + (2LL * nd.gslot) * g.slot_b;
-                pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
-                pn.s4 = g.gb + (2LL * nd.gslot + 1) * g.slot_b;
+                if (g.wino) {  // residue operands for the Winograd engine
+                    pn.s1 = pn.s2 = pn.a22 = pn.s4 = nullptr;
+                    pn.ld_op = g.kw;
+                    pn.op_stride = (long long)g.h * g.kw;
+                    pn.r_op = g.res + 4LL * nd.gslot * pn.op_stride;
+                    if (pn.ld_op % 4 != 0) a.aligned = 0;
+                } else {
+                    pn.s1 = g.ga + (2LL * nd.gslot) * g.slot;       // P4 = S1 S2^T : problem 2s
+                    pn.s2 = g.gb + (2LL * nd.gslot) * g.slot_b;
+                    pn.a22 = g.ga + (2LL * nd.gslot + 1) * g.slot;  // P3 = A22 S4^T: problem 2s+1
+                    pn.s4 = g.gb + (2LL * nd.gslot + 1) * g.slot_b;
+                }
                 const Node& q0 = nodes[nd.ch[0]];
                 const Node& q1 = nodes[nd.ch[1]];
                 const Node& q2 = nodes[nd.ch[2]];
@@ -970,6 +1045,11 @@ struct Plan {
             int8_macs += (uint64_t)lg.count * lg.ntiles * (uint64_t)BMt * BN * lg.kpad * sch.nterms;
         }
         for (auto& gg : gemms) {
+            if (gg.wino) {  // one Winograd level: 7 half-size products (the engine may go deeper)
+                tensor_macs += (uint64_t)2 * gg.count * 7 * (gg.h / 2) * (gg.h / 2) * (gg.kw / 2);
+                ew_adds += (uint64_t)gg.count * (4ull * gg.h * gg.kw + 4ull * gg.h * gg.h);
+                continue;
+            }
             tensor_macs += (uint64_t)2 * gg.count * gg.h * gg.h * gg.kw;
             int8_macs += (uint64_t)2 * gg.count * ((gg.h + BMt - 1) / BMt) * ((gg.h + BN - 1) / BN) * (uint64_t)BMt *
                          BN * gg.kpad * sch.nterms;
@@ -1011,7 +1091,8 @@ struct Plan {
           << ", \"limbs\": " << L << ", \"block_n\": " << BN
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
           << "}, \"nodes\": " << nodes.size() << ", \"post_rounds\": " << nrounds
-          << ", \"arena_bytes\": " << arena_bytes
+          << ", \"arena_bytes\": " << arena_bytes << ", \"schedule\": \"" << (lowmem ? "low-memory" : "wide") << "\""
+          << ", \"tree_prep\": " << tree_depth << ", \"winograd_groups\": " << std::count_if(gemms.begin(), gemms.end(), [](const GemmGroup& g) { return g.wino != 0; })
           << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs
           << ", \"prep_bytes\": " << prep_bytes << ", \"post_bytes\": " << post_bytes
           << ", \"post_cin_bytes\": " << post_cin_bytes << ", \"convert_bytes\": " << convert_bytes
@@ -1040,6 +1121,8 @@ struct Plan {
         if (!want || colmap || partitioned || idle || nodes.empty() || nodes[0].kind != LEVEL || !nodes[0].in64 ||
             !split_leaves.empty())
             return;
+        for (const GemmGroup& gg : gemms)
+            if (gg.wino) return;  // residue operands: the per-depth kernels write them
         std::vector<std::vector<int>> lv(1, std::vector<int>{0});
         int D = 0;
         for (;;) {
@@ -1095,6 +1178,31 @@ struct Plan {
         tree_depth = D;
     }
 
+    // The Winograd groups' products: P4 = S1 S2^T and P3 = A22 S4^T of every member node through
+    // the Strassen-Winograd engine (one grouped tensor-core launch of all base products); the
+    // low-memory schedule's root products land in C12 like the direct ones.
+    void run_wino(cudaStream_t s, const uint32_t* lm_p4, long long ldc) {
+        for (GemmGroup& gg : gemms) {
+            if (!gg.wino) continue;
+            const long long st = (long long)gg.h * gg.kw, hh = (long long)gg.h * gg.h;
+            std::vector<WinoProblem> probs;
+            for (int q = 0; q < gg.count; ++q) {
+                const uint32_t* r = gg.res + 4LL * q * st;
+                uint32_t* p4 = gg.out + 2LL * q * hh;
+                long long ldo = gg.h;
+                uint32_t* p3 = p4 + hh;
+                if (gg.root && lm_p4) {
+                    p4 = const_cast<uint32_t*>(lm_p4);
+                    p3 = p4 + gg.h;
+                    ldo = 2 * ldc;
+                }
+                probs.push_back(WinoProblem{r, gg.kw, r + st, gg.kw, p4, ldo});            // P4 = S1 S2^T
+                probs.push_back(WinoProblem{r + 2 * st, gg.kw, r + 3 * st, gg.kw, p3, ldo});  // P3 = A22 S4^T
+            }
+            wino_gemm_multi(p, probs, gg.h, gg.h, gg.kw, gg.wino_pol, s);
+        }
+    }
+
     void execute(const uint64_t* a_dev, long long lda, uint64_t* c_dev, long long ldc, uint32_t alpha,
                  uint32_t beta, bool mirror, cudaStream_t s) {
         int counts[5] = {0, 0, 0, 0, 0};
@@ -1111,6 +1219,25 @@ struct Plan {
         }
         mark(0);
         const Node& root = nodes[0];
+        const uint32_t* lm_p4 = nullptr;  // low-memory schedule: P4 | P3 rows inside C12
+        if (lowmem) {
+            if (ldc % 2 != 0 || reinterpret_cast<uintptr_t>(c_dev) % 16 != 0)
+                fail(FSYRK_B200_EINVAL, "low-memory schedule: C needs an even row stride and 16-byte alignment");
+            lm_p4 = reinterpret_cast<const uint32_t*>(c_dev + root.h);
+            if (c_dev != lm_c || ldc != lm_ldc) {
+                for (auto& pl : prods)
+                    for (int gi = 0; gi < pl.args.ngroups; ++gi)
+                        if (!pl.members[gi].leaf && gemms[pl.members[gi].idx].root) {
+                            GroupDesc& g = pl.args.g[gi];
+                            g.out = const_cast<uint32_t*>(lm_p4);
+                            g.ldo = 2 * ldc;
+                            g.out_bs = root.h;  // P4 in the first half of each C12 row, P3 in the second
+                            modmm_set_output_map(g, 2);
+                        }
+                lm_c = c_dev;
+                lm_ldc = ldc;
+            }
+        }
         cudaEvent_t ev_conv = nullptr;  // phase timing: end of the conversion pass
         // 1. syrkd: convert the reference-layout input with the column transform folded in;
         //    otherwise the top-level pre-additions read the caller's uint64 matrix directly
@@ -1175,6 +1302,11 @@ struct Plan {
                 a.nodes = pg.dev_post;
                 a.nnodes = (int)pg.nodes.size();
                 if (pg.depth == 0) {  // the root writes alpha X + beta C into the caller's C
+                    if (lm_p4) {
+                        a.p4o = lm_p4;
+                        a.p3o = lm_p4 + root.h;
+                        a.ld34o = 2 * ldc;
+                    }
                     a.out64 = 1;
                     a.c64 = c_dev;
                     a.ldc = ldc;
@@ -1245,6 +1377,7 @@ struct Plan {
             }
             mark(2);
             for (auto& pl : prods) run_prod(pl, s);
+            run_wino(s, lm_p4, ldc);
             mark(3);
             for (auto& pg : posts) run_post(pg, s);
             mark(4);
@@ -1332,11 +1465,25 @@ struct PlanKey {
     uint64_t thr, lev;
     bool colmap;
     int dev, rank, nranks;
+    bool lowmem;
+    uint64_t wino_min;
     bool operator<(const PlanKey& o) const {
-        return std::tie(p, n, kin, k, thr, lev, colmap, dev, rank, nranks) <
-               std::tie(o.p, o.n, o.kin, o.k, o.thr, o.lev, o.colmap, o.dev, o.rank, o.nranks);
+        return std::tie(p, n, kin, k, thr, lev, colmap, dev, rank, nranks, lowmem, wino_min) <
+               std::tie(o.p, o.n, o.kin, o.k, o.thr, o.lev, o.colmap, o.dev, o.rank, o.nranks, o.lowmem, o.wino_min);
     }
 };
+
+// Process-wide workspace limit (fsyrk_b200_set_workspace_limit): 0 = none.  A plan whose wide
+// workspace exceeds it uses the low-memory schedule; one that exceeds it even so is refused.
+std::atomic<uint64_t> g_ws_limit{0};
+std::atomic<int> g_force_lowmem{0};  // fsyrk_b200_set_low_memory(1): every applicable plan
+
+uint64_t dry_arena(uint64_t p, int n, int kin, int k, fsyrk_b200_policy pol, bool colmap, int rank, int nranks,
+                   bool lowmem) {
+    Plan plan;
+    plan.create(p, n, kin, k, pol, colmap, rank, nranks, true, lowmem);
+    return plan.arena_bytes;
+}
 
 std::mutex g_cache_mu;
 std::map<PlanKey, std::shared_ptr<Plan>> g_cache;  // guarded by g_cache_mu
@@ -1347,12 +1494,33 @@ std::shared_ptr<Plan> get_plan(uint64_t p, int n, int kin, int k, fsyrk_b200_pol
                                int nranks = 1) {
     int dev = 0;
     cudaGetDevice(&dev);
-    PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev, rank, nranks};
+    bool lowmem = g_force_lowmem.load() != 0;
+    if (const uint64_t limit = g_ws_limit.load(); limit && !lowmem) {
+        // the schedule decision per (shape, limit) is made once (two host-only dry layouts)
+        static std::mutex mu;
+        static std::map<std::pair<PlanKey, uint64_t>, bool> decided;
+        const PlanKey k0{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev, rank, nranks, false, g_wino_min.load()};
+        std::lock_guard<std::mutex> lk(mu);
+        auto d = decided.find({k0, limit});
+        if (d != decided.end()) {
+            lowmem = d->second;
+        } else {
+            if (dry_arena(p, n, kin, k, pol, colmap, rank, nranks, false) > limit) {
+                lowmem = true;
+                const uint64_t lm = dry_arena(p, n, kin, k, pol, colmap, rank, nranks, true);
+                if (lm > limit)
+                    fail(FSYRK_B200_EINVAL, "workspace limit of " + std::to_string(limit) + " bytes is below the " +
+                                                std::to_string(lm) + " bytes of the low-memory schedule");
+            }
+            decided[{k0, limit}] = lowmem;
+        }
+    }
+    PlanKey key{p, n, kin, k, pol.threshold, pol.max_levels, colmap, dev, rank, nranks, lowmem, g_wino_min.load()};
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) return it->second;
     auto plan = std::make_shared<Plan>();
-    plan->create(p, n, kin, k, pol, colmap, rank, nranks);
+    plan->create(p, n, kin, k, pol, colmap, rank, nranks, false, lowmem);
     g_cache[key] = plan;
     return plan;
 }
@@ -1692,14 +1860,16 @@ void gemm_nt_dev(uint64_t p, const uint64_t* a, size_t m, size_t k, size_t lda, 
 // C22 = M1 + M6 + M7 + M5; all 7^levels base products of a call run as ONE grouped
 // tensor-core launch.  Levels stop where a dimension is odd or below the policy threshold
 // (the reference peels odd dimensions instead; the result is the same exact product).
-void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const uint32_t* B, long long ldb, size_t n,
-                   size_t k, uint32_t* C, long long ldc, fsyrk_b200_policy pol, cudaStream_t s) {
+void wino_gemm_multi(uint64_t p, const std::vector<WinoProblem>& probs, size_t m, size_t n, size_t k,
+                     fsyrk_b200_policy pol, cudaStream_t s) {
     struct Prob {
         GemmOperand a, b;
         uint32_t* c;
         long long ldc;
     };
-    std::vector<Prob> cur{{operand_u32(A, lda), operand_u32(B, ldb), C, ldc}};
+    std::vector<Prob> cur;
+    for (const WinoProblem& w : probs) cur.push_back({operand_u32(w.a, w.lda), operand_u32(w.b, w.ldb), w.c, w.ldc});
+    if (cur.empty()) return;
     struct Level {
         std::vector<Prob> parents;
         uint32_t* m_out;  // 7 x parents.size() products of hm x hn, child-major order
@@ -1770,9 +1940,9 @@ void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const
         ea.push_back(pr.a);
         eb.push_back(pr.b);
     }
-    if (levels.empty())
-        gemm_batch_dev(p, cm, cn, ck_, ea, eb, C, ldc, 0, s);
-    else
+    if (levels.empty()) {
+        for (size_t q = 0; q < cur.size(); ++q) gemm_batch_dev(p, cm, cn, ck_, {ea[q]}, {eb[q]}, cur[q].c, cur[q].ldc, 0, s);
+    } else
         gemm_batch_dev(p, cm, cn, ck_, ea, eb, levels.back().m_out, (long long)cn, (long long)cm * cn, s);
     // post-additions, deepest level first
     for (size_t l = levels.size(); l-- > 0;) {
@@ -1785,6 +1955,11 @@ void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const
         }
     }
     ck(cudaStreamSynchronize(s), "sync");
+}
+
+void wino_gemm_dev(uint64_t p, const uint32_t* A, long long lda, size_t m, const uint32_t* B, long long ldb, size_t n,
+                   size_t k, uint32_t* C, long long ldc, fsyrk_b200_policy pol, cudaStream_t s) {
+    wino_gemm_multi(p, {WinoProblem{A, lda, B, ldb, C, ldc}}, m, n, k, pol, s);
 }
 
 // Core device call: everything resident on the device.
@@ -2484,18 +2659,29 @@ int fsyrk_b200_syrkd(uint64_t p, uint64_t alpha, const uint64_t* a, size_t n, si
     });
 }
 
-int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, uint64_t* arena,
+int fsyrk_b200_set_workspace_limit(uint64_t bytes) {
+    g_ws_limit.store(bytes);
+    return FSYRK_B200_OK;
+}
+
+int fsyrk_b200_set_winograd_min(uint64_t min_dim) {
+    g_wino_min.store(min_dim);
+    return FSYRK_B200_OK;
+}
+
+int fsyrk_b200_set_low_memory(int enable) {
+    g_force_lowmem.store(enable != 0);
+    return FSYRK_B200_OK;
+}
+
+int fsyrk_b200_workspace_bytes(uint64_t p, size_t n, size_t k, fsyrk_b200_policy policy, int lowmem, uint64_t* arena,
                                uint64_t* host_call) {
     return guarded([&] {
         validate_field(p);
         validate_policy(policy);
         validate_shapes(n, k, k, n);
         uint64_t bytes = 0;
-        if (n > 0 && k > 0) {
-            Plan plan;
-            plan.create(p, (int)n, (int)k, (int)k, policy, false, 0, 1, true);
-            bytes = plan.arena_bytes;
-        }
+        if (n > 0 && k > 0) bytes = dry_arena(p, (int)n, (int)k, (int)k, policy, false, 0, 1, lowmem != 0);
         if (arena) *arena = bytes;
         // host entry points also stage A and C on the device as uint64 rows
         if (host_call) *host_call = bytes + (uint64_t)n * k * 8 + (uint64_t)n * n * 8;

@@ -250,10 +250,18 @@ __global__ void prep_kernel(const PrepArgs args) {
         const uint32_t s3 = subm(s1[t], a22[t], p);
         const uint32_t s4 = addm(s3, a12[t], p);
         const long long go = (long long)i * args.g_row + c;
-        put_planes<L, Scheme<L>::PA>(nd.s1, args.g_plane, go, s1[t], p);  // A-role: first PA planes
-        put_planes<L, Scheme<L>::PA>(nd.a22, args.g_plane, go, a22[t], p);
-        put_planes<L, Scheme<L>::PB>(nd.s2, args.g_plane, go, s2, p);  // B-role: first PB planes
-        put_planes<L, Scheme<L>::PB>(nd.s4, args.g_plane, go, s4, p);
+        if (nd.s1) {
+            put_planes<L, Scheme<L>::PA>(nd.s1, args.g_plane, go, s1[t], p);  // A-role: first PA planes
+            put_planes<L, Scheme<L>::PA>(nd.a22, args.g_plane, go, a22[t], p);
+            put_planes<L, Scheme<L>::PB>(nd.s2, args.g_plane, go, s2, p);  // B-role: first PB planes
+            put_planes<L, Scheme<L>::PB>(nd.s4, args.g_plane, go, s4, p);
+        } else {  // Winograd operands: residues
+            uint32_t* r = nd.r_op + (long long)i * nd.ld_op + c;
+            r[0] = s1[t];
+            r[nd.op_stride] = s2;
+            r[2 * nd.op_stride] = a22[t];
+            r[3 * nd.op_stride] = s4;
+        }
         if (c < kh) {
             if (nd.c_a11) put_planes<L>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
             if (nd.c_a12) put_planes<L>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
@@ -368,10 +376,18 @@ __device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNo
         const long long go = (long long)i * args.g_row + c;
         // GEMM operands keep the planes of their role; leaf operands (read as A and B) all
         constexpr int PA = Scheme<S>::PA, PB = Scheme<S>::PB;
-        put_planes4<S, PA>(nd.s1, args.g_plane, go, s1[t], p);
-        put_planes4<S, PA>(nd.a22, args.g_plane, go, a22[t], p);
-        put_planes4<S, PB>(nd.s2, args.g_plane, go, s2, p);
-        put_planes4<S, PB>(nd.s4, args.g_plane, go, s4, p);
+        if (nd.s1) {
+            put_planes4<S, PA>(nd.s1, args.g_plane, go, s1[t], p);
+            put_planes4<S, PA>(nd.a22, args.g_plane, go, a22[t], p);
+            put_planes4<S, PB>(nd.s2, args.g_plane, go, s2, p);
+            put_planes4<S, PB>(nd.s4, args.g_plane, go, s4, p);
+        } else {  // Winograd operands: residues (ld_op % 4 == 0, driver-checked via `aligned`)
+            uint32_t* r = nd.r_op + (long long)i * nd.ld_op + c;
+            *reinterpret_cast<uint4*>(r) = s1[t];
+            *reinterpret_cast<uint4*>(r + nd.op_stride) = s2;
+            *reinterpret_cast<uint4*>(r + 2 * nd.op_stride) = a22[t];
+            *reinterpret_cast<uint4*>(r + 3 * nd.op_stride) = s4;
+        }
         if (nd.c_a11) put_planes4<S>(nd.c_a11, args.c_plane, (long long)i * args.c_row + c, a11[t], p);
         if (nd.c_a12) put_planes4<S>(nd.c_a12, args.c_plane, (long long)i * args.c_row + c, a12[t], p);
         if (nd.c_s3) put_planes4<S>(nd.c_s3, args.c3_plane, (long long)i * args.c3_row + c, s3, p);
@@ -657,7 +673,7 @@ __global__ void post_kernel(const PostArgs args) {
     pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];  // Low(P1 + P5), tile (I, J)
     __shared__ uint32_t sT[TS][TS + 1];  // P4 tile (J, I)
-    const PostNode nd = args.nodes[blockIdx.z];
+    const PostNode nd = post_node(args, args.nodes[blockIdx.z]);
     const uint32_t p = args.m.p;
     const int h = args.h;
     const PostOut out = make_out(args, nd);
@@ -766,7 +782,7 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const Po
     pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
-    const PostNode nd = args.nodes[blockIdx.z];
+    const PostNode nd = post_node(args, args.nodes[blockIdx.z]);
     int I, J;
     if (args.pairs) {
         I = args.pairs[blockIdx.x].x;
@@ -790,7 +806,7 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_rounds_kernel(const
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
     __shared__ int s_idx;
-    const PostNode nd = args.nodes[0];
+    const PostNode nd = post_node(args, args.nodes[0]);
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     int ready_round = -1;  // rounds <= ready_round are known complete
     for (;;) {

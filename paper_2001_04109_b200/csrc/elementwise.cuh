@@ -42,6 +42,10 @@ struct PrepNode {
     int8_t* c_s3;
     uint32_t* r_s3;  // residue S3 for a non-leaf child (nullable)
     long long ld_s3;
+    // Winograd general products (s1 == nullptr): S1, S2, A22, S4 as uint32 residues at
+    // r_op + {0, 1, 2, 3} * op_stride, row stride ld_op (the Winograd engine's operands)
+    uint32_t* r_op;
+    long long ld_op, op_stride;
 };
 
 struct PrepArgs {
@@ -105,7 +109,22 @@ struct PostArgs {
     // multi-GPU partition: only these 32 x 32 tile pairs (I >= J); nullptr = all pairs
     const int2* pairs;
     int npairs;
+    // low-memory schedule: the root's P4 / P3 live in the caller's scratch quadrant C12
+    // (uint32 pairs per uint64 row, ld34 = 2 ldc); nullptr = the node table's buffers
+    const uint32_t *p4o, *p3o;
+    long long ld34o;
 };
+
+// the node of this block, with the per-call P3 / P4 override of the low-memory schedule
+__host__ __device__ inline PostNode post_node(const PostArgs& a, const PostNode& n) {
+    PostNode r = n;
+    if (a.p4o) {
+        r.p4 = a.p4o;
+        r.p3 = a.p3o;
+        r.ld3 = r.ld4 = a.ld34o;
+    }
+    return r;
+}
 
 struct AddNode {
     const uint32_t *x1, *x2;

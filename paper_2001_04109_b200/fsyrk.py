@@ -98,6 +98,7 @@ EXPORTS = (
     "fsyrk_b200_syrk_mgpu", "fsyrk_b200_nccl_unique_id", "fsyrk_b200_comm_init_rank", "fsyrk_b200_comm_destroy",
     "fsyrk_b200_syrk_mgpu_rank", "fsyrk_b200_share_pairs", "fsyrk_b200_opcount_syrk", "fsyrk_b200_opcount_syrkd",
     "fsyrk_b200_opcount_syrkbd", "fsyrk_b200_opcount_fp2", "fsyrk_b200_workspace_bytes",
+    "fsyrk_b200_set_workspace_limit", "fsyrk_b200_set_low_memory", "fsyrk_b200_set_winograd_min",
 )
 
 
@@ -116,8 +117,11 @@ def lib() -> ctypes.CDLL:
     L.fsyrk_b200_skew_orthogonal.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.POINTER(_Skew)]
     L.fsyrk_b200_random_matrix.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                            _u64p, ctypes.c_size_t]
-    L.fsyrk_b200_workspace_bytes.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _Policy,
+    L.fsyrk_b200_workspace_bytes.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _Policy, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+    L.fsyrk_b200_set_workspace_limit.argtypes = [ctypes.c_uint64]
+    L.fsyrk_b200_set_low_memory.argtypes = [ctypes.c_int]
+    L.fsyrk_b200_set_winograd_min.argtypes = [ctypes.c_uint64]
     L.fsyrk_b200_opcount_syrk.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                           ctypes.c_uint64, _Policy, ctypes.POINTER(_OpCount)]
     L.fsyrk_b200_opcount_syrkd.argtypes = [ctypes.c_uint64, ctypes.c_size_t, ctypes.c_size_t, _u64p, ctypes.c_uint64,
@@ -643,13 +647,29 @@ def level_blocks(f: PrimeField, a: np.ndarray):
             "P1": P[0], "P2": P[1], "P3": P[2], "P4": P[3], "P5": P[4], "kw": kw}
 
 
-def workspace_bytes(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None) -> dict:
-    """Device memory of a call without allocating it (host only): the plan's workspace and, for
-    the host entry points, workspace + device staging of A and C."""
+def workspace_bytes(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None, lowmem: bool = False) -> dict:
+    """Device memory of a call without allocating it (host only): the plan's workspace (wide or
+    low-memory schedule) and, for the host entry points, workspace + device staging of A and C."""
     ar, hc = ctypes.c_uint64(0), ctypes.c_uint64(0)
-    _check(lib().fsyrk_b200_workspace_bytes(int(p), int(n), int(k), (policy or RecursionPolicy())._c(),
+    _check(lib().fsyrk_b200_workspace_bytes(int(p), int(n), int(k), (policy or RecursionPolicy())._c(), int(lowmem),
                                             ctypes.byref(ar), ctypes.byref(hc)))
     return {"arena": int(ar.value), "host_call": int(hc.value)}
+
+
+def set_workspace_limit(nbytes: int) -> None:
+    """Process-wide workspace limit (0 = none): larger plans run the low-memory schedule."""
+    _check(lib().fsyrk_b200_set_workspace_limit(int(nbytes)))
+
+
+def set_winograd_min(min_dim: int) -> None:
+    """Process-wide: top-level general products with min(h, kw) >= min_dim run Strassen-Winograd
+    levels (0 = never; default 16384)."""
+    _check(lib().fsyrk_b200_set_winograd_min(int(min_dim)))
+
+
+def set_low_memory(enable: bool) -> None:
+    """Process-wide: run every plan created afterwards with the low-memory schedule."""
+    _check(lib().fsyrk_b200_set_low_memory(int(bool(enable))))
 
 
 def reference_opcount(p: int, n: int, k: int, policy: Optional[RecursionPolicy] = None, alpha: int = 1, beta: int = 0,

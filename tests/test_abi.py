@@ -107,3 +107,19 @@ def test_python_mirror_rejects_reversed_or_overlapping_rows(fsyrk):
     a2 = np.ones((4, 3, 2), np.uint64)
     with pytest.raises(fsyrk.DimensionError):
         fsyrk.herk_fast(fsyrk.QuadExtField(7), a2[::-1], fsyrk.make_herk_plan(fsyrk.QuadExtField(7), fsyrk.RecursionPolicy(2)))
+
+
+def test_workspace_bytes_host_only(fsyrk):
+    # the plan's device workspace is reported without touching a device (layout dry run);
+    # the low-memory schedule moves the top level's P4 / P3 (2 h^2 uint32) into C12
+    U = fsyrk.UNLIMITED_LEVELS
+    for (p, n, k, thr, lev) in ((131071, 4096, 4096, 1024, U), (131071, 32768, 1024, 2, 1), (65521, 8192, 2048, 2, 1)):
+        pol = fsyrk.RecursionPolicy(thr, lev)
+        wide = fsyrk.workspace_bytes(p, n, k, pol)
+        low = fsyrk.workspace_bytes(p, n, k, pol, lowmem=True)
+        h = n // 2
+        assert wide["arena"] - low["arena"] == 2 * h * h * 4
+        assert wide["host_call"] == wide["arena"] + n * k * 8 + n * n * 8
+    # a root leaf has no top-level products: both schedules coincide
+    pol = fsyrk.RecursionPolicy(2, 0)
+    assert fsyrk.workspace_bytes(7, 64, 64, pol)["arena"] == fsyrk.workspace_bytes(7, 64, 64, pol, lowmem=True)["arena"]

@@ -1147,7 +1147,7 @@ struct Plan {
         if (leaf.n != (n >> D) || leaf.k != (k >> D) || leaf.n * (1 << D) != n || leaf.k * (1 << D) != k) return;
         const int ncol = y.form == 1 ? leaf.k / 2 : leaf.k;  // columns (pairs) of the fine block
         if ((y.form == 1 && leaf.k % 2 != 0) || ncol % 4 != 0) return;
-        int cp = 32;  // kTreeCP (elementwise.cu)
+        int cp = D == 3 ? 32 : 128;  // kTreeCP / kTreeCP2 (elementwise.cu): 128 work items per level-0 CTA
         while (ncol % cp) cp /= 2;
         PrepTreeArgs& a = tree_args;
         a = PrepTreeArgs{};

@@ -429,7 +429,8 @@ __global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const Pr
 // (fine block column bj, half e).  A quadrant is a half in each direction; the Pair partner of
 // virtual column v (< V/2) of a V-wide quadrant is v + V/2.  Levels alternate between two
 // buffers (level 0 and 2 in one, level 1 in the other).
-constexpr int kTreeCP = 32;       // columns (column pairs) per CTA (at most)
+// columns (column pairs) per CTA at most: 128 work items at level 0 for D = 3 (32) and D = 2 (128)
+constexpr int kTreeCP = 32, kTreeCP2 = 128;
 constexpr int kTreeThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -573,8 +574,8 @@ cudaError_t prep_tree_dispatch(const PrepTreeArgs& a, int nsm, cudaStream_t s) {
     (void)nsm;
     const bool pair = a.pair != 0;
     const int nc = pair ? 2 : 1;
-    if (a.cp < 4 || a.cp > kTreeCP || (a.cp & (a.cp - 1)) || (a.w / nc) % a.cp || (pair && a.w % 2) ||
-        a.depth < 2 || a.depth > 3)
+    if (a.cp < 4 || a.cp > (a.depth == 3 ? kTreeCP : kTreeCP2) || (a.cp & (a.cp - 1)) || (a.w / nc) % a.cp ||
+        (pair && a.w % 2) || a.depth < 2 || a.depth > 3)
         return cudaErrorInvalidValue;
     const size_t smem = prep_tree_smem(a.depth, pair, a.cp);
     dim3 grid(a.w / nc / a.cp, a.rows);
@@ -586,7 +587,7 @@ cudaError_t prep_tree_dispatch(const PrepTreeArgs& a, int nsm, cudaStream_t s) {
                                      : (pair ? static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, true, 2>>())
                                              : static_cast<DeviceOnce&>(per_device<TreeAttrOnce<S, false, 2>>()));
     std::call_once(once.flag, [&] {
-        once.result = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_tree_smem(3, true, kTreeCP));
+        once.result = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max(prep_tree_smem(3, true, kTreeCP), prep_tree_smem(2, true, kTreeCP2)));
     });
     if (once.result != cudaSuccess) return once.result;
     return launch_pdl(kern, grid, dim3(kTreeThreads), smem, s, a);

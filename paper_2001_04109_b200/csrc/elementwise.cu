@@ -730,25 +730,20 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
     const int i = I * TS + r, j = J * TS + c0;        // tile (I, J)
     const int it = J * TS + r, jt = I * TS + c0;      // tile (J, I)
     const bool ok = i < h && j < h, okt = it < h && jt < h;
-    // every global load of the pair is issued before the barrier (one memory round trip per
-    // pair instead of two: the kernel is latency-bound, ncu DRAM ~33%)
-    uint4 p1 = {0, 0, 0, 0}, p5 = p1, p4t = p1, p4 = p1, p3 = p1, p2 = p1, p3t = p1;
+    uint4 p1 = {0, 0, 0, 0}, p5 = p1, p4t = p1;
     if (ok) {
         p1 = *reinterpret_cast<const uint4*>(nd.p1 + (long long)i * nd.ld1 + j);
         p5 = *reinterpret_cast<const uint4*>(nd.p5 + (long long)i * nd.ld5 + j);
-        p4 = *reinterpret_cast<const uint4*>(nd.p4 + (long long)i * nd.ld4 + j);
-        p3 = *reinterpret_cast<const uint4*>(nd.p3 + (long long)i * nd.ld3 + j);
-        p2 = *reinterpret_cast<const uint4*>(nd.p2 + (long long)i * nd.ld2 + j);
     }
-    if (okt) {
-        p4t = *reinterpret_cast<const uint4*>(nd.p4 + (long long)it * nd.ld4 + jt);
-        if (I != J) p3t = *reinterpret_cast<const uint4*>(nd.p3 + (long long)it * nd.ld3 + jt);
-    }
+    if (okt) p4t = *reinterpret_cast<const uint4*>(nd.p4 + (long long)it * nd.ld4 + jt);
     const uint4 l15 = add4(p1, p5, p);
     sU[r][c0] = l15.x; sU[r][c0 + 1] = l15.y; sU[r][c0 + 2] = l15.z; sU[r][c0 + 3] = l15.w;
     sT[r][c0] = p4t.x; sT[r][c0 + 1] = p4t.y; sT[r][c0 + 2] = p4t.z; sT[r][c0 + 3] = p4t.w;
     __syncthreads();
     if (ok) {
+        const uint4 p4 = *reinterpret_cast<const uint4*>(nd.p4 + (long long)i * nd.ld4 + j);
+        const uint4 p3 = *reinterpret_cast<const uint4*>(nd.p3 + (long long)i * nd.ld3 + j);
+        const uint4 p2 = *reinterpret_cast<const uint4*>(nd.p2 + (long long)i * nd.ld2 + j);
         uint32_t u1[4], t4[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -775,6 +770,7 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
         }
     }
     if (I != J && okt) {
+        const uint4 p3t = *reinterpret_cast<const uint4*>(nd.p3 + (long long)it * nd.ld3 + jt);
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = addm(sU[c0 + e][r], sT[r][c0 + e], p);

@@ -241,3 +241,36 @@ def test_communicator_single_rank(gpu):
         assert orc.lower_equal(c, orc.syrk_classical(p, a))
     finally:
         comm.close()
+
+
+def test_bench_gpus_flag_self_launches_torchrun(monkeypatch):
+    # `bench.py --gpus N` without WORLD_SIZE starts N ranks itself (one process per GPU) with
+    # torchrun on 127.0.0.1 and NCCL_DEBUG=INFO, instead of silently running one rank
+    sys.path.insert(0, REPO)
+    import bench
+    seen = {}
+
+    class _Done:
+        returncode = 0
+
+    def fake_run(cmd, env=None, **kw):
+        seen["cmd"], seen["env"] = cmd, env
+        return _Done()
+
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 8)
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=2" in cmd and "--master-addr=127.0.0.1" in cmd and "--nnodes=1" in cmd
+    assert cmd[-6:] == ["--gpus", "2", "--steps", "3", "--warmup", "3"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
+    # fewer visible devices than requested: refused, not a one-rank run
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 1)
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 2

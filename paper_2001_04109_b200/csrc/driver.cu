@@ -1084,7 +1084,7 @@ struct Plan {
 
     std::string json() const {
         std::ostringstream o;
-        static const char* scheme_names[] = {"limb2", "limb3", "limb4", "m17", "m31"};
+        static const char* scheme_names[] = {"limb2", "limb3", "limb4", "m17", "m31", "m17n"};
         o << "{\"p\": " << p << ", \"n\": " << n << ", \"k\": " << k << ", \"scheme\": \"" << scheme_names[sch.id]
           << "\", \"planes\": " << L << ", \"terms\": " << sch.products << ", \"mmas_per_kstep\": " << sch.nterms
           << ", \"accumulators\": " << sch.nacc

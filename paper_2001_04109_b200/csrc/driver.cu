@@ -386,6 +386,12 @@ struct Plan {
     PrepTreeArgs tree_args{};
     PrepNode* tree_dev = nullptr;  // depth-ordered PrepNode tables in tree order
 
+    // the two deepest post-addition levels fused (post2_kernel): parent depth (-1: off), the
+    // parents' and the deepest nodes' PostNode tables in tree order
+    int post2_parent_depth = -1;
+    int post2_h2 = 0, post2_nparents = 0;
+    PostNode* post2_dev = nullptr;
+
     // side stream + events: the top level's general products overlap the deeper pre/post-additions
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -412,6 +418,7 @@ struct Plan {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (tree_dev) cudaFree(tree_dev);
+        if (post2_dev) cudaFree(post2_dev);
     }
 
     int build(int n_, int k_, uint64_t levels, int depth, int parent, int role) {
@@ -986,6 +993,7 @@ struct Plan {
                "upload prep table");
         }
         setup_tree_prep(host_prep);
+        std::vector<PostNode> host_post(nodes.size());
         for (auto& pg : posts) {
             if (pg.kind == LEVEL) {
                 std::vector<PostNode> tab;
@@ -1005,6 +1013,7 @@ struct Plan {
                     pn.x = nd.x;
                     pn.ldx = nd.ldx;
                     tab.push_back(pn);
+                    host_post[ni] = pn;
                 }
                 pg.dev_post = reinterpret_cast<PostNode*>(arena + pg.off_nodes);
                 ck(cudaMemcpy(pg.dev_post, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
@@ -1033,6 +1042,7 @@ struct Plan {
                    "upload add table");
             }
         }
+        setup_post2(host_post);
         // the arena clear and the table uploads above ran on the legacy stream with pageable
         // sources (the DMA may still be in flight when cudaMemcpy returns); the calls run on
         // non-blocking streams, so finish them here
@@ -1079,6 +1089,9 @@ struct Plan {
             }
             post_bytes += lower(nd.n) * (nd.parent < 0 ? 8 : 4);  // X (the root: the caller's uint64 C)
             if (nd.parent < 0) post_cin_bytes = lower(nd.n) * 8;   // + C_in when beta != 0
+            // fused two-level post: the deepest nodes' X stay on chip (not written, not read back)
+            if (post2_parent_depth >= 0 && nd.kind == LEVEL && nd.depth == post2_parent_depth + 1)
+                post_bytes -= 2 * lower(nd.n) * 4;
         }
     }
 
@@ -1092,7 +1105,7 @@ struct Plan {
           << ", \"skew\": {\"form\": \"" << (y.form ? "pair" : "scalar") << "\", \"a\": " << y.a << ", \"b\": " << y.b
           << "}, \"nodes\": " << nodes.size() << ", \"post_rounds\": " << nrounds
           << ", \"arena_bytes\": " << arena_bytes << ", \"schedule\": \"" << (lowmem ? "low-memory" : "wide") << "\""
-          << ", \"tree_prep\": " << tree_depth << ", \"winograd_groups\": " << std::count_if(gemms.begin(), gemms.end(), [](const GemmGroup& g) { return g.wino != 0; })
+          << ", \"tree_prep\": " << tree_depth << ", \"post2\": " << (post2_parent_depth >= 0 ? 1 : 0) << ", \"winograd_groups\": " << std::count_if(gemms.begin(), gemms.end(), [](const GemmGroup& g) { return g.wino != 0; })
           << ", \"tensor_macs\": " << tensor_macs << ", \"int8_macs\": " << int8_macs
           << ", \"prep_bytes\": " << prep_bytes << ", \"post_bytes\": " << post_bytes
           << ", \"post_cin_bytes\": " << post_cin_bytes << ", \"convert_bytes\": " << convert_bytes
@@ -1106,6 +1119,61 @@ struct Plan {
               << ", \"count\": " << gemms[i].count << "}";
         o << "], \"prep_groups\": " << preps.size() << ", \"post_groups\": " << posts.size() << "}";
         return o.str();
+    }
+
+    // Levels of a complete uniform tree: lv[d] = the depth-d nodes in tree order (node t's
+    // children at 3t, 3t + 1, 3t + 2 of lv[d + 1]); every node above depth D a LEVEL node of one
+    // shape, unpadded, all depth-D nodes leaves of one shape.  Returns D (0: not such a tree or
+    // deeper than max_depth).
+    int uniform_levels(std::vector<std::vector<int>>& lv, int max_depth) const {
+        lv.assign(1, std::vector<int>{0});
+        int D = 0;
+        for (;;) {
+            const std::vector<int>& cur = lv.back();
+            const Node& f0 = nodes[cur[0]];
+            bool all_level = true, all_leaf = true;
+            for (int i : cur) {
+                const Node& nd = nodes[i];
+                all_level &= nd.kind == LEVEL && !nd.padded && nd.n == f0.n && nd.k == f0.k;
+                all_leaf &= nd.kind == LEAF && nd.n == f0.n && nd.k == f0.k;
+            }
+            if (all_leaf) return D;
+            if (!all_level || D >= max_depth) return 0;
+            std::vector<int> next;
+            for (int i : cur)
+                for (int r = 0; r < 3; ++r) next.push_back(nodes[i].ch[r]);
+            lv.push_back(next);
+            ++D;
+        }
+    }
+
+    // The two deepest post-addition levels as one launch (post2_kernel) when the tree is
+    // complete and uniform with at least two levels and the deepest quadrants are whole 32 x 32
+    // tiles.  FSYRK_B200_POST2=0 keeps one launch per depth.
+    void setup_post2(const std::vector<PostNode>& host_post) {
+        static const bool want = [] {
+            const char* e = getenv("FSYRK_B200_POST2");
+            return !(e && atoi(e) == 0);
+        }();
+        post2_parent_depth = -1;
+        if (!want || partitioned || idle || nrounds || nodes.empty() || nodes[0].kind != LEVEL) return;
+        std::vector<std::vector<int>> lv;
+        const int D = uniform_levels(lv, 8);
+        if (D < 2) return;
+        const Node& deep = nodes[lv[D - 1][0]];
+        if (deep.h % 32 != 0 || nodes[lv[D - 2][0]].h != 2 * deep.h) return;  // whole 32 x 32 post2 tiles
+        // parents below the root only: with the root as parent (two-level trees, e.g. cfg4) the
+        // fused launch measured slower than the per-depth pair (profiles/r02/post2.txt)
+        if (D - 2 < 1) return;
+        std::vector<PostNode> tab;
+        for (int i : lv[D - 2]) tab.push_back(host_post[i]);
+        for (int i : lv[D - 1]) tab.push_back(host_post[i]);
+        ck(cudaMalloc(&post2_dev, tab.size() * sizeof(PostNode)), "cudaMalloc(post2 tables)");
+        ck(cudaMemcpy(post2_dev, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
+           "upload post2 tables");
+        post2_parent_depth = D - 2;
+        post2_h2 = deep.h;
+        post2_nparents = (int)lv[D - 2].size();
     }
 
     // One launch for all pre-additions when the tree is complete and uniform below the root
@@ -1123,25 +1191,8 @@ struct Plan {
             return;
         for (const GemmGroup& gg : gemms)
             if (gg.wino) return;  // residue operands: the per-depth kernels write them
-        std::vector<std::vector<int>> lv(1, std::vector<int>{0});
-        int D = 0;
-        for (;;) {
-            const std::vector<int>& cur = lv.back();
-            const Node& f0 = nodes[cur[0]];
-            bool all_level = true, all_leaf = true;
-            for (int i : cur) {
-                const Node& nd = nodes[i];
-                all_level &= nd.kind == LEVEL && !nd.padded && nd.n == f0.n && nd.k == f0.k;
-                all_leaf &= nd.kind == LEAF && nd.n == f0.n && nd.k == f0.k;
-            }
-            if (all_leaf) break;
-            if (!all_level || lv.size() > 3) return;
-            std::vector<int> next;
-            for (int i : cur)
-                for (int r = 0; r < 3; ++r) next.push_back(nodes[i].ch[r]);
-            lv.push_back(next);
-            ++D;
-        }
+        std::vector<std::vector<int>> lv;
+        const int D = uniform_levels(lv, 3);
         if (D < 2 || D > 3) return;
         const Node& leaf = nodes[lv[D][0]];
         if (leaf.n != (n >> D) || leaf.k != (k >> D) || leaf.n * (1 << D) != n || leaf.k * (1 << D) != k) return;
@@ -1294,13 +1345,13 @@ struct Plan {
             counts[0]++;
         };
         bool root_done = false;
-        auto run_post = [&](PostGroup& pg, cudaStream_t st) {
+        auto run_post = [&](PostGroup& pg, cudaStream_t st, bool fused2 = false) {
             if (pg.kind == LEVEL) {
                 PostArgs a{};
                 a.m = m;
                 a.h = pg.n / 2;
-                a.nodes = pg.dev_post;
-                a.nnodes = (int)pg.nodes.size();
+                a.nodes = fused2 ? post2_dev : pg.dev_post;
+                a.nnodes = fused2 ? post2_nparents : (int)pg.nodes.size();
                 if (pg.depth == 0) {  // the root writes alpha X + beta C into the caller's C
                     if (lm_p4) {
                         a.p4o = lm_p4;
@@ -1321,7 +1372,16 @@ struct Plan {
                         a.npairs = (int)root_pairs.size();
                     }
                 }
-                traced("post d" + std::to_string(pg.depth), st, [&] { ck(launch_post(a, st), "post"); });
+                if (fused2) {  // this level and the one below it in one launch
+                    Post2Args a2{};
+                    a2.par = a;
+                    a2.ch = post2_dev + post2_nparents;
+                    a2.h2 = post2_h2;
+                    traced("post d" + std::to_string(pg.depth) + "+" + std::to_string(pg.depth + 1), st,
+                           [&] { ck(launch_post2(a2, st), "post2"); });
+                } else {
+                    traced("post d" + std::to_string(pg.depth), st, [&] { ck(launch_post(a, st), "post"); });
+                }
             } else {
                 ck(launch_add_lower(pg.dev_add, (int)pg.nodes.size(), pg.n, (uint32_t)p, st), "add_lower");
             }
@@ -1379,7 +1439,10 @@ struct Plan {
             for (auto& pl : prods) run_prod(pl, s);
             run_wino(s, lm_p4, ldc);
             mark(3);
-            for (auto& pg : posts) run_post(pg, s);
+            for (auto& pg : posts) {
+                if (post2_parent_depth >= 0 && pg.kind == LEVEL && pg.depth == post2_parent_depth + 1) continue;
+                run_post(pg, s, post2_parent_depth >= 0 && pg.kind == LEVEL && pg.depth == post2_parent_depth);
+            }
             mark(4);
         } else {
             // The top level's two general products need only the top pre-additions; they run on

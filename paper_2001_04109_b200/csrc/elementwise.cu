@@ -568,6 +568,7 @@ size_t prep_tree_smem(int D, bool pair, int cp) {
 
 template <int S, bool PAIR, int D>
 struct TreeAttrOnce : DeviceOnce {};
+struct Post2AttrOnce : DeviceOnce {};
 
 template <int S>
 cudaError_t prep_tree_dispatch(const PrepTreeArgs& a, int nsm, cudaStream_t s) {
@@ -792,6 +793,150 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const Po
         tri_decode(blockIdx.x, I, J);
     }
     post_vec_pair(args, nd, I, J, sU, sT);
+}
+
+// ------------------------------------------------------------ post (two levels fused)
+// A block owns one 32 x 32 tile pair (i, j) of the deepest nodes' quadrants for one parent t.
+// Phase A: the three children (P1, P2, P5 of t) run their post-addition of pair (i, j) into
+// shared memory: 4 output tiles each (slots 0: X11(i,j), 1: X21(i,j), 2: X21(j,i), 3: X22(i,j);
+// slot 2 is slot 1 when i == j).  Slot s of a child's output is tile (I_s, J_s) of the child's
+// X = the parent's quadrant, with (I_s, J_s) = (i,j), (T+i,j), (T+j,i), (T+i,T+j), T = h2 / 32:
+// exactly the tile the parent's pair (I_s, J_s) reads from P1, P2, P5.  Phase B: the parent's
+// pairs (I_s, J_s) from those tiles and its P3 / P4 in HBM.  The children's X never round-trip
+// through HBM and one launch replaces two; every global load of a phase is issued before its
+// barrier (3 blocks / SM by shared memory, so the registers allow it).
+#ifndef FSYRK_POST2_TILE
+#define FSYRK_POST2_TILE 32  // measured: 16 -> cfg2 post 61 us, 32 -> 53 us (per-depth: 51 us, but one launch more)
+#endif
+constexpr int PT = FSYRK_POST2_TILE;  // post2 tile (PT x PT), PT / 4 x PT threads, 4 columns each
+constexpr int kPostTile = PT * (PT + 1);
+
+__device__ __forceinline__ uint4 ld4g(const uint32_t* base, long long ld, int i, int j, bool ok) {
+    return ok ? *reinterpret_cast<const uint4*>(base + (long long)i * ld + j) : make_uint4(0, 0, 0, 0);
+}
+__device__ __forceinline__ void st4s(uint32_t* t, int r, int c, uint4 v) {
+    t[r * (PT + 1) + c] = v.x;
+    t[r * (PT + 1) + c + 1] = v.y;
+    t[r * (PT + 1) + c + 2] = v.z;
+    t[r * (PT + 1) + c + 3] = v.w;
+}
+__device__ __forceinline__ uint4 ld4s(const uint32_t* t, int r, int c) {
+    return make_uint4(t[r * (PT + 1) + c], t[r * (PT + 1) + c + 1], t[r * (PT + 1) + c + 2], t[r * (PT + 1) + c + 3]);
+}
+// 4 consecutive columns c .. c + 3 of row r of the transpose of tile t
+__device__ __forceinline__ uint4 ld4sT(const uint32_t* t, int r, int c) {
+    return make_uint4(t[c * (PT + 1) + r], t[(c + 1) * (PT + 1) + r], t[(c + 2) * (PT + 1) + r], t[(c + 3) * (PT + 1) + r]);
+}
+// U1 tile (P1 + P5), symmetrised from its lower triangle on a diagonal pair
+__device__ __forceinline__ uint4 u1_row(const uint32_t* u, int r, int c0, bool diag) {
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int c = c0 + e;
+        v[e] = (diag && c > r) ? u[c * (PT + 1) + r] : u[r * (PT + 1) + c];
+    }
+    return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+__global__ void __launch_bounds__(PT * PT / 4, 2) post2_kernel(const Post2Args args) {
+    pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
+    pdl_trigger();
+    extern __shared__ __align__(16) uint32_t psm[];
+    uint32_t* sX = psm;                     // [3 children][4 slots] tiles
+    uint32_t* sU = psm + 12 * kPostTile;    // [4] U1 tiles (children, then parent slots)
+    uint32_t* sT = sU + 4 * kPostTile;      // [4] transposed-P4 tiles
+    const uint32_t p = args.par.m.p;
+    const int h2 = args.h2, T = h2 / PT;
+    int i2, j2;
+    tri_decode(blockIdx.x, i2, j2);
+    const bool dg = i2 == j2;
+    const int t = blockIdx.z;
+    const int tx = threadIdx.x, r = threadIdx.y, c0 = 4 * tx;
+    // ---- phase A: the three children's pair (i2, j2), outputs to shared memory
+    {
+        const int i = i2 * PT + r, j = j2 * PT + c0, it = j2 * PT + r, jt = i2 * PT + c0;
+        uint4 p1[3], p2[3], p3[3], p4[3], p3t[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const PostNode nd = args.ch[3 * t + c];
+            p1[c] = ld4g(nd.p1, nd.ld1, i, j, true);
+            const uint4 p5 = ld4g(nd.p5, nd.ld5, i, j, true);
+            const uint4 p4t = ld4g(nd.p4, nd.ld4, it, jt, true);
+            p4[c] = ld4g(nd.p4, nd.ld4, i, j, true);
+            p3[c] = ld4g(nd.p3, nd.ld3, i, j, true);
+            p2[c] = ld4g(nd.p2, nd.ld2, i, j, true);
+            p3t[c] = ld4g(nd.p3, nd.ld3, it, jt, !dg);
+            st4s(sU + c * kPostTile, r, c0, add4(p1[c], p5, p));
+            st4s(sT + c * kPostTile, r, c0, p4t);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t* u = sU + c * kPostTile;
+            const uint32_t* tt = sT + c * kPostTile;
+            uint32_t* x = sX + 4 * c * kPostTile;
+            const uint4 u2 = add4(u1_row(u, r, c0, dg), p4[c], p);
+            st4s(x + 0 * kPostTile, r, c0, add4(p1[c], p2[c], p));           // X11(i,j)
+            st4s(x + 1 * kPostTile, r, c0, add4(u2, p3[c], p));              // X21(i,j)
+            st4s(x + 3 * kPostTile, r, c0, add4(u2, ld4sT(tt, r, c0), p));   // X22(i,j)
+            if (!dg)                                                           // X21(j,i)
+                st4s(x + 2 * kPostTile, r, c0, add4(add4(ld4sT(u, r, c0), ld4s(tt, r, c0), p), p3t[c], p));
+        }
+        __syncthreads();
+    }
+    // ---- phase B: the parent's pairs at the children's four output slots
+    const PostNode pn = post_node(args.par, args.par.nodes[t]);
+    const PostOut out = make_out(args.par, pn);
+    const int h = args.par.h;
+    int PI[4], PJ[4];
+    PI[0] = i2; PJ[0] = j2;
+    PI[1] = T + i2; PJ[1] = j2;
+    PI[2] = T + j2; PJ[2] = i2;
+    PI[3] = T + i2; PJ[3] = T + j2;
+    uint4 q4[4], q3[4], q3t[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (s == 2 && dg) continue;
+        const int I = PI[s], J = PJ[s];
+        const int i = I * PT + r, j = J * PT + c0, it = J * PT + r, jt = I * PT + c0;
+        q4[s] = ld4g(pn.p4, pn.ld4, i, j, true);
+        q3[s] = ld4g(pn.p3, pn.ld3, i, j, true);
+        q3t[s] = ld4g(pn.p3, pn.ld3, it, jt, I != J);
+        st4s(sT + s * kPostTile, r, c0, ld4g(pn.p4, pn.ld4, it, jt, true));
+        st4s(sU + s * kPostTile, r, c0,
+             add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 2 + s) * kPostTile, r, c0), p));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        if (s == 2 && dg) continue;
+        const int I = PI[s], J = PJ[s];
+        const bool pdiag = I == J;
+        const int i = I * PT + r, j = J * PT + c0;
+        const uint32_t* u = sU + s * kPostTile;
+        const uint32_t* tt = sT + s * kPostTile;
+        const uint4 u2 = add4(u1_row(u, r, c0, pdiag), q4[s], p);
+        const uint4 x21 = add4(u2, q3[s], p);
+        const uint4 x22 = add4(u2, ld4sT(tt, r, c0), p);
+        const uint4 x11 = add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 1 + s) * kPostTile, r, c0), p);
+        out.put4(h + i, j, x21);
+        if (!out.out64 || !pdiag) {
+            out.put4(h + i, h + j, x22);
+            out.put4(i, j, x11);
+        } else {  // diagonal tile of the caller's C: lower entries only
+            const uint32_t a22[4] = {x22.x, x22.y, x22.z, x22.w}, a11[4] = {x11.x, x11.y, x11.z, x11.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (c0 + e <= r) {
+                    out.put(h + i, h + j + e, a22[e]);
+                    out.put(i, j + e, a11[e]);
+                }
+        }
+        if (!pdiag) {
+            const int it = J * PT + r, jt = I * PT + c0;
+            out.put4(h + it, jt, add4(add4(ld4sT(u, r, c0), ld4s(tt, r, c0), p), q3t[s], p));
+        }
+    }
 }
 
 // Root post-addition overlapped with the product kernel (driver.cu, Plan::rounds).  Launched as
@@ -1150,6 +1295,19 @@ cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
     if (args.h % 4 == 0) return launch_pdl(post_vec_kernel, grid, dim3(8, 32), 0, s, args);
     return launch_pdl(post_kernel, grid, dim3(32, 8), 0, s, args);
+}
+
+cudaError_t launch_post2(const Post2Args& a, cudaStream_t s) {
+    if (a.h2 == 0 || a.par.nnodes == 0) return cudaSuccess;
+    if (a.h2 % PT != 0 || a.par.h != 2 * a.h2) return cudaErrorInvalidValue;
+    const int T = a.h2 / PT;
+    const size_t smem = (size_t)20 * kPostTile * 4;
+    DeviceOnce& once = per_device<Post2AttrOnce>();
+    std::call_once(once.flag, [&] {
+        once.result = cudaFuncSetAttribute(post2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (once.result != cudaSuccess) return once.result;
+    return launch_pdl(post2_kernel, dim3(T * (T + 1) / 2, 1, a.par.nnodes), dim3(PT / 4, PT), smem, s, a);
 }
 
 cudaError_t launch_post_rounds(const PostArgs& args, const int* round_done, const int* target, int* next_pair,

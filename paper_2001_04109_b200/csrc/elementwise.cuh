@@ -126,6 +126,16 @@ __host__ __device__ inline PostNode post_node(const PostArgs& a, const PostNode&
     return r;
 }
 
+// The two deepest post-addition levels fused (post2_kernel): the deepest level nodes (whose
+// three products are leaves) and their parents in one launch.  par.nodes are the parents in
+// tree order, ch the deepest nodes (parent t's children P1, P2, P5 at 3t, 3t + 1, 3t + 2);
+// par.h is the parents' quadrant size, h2 = par.h / 2 the children's (a multiple of 32).
+struct Post2Args {
+    PostArgs par;
+    const PostNode* ch;
+    int h2;
+};
+
 struct AddNode {
     const uint32_t *x1, *x2;
     long long ld1, ld2;
@@ -146,6 +156,7 @@ cudaError_t launch_split_planes(int L, const InView& in, const uint64_t* a64, lo
 cudaError_t launch_prep(const PrepArgs& args, cudaStream_t s);
 cudaError_t launch_prep_tree(const PrepTreeArgs& args, int nsm, cudaStream_t s);
 cudaError_t launch_post(const PostArgs& args, cudaStream_t s);
+cudaError_t launch_post2(const Post2Args& args, cudaStream_t s);
 cudaError_t launch_add_lower(const AddNode* nodes, int nnodes, int n, uint32_t p, cudaStream_t s);
 // C (uint64) <- alpha * X + beta * C on the lower triangle (X == nullptr: X = 0).
 cudaError_t launch_finalize(const uint32_t* x, long long ldx, int n, uint64_t* c, long long ldc, const ModP& m,

@@ -64,3 +64,24 @@ def test_tree_prep_extreme_and_noncanonical(gpu):
         a = rng.integers(0, 1 << 63, size=(128, 128), dtype=np.uint64)
         c = fs.syrk_fast(f, a, fs.make_syrk_plan(f, fs.RecursionPolicy(32)))
         assert orc.lower_equal(c, orc.syrk_classical(p, a % np.uint64(p))), p
+
+
+@pytest.mark.parametrize("p", [131071, 65521, 2147483647, 1000000007])
+def test_fused_two_level_post(gpu, p):
+    # three-level uniform trees run the two deepest post-addition levels as one launch
+    # (post2_kernel): the deepest nodes' X stay in shared memory; plain and accumulating forms
+    fs = gpu
+    f = fs.PrimeField(p)
+    rng = np.random.default_rng(p % 101)
+    for (n, k, thr) in ((1024, 1024, 256), (256, 256, 64), (512, 256, 64)):
+        a = orc.random_matrix(p, n, k, n + k + 1)
+        plan = fs.make_syrk_plan(f, fs.RecursionPolicy(thr))
+        c = fs.syrk_fast(f, a, plan)
+        assert fs.last_plan()["post2"] == 1, (p, n, k, fs.last_plan())
+        assert fs.last_launch_counts()["post"] == 2, fs.last_launch_counts()
+        assert orc.lower_equal(c, orc.syrk_classical(p, a)), (p, n, k)
+        c0 = orc.random_matrix(p, n, n, 3)
+        alpha, beta = int(rng.integers(1, p)), int(rng.integers(1, p))
+        c = c0.copy()
+        fs.syrk_fast_acc(f, alpha, a, beta, c, plan)
+        assert orc.lower_equal(c, orc.syrk_classical(p, a, alpha, beta, c0)), (p, n, k, "acc")

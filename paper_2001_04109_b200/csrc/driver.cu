@@ -1151,9 +1151,9 @@ struct Plan {
     // complete and uniform with at least two levels and the deepest quadrants are whole 32 x 32
     // tiles.  FSYRK_B200_POST2=0 keeps one launch per depth.
     void setup_post2(const std::vector<PostNode>& host_post) {
-        static const bool want = [] {
+        static const int want = [] {  // 0 off, 1 parents below the root only, 2 any parent (default)
             const char* e = getenv("FSYRK_B200_POST2");
-            return !(e && atoi(e) == 0);
+            return e ? atoi(e) : 2;
         }();
         post2_parent_depth = -1;
         if (!want || partitioned || idle || nrounds || nodes.empty() || nodes[0].kind != LEVEL) return;
@@ -1162,9 +1162,7 @@ struct Plan {
         if (D < 2) return;
         const Node& deep = nodes[lv[D - 1][0]];
         if (deep.h % 32 != 0 || nodes[lv[D - 2][0]].h != 2 * deep.h) return;  // whole 32 x 32 post2 tiles
-        // parents below the root only: with the root as parent (two-level trees, e.g. cfg4) the
-        // fused launch measured slower than the per-depth pair (profiles/r02/post2.txt)
-        if (D - 2 < 1) return;
+        if (D - 2 < 1 && want < 2) return;  // FSYRK_B200_POST2=1: not with the root as the parent
         std::vector<PostNode> tab;
         for (int i : lv[D - 2]) tab.push_back(host_post[i]);
         for (int i : lv[D - 1]) tab.push_back(host_post[i]);

@@ -838,13 +838,13 @@ __device__ __forceinline__ uint4 u1_row(const uint32_t* u, int r, int c0, bool d
     return make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-__global__ void __launch_bounds__(PT * PT / 4, 2) post2_kernel(const Post2Args args) {
+__global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const Post2Args args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
     extern __shared__ __align__(16) uint32_t psm[];
-    uint32_t* sX = psm;                     // [3 children][4 slots] tiles
-    uint32_t* sU = psm + 12 * kPostTile;    // [4] U1 tiles (children, then parent slots)
-    uint32_t* sT = sU + 4 * kPostTile;      // [4] transposed-P4 tiles
+    uint32_t* sX = psm;                     // [3 children][4 slots] output tiles
+    uint32_t* sU = psm + 12 * kPostTile;    // U1 tile of the current step (P1 + P5)
+    uint32_t* sT = sU + kPostTile;          // P4 tile (J, I) of the current step, read transposed
     const uint32_t p = args.par.m.p;
     const int h2 = args.h2, T = h2 / PT;
     int i2, j2;
@@ -852,90 +852,88 @@ __global__ void __launch_bounds__(PT * PT / 4, 2) post2_kernel(const Post2Args a
     const bool dg = i2 == j2;
     const int t = blockIdx.z;
     const int tx = threadIdx.x, r = threadIdx.y, c0 = 4 * tx;
-    // ---- phase A: the three children's pair (i2, j2), outputs to shared memory
-    {
-        const int i = i2 * PT + r, j = j2 * PT + c0, it = j2 * PT + r, jt = i2 * PT + c0;
-        uint4 p1[3], p2[3], p3[3], p4[3], p3t[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const PostNode nd = args.ch[3 * t + c];
-            p1[c] = ld4g(nd.p1, nd.ld1, i, j, true);
-            const uint4 p5 = ld4g(nd.p5, nd.ld5, i, j, true);
-            const uint4 p4t = ld4g(nd.p4, nd.ld4, it, jt, true);
-            p4[c] = ld4g(nd.p4, nd.ld4, i, j, true);
-            p3[c] = ld4g(nd.p3, nd.ld3, i, j, true);
-            p2[c] = ld4g(nd.p2, nd.ld2, i, j, true);
-            p3t[c] = ld4g(nd.p3, nd.ld3, it, jt, !dg);
-            st4s(sU + c * kPostTile, r, c0, add4(p1[c], p5, p));
-            st4s(sT + c * kPostTile, r, c0, p4t);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const uint32_t* u = sU + c * kPostTile;
-            const uint32_t* tt = sT + c * kPostTile;
-            uint32_t* x = sX + 4 * c * kPostTile;
-            const uint4 u2 = add4(u1_row(u, r, c0, dg), p4[c], p);
-            st4s(x + 0 * kPostTile, r, c0, add4(p1[c], p2[c], p));           // X11(i,j)
-            st4s(x + 1 * kPostTile, r, c0, add4(u2, p3[c], p));              // X21(i,j)
-            st4s(x + 3 * kPostTile, r, c0, add4(u2, ld4sT(tt, r, c0), p));   // X22(i,j)
-            if (!dg)                                                           // X21(j,i)
-                st4s(x + 2 * kPostTile, r, c0, add4(add4(ld4sT(u, r, c0), ld4s(tt, r, c0), p), p3t[c], p));
-        }
-        __syncthreads();
-    }
-    // ---- phase B: the parent's pairs at the children's four output slots
     const PostNode pn = post_node(args.par, args.par.nodes[t]);
     const PostOut out = make_out(args.par, pn);
     const int h = args.par.h;
-    int PI[4], PJ[4];
-    PI[0] = i2; PJ[0] = j2;
-    PI[1] = T + i2; PJ[1] = j2;
-    PI[2] = T + j2; PJ[2] = i2;
-    PI[3] = T + i2; PJ[3] = T + j2;
-    uint4 q4[4], q3[4], q3t[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        if (s == 2 && dg) continue;
-        const int I = PI[s], J = PJ[s];
-        const int i = I * PT + r, j = J * PT + c0, it = J * PT + r, jt = I * PT + c0;
-        q4[s] = ld4g(pn.p4, pn.ld4, i, j, true);
-        q3[s] = ld4g(pn.p3, pn.ld3, i, j, true);
-        q3t[s] = ld4g(pn.p3, pn.ld3, it, jt, I != J);
-        st4s(sT + s * kPostTile, r, c0, ld4g(pn.p4, pn.ld4, it, jt, true));
-        st4s(sU + s * kPostTile, r, c0,
-             add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 2 + s) * kPostTile, r, c0), p));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        if (s == 2 && dg) continue;
-        const int I = PI[s], J = PJ[s];
-        const bool pdiag = I == J;
-        const int i = I * PT + r, j = J * PT + c0;
-        const uint32_t* u = sU + s * kPostTile;
-        const uint32_t* tt = sT + s * kPostTile;
-        const uint4 u2 = add4(u1_row(u, r, c0, pdiag), q4[s], p);
-        const uint4 x21 = add4(u2, q3[s], p);
-        const uint4 x22 = add4(u2, ld4sT(tt, r, c0), p);
-        const uint4 x11 = add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 1 + s) * kPostTile, r, c0), p);
-        out.put4(h + i, j, x21);
-        if (!out.out64 || !pdiag) {
-            out.put4(h + i, h + j, x22);
-            out.put4(i, j, x11);
-        } else {  // diagonal tile of the caller's C: lower entries only
-            const uint32_t a22[4] = {x22.x, x22.y, x22.z, x22.w}, a11[4] = {x11.x, x11.y, x11.z, x11.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (c0 + e <= r) {
-                    out.put(h + i, h + j + e, a22[e]);
-                    out.put(i, j + e, a11[e]);
-                }
+    // parent pair of child output slot s
+    const int PI[4] = {i2, T + i2, T + j2, T + i2}, PJ[4] = {j2, j2, i2, T + j2};
+    // Seven steps, one tile pair each: the three children's pair (i2, j2) (outputs to shared
+    // memory), then the parent's pairs at the children's output slots (outputs to HBM).  The
+    // next step's global loads are issued before the current step's barrier (software
+    // pipelining: two temporary tiles instead of one per step, 3 blocks / SM).
+    auto load = [&](int st, uint4 (&v)[7]) {
+        if (st < 3) {
+            const PostNode nd = args.ch[3 * t + st];
+            const int i = i2 * PT + r, j = j2 * PT + c0, it = j2 * PT + r, jt = i2 * PT + c0;
+            v[0] = ld4g(nd.p1, nd.ld1, i, j, true);
+            v[1] = ld4g(nd.p5, nd.ld5, i, j, true);
+            v[2] = ld4g(nd.p4, nd.ld4, it, jt, true);
+            v[3] = ld4g(nd.p4, nd.ld4, i, j, true);
+            v[4] = ld4g(nd.p3, nd.ld3, i, j, true);
+            v[5] = ld4g(nd.p2, nd.ld2, i, j, true);
+            v[6] = ld4g(nd.p3, nd.ld3, it, jt, !dg);
+        } else {
+            const int s = st - 3, I = PI[s], J = PJ[s];
+            const int i = I * PT + r, j = J * PT + c0, it = J * PT + r, jt = I * PT + c0;
+            v[2] = ld4g(pn.p4, pn.ld4, it, jt, true);
+            v[3] = ld4g(pn.p4, pn.ld4, i, j, true);
+            v[4] = ld4g(pn.p3, pn.ld3, i, j, true);
+            v[6] = ld4g(pn.p3, pn.ld3, it, jt, I != J);
         }
-        if (!pdiag) {
-            const int it = J * PT + r, jt = I * PT + c0;
-            out.put4(h + it, jt, add4(add4(ld4sT(u, r, c0), ld4s(tt, r, c0), p), q3t[s], p));
+    };
+    uint4 cur[7], nxt[7];
+    load(0, cur);
+#pragma unroll
+    for (int st = 0; st < 7; ++st) {
+        if (st == 5 && dg) continue;  // parent slot 2 is slot 1 on a diagonal pair
+        const int s = st - 3;
+        if (st < 3) {
+            st4s(sU, r, c0, add4(cur[0], cur[1], p));
+        } else {
+            st4s(sU, r, c0, add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 2 + s) * kPostTile, r, c0), p));
         }
+        st4s(sT, r, c0, cur[2]);
+        const int nst = st + 1 + ((st + 1 == 5 && dg) ? 1 : 0);
+        if (nst < 7) load(nst, nxt);
+        __syncthreads();
+        if (st < 3) {  // child st: its four output slots into shared memory
+            uint32_t* x = sX + 4 * st * kPostTile;
+            const uint4 u2 = add4(u1_row(sU, r, c0, dg), cur[3], p);
+            st4s(x + 0 * kPostTile, r, c0, add4(cur[0], cur[5], p));          // X11(i,j) = P1 + P2
+            st4s(x + 1 * kPostTile, r, c0, add4(u2, cur[4], p));              // X21(i,j)
+            st4s(x + 3 * kPostTile, r, c0, add4(u2, ld4sT(sT, r, c0), p));    // X22(i,j)
+            if (!dg)                                                            // X21(j,i)
+                st4s(x + 2 * kPostTile, r, c0, add4(add4(ld4sT(sU, r, c0), ld4s(sT, r, c0), p), cur[6], p));
+        } else {  // the parent's pair at child slot s
+            const int I = PI[s], J = PJ[s];
+            const bool pdiag = I == J;
+            const int i = I * PT + r, j = J * PT + c0;
+            const uint4 u2 = add4(u1_row(sU, r, c0, pdiag), cur[3], p);
+            const uint4 x21 = add4(u2, cur[4], p);
+            const uint4 x22 = add4(u2, ld4sT(sT, r, c0), p);
+            const uint4 x11 =
+                add4(ld4s(sX + (4 * 0 + s) * kPostTile, r, c0), ld4s(sX + (4 * 1 + s) * kPostTile, r, c0), p);
+            out.put4(h + i, j, x21);
+            if (!out.out64 || !pdiag) {
+                out.put4(h + i, h + j, x22);
+                out.put4(i, j, x11);
+            } else {  // diagonal tile of the caller's C: lower entries only
+                const uint32_t a22[4] = {x22.x, x22.y, x22.z, x22.w}, a11[4] = {x11.x, x11.y, x11.z, x11.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (c0 + e <= r) {
+                        out.put(h + i, h + j + e, a22[e]);
+                        out.put(i, j + e, a11[e]);
+                    }
+            }
+            if (!pdiag) {
+                const int it = J * PT + r, jt = I * PT + c0;
+                out.put4(h + it, jt, add4(add4(ld4sT(sU, r, c0), ld4s(sT, r, c0), p), cur[6], p));
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 7; ++q) cur[q] = nxt[q];
     }
 }
 
@@ -1301,7 +1299,7 @@ cudaError_t launch_post2(const Post2Args& a, cudaStream_t s) {
     if (a.h2 == 0 || a.par.nnodes == 0) return cudaSuccess;
     if (a.h2 % PT != 0 || a.par.h != 2 * a.h2) return cudaErrorInvalidValue;
     const int T = a.h2 / PT;
-    const size_t smem = (size_t)20 * kPostTile * 4;
+    const size_t smem = (size_t)14 * kPostTile * 4;  // 12 child output tiles + 2 step temporaries
     DeviceOnce& once = per_device<Post2AttrOnce>();
     std::call_once(once.flag, [&] {
         once.result = cudaFuncSetAttribute(post2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -7,6 +7,8 @@ subtree prep (automatic for complete uniform trees), the low-memory schedule
 Random shapes (odd, ragged, k > n, Pair padding), primes over every digit scheme and both skew
 forms, and recursion policies; Low(C) must equal the oracle's in every combination.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -25,7 +27,10 @@ def switches(gpu):
     gpu.release_cache()
 
 
-@pytest.mark.parametrize("seed", range(6))
+SEEDS = int(os.environ.get("FSYRK_COMBO_SEEDS", "6"))  # stress runs: FSYRK_COMBO_SEEDS=60
+
+
+@pytest.mark.parametrize("seed", range(SEEDS))
 def test_switch_combinations(switches, seed):
     fs = switches
     rng = np.random.default_rng(1000 + seed)

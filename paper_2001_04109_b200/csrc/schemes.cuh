@@ -66,19 +66,33 @@ struct Scheme;
 #ifndef FSYRK_LIMB2_STAGES
 #define FSYRK_LIMB2_STAGES (FSYRK_PAIR ? 4 : 3)
 #endif
+// LIMB2 wide-B (default): the two B digit planes sit next to each other in the stage, so one
+// N = 2 BN MMA per A digit computes d_a [e0 | e1] into two adjacent accumulators: 2 MMAs of
+// N = 256 instead of 4 of N = 128 per K step.  The tensor pipe time is the same, but every A
+// operand byte read from shared memory now feeds 256 columns instead of 128 -- the operand
+// reads per MMA cycle drop from 128 to 96 B (LIMB2 had the highest operand bandwidth of all
+// schemes).  Four accumulators T00 | T01 | T10 | T11 (all 512 TMEM columns); the fold weights
+// T01 and T10 alike (shift 1).
+#ifndef FSYRK_LIMB2_WIDE
+#define FSYRK_LIMB2_WIDE 1
+#endif
 template <>
 struct Scheme<SCHEME_LIMB2> {
-    static constexpr int PA = 2, PB = 2, NACC = 3, NT = 4, BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK,
-                         STAGES = FSYRK_LIMB2_STAGES;
+    static constexpr bool WIDE = FSYRK_LIMB2_WIDE && !FSYRK_PAIR;
+    static constexpr int PA = 2, PB = 2, NACC = WIDE ? 4 : 3, NT = WIDE ? 2 : 4, NB = WIDE ? 2 : 1,
+                         BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK, STAGES = FSYRK_LIMB2_STAGES;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
-        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
-        return T[q];
+        constexpr Term T[4] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
+        constexpr Term W[2] = {{0, 0, 0}, {1, 0, 2}};  // B planes 0..1 as one operand
+        return WIDE ? W[q] : T[q];
     }
+    // digit shift (weight 256^shift) of accumulator s
+    __host__ __device__ static constexpr int shift(int s) { return WIDE ? (s >> 1) + (s & 1) : s; }
 };
 template <>
 struct Scheme<SCHEME_LIMB3> {
-    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, BN = 96, BK = 128, STAGES = FSYRK_PAIR ? 3 : 2;
+    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, NB = 1, BN = 96, BK = 128, STAGES = FSYRK_PAIR ? 3 : 2;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
@@ -88,7 +102,7 @@ struct Scheme<SCHEME_LIMB3> {
 };
 template <>
 struct Scheme<SCHEME_LIMB4> {
-    static constexpr int PA = 4, PB = 4, NACC = 7, NT = 16, BN = 64, BK = 128, STAGES = 2;
+    static constexpr int PA = 4, PB = 4, NACC = 7, NT = 16, NB = 1, BN = 64, BK = 128, STAGES = 2;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2},
@@ -112,7 +126,7 @@ struct Scheme<SCHEME_LIMB4> {
 template <>
 struct Scheme<SCHEME_M17> {
     static constexpr bool UNSIGNED = true, PAIR = FSYRK_PAIR;
-    static constexpr int PA = PAIR ? 3 : 5, PB = PAIR ? 5 : 3, NACC = 3, NT = 9, BN = FSYRK_M17_BN,
+    static constexpr int PA = PAIR ? 3 : 5, PB = PAIR ? 5 : 3, NACC = 3, NT = 9, NB = 1, BN = FSYRK_M17_BN,
                          BK = FSYRK_M17_BK, STAGES = FSYRK_M17_STAGES;
     __host__ __device__ static constexpr Term term(int q) {
         // acc0: d0 e0 + 2^18 (d1 e2 + d2 e1);  acc1: d0 e1 + d1 e0 + 2^18 d2 e2 (weight 2^6);
@@ -149,7 +163,7 @@ struct Scheme<SCHEME_M17N> : Scheme<SCHEME_M17> {
 template <>
 struct Scheme<SCHEME_M31> {
     static constexpr bool ACC4 = FSYRK_M31_ACC4;
-    static constexpr int PA = 5, PB = 5, NACC = ACC4 ? 4 : 5, NT = ACC4 ? 17 : 16, BN = ACC4 ? 128 : 96,
+    static constexpr int PA = 5, PB = 5, NACC = ACC4 ? 4 : 5, NT = ACC4 ? 17 : 16, NB = 1, BN = ACC4 ? 128 : 96,
                          BK = FSYRK_M31_BK, STAGES = FSYRK_M31_STAGES;
     static constexpr bool UNSIGNED = true, PAIR = FSYRK_M31_PAIR;
     __host__ __device__ static constexpr Term term(int q) {
@@ -260,10 +274,13 @@ struct SplitFold<SCHEME_LIMB2> {
     static constexpr bool ok = true;
     using V = int64_t;
     __device__ __forceinline__ static V partial(const uint32_t* a, bool) {
+        if constexpr (Scheme<SCHEME_LIMB2>::WIDE)  // T00 | T01 | T10 | T11
+            return (int64_t)(int32_t)a[0] + ((int64_t)(int32_t)a[1] + (int64_t)(int32_t)a[2]) * 256 +
+                   (int64_t)(int32_t)a[3] * 65536;
         return (int64_t)(int32_t)a[0] + (int64_t)(int32_t)a[1] * 256 + (int64_t)(int32_t)a[2] * 65536;
     }
     __device__ __forceinline__ static V term(int s, uint32_t a, bool) {
-        return (int64_t)(int32_t)a << (8 * s);
+        return (int64_t)(int32_t)a << (8 * Scheme<SCHEME_LIMB2>::shift(s));
     }
     __device__ __forceinline__ static uint32_t final(V v, const ModP& m) { return mod_s64(v, m); }
 };

@@ -49,8 +49,10 @@ template <int S>
 SchemeInfo info() {
     using Sc = Scheme<S>;
     // M31 with 4 accumulators issues d2 e2 twice (weight 2): 17 MMAs for 16 digit products
-    const int products = (S == SCHEME_M31 && Sc::NT == 17) ? 16 : Sc::NT;
-    return SchemeInfo{S,      planes_of<S>(), Sc::PA,   Sc::PB,         Sc::NACC,       Sc::NT,
+    // MMAs per 32-deep K step counted in BN-wide units (a wide-B MMA covers NB of them)
+    const int nt = Sc::NT * Sc::NB;
+    const int products = (S == SCHEME_M31 && Sc::NT == 17) ? 16 : nt;
+    return SchemeInfo{S,      planes_of<S>(), Sc::PA,   Sc::PB,         Sc::NACC,       nt,
                       products, Sc::BN,       Sc::BK,   Cfg<S>::TILE_M, Cfg<S>::B_ROWS, Sc::UNSIGNED};
 }
 
@@ -109,7 +111,9 @@ void fill_fold_weights(const SchemeInfo& s, uint64_t p, int32_t* w) {
     for (int i = 0; i < 8; ++i) w[i] = 0;
     if (s.id == SCHEME_M17 || s.id == SCHEME_M17N || s.id == SCHEME_M31) return;  // constants inside fold_acc
     for (int i = 0; i < 8; ++i) {
-        uint64_t v = powmod(256, (uint64_t)i, p);
+        // accumulator i carries digit shift i, except in the wide-B LIMB2 layout T00|T01|T10|T11
+        const int sh = s.id == SCHEME_LIMB2 ? Scheme<SCHEME_LIMB2>::shift(i) : i;
+        uint64_t v = powmod(256, (uint64_t)sh, p);
         w[i] = v > p / 2 ? (int32_t)((int64_t)v - (int64_t)p) : (int32_t)v;
     }
 }

@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ------------------------------------------------ MMA issuer (the leader of a pair)
-            constexpr uint32_t idesc = sm100::idesc_i8(C::TILE_M, BN, !Sc::UNSIGNED);
+            // N = NB * BN: a wide-B scheme multiplies one A digit by NB adjacent B digit planes
+            constexpr uint32_t idesc = sm100::idesc_i8(C::TILE_M, BN * Sc::NB, !Sc::UNSIGNED);
+            static_assert(BN * Sc::NB <= 256 && (Sc::NB == 1 || !PAIR), "UMMA N");
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;

@@ -472,9 +472,13 @@ __device__ __forceinline__ void tree_level(const PrepTreeArgs& a, const uint64_t
                 // reduce only the ones that are not
                 const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(raw + o);
                 const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(raw + o + 2);
-                if ((x.x | x.y | y.x | y.y) >> 31 || x.x >= p || x.y >= p || y.x >= p || y.y >= p)
-                    return make_uint4(mod_u64(x.x, m), mod_u64(x.y, m), mod_u64(y.x, m), mod_u64(y.y, m));
-                return make_uint4((uint32_t)x.x, (uint32_t)x.y, (uint32_t)y.x, (uint32_t)y.y);
+                // branch-free canonical test: every high word zero and every low word < p
+                const uint32_t l0 = (uint32_t)x.x, l1 = (uint32_t)x.y, l2 = (uint32_t)y.x, l3 = (uint32_t)y.y;
+                const uint32_t hi = (uint32_t)(x.x >> 32) | (uint32_t)(x.y >> 32) | (uint32_t)(y.x >> 32) |
+                                    (uint32_t)(y.y >> 32);
+                const bool ok = (hi == 0) & (l0 < p) & (l1 < p) & (l2 < p) & (l3 < p);
+                if (!ok) return make_uint4(mod_u64(x.x, m), mod_u64(x.y, m), mod_u64(y.x, m), mod_u64(y.y, m));
+                return make_uint4(l0, l1, l2, l3);
             }
         };
 #pragma unroll

@@ -377,6 +377,9 @@ struct Plan {
     // P4, P3 are written into the caller's C12 quadrant -- strict upper triangle, scratch in the
     // reference too (fast_syrk.hpp:271-273), which also keeps its S blocks there (:96-98) --
     // instead of the arena; the root post-addition reads them from there
+    // a root-leaf plan (depth 0: one classical product over the whole problem) has the product
+    // epilogue write alpha X + beta C into the caller's C (no uint32 X, no finalize pass)
+    bool root_direct = false;
     bool lowmem = false;
     const uint64_t* lm_c = nullptr;  // C the root group's output map was last encoded for
     long long lm_ldc = 0;
@@ -521,6 +524,10 @@ struct Plan {
                 idle = prank != 0;  // not partitionable: rank 0 computes everything
             }
         }
+        // measured (profiles/r02/depth0.txt): pays from ~2048^2 outputs (cfg2 / cfg3 / cfg5 shapes at
+        // depth 0); below, the separate finalize pass is cheaper than the heavier epilogue
+        root_direct = pnranks == 1 && nodes[0].kind == LEAF && (long long)n_ * n_ >= (2048ll << 11) &&
+                      getenv("FSYRK_B200_NO_ROOT_DIRECT") == nullptr;
         // the low-memory schedule applies to a single-rank plan whose top level is a 2 x 2 level
         lowmem = lowmem_ && pnranks == 1 && nodes[0].kind == LEVEL && nodes[0].h % 4 == 0;
         // any K is exact: the product kernel drains its int32 accumulators mod p every
@@ -1268,6 +1275,22 @@ struct Plan {
         }
         mark(0);
         const Node& root = nodes[0];
+        bool root_done = false;
+        if (root_direct) {  // the root leaf's products write the caller's C themselves
+            for (auto& pl : prods)
+                for (int gi = 0; gi < pl.args.ngroups; ++gi)
+                    if (pl.members[gi].leaf && pl.members[gi].idx == root.lgroup) {
+                        GroupDesc& g = pl.args.g[gi];
+                        g.out64 = 1;
+                        g.c64 = c_dev;
+                        g.ldc64 = ldc;
+                        g.alpha = alpha;
+                        g.beta = beta;
+                        g.calpha = make_mulconst(alpha, (uint32_t)p);
+                        g.cbeta = make_mulconst(beta, (uint32_t)p);
+                    }
+            root_done = true;
+        }
         const uint32_t* lm_p4 = nullptr;  // low-memory schedule: P4 | P3 rows inside C12
         if (lowmem) {
             if (ldc % 2 != 0 || reinterpret_cast<uintptr_t>(c_dev) % 16 != 0)
@@ -1342,7 +1365,6 @@ struct Plan {
                    [&] { ck(modmm_launch(sch, pl.args, std::min(ncta, pl.args.ntiles * (BMt / 128)), st), "modmm"); });
             counts[0]++;
         };
-        bool root_done = false;
         auto run_post = [&](PostGroup& pg, cudaStream_t st, bool fused2 = false) {
             if (pg.kind == LEVEL) {
                 PostArgs a{};

@@ -31,6 +31,14 @@ struct alignas(64) GroupDesc {
     uint32_t* out;    // residues, problem b at out + b * out_bs
     long long out_bs;
     long long ldo;
+    // out64 (one-problem groups): the epilogue writes C <- alpha X + beta C_in straight into the
+    // caller's uint64 C (Low only for syrk) instead of uint32 residues -- a root-leaf plan's
+    // finalisation fused into the products (out stays the K-chunk partial scratch)
+    int out64;
+    uint64_t* c64;
+    long long ldc64;
+    uint32_t alpha, beta;
+    MulConst calpha, cbeta;
 };
 
 struct GroupedArgs {

@@ -393,7 +393,49 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             const int nch = (BN / 16 - part + kParts - 1) / kParts;  // chunks c0 = 16 (part + j kParts)
             auto col_of = [&](int j) { return 16 * (part + j * kParts); };
             // direct stores (outputs a TMA box cannot describe): this lane's row, 16 columns
+            // out64: C <- alpha X + beta C_in in the caller's uint64 C (scale_lower-style, the
+            // reference's syrk_classical accumulate, matrix.hpp:372-407); canonical C_in is the
+            // contract, others are reduced
+            uint64_t* crow = g.out64 ? g.c64 + grow * g.ldc64 : nullptr;
+            auto acc64 = [&](uint32_t x, uint64_t cin) -> uint64_t {
+                uint32_t r = g.alpha == 1 ? x : mulc(x, g.calpha, m.p);
+                if (g.beta != 0) {
+                    const uint32_t ci = cin < m.p ? (uint32_t)cin : mod_u64(cin, m);
+                    r = addm(r, g.beta == 1 ? ci : mulc(ci, g.cbeta, m.p), m.p);
+                }
+                return r;
+            };
+            auto store64 = [&](const uint32_t (&res)[16], int c0) {
+                const long long gc0 = (long long)tile.w * BN + c0;
+                if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
+                const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) &&
+                                        (reinterpret_cast<uintptr_t>(crow + gc0) & 15) == 0;
+                if (full_chunk) {
+                    ulonglong2* q = reinterpret_cast<ulonglong2*>(crow + gc0);
+                    ulonglong2 cin[8];
+                    if (g.beta != 0) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) cin[e] = q[e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const uint64_t c0v = g.beta != 0 ? cin[e].x : 0, c1v = g.beta != 0 ? cin[e].y : 0;
+                        q[e] = make_ulonglong2(acc64(res[2 * e], c0v), acc64(res[2 * e + 1], c1v));
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const long long gc = gc0 + c;
+                        if (gc < g.N && (!g.syrk || gc <= grow))
+                            crow[gc] = acc64(res[c], g.beta != 0 ? crow[gc] : 0);
+                    }
+                }
+            };
             auto store_direct = [&](const uint32_t (&res)[16], int c0) {
+                if (g.out64) {
+                    store64(res, c0);
+                    return;
+                }
                 const long long gc0 = (long long)tile.w * BN + c0;
                 if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
                 const bool full_chunk = gc0 + 16 <= g.N && (!g.syrk || gc0 + 15 <= grow) && g.vec_ok;
@@ -485,7 +527,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             release();
             continue;
 #endif
-            const bool staged = C::TSTORE && g.tma_ok;
+            const bool staged = C::TSTORE && g.tma_ok && !g.out64;
             uint32_t ra[C::NACC][16];
             if (nchunks > 1) {
                 // K-chunked tile (K beyond the int32 exactness bound): every chunk's accumulators
@@ -506,7 +548,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                                 const long long gc = gc0 + c;
                                 if (gc < g.N && (!g.syrk || gc <= grow)) {
                                     const uint32_t s2 = (kc == 0 ? 0u : out[gc]) + res[c];
-                                    out[gc] = s2 >= m.p ? s2 - m.p : s2;
+                                    const uint32_t r2 = s2 >= m.p ? s2 - m.p : s2;
+                                    if (g.out64 && kc + 1 == nchunks)
+                                        crow[gc] = acc64(r2, g.beta != 0 ? crow[gc] : 0);
+                                    else
+                                        out[gc] = r2;
                                 }
                             }
                         }

@@ -76,12 +76,23 @@ struct Scheme;
 #ifndef FSYRK_LIMB2_WIDE
 #define FSYRK_LIMB2_WIDE 1
 #endif
+// FSYRK_LIMB2_PAIR = 1: the wide-B layout on CTA pairs (cta_group::2, 256 x 128 tiles).  The
+// N = 256 operand [e0 | e1] of a pair MMA is split by rows between the two CTAs, i.e. by
+// PLANE: CTA r stages B digit plane r only (all BN rows) next to its own 128 rows of both A
+// planes.  Per SM and 32-deep K step that is 12 KB of operands pulled from L2 instead of 16 KB
+// (LIMB2 at full MMA rate asks for 64 B/clk/SM, above what L2 delivers to 148 SMs) and 64
+// instead of 96 B/clk of shared-memory operand reads.
+#ifndef FSYRK_LIMB2_PAIR
+#define FSYRK_LIMB2_PAIR FSYRK_PAIR
+#endif
 template <>
 struct Scheme<SCHEME_LIMB2> {
-    static constexpr bool WIDE = FSYRK_LIMB2_WIDE && !FSYRK_PAIR;
+    static constexpr bool UNSIGNED = false, PAIR = FSYRK_LIMB2_PAIR;
+    static constexpr bool WIDE = FSYRK_LIMB2_WIDE;
+    static constexpr bool SPLITB = WIDE && PAIR;  // B planes split across the CTA pair
     static constexpr int PA = 2, PB = 2, NACC = WIDE ? 4 : 3, NT = WIDE ? 2 : 4, NB = WIDE ? 2 : 1,
-                         BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK, STAGES = FSYRK_LIMB2_STAGES;
-    static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
+                         BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK,
+                         STAGES = SPLITB && FSYRK_LIMB2_BK == 128 ? 4 : FSYRK_LIMB2_STAGES;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[4] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
         constexpr Term W[2] = {{0, 0, 0}, {1, 0, 2}};  // B planes 0..1 as one operand

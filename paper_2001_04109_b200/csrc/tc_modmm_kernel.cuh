@@ -80,13 +80,28 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 #endif
 
+// Scheme<S>::SPLITB if the scheme declares it
+template <int S, class = void>
+struct SplitB : std::false_type {};
+template <int S>
+struct SplitB<S, std::void_t<decltype(Scheme<S>::SPLITB)>> : std::bool_constant<Scheme<S>::SPLITB> {};
+template <int S>
+constexpr bool splitb_of() {
+    return SplitB<S>::value;
+}
+
 template <int S>
 struct Cfg {
     using Sc = Scheme<S>;
     static constexpr bool PAIR = Sc::PAIR;
     static constexpr int BN = Sc::BN, BK = Sc::BK, STAGES = Sc::STAGES, NACC = Sc::NACC;
     static constexpr int TILE_M = PAIR ? 2 * BM : BM;  // output rows per tile
-    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA
+    // CTA pairs split the B operand's rows: BN / 2 rows of every plane per CTA, or (wide-B: the
+    // N = NB * BN operand is the planes side by side) all BN rows of one plane each
+    static constexpr bool SPLITB = splitb_of<S>();
+    static_assert(!SPLITB || (PAIR && Sc::NB == 2 && Sc::PB == 2), "plane split needs a pair and two B planes");
+    static constexpr int B_ROWS = PAIR && !SPLITB ? BN / 2 : BN;  // B rows staged per CTA
+    static constexpr int PB_STAGE = SPLITB ? 1 : Sc::PB;           // B planes staged per CTA
     static_assert(BK == 128 || BK == 64 || BK == 32, "BK must match a swizzle mode");
     static constexpr int COLS_USED = NACC * BN;
     // two accumulator sets when they fit: the MMAs of tile i+1 run while the epilogue drains tile i
@@ -99,7 +114,7 @@ struct Cfg {
     static constexpr int A_TILE = BM * BK;
     static constexpr int B_TILE = B_ROWS * BK;
     static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
-    static constexpr int STAGE_BYTES = Sc::PA * A_TILE + Sc::PB * B_TILE;
+    static constexpr int STAGE_BYTES = Sc::PA * A_TILE + PB_STAGE * B_TILE;
     static constexpr int BAR_BYTES = 256;  // mbarriers + TMEM slot
     static constexpr int EPI_WARPS = kEpiWarpsDefault;
     static constexpr int NCW = (BN / 16 + EPI_WARPS / 4 - 1) / (EPI_WARPS / 4);  // chunks per epilogue warp
@@ -142,7 +157,10 @@ __host__ __device__ constexpr int first_term(int acc) {
     return -1;
 }
 
-template <int S, int EPI = kEpiWarpsDefault>
+// O64: the variant whose epilogue can write alpha X + beta C_in into the caller's uint64 C
+// (GroupDesc::out64, root-leaf plans).  A separate instantiation: the uint64 path's registers
+// made the regular LIMB2 epilogue spill (160 bytes of stack, cfg3 products 0.203 -> 0.242 ms).
+template <int S, int EPI = kEpiWarpsDefault, bool O64 = false>
 __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     modmm_kernel(const __grid_constant__ GroupedArgs args) {
     using C = Cfg<S>;
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
                 const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
                 const int arow = tile.z * C::TILE_M + (int)rank * BM;
-                const int brow = tile.w * BN + (int)rank * C::B_ROWS;
+                const int brow = tile.w * BN + (C::SPLITB ? 0 : (int)rank * C::B_ROWS);
                 for (int kb = 0; kb < g.k_blocks; ++kb) {
                     sm100::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* st = smem + stage * C::STAGE_BYTES;
@@ -223,10 +241,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
 #pragma unroll
                         for (int l = 0; l < Sc::PA; ++l)
                             sm100::tma_load_4d_pair(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
+                        if constexpr (C::SPLITB) {  // this CTA's B digit plane
+                            sm100::tma_load_4d_pair(st + Sc::PA * C::A_TILE, &g.tmB, &full[stage], kb * BK, brow,
+                                                    (int)rank, bB);
+                        } else {
 #pragma unroll
-                        for (int l = 0; l < Sc::PB; ++l)
-                            sm100::tma_load_4d_pair(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
-                                                    kb * BK, brow, l, bB);
+                            for (int l = 0; l < Sc::PB; ++l)
+                                sm100::tma_load_4d_pair(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
+                                                        kb * BK, brow, l, bB);
+                        }
                     } else {
                         sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
 #pragma unroll
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             // ------------------------------------------------ MMA issuer (the leader of a pair)
             // N = NB * BN: a wide-B scheme multiplies one A digit by NB adjacent B digit planes
             constexpr uint32_t idesc = sm100::idesc_i8(C::TILE_M, BN * Sc::NB, !Sc::UNSIGNED);
-            static_assert(BN * Sc::NB <= 256 && (Sc::NB == 1 || !PAIR), "UMMA N");
+            static_assert(BN * Sc::NB <= 256 && (Sc::NB == 1 || !PAIR || C::SPLITB), "UMMA N");
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
@@ -396,7 +419,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             // out64: C <- alpha X + beta C_in in the caller's uint64 C (scale_lower-style, the
             // reference's syrk_classical accumulate, matrix.hpp:372-407); canonical C_in is the
             // contract, others are reduced
-            uint64_t* crow = g.out64 ? g.c64 + grow * g.ldc64 : nullptr;
+            const bool o64 = O64 && g.out64;
+            uint64_t* crow = o64 ? g.c64 + grow * g.ldc64 : nullptr;
             auto acc64 = [&](uint32_t x, uint64_t cin) -> uint64_t {
                 uint32_t r = g.alpha == 1 ? x : mulc(x, g.calpha, m.p);
                 if (g.beta != 0) {
@@ -432,9 +456,11 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                 }
             };
             auto store_direct = [&](const uint32_t (&res)[16], int c0) {
-                if (g.out64) {
-                    store64(res, c0);
-                    return;
+                if constexpr (O64) {
+                    if (o64) {
+                        store64(res, c0);
+                        return;
+                    }
                 }
                 const long long gc0 = (long long)tile.w * BN + c0;
                 if (!row_ok || gc0 >= g.N || (g.syrk && gc0 > grow)) return;
@@ -527,7 +553,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             release();
             continue;
 #endif
-            const bool staged = C::TSTORE && g.tma_ok && !g.out64;
+            const bool staged = C::TSTORE && g.tma_ok && !o64;
             uint32_t ra[C::NACC][16];
             if (nchunks > 1) {
                 // K-chunked tile (K beyond the int32 exactness bound): every chunk's accumulators
@@ -549,7 +575,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                                 if (gc < g.N && (!g.syrk || gc <= grow)) {
                                     const uint32_t s2 = (kc == 0 ? 0u : out[gc]) + res[c];
                                     const uint32_t r2 = s2 >= m.p ? s2 - m.p : s2;
-                                    if (g.out64 && kc + 1 == nchunks)
+                                    if (o64 && kc + 1 == nchunks)
                                         crow[gc] = acc64(r2, g.beta != 0 ? crow[gc] : 0);
                                     else
                                         out[gc] = r2;
@@ -695,15 +721,15 @@ cudaLaunchConfig_t launch_config(int grid, cudaStream_t stream, cudaLaunchAttrib
     return cfg;
 }
 
-template <int S, int EPI>
+template <int S, int EPI, bool O64>
 struct SmemAttrOnce : DeviceOnce {};
 
-template <int S, int EPI = kEpiWarpsDefault>
-cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
+template <int S, int EPI, bool O64>
+cudaError_t launch_variant(const GroupedArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<S>;
-    auto kern = modmm_kernel<S, EPI>;
+    auto kern = modmm_kernel<S, EPI, O64>;
     // thread-safe one-time setup per device (the attribute applies to the current device only)
-    DeviceOnce& once = per_device<SmemAttrOnce<S, EPI>>();
+    DeviceOnce& once = per_device<SmemAttrOnce<S, EPI, O64>>();
     std::call_once(once.flag, [&] {
         once.result = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     });
@@ -712,6 +738,13 @@ cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = launch_config<S, EPI>(grid, stream, attr);
     return cudaLaunchKernelEx(&cfg, kern, args);
+}
+
+template <int S, int EPI = kEpiWarpsDefault>
+cudaError_t launch_cfg(const GroupedArgs& args, int grid, cudaStream_t stream) {
+    bool o64 = false;
+    for (int g = 0; g < args.ngroups; ++g) o64 |= args.g[g].out64 != 0;
+    return o64 ? launch_variant<S, EPI, true>(args, grid, stream) : launch_variant<S, EPI, false>(args, grid, stream);
 }
 
 // CTAs per launch: one per SM, or as many CTA pairs as can be co-resident.

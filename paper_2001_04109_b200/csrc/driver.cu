@@ -1262,11 +1262,25 @@ struct Plan {
     void execute(const uint64_t* a_dev, long long lda, uint64_t* c_dev, long long ldc, uint32_t alpha,
                  uint32_t beta, bool mirror, cudaStream_t s) {
         int counts[5] = {0, 0, 0, 0, 0};
-        cudaEvent_t ev[6];
+        // Phase timing: an event is recorded only at a boundary that has launches behind it since
+        // the previous one -- an empty interval between two recorded events still reads ~2.7 us
+        // (B200), which used to be charged to "pre" (three records before the first kernel) and
+        // to "convert" on plans without a conversion pass.  at[i]: the event that stands for mark i.
+        cudaEvent_t ev[7], at[7] = {};
+        int marked_launches = -1;
+        cudaEvent_t last_ev = nullptr;
         if (g_phase_timing)
             for (auto& e : ev) ck(cudaEventCreate(&e), "event");
         auto mark = [&](int i) {
-            if (g_phase_timing) ck(cudaEventRecord(ev[i], s), "event record");
+            if (!g_phase_timing) return;
+            const int total = counts[0] + counts[1] + counts[2] + counts[3] + counts[4];
+            if (last_ev && total == marked_launches) {
+                at[i] = last_ev;
+                return;
+            }
+            ck(cudaEventRecord(ev[i], s), "event record");
+            at[i] = last_ev = ev[i];
+            marked_launches = total;
         };
         if (idle) {  // multi-GPU rank without a share (top level not partitionable)
             std::fill(g_launch_counts, g_launch_counts + 5, 0);
@@ -1310,17 +1324,13 @@ struct Plan {
                 lm_ldc = ldc;
             }
         }
-        cudaEvent_t ev_conv = nullptr;  // phase timing: end of the conversion pass
         // 1. syrkd: convert the reference-layout input with the column transform folded in;
         //    otherwise the top-level pre-additions read the caller's uint64 matrix directly
         if (colmap) {
             ck(launch_convert_in(a_dev, lda, n, kin, k, dev_colmap, (uint32_t)p, root_in, root.ldin, s), "convert_in");
             counts[3]++;
         }
-        if (g_phase_timing) {
-            ck(cudaEventCreate(&ev_conv), "event");
-            ck(cudaEventRecord(ev_conv, s), "event record");
-        }
+        mark(6);  // end of the conversion pass
         // 2. leaf operands that are plain views (root leaf, split-on-k children)
         for (int li : split_leaves) {
             const Node& nd = nodes[li];
@@ -1520,20 +1530,17 @@ struct Plan {
         }
         std::copy(counts, counts + 5, g_launch_counts);
         if (g_phase_timing) {
-            ck(cudaEventSynchronize(ev[5]), "event sync");
-            float t;
+            ck(cudaEventSynchronize(at[5]), "event sync");
             // kinds: 0 products, 1 pre (split + prep), 2 post, 3 convert/finalize
-            cudaEventElapsedTime(&t, ev[2], ev[3]); g_phase_ms[0] = t;
-            float tc = 0, t1 = 0, t2 = 0;  // convert (ev0 -> ev_conv), pre (ev_conv -> ev2)
-            cudaEventElapsedTime(&tc, ev[0], ev_conv);
-            cudaEventElapsedTime(&t1, ev_conv, ev[1]);
-            cudaEventElapsedTime(&t2, ev[1], ev[2]);
-            g_phase_ms[1] = t1 + t2;
-            cudaEventElapsedTime(&t, ev[3], ev[4]); g_phase_ms[2] = t;
-            float t5;
-            cudaEventElapsedTime(&t5, ev[4], ev[5]);
-            g_phase_ms[3] = tc + t5;
-            cudaEventDestroy(ev_conv);
+            auto span = [&](int a, int b) {
+                float ms = 0;
+                if (at[a] && at[b] && at[a] != at[b]) cudaEventElapsedTime(&ms, at[a], at[b]);
+                return ms;
+            };
+            g_phase_ms[0] = span(2, 3);
+            g_phase_ms[1] = span(6, 2);               // pre: end of conversion -> end of pre-additions
+            g_phase_ms[2] = span(3, 4);
+            g_phase_ms[3] = span(0, 6) + span(4, 5);  // convert + finalize / mirror
             g_phase_ms[4] = 0;
             for (auto& e : ev) cudaEventDestroy(e);
         }

@@ -38,11 +38,17 @@ __device__ __forceinline__ uint32_t mod_u64(uint64_t x, const ModP& m) {
 // v mod p for signed |v| < 2^62.
 __device__ __forceinline__ uint32_t mod_s64(int64_t v, const ModP& m) { return mod_u64((uint64_t)(v + (int64_t)m.off), m); }
 
+// Branch-free forms (a, b < p < 2^31): the wrong candidate wraps around 2^32 and loses the
+// unsigned min -- add, add, min instead of add, compare, add, select (the pre-addition kernels
+// are integer-issue bound: profiles/r02/ncu_prep_tree_cfg2.md).
 __device__ __forceinline__ uint32_t addm(uint32_t a, uint32_t b, uint32_t p) {
-    uint32_t s = a + b;
-    return s >= p ? s - p : s;
+    const uint32_t s = a + b;
+    return min(s, s - p);
 }
-__device__ __forceinline__ uint32_t subm(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
+__device__ __forceinline__ uint32_t subm(uint32_t a, uint32_t b, uint32_t p) {
+    const uint32_t d = a - b;
+    return min(d, d + p);
+}
 __device__ __forceinline__ uint32_t mulm(uint32_t a, uint32_t b, const ModP& m) {
     return mod_u64((uint64_t)a * b, m);
 }
@@ -98,8 +104,8 @@ __host__ __device__ inline MulConst make_mulconst(uint32_t w, uint32_t p) {
 }
 __device__ __forceinline__ uint32_t mulc(uint32_t x, MulConst c, uint32_t p) {
     const uint32_t q = __umulhi(x, c.wq);
-    uint32_t r = x * c.w - q * p;  // exact mod 2^32, true value in [0, 2p)
-    return r >= p ? r - p : r;
+    const uint32_t r = x * c.w - q * p;  // exact mod 2^32, true value in [0, 2p)
+    return min(r, r - p);
 }
 
 }  // namespace fsyrk_b200

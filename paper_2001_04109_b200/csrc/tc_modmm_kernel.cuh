@@ -115,6 +115,12 @@ struct Cfg {
     static constexpr int B_TILE = B_ROWS * BK;
     static_assert(B_TILE % 1024 == 0 && A_TILE % 1024 == 0, "tiles must be whole swizzle atoms");
     static constexpr int STAGE_BYTES = Sc::PA * A_TILE + PB_STAGE * B_TILE;
+#ifdef FSYRK_M17_FAKE3  // timing experiment (wrong results, profiles/r02/operand_feed.txt): only the
+    static constexpr int PA_LOAD = digits_of<S> == SCHEME_M17 ? 3 : Sc::PA;  // 3 digit planes of A are loaded
+#else
+    static constexpr int PA_LOAD = Sc::PA;
+#endif
+    static constexpr int LOAD_BYTES = PA_LOAD * A_TILE + PB_STAGE * B_TILE;
     static constexpr int BAR_BYTES = 256;  // mbarriers + TMEM slot
     static constexpr int EPI_WARPS = kEpiWarpsDefault;
     static constexpr int NCW = (BN / 16 + EPI_WARPS / 4 - 1) / (EPI_WARPS / 4);  // chunks per epilogue warp
@@ -251,9 +257,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                                                         kb * BK, brow, l, bB);
                         }
                     } else {
-                        sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                        sm100::mbar_arrive_expect_tx(&full[stage], C::LOAD_BYTES);
 #pragma unroll
-                        for (int l = 0; l < Sc::PA; ++l)
+                        for (int l = 0; l < C::PA_LOAD; ++l)
                             sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
 #pragma unroll
                         for (int l = 0; l < Sc::PB; ++l)
@@ -296,7 +302,8 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     constexpr int q = decltype(qc)::value;
                     constexpr Term tm = Sc::term(q);
                     constexpr bool first = first_term<S>(tm.acc) == q;
-                    const uint64_t ad = sm100::sdesc_kmajor(st + tm.a * C::A_TILE, SW, 8 * BK);
+                    constexpr int ta = tm.a >= C::PA_LOAD ? tm.a - 2 : tm.a;  // (FAKE3: the undoubled plane)
+                    const uint64_t ad = sm100::sdesc_kmajor(st + ta * C::A_TILE, SW, 8 * BK);
                     const uint64_t bd = sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
 #pragma unroll
                     for (int kk = 0; kk < BK / 32; ++kk) {

@@ -314,6 +314,7 @@ struct PostGroup {
     int depth, n, kind;
     std::vector<int> nodes;
     PostNode* dev_post = nullptr;
+    std::vector<PostNode> host_post;  // the same table on the host (small ones travel in the launch parameters)
     AddNode* dev_add = nullptr;
     size_t off_nodes = 0;
 };
@@ -394,6 +395,7 @@ struct Plan {
     int post2_parent_depth = -1;
     int post2_h2 = 0, post2_nparents = 0;
     PostNode* post2_dev = nullptr;
+    std::vector<PostNode> post2_host;  // parents, then the deepest nodes (as uploaded to post2_dev)
 
     // side stream + events: the top level's general products overlap the deeper pre/post-additions
     cudaStream_t side = nullptr;
@@ -996,6 +998,8 @@ struct Plan {
             pg.dev_nodes = reinterpret_cast<PrepNode*>(arena + pg.off_nodes);
             a.nodes = pg.dev_nodes;
             a.nnodes = (int)tab.size();
+            a.ninl = tab.size() <= (size_t)kInlineNodes ? (int)tab.size() : 0;
+            for (int i = 0; i < a.ninl; ++i) a.inl[i] = tab[i];
             ck(cudaMemcpy(pg.dev_nodes, tab.data(), tab.size() * sizeof(PrepNode), cudaMemcpyHostToDevice),
                "upload prep table");
         }
@@ -1023,6 +1027,7 @@ struct Plan {
                     host_post[ni] = pn;
                 }
                 pg.dev_post = reinterpret_cast<PostNode*>(arena + pg.off_nodes);
+                pg.host_post = tab;
                 ck(cudaMemcpy(pg.dev_post, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
                    "upload post table");
                 if ((partitioned || nrounds) && pg.depth == 0 && !root_pairs.empty()) {
@@ -1173,6 +1178,7 @@ struct Plan {
         std::vector<PostNode> tab;
         for (int i : lv[D - 2]) tab.push_back(host_post[i]);
         for (int i : lv[D - 1]) tab.push_back(host_post[i]);
+        post2_host = tab;
         ck(cudaMalloc(&post2_dev, tab.size() * sizeof(PostNode)), "cudaMalloc(post2 tables)");
         ck(cudaMemcpy(post2_dev, tab.data(), tab.size() * sizeof(PostNode), cudaMemcpyHostToDevice),
            "upload post2 tables");
@@ -1231,6 +1237,11 @@ struct Plan {
         ck(cudaMemcpy(tree_dev, tab.data(), tab.size() * sizeof(PrepNode), cudaMemcpyHostToDevice),
            "upload tree prep table");
         for (int d = 0; d < D; ++d) a.nodes[d] = tree_dev + start[d];
+        for (int d = 0, q = 0; d < D; ++d)
+            for (size_t i = 0; i < lv[d].size(); ++i, ++q) {
+                const PrepNode& pn = host_prep[lv[d][i]];
+                a.tp[q] = PrepTreeArgs::Ptrs{pn.s1, pn.a22, pn.s2, pn.s4, pn.c_a11, pn.c_a12, pn.c_s3};
+            }
         tree_depth = D;
     }
 
@@ -1382,6 +1393,11 @@ struct Plan {
                 a.h = pg.n / 2;
                 a.nodes = fused2 ? post2_dev : pg.dev_post;
                 a.nnodes = fused2 ? post2_nparents : (int)pg.nodes.size();
+                {
+                    const std::vector<PostNode>& tab = fused2 ? post2_host : pg.host_post;
+                    a.ninl = a.nnodes <= kInlineNodes && (int)tab.size() >= a.nnodes ? a.nnodes : 0;
+                    for (int i = 0; i < a.ninl; ++i) a.inl[i] = tab[i];
+                }
                 if (pg.depth == 0) {  // the root writes alpha X + beta C into the caller's C
                     if (lm_p4) {
                         a.p4o = lm_p4;
@@ -1407,6 +1423,9 @@ struct Plan {
                     a2.par = a;
                     a2.ch = post2_dev + post2_nparents;
                     a2.h2 = post2_h2;
+                    const int nch = (int)post2_host.size() - post2_nparents;
+                    a2.nchi = nch <= kInlineChildren ? nch : 0;
+                    for (int i = 0; i < a2.nchi; ++i) a2.chi[i] = post2_host[post2_nparents + i];
                     traced("post d" + std::to_string(pg.depth) + "+" + std::to_string(pg.depth + 1), st,
                            [&] { ck(launch_post2(a2, st), "post2"); });
                 } else {

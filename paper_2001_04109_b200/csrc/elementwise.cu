@@ -207,10 +207,10 @@ __device__ __forceinline__ void pair_y(uint32_t u, uint32_t v, MulConst ca, MulC
 
 // Scalar variant: one thread per (row i, column j) or, in Pair form, per column pair (j, j + half).
 template <int L>
-__global__ void prep_kernel(const PrepArgs args) {
+__global__ void prep_kernel(const __grid_constant__ PrepArgs args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
-    const PrepNode nd = args.nodes[blockIdx.z];
+    const PrepNode nd = args.ninl ? args.inl[blockIdx.z] : args.nodes[blockIdx.z];
     const ModP m = args.m;
     const uint32_t p = m.p;
     const int h = args.h, kh = args.kh, half = args.half;
@@ -398,16 +398,15 @@ __device__ __forceinline__ void prep_vec_body(const PrepArgs& args, const PrepNo
 // Vector variant (kh % 4 == 0, half % 4 == 0, no padding): 4 columns (and, in
 // Pair form, their 4 partners) per thread; one specialised body per input kind.
 template <int S, bool PAIR>
-__global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const PrepArgs args) {
+__global__ void __launch_bounds__(256, FSYRK_PREP_MINB) prep_vec_kernel(const __grid_constant__ PrepArgs args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
-    const PrepNode& nd = args.nodes[blockIdx.z];
     const int ncg = (PAIR ? args.half : args.kh) / 4;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y * blockDim.y + threadIdx.y;
     if (g >= ncg || i >= args.h) return;
     if (args.part_block && !((args.need_mask >> (i / args.part_block)) & 1ull)) return;  // not this rank's rows
-    const PrepNode local = nd;
+    const PrepNode local = args.ninl ? args.inl[blockIdx.z] : args.nodes[blockIdx.z];
     if (local.in.in64) prep_vec_body<S, PAIR, true>(args, local, i, g);
     else prep_vec_body<S, PAIR, false>(args, local, i, g);
 }
@@ -461,7 +460,7 @@ __device__ __forceinline__ void tree_level(const PrepTreeArgs& a, const uint64_t
         const int g = it & (G - 1);
         const int rest = it >> lgG;
         const int u = rest % U, qi = (rest / U) % Bq, t = rest / (U * Bq);
-        const PrepNode& nd = a.nodes[d][t];
+        const PrepTreeArgs::Ptrs& nd = a.tp[(d == 0 ? 0 : d == 1 ? 1 : 4) + t];
         uint4 a11[NU], a12[NU], a21[NU], a22[NU], s1[NU], ay[NU];
         auto at = [&](int bi, int v) -> uint4 {
             const int o = ((t * B + bi) * W2 + v) * CP + 4 * g;
@@ -526,7 +525,7 @@ __device__ __forceinline__ void tree_level(const PrepTreeArgs& a, const uint64_t
 }
 
 template <int S, bool PAIR, int D>
-__global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kernel(const PrepTreeArgs a) {
+__global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kernel(const __grid_constant__ PrepTreeArgs a) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
     extern __shared__ __align__(16) uint32_t tsm[];
@@ -674,12 +673,12 @@ __device__ __forceinline__ PostOut make_out(const PostArgs& a, const PostNode& n
 }
 
 // Block (32 x 8) per tile pair (I >= J) of one node.
-__global__ void post_kernel(const PostArgs args) {
+__global__ void post_kernel(const __grid_constant__ PostArgs args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];  // Low(P1 + P5), tile (I, J)
     __shared__ uint32_t sT[TS][TS + 1];  // P4 tile (J, I)
-    const PostNode nd = post_node(args, args.nodes[blockIdx.z]);
+    const PostNode nd = post_node(args, args.ninl ? args.inl[blockIdx.z] : args.nodes[blockIdx.z]);
     const uint32_t p = args.m.p;
     const int h = args.h;
     const PostOut out = make_out(args, nd);
@@ -783,12 +782,14 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
     }
 }
 
-__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const PostArgs args) {
+// INL: the node table is read from the launch parameters (PostArgs::inl) instead of HBM
+template <bool INL>
+__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const __grid_constant__ PostArgs args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
-    const PostNode nd = post_node(args, args.nodes[blockIdx.z]);
+    const PostNode nd = post_node(args, INL ? args.inl[blockIdx.z] : args.nodes[blockIdx.z]);
     int I, J;
     if (args.pairs) {
         I = args.pairs[blockIdx.x].x;
@@ -842,7 +843,8 @@ __device__ __forceinline__ uint4 u1_row(const uint32_t* u, int r, int c0, bool d
     return make_uint4(v[0], v[1], v[2], v[3]);
 }
 
-__global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const Post2Args args) {
+template <bool INL>
+__global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const __grid_constant__ Post2Args args) {
     pdl_wait();  // the previous kernel of the call has finished writing (pdl.cuh)
     pdl_trigger();
     extern __shared__ __align__(16) uint32_t psm[];
@@ -856,7 +858,7 @@ __global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const Post2Args a
     const bool dg = i2 == j2;
     const int t = blockIdx.z;
     const int tx = threadIdx.x, r = threadIdx.y, c0 = 4 * tx;
-    const PostNode pn = post_node(args.par, args.par.nodes[t]);
+    const PostNode pn = post_node(args.par, INL ? args.par.inl[t] : args.par.nodes[t]);
     const PostOut out = make_out(args.par, pn);
     const int h = args.par.h;
     // parent pair of child output slot s
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const Post2Args a
     // pipelining: two temporary tiles instead of one per step, 3 blocks / SM).
     auto load = [&](int st, uint4 (&v)[7]) {
         if (st < 3) {
-            const PostNode nd = args.ch[3 * t + st];
+            const PostNode nd = INL ? args.chi[3 * t + st] : args.ch[3 * t + st];
             const int i = i2 * PT + r, j = j2 * PT + c0, it = j2 * PT + r, jt = i2 * PT + c0;
             v[0] = ld4g(nd.p1, nd.ld1, i, j, true);
             v[1] = ld4g(nd.p5, nd.ld5, i, j, true);
@@ -948,13 +950,13 @@ __global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const Post2Args a
 // (round_done[r] >= target[r], counted by the product kernel's epilogue warps).  No
 // griddepcontrol.wait: the products are still running.  A wait that never ends (a broken
 // count) traps after ~4 s instead of hanging the device.
-__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_rounds_kernel(const PostArgs args,
+__global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_rounds_kernel(const __grid_constant__ PostArgs args,
                                                                           const int* round_done,
                                                                           const int* target, int* next_pair) {
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
     __shared__ int s_idx;
-    const PostNode nd = post_node(args, args.nodes[0]);
+    const PostNode nd = post_node(args, args.ninl ? args.inl[0] : args.nodes[0]);
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     int ready_round = -1;  // rounds <= ready_round are known complete
     for (;;) {
@@ -1295,7 +1297,9 @@ cudaError_t launch_post(const PostArgs& args, cudaStream_t s) {
     dim3 grid(args.pairs ? args.npairs : T * (T + 1) / 2, 1, args.nnodes);
     if (grid.x == 0) return cudaSuccess;
     // vector loads need h % 4 == 0 (every ld in the plan is h or a multiple of 4 then)
-    if (args.h % 4 == 0) return launch_pdl(post_vec_kernel, grid, dim3(8, 32), 0, s, args);
+    if (args.h % 4 == 0)
+        return args.ninl == args.nnodes ? launch_pdl(post_vec_kernel<true>, grid, dim3(8, 32), 0, s, args)
+                                        : launch_pdl(post_vec_kernel<false>, grid, dim3(8, 32), 0, s, args);
     return launch_pdl(post_kernel, grid, dim3(32, 8), 0, s, args);
 }
 
@@ -1306,10 +1310,16 @@ cudaError_t launch_post2(const Post2Args& a, cudaStream_t s) {
     const size_t smem = (size_t)14 * kPostTile * 4;  // 12 child output tiles + 2 step temporaries
     DeviceOnce& once = per_device<Post2AttrOnce>();
     std::call_once(once.flag, [&] {
-        once.result = cudaFuncSetAttribute(post2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        once.result = cudaFuncSetAttribute(post2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (once.result == cudaSuccess)
+            once.result =
+                cudaFuncSetAttribute(post2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
     if (once.result != cudaSuccess) return once.result;
-    return launch_pdl(post2_kernel, dim3(T * (T + 1) / 2, 1, a.par.nnodes), dim3(PT / 4, PT), smem, s, a);
+    const dim3 grid(T * (T + 1) / 2, 1, a.par.nnodes), block(PT / 4, PT);
+    const bool inl = a.par.ninl == a.par.nnodes && a.nchi == 3 * a.par.nnodes;
+    return inl ? launch_pdl(post2_kernel<true>, grid, block, smem, s, a)
+               : launch_pdl(post2_kernel<false>, grid, block, smem, s, a);
 }
 
 cudaError_t launch_post_rounds(const PostArgs& args, const int* round_done, const int* target, int* next_pair,

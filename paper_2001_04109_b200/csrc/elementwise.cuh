@@ -62,6 +62,11 @@ struct PrepArgs {
     long long c3_plane, c3_row;  // leaf operand planes for S3 (k = kw)
     const PrepNode* nodes;
     int nnodes;
+    // ninl = nnodes when the node table also travels by value in inl[] (<= kInlineNodes nodes):
+    // the kernels then read it from their parameter (constant) space instead of starting every
+    // block with a dependent global load (measured on the fused subtree kernel: -8% of its time)
+    int ninl;
+    PrepNode inl[3];
     int aligned;  // every node's input rows allow 16-byte vector loads at 4-column steps (driver-checked)
     // multi-GPU partition: only rows i of blocks (i / part_block) set in need_mask are prepared
     // (the row blocks of this rank's block pairs); part_block = 0: all rows
@@ -86,6 +91,12 @@ struct PrepTreeArgs {
     long long g_plane[4], g_row[4];  // GEMM operand plane / row stride per depth
     long long c_plane, c_row;        // leaf operand planes (depth D)
     const PrepNode* nodes[4];
+    // The nodes' operand bases by value (node index: level 0 -> 0, level 1 -> 1 + t, level 2 ->
+    // 4 + t): they reach the kernel in its parameter (constant) space, so an item's stores do
+    // not wait on a dependent global load of the node table first.
+    struct Ptrs {
+        int8_t *s1, *a22, *s2, *s4, *c_a11, *c_a12, *c_s3;
+    } tp[13];
 };
 
 struct PostNode {
@@ -100,6 +111,8 @@ struct PostArgs {
     int h;
     const PostNode* nodes;
     int nnodes;
+    int ninl;         // nodes also by value in inl[] (see PrepArgs::ninl); 0: read the device table
+    PostNode inl[3];
     // out64: the root writes the caller's C directly: C <- alpha X + beta C on Low(C)
     int out64;
     uint64_t* c64;
@@ -134,7 +147,10 @@ struct Post2Args {
     PostArgs par;
     const PostNode* ch;
     int h2;
+    int nchi;          // children also by value in chi[] (<= 9); 0: read the device table
+    PostNode chi[9];
 };
+constexpr int kInlineNodes = 3, kInlineChildren = 9;
 
 struct AddNode {
     const uint32_t *x1, *x2;

@@ -101,25 +101,66 @@ struct Scheme<SCHEME_LIMB2> {
     // digit shift (weight 256^shift) of accumulator s
     __host__ __device__ static constexpr int shift(int s) { return WIDE ? (s >> 1) + (s & 1) : s; }
 };
+// A wide-B term over overlapped accumulators: A digit plane a times the nb adjacent B digit
+// planes b .. b + nb - 1 (one N = nb * BN MMA) into the adjacent accumulators acc .. acc + nb - 1.
+// init: on the first 32-deep K step of a chunk the MMA overwrites instead of accumulating.
+struct WideTerm {
+    int8_t a, b, acc, nb, init;
+};
+// LIMB3 wide-B (FSYRK_LIMB3_WIDE): like LIMB4 below with 80-column tiles, 3 MMAs of N = 240 per
+// 32-deep K step (360 cycles per 128 x 80 tile) instead of 9 of N = 96 (505 per 128 x 96).
+#ifndef FSYRK_LIMB3_WIDE
+#define FSYRK_LIMB3_WIDE 1
+#endif
 template <>
 struct Scheme<SCHEME_LIMB3> {
-    static constexpr int PA = 3, PB = 3, NACC = 5, NT = 9, NB = 1, BN = 96, BK = 128, STAGES = FSYRK_PAIR ? 3 : 2;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
+    static constexpr bool OVERLAP = FSYRK_LIMB3_WIDE && !FSYRK_PAIR;
+    static constexpr int PA = 3, PB = 3, NACC = 5, NT = OVERLAP ? 3 : 9, NB = OVERLAP ? 3 : 1, BN = OVERLAP ? 80 : 96,
+                         BK = 128, STAGES = FSYRK_PAIR ? 3 : 2;
     __host__ __device__ static constexpr Term term(int q) {
-        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
-                                   {2, 0, 2}, {1, 2, 3}, {2, 1, 3}, {2, 2, 4}};
-        return T[q];
+        constexpr Term T[9] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
+                               {2, 0, 2}, {1, 2, 3}, {2, 1, 3}, {2, 2, 4}};
+        constexpr Term W[3] = {{0, 0, 0}, {1, 0, 1}, {2, 0, 2}};  // B planes 0..2 as one operand
+        return OVERLAP ? W[q] : T[q];
+    }
+    // first K block of a chunk (OVERLAP): d2 [e1 | e2] initialises accumulators 3, 4; d0 [e0..e2]
+    // initialises 0..2; d2 e0 and d1 [e0..e2] accumulate
+    static constexpr int NT0 = 4;
+    __host__ __device__ static constexpr WideTerm term0(int q) {
+        constexpr WideTerm F[NT0] = {{2, 1, 3, 2, 1}, {0, 0, 0, 3, 1}, {2, 0, 2, 1, 0}, {1, 0, 1, 3, 0}};
+        return F[q];
     }
 };
+// LIMB4 wide-B (default): accumulator s (digit shift s = i + j) sits at TMEM columns s * BN, so
+// d_i [e0 | e1 | e2 | e3] lands on the adjacent accumulators i .. i + 3: 4 MMAs of N = 256 per
+// 32-deep K step instead of 16 of N = 64.  An int8 MMA costs max(~54, N / 2) cycles
+// (profiles/ubench/ubench_mma_rate.cu), so the 16 narrow ones ran at 60% of the tensor rate:
+// 858 -> 512 cycles per K step.  Accumulators overlap between MMAs, so overwrite-vs-accumulate
+// cannot be per accumulator: the first K block of a chunk issues d3 as d3 [e1 | e2 | e3]
+// (initialising accumulators 4..6) and d3 e0 (accumulating into 3, after d0 [e0..e3] has
+// initialised 0..3); MMAs into the same columns complete in issue order.
+#ifndef FSYRK_LIMB4_WIDE
+#define FSYRK_LIMB4_WIDE 1
+#endif
 template <>
 struct Scheme<SCHEME_LIMB4> {
-    static constexpr int PA = 4, PB = 4, NACC = 7, NT = 16, NB = 1, BN = 64, BK = 128, STAGES = 2;
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_PAIR;
+    static constexpr bool OVERLAP = FSYRK_LIMB4_WIDE && !FSYRK_PAIR;
+    static constexpr int PA = 4, PB = 4, NACC = 7, NT = OVERLAP ? 4 : 16, NB = OVERLAP ? 4 : 1, BN = 64, BK = 128,
+                         STAGES = 2;
     __host__ __device__ static constexpr Term term(int q) {
-        constexpr Term T[NT] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2},
-                                   {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}, {1, 3, 4}, {2, 2, 4},
-                                   {3, 1, 4}, {2, 3, 5}, {3, 2, 5}, {3, 3, 6}};
-        return T[q];
+        constexpr Term T[16] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2},
+                                {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}, {1, 3, 4}, {2, 2, 4},
+                                {3, 1, 4}, {2, 3, 5}, {3, 2, 5}, {3, 3, 6}};
+        constexpr Term W[4] = {{0, 0, 0}, {1, 0, 1}, {2, 0, 2}, {3, 0, 3}};  // B planes 0..3 as one operand
+        return OVERLAP ? W[q] : T[q];
+    }
+    // first K block of a chunk (OVERLAP)
+    static constexpr int NT0 = 5;
+    __host__ __device__ static constexpr WideTerm term0(int q) {
+        constexpr WideTerm F[NT0] = {{3, 1, 4, 3, 1}, {0, 0, 0, 4, 1}, {3, 0, 3, 1, 0}, {1, 0, 1, 4, 0}, {2, 0, 2, 4, 0}};
+        return F[q];
     }
 };
 // planes (stored): {d0, d1, d2, 2 d1, 2 d2}.  Single CTA: A reads all 5, B the first 3.

@@ -14,9 +14,11 @@
 //   p = 2^31 - 1 : M31  (default ACC4: 17 MMAs -- d2 e2 issued twice -- into
 //                        4 accumulators, 128 x 128 tiles; without ACC4:
 //                        16 MMAs, 5 accumulators, 128 x 96)
-//   p <= 2^16    : LIMB2 (4 MMAs, 3 accumulators, 128 x 128)
-//   p <= 2^24    : LIMB3 (9 MMAs, 5 accumulators, 128 x 96)
-//   otherwise    : LIMB4 (16 MMAs, 7 accumulators, 128 x 64)
+//   p <= 2^16    : LIMB2 (wide-B: 2 MMAs of N = 256 into 4 accumulators, 128 x 128)
+//   p <= 2^24    : LIMB3 (wide-B over overlapped accumulators: 3 MMAs of N = 240 into
+//                        5 accumulators, 128 x 80)
+//   otherwise    : LIMB4 (wide-B over overlapped accumulators: 4 MMAs of N = 256 into
+//                        7 accumulators, 128 x 64)
 // Above modmm_k_limit the kernel drains its int32 accumulators mod p every
 // K chunk, so any inner dimension is exact.
 // The tile N is as large as TMEM allows for the accumulators: the

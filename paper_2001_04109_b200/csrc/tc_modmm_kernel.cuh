@@ -89,6 +89,11 @@ template <int S>
 constexpr bool splitb_of() {
     return SplitB<S>::value;
 }
+// Scheme<S>::OVERLAP (wide-B MMAs over overlapped accumulators, schemes.cuh) if declared
+template <int S, class = void>
+struct Overlap : std::false_type {};
+template <int S>
+struct Overlap<S, std::void_t<decltype(Scheme<S>::OVERLAP)>> : std::bool_constant<Scheme<S>::OVERLAP> {};
 
 template <int S>
 struct Cfg {
@@ -315,6 +320,20 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                             sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idesc, accum);
                     }
                 };
+                // Overlapped wide-B schemes, first K block of a chunk: the scheme's term0 list, whose
+                // init terms overwrite their accumulators on the first 32-deep step
+                auto issue0 = [&](auto qc, uint32_t st) {
+                    if constexpr (Overlap<S>::value) {
+                        constexpr WideTerm tm = Sc::term0(decltype(qc)::value);
+                        constexpr uint32_t idn = sm100::idesc_i8(C::TILE_M, BN * tm.nb, !Sc::UNSIGNED);
+                        const uint64_t ad = sm100::sdesc_kmajor(st + tm.a * C::A_TILE, SW, 8 * BK);
+                        const uint64_t bd = sm100::sdesc_kmajor(st + Sc::PA * C::A_TILE + tm.b * C::B_TILE, SW, 8 * BK);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 32; ++kk)
+                            sm100::mma_i8(acc_base + tm.acc * BN, ad + 2 * kk, bd + 2 * kk, idn,
+                                          (kk > 0 || !tm.init) ? 1u : 0u);
+                    }
+                };
                 auto advance = [&](int& s, uint32_t& ph) {
                     if (++s == STAGES) {
                         s = 0;
@@ -364,7 +383,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                     sm100::mbar_wait(&full[stage], phase);
                     sm100::tc_fence_after();
                     const uint32_t st = sm100::smem_u32(smem + stage * C::STAGE_BYTES);
-                    static_for<Sc::NT>([&](auto qc) { issue(qc, st, kb); });
+                    if constexpr (Overlap<S>::value) {
+                        static_assert(!Overlap<S>::value || (!PAIR && !C::STAGGER), "overlapped accumulators: single CTA");
+                        if (kb == kc)
+                            static_for<Sc::NT0>([&](auto qc) { issue0(qc, st); });
+                        else
+                            static_for<Sc::NT>([&](auto qc) { issue(qc, st, kb); });
+                    } else {
+                        static_for<Sc::NT>([&](auto qc) { issue(qc, st, kb); });
+                    }
                     if constexpr (PAIR)
                         sm100::tc_commit_pair(&empty[stage]);
                     else

@@ -57,6 +57,13 @@ struct Term {
 template <int S>
 struct Scheme;
 
+// A wide-B term over overlapped accumulators: A digit plane a times the nb adjacent B digit
+// planes b .. b + nb - 1 (one N = nb * BN MMA) into the adjacent accumulators acc .. acc + nb - 1.
+// init: on the first 32-deep K step of a chunk the MMA overwrites instead of accumulating.
+struct WideTerm {
+    int8_t a, b, acc, nb, init;
+};
+
 #ifndef FSYRK_LIMB2_BN
 #define FSYRK_LIMB2_BN 128
 #endif
@@ -85,27 +92,33 @@ struct Scheme;
 #ifndef FSYRK_LIMB2_PAIR
 #define FSYRK_LIMB2_PAIR FSYRK_PAIR
 #endif
+#ifndef FSYRK_LIMB2_OVERLAP
+#define FSYRK_LIMB2_OVERLAP 0
+#endif
 template <>
 struct Scheme<SCHEME_LIMB2> {
     static constexpr bool UNSIGNED = false, PAIR = FSYRK_LIMB2_PAIR;
     static constexpr bool WIDE = FSYRK_LIMB2_WIDE;
     static constexpr bool SPLITB = WIDE && PAIR;  // B planes split across the CTA pair
-    static constexpr int PA = 2, PB = 2, NACC = WIDE ? 4 : 3, NT = WIDE ? 2 : 4, NB = WIDE ? 2 : 1,
+    // FSYRK_LIMB2_OVERLAP: three accumulators, one per digit shift, the two wide MMAs overlapping
+    // in the middle one (like LIMB3 / LIMB4 below): a quarter less TMEM to drain per tile
+    static constexpr bool OVERLAP = FSYRK_LIMB2_OVERLAP && WIDE && !PAIR;
+    static constexpr int PA = 2, PB = 2, NACC = WIDE && !OVERLAP ? 4 : 3, NT = WIDE ? 2 : 4, NB = WIDE ? 2 : 1,
                          BN = FSYRK_LIMB2_BN, BK = FSYRK_LIMB2_BK,
                          STAGES = SPLITB && FSYRK_LIMB2_BK == 128 ? 4 : FSYRK_LIMB2_STAGES;
     __host__ __device__ static constexpr Term term(int q) {
         constexpr Term T[4] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 2}};
         constexpr Term W[2] = {{0, 0, 0}, {1, 0, 2}};  // B planes 0..1 as one operand
-        return WIDE ? W[q] : T[q];
+        constexpr Term O[2] = {{0, 0, 0}, {1, 0, 1}};
+        return OVERLAP ? O[q] : WIDE ? W[q] : T[q];
+    }
+    static constexpr int NT0 = 3;  // first K block of a chunk (OVERLAP)
+    __host__ __device__ static constexpr WideTerm term0(int q) {
+        constexpr WideTerm F[NT0] = {{1, 1, 2, 1, 1}, {0, 0, 0, 2, 1}, {1, 0, 1, 1, 0}};
+        return F[q];
     }
     // digit shift (weight 256^shift) of accumulator s
-    __host__ __device__ static constexpr int shift(int s) { return WIDE ? (s >> 1) + (s & 1) : s; }
-};
-// A wide-B term over overlapped accumulators: A digit plane a times the nb adjacent B digit
-// planes b .. b + nb - 1 (one N = nb * BN MMA) into the adjacent accumulators acc .. acc + nb - 1.
-// init: on the first 32-deep K step of a chunk the MMA overwrites instead of accumulating.
-struct WideTerm {
-    int8_t a, b, acc, nb, init;
+    __host__ __device__ static constexpr int shift(int s) { return WIDE && !OVERLAP ? (s >> 1) + (s & 1) : s; }
 };
 // LIMB3 wide-B (FSYRK_LIMB3_WIDE): like LIMB4 below with 80-column tiles, 3 MMAs of N = 240 per
 // 32-deep K step (360 cycles per 128 x 80 tile) instead of 9 of N = 96 (505 per 128 x 96).
@@ -326,7 +339,7 @@ struct SplitFold<SCHEME_LIMB2> {
     static constexpr bool ok = true;
     using V = int64_t;
     __device__ __forceinline__ static V partial(const uint32_t* a, bool) {
-        if constexpr (Scheme<SCHEME_LIMB2>::WIDE)  // T00 | T01 | T10 | T11
+        if constexpr (Scheme<SCHEME_LIMB2>::WIDE && !Scheme<SCHEME_LIMB2>::OVERLAP)  // T00 | T01 | T10 | T11
             return (int64_t)(int32_t)a[0] + ((int64_t)(int32_t)a[1] + (int64_t)(int32_t)a[2]) * 256 +
                    (int64_t)(int32_t)a[3] * 65536;
         return (int64_t)(int32_t)a[0] + (int64_t)(int32_t)a[1] * 256 + (int64_t)(int32_t)a[2] * 65536;

@@ -34,6 +34,7 @@
 #include <thread>
 #include <tuple>
 #include <type_traits>
+#include <queue>
 #include <vector>
 
 #include "../../include/fsyrk_b200.h"
@@ -318,6 +319,8 @@ struct PostGroup {
     AddNode* dev_add = nullptr;
     size_t off_nodes = 0;
 };
+
+constexpr size_t kTileOffBytes = 4096;  // per-unit tile ranges behind a launch's tile list (<= 1023 units)
 
 struct Arena {
     size_t size = 0;
@@ -670,7 +673,7 @@ struct Plan {
                         for (int b = 0; b < lg.count; ++b) push_tiles(gi, b, lg.n, lg.n, true);
                     }
                 }
-                pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4));
+                pl.off_tiles = ar.take(pl.host_tiles.size() * sizeof(int4) + kTileOffBytes);  // + per-unit ranges
                 prods.push_back(std::move(pl));
                 c0 = c;
             }
@@ -830,8 +833,15 @@ struct Plan {
             a.ntiles = (int)pl.host_tiles.size();
             int4* tiles = reinterpret_cast<int4*>(arena + pl.off_tiles);
             a.tiles = tiles;
+            std::vector<int> tile_off = balance_tiles(pl);
             ck(cudaMemcpy(tiles, pl.host_tiles.data(), pl.host_tiles.size() * sizeof(int4), cudaMemcpyHostToDevice),
                "upload tile list");
+            if (!tile_off.empty()) {
+                int* off = reinterpret_cast<int*>(tiles + pl.host_tiles.size());
+                ck(cudaMemcpy(off, tile_off.data(), tile_off.size() * sizeof(int), cudaMemcpyHostToDevice),
+                   "upload tile ranges");
+                a.tile_off = off;
+            }
             for (int gi = 0; gi < a.ngroups; ++gi) {
                 GroupDesc& g = a.g[gi];
                 g.a_mult = g.b_mult = 1;
@@ -1185,6 +1195,67 @@ struct Plan {
         post2_parent_depth = D - 2;
         post2_h2 = deep.h;
         post2_nparents = (int)lv[D - 2].size();
+    }
+
+    // Balanced tile schedule of a persistent product launch.  The default gives unit u the tiles
+    // u, u + units, ... of the longest-K-first list; with tiles of three or four different lengths
+    // and 8-9 tiles per CTA the last CTA finished ~7% after a perfect split would (cfg2:
+    // profiles/r01/variants.txt, load balance).  Here the list is dealt out in its own order, each
+    // tile to the unit with the least work so far (cost: its K blocks plus an epilogue's worth),
+    // so tiles still run at about the time they did (the L2 sharing of a wave of neighbouring
+    // tiles survives) and every unit ends within one short tile of the others.  Returns the
+    // per-unit ranges (empty: keep the strided default) and reorders pl.host_tiles by unit.
+    std::vector<int> balance_tiles(ProdLaunch& pl) {
+        static const bool want = [] {
+            const char* e = getenv("FSYRK_B200_BALANCE");
+            return !(e && atoi(e) == 0);
+        }();
+        const int per = BMt / 128;
+        int grid = std::min(ncta, (int)pl.host_tiles.size() * per);
+        if (per == 2) grid &= ~1;
+        const int units = grid / per;
+        if (!want || nrounds || units < 2 || (int)pl.host_tiles.size() <= units ||
+            (size_t)(units + 1) * sizeof(int) > kTileOffBytes)
+            return {};
+        // the MMA wait a tile's epilogue costs, in 128-deep K blocks of the scheme's MMAs (per-tile
+        // traces, profiles/r01/variants.txt: M17 3.2k cycles against 2.9k per block, LIMB2 1.9k / 1.0k)
+        static const double epi_env = [] {
+            const char* e = getenv("FSYRK_B200_BALANCE_EPI");
+            return e ? atof(e) : -1.0;
+        }();
+        const double epi = epi_env >= 0 ? epi_env
+                           : sch.id == SCHEME_LIMB2 ? 1.9
+                           : sch.id == SCHEME_M31   ? 0.5
+                           : sch.id == SCHEME_LIMB3 ? 1.7
+                           : sch.id == SCHEME_LIMB4 ? 1.5
+                                                    : 1.1;
+        std::vector<double> cost(pl.members.size());
+        for (size_t gi = 0; gi < pl.members.size(); ++gi) {
+            const int kpad = pl.members[gi].leaf ? leaves[pl.members[gi].idx].kpad : gemms[pl.members[gi].idx].kpad;
+            cost[gi] = (double)kpad / BK + epi * 128 / BK;  // K blocks + the epilogue's share
+        }
+        // least-loaded unit first; ties by index (deterministic)
+        using Slot = std::pair<double, int>;
+        std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> pq;
+        for (int u = 0; u < units; ++u) pq.push({0.0, u});
+        std::vector<std::vector<int4>> lists(units);
+        for (const int4& t : pl.host_tiles) {
+            Slot s = pq.top();
+            pq.pop();
+            lists[s.second].push_back(t);
+            s.first += cost[t.x & ((1 << kTileGroupBits) - 1)];
+            pq.push(s);
+        }
+        std::vector<int> off(units + 1, 0);
+        std::vector<int4> ordered;
+        ordered.reserve(pl.host_tiles.size());
+        for (int u = 0; u < units; ++u) {
+            off[u] = (int)ordered.size();
+            ordered.insert(ordered.end(), lists[u].begin(), lists[u].end());
+        }
+        off[units] = (int)ordered.size();
+        pl.host_tiles = std::move(ordered);
+        return off;
     }
 
     // One launch for all pre-additions when the tree is complete and uniform below the root

@@ -48,6 +48,10 @@ struct GroupedArgs {
     int ngroups;
     int ntiles;
     const int4* tiles;  // (group | round << 8, batch, tm, tn), longest K first
+    // Balanced schedule (driver.cu, Plan::balance_tiles): scheduling unit u (CTA, or CTA pair)
+    // runs tiles[tile_off[u] .. tile_off[u + 1]) in order; nullptr: unit u runs tiles u, u +
+    // units, u + 2 units, ...
+    const int* tile_off;
     // Root post overlap (driver.cu, Plan::rounds): every epilogue warp adds 1 to round_done[round
     // of the tile] once its stores of the tile are globally visible, and the launch lets its
     // programmatic dependent (the round-aware post kernel) start as soon as every CTA is past

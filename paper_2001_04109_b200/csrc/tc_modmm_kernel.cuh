@@ -233,12 +233,19 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     // spins on round_done, so it can never hold resources this grid or its producers need)
     if (args.round_done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+    // this unit's tiles: a contiguous range of the balanced list, or the strided default
+    int t_beg = unit, t_end = args.ntiles, t_step = nunits;
+    if (args.tile_off) {
+        t_beg = args.tile_off[unit];
+        t_end = args.tile_off[unit + 1];
+        t_step = 1;
+    }
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer (both CTAs of a pair)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = unit; t < args.ntiles; t += nunits) {
+            for (int t = t_beg; t < t_end; t += t_step) {
                 const int4 tile = args.tiles[t];
                 const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
                 const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
-            for (int t = unit; t < args.ntiles; t += nunits) {
+            for (int t = t_beg; t < t_end; t += t_step) {
               const GroupDesc& g = args.g[args.tiles[t].x & ((1 << kTileGroupBits) - 1)];
               // K chunks: the accumulators are drained every chunk_blocks K-blocks (exactness
               // bound of the int32 accumulators); one chunk is one use of the TMEM buffer
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             report_round = -1;
         };
         uint32_t it = 0;
-        for (int t = unit; t < args.ntiles; t += nunits) {
+        for (int t = t_beg; t < t_end; t += t_step) {
           const int4 tile = args.tiles[t];
           const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
           const int nchunks = (g.k_blocks + g.chunk_blocks - 1) / g.chunk_blocks;

@@ -833,11 +833,21 @@ struct Plan {
             a.ntiles = (int)pl.host_tiles.size();
             int4* tiles = reinterpret_cast<int4*>(arena + pl.off_tiles);
             a.tiles = tiles;
-            std::vector<int> tile_off = balance_tiles(pl);
+            // schedule of the launch: FSYRK_B200_SCHED = dynamic | balanced (default) | strided
+            static const int sched_mode = [] {
+                const char* e = getenv("FSYRK_B200_SCHED");
+                return !e ? 1 : !strcmp(e, "dynamic") ? 2 : !strcmp(e, "strided") ? 0 : 1;
+            }();
+            int* extra = reinterpret_cast<int*>(tiles + pl.host_tiles.size());  // kTileOffBytes, zeroed with the arena
+            std::vector<int> tile_off;
+            if (sched_mode == 2 && BMt == 128 && !nrounds && (int)pl.host_tiles.size() > ncta)
+                a.dyn = extra;  // two counters, zero between launches (the kernel rearms them)
+            else if (sched_mode == 1)
+                tile_off = balance_tiles(pl);
             ck(cudaMemcpy(tiles, pl.host_tiles.data(), pl.host_tiles.size() * sizeof(int4), cudaMemcpyHostToDevice),
                "upload tile list");
             if (!tile_off.empty()) {
-                int* off = reinterpret_cast<int*>(tiles + pl.host_tiles.size());
+                int* off = extra + 2;
                 ck(cudaMemcpy(off, tile_off.data(), tile_off.size() * sizeof(int), cudaMemcpyHostToDevice),
                    "upload tile ranges");
                 a.tile_off = off;
@@ -1215,7 +1225,7 @@ struct Plan {
         if (per == 2) grid &= ~1;
         const int units = grid / per;
         if (!want || nrounds || units < 2 || (int)pl.host_tiles.size() <= units ||
-            (size_t)(units + 1) * sizeof(int) > kTileOffBytes)
+            (size_t)(units + 3) * sizeof(int) > kTileOffBytes)
             return {};
         // the MMA wait a tile's epilogue costs, in 128-deep K blocks of the scheme's MMAs (per-tile
         // traces, profiles/r01/variants.txt: M17 3.2k cycles against 2.9k per block, LIMB2 1.9k / 1.0k)

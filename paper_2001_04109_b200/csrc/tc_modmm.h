@@ -52,6 +52,10 @@ struct GroupedArgs {
     // runs tiles[tile_off[u] .. tile_off[u + 1]) in order; nullptr: unit u runs tiles u, u +
     // units, u + 2 units, ...
     const int* tile_off;
+    // Dynamic schedule (single-CTA schemes): dyn[0] is the next unclaimed position of the tile
+    // list (after the first `units` tiles, which are claimed by CTA index), dyn[1] counts finished
+    // CTAs; the last one to finish resets both for the next launch.  nullptr: static schedule.
+    int* dyn;
     // Root post overlap (driver.cu, Plan::rounds): every epilogue warp adds 1 to round_done[round
     // of the tile] once its stores of the tile are globally visible, and the launch lets its
     // programmatic dependent (the round-aware post kernel) start as soon as every CTA is past

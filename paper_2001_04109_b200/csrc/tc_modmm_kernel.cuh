@@ -126,7 +126,7 @@ struct Cfg {
     static constexpr int PA_LOAD = Sc::PA;
 #endif
     static constexpr int LOAD_BYTES = PA_LOAD * A_TILE + PB_STAGE * B_TILE;
-    static constexpr int BAR_BYTES = 256;  // mbarriers + TMEM slot
+    static constexpr int BAR_BYTES = 384;  // mbarriers + TMEM slot + the tile-schedule ring
     static constexpr int EPI_WARPS = kEpiWarpsDefault;
     static constexpr int NCW = (BN / 16 + EPI_WARPS / 4 - 1) / (EPI_WARPS / 4);  // chunks per epilogue warp
     // TMA-store staging: one 32 x 16 u32 box (2 KB, 64-byte swizzle) per epilogue warp
@@ -191,6 +191,14 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     uint64_t* tmem_empty = tmem_full + C::NBUF;  // [NBUF] (the leader's counts both CTAs' epilogues)
     uint64_t* acc_empty = tmem_empty + C::NBUF;  // [NACC] staggered release: accumulator s drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::NACC);
+    // dynamic schedule: the producer publishes the tile it claimed in a ring of kSched slots; the
+    // MMA thread and every epilogue warp read it there
+    constexpr int kSched = 4;
+    uint64_t* sched_full = acc_empty + C::NACC + 1;  // [kSched], one arrival (the producer)
+    uint64_t* sched_empty = sched_full + kSched;     // [kSched], 1 + EPI arrivals (the readers)
+    int* sched = reinterpret_cast<int*>(sched_empty + kSched);
+    static_assert((2 * STAGES + 2 * C::NBUF + C::NACC + 1 + 2 * kSched) * 8 + kSched * 4 <= C::BAR_BYTES, "barrier area");
+    const bool dyn = !PAIR && args.dyn != nullptr;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? sm100::cluster_rank() : 0;
@@ -212,6 +220,10 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             sm100::mbar_init(&tmem_empty[b], (PAIR ? 2 : 1) * EPI);
         }
         for (int s = 0; s < C::NACC; ++s) sm100::mbar_init(&acc_empty[s], EPI);
+        for (int s = 0; s < kSched; ++s) {
+            sm100::mbar_init(&sched_full[s], 1);
+            sm100::mbar_init(&sched_empty[s], 1 + EPI);
+        }
         sm100::fence_mbar_init();
     } else if (warp == 2 && lane == 0) {
         for (int g = 0; g < args.ngroups; ++g) {
@@ -240,13 +252,40 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
         t_end = args.tile_off[unit + 1];
         t_step = 1;
     }
+    // reader side of the schedule: the n-th tile of this CTA, or -1 after the last one
+    // (whole_warp: called by all 32 lanes, one arrival per warp; else by a single thread)
+    auto next_tile = [&](int n, bool whole_warp) -> int {
+        if (!dyn) {
+            const int t = t_beg + n * t_step;
+            return t < t_end ? t : -1;
+        }
+        const int slot = n & (kSched - 1);
+        sm100::mbar_wait(&sched_full[slot], (uint32_t)(n / kSched) & 1u);
+        const int t = sched[slot];
+        if (whole_warp) __syncwarp();  // every lane has read the slot before it is handed back
+        if (!whole_warp || lane == 0) sm100::mbar_arrive(&sched_empty[slot]);
+        return t;
+    };
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer (both CTAs of a pair)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = t_beg; t < t_end; t += t_step) {
+            int t = dyn ? unit : t_beg;
+            for (int n = 0;; ++n) {
+                if (dyn) {  // publish the claimed tile (or the end marker)
+                    const int slot = n & (kSched - 1);
+                    sm100::mbar_wait(&sched_empty[slot], ((uint32_t)(n / kSched) & 1u) ^ 1u);
+                    sched[slot] = t < args.ntiles ? t : -1;
+                    sm100::mbar_arrive(&sched_full[slot]);
+                    if (t >= args.ntiles) break;
+                } else if (t >= t_end) {
+                    break;
+                }
+                // claim the next tile now: the atomic's round trip overlaps this tile's loads
+                const int t_next = dyn ? atomicAdd(args.dyn, 1) + nunits : t + t_step;
                 const int4 tile = args.tiles[t];
+                t = t_next;
                 const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
                 const int bA = tile.y * g.a_mult + g.a_off, bB = tile.y * g.b_mult + g.b_off;
                 const int arow = tile.z * C::TILE_M + (int)rank * BM;
@@ -294,7 +333,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t it = 0;
-            for (int t = t_beg; t < t_end; t += t_step) {
+            for (int n = 0;; ++n) {
+              const int t = next_tile(n, false);
+              if (t < 0) break;
               const GroupDesc& g = args.g[args.tiles[t].x & ((1 << kTileGroupBits) - 1)];
               // K chunks: the accumulators are drained every chunk_blocks K-blocks (exactness
               // bound of the int32 accumulators); one chunk is one use of the TMEM buffer
@@ -438,7 +479,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             report_round = -1;
         };
         uint32_t it = 0;
-        for (int t = t_beg; t < t_end; t += t_step) {
+        for (int n = 0;; ++n) {
+          const int t = next_tile(n, true);
+          if (t < 0) break;
           const int4 tile = args.tiles[t];
           const GroupDesc& g = args.g[tile.x & ((1 << kTileGroupBits) - 1)];
           const int nchunks = (g.k_blocks + g.chunk_blocks - 1) / g.chunk_blocks;
@@ -733,6 +776,15 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
     pdl_trigger_mm();  // this CTA's work is issued: the next kernel of the call may begin launching
     sm100::tc_fence_before();
     __syncthreads();
+    if (dyn && threadIdx.x == 0) {
+        // thread 0 made all of this CTA's claims; the last CTA to get here rearms the counters
+        __threadfence();
+        if (atomicAdd(args.dyn + 1, 1) == (int)gridDim.x - 1) {
+            args.dyn[0] = 0;
+            args.dyn[1] = 0;
+            __threadfence();
+        }
+    }
     if constexpr (PAIR) sm100::cluster_sync();  // no CTA leaves while its peer may still signal it
     sm100::tc_fence_after();
     if (warp == 0) {

@@ -4,6 +4,7 @@
 O=gpurun_out/r02f
 mkdir -p $O/bench
 nvidia-smi -L
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?; tail -1 $O/smoke.log
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -2 $O/pytest_gpu.log
 for c in cfg2 cfg1 cfg3 cfg4 cfg5; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 > $O/bench/$c.json 2> $O/bench/$c.err; echo "$c rc=$?"

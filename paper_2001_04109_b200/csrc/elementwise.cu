@@ -43,16 +43,17 @@ namespace fsyrk_b200 {
 #ifndef FSYRK_CONVERT_ROWS
 #define FSYRK_CONVERT_ROWS 1  // rows per iteration of the conversion (4: 0.161 vs 0.149 ms on cfg5)
 #endif
-// Fused subtree prep staging.  0 (default): cp.async of the caller's raw uint64 values, 44 KB per
-// block and 5 blocks / SM.  1: the values are narrowed to uint32 on their way into shared
-// memory (register-staged 16-byte loads, two batches), 28 KB and 7 blocks / SM -- measured
-// slower (cfg2 prep 67.0 -> 84.5 us, cfg4 0.89 -> 1.16 ms, profiles/r02/tree_narrow.txt): the
-// asynchronous copies matter more than the occupancy.
-#ifndef FSYRK_TREE_NARROW
-#define FSYRK_TREE_NARROW 0
+// Fused subtree prep staging (cp.async of the caller's raw uint64 values, 44 KB per block and
+// 5 blocks / SM).  FSYRK_TREE_OWN = 1: each thread copies exactly the 16 chunks its own level-0
+// item reads and waits for those alone (no barrier before level 0); 0: chunks dealt out
+// linearly, one barrier.  (A register-staged variant that narrowed to uint32 on the way in --
+// 28 KB, 7 blocks / SM -- measured slower: profiles/r02/tree_narrow.txt.)
+#ifndef FSYRK_TREE_OWN
+#define FSYRK_TREE_OWN 1
 #endif
+#define FSYRK_TREE_NARROW 0
 #ifndef FSYRK_TREE_MINB
-#define FSYRK_TREE_MINB (FSYRK_TREE_NARROW ? 7 : 5)  // fused subtree prep: blocks per SM the registers must allow
+#define FSYRK_TREE_MINB 5  // fused subtree prep: blocks per SM the registers must allow
 #endif
 #ifndef FSYRK_POST_MINB
 #define FSYRK_POST_MINB 6  // measured: cfg2 post 60 -> 55 us, cfg5 2.53 -> 2.13 ms
@@ -544,44 +545,39 @@ __global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kerne
     // buffer 0: the root's input (raw uint64, or narrowed to uint32), later level 2; buffer 1: level 1
     constexpr int kSegs = B * B * NC;
     uint64_t* raw = reinterpret_cast<uint64_t*>(tsm);
-#if FSYRK_TREE_NARROW
-    uint32_t* buf1 = tsm + (kSegs << lgCP);
+    uint32_t* buf1 = tsm + 2 * (kSegs << lgCP);
+    const int lgG = lgCP - 2;
+#if FSYRK_TREE_OWN
     {
-        // the CTA's 4^D x NC segments of CP columns, 4 columns (two 16-byte loads) per step and
-        // thread, kBatch steps in flight; canonical residues are the contract (fields.hpp:32-36):
-        // only values that are not get reduced
-        const ModP m = a.m;
-        const uint32_t p = m.p;
-        const int groups = (kSegs << lgCP) / 4;
-        constexpr int kBatch = 4;
-        for (int g0 = threadIdx.x; g0 < groups; g0 += kBatch * kTreeThreads) {
-            ulonglong2 x[kBatch], y[kBatch];
+        // Every raw value is read exactly once, by the level-0 work item that owns its four
+        // columns: each thread copies its own item's 16 chunks (8 locations x 32 bytes) and waits
+        // for those alone -- no block-wide barrier before level 0.
+        constexpr int Bq = B / 2, V = Bq * NC, W2 = 2 * V, U = PAIR ? V / 2 : V, NU = PAIR ? 2 : 1;
+        const int it = threadIdx.x;
+        if (it < (Bq * U << lgG)) {
+            const int g = it & ((1 << lgG) - 1), rest = it >> lgG;
+            const int u = rest % U, qi = (rest / U) % Bq;
 #pragma unroll
-            for (int q = 0; q < kBatch; ++q) {
-                const int idx = 4 * min(g0 + q * kTreeThreads, groups - 1), cp = idx & (CP - 1), seg = idx >> lgCP;
-                const int v = seg % (B * NC), bi = seg / (B * NC);
-                const long long row = (long long)bi * a.rows + r;
-                const long long col = (long long)(v / NC) * a.w + c0 + cp + (v % NC) * half;
-                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(a.a64 + row * a.ld64 + col);
-                x[q] = __ldcs(src);
-                y[q] = __ldcs(src + 1);
-            }
+            for (int e = 0; e < NU; ++e) {
+                const int ue = u + e * (V / 2);
+                const int bis[2] = {qi, Bq + qi}, vs[2] = {ue, V + ue};
 #pragma unroll
-            for (int q = 0; q < kBatch; ++q) {
-                if (g0 + q * kTreeThreads >= groups) break;
-                const uint32_t l0 = (uint32_t)x[q].x, l1 = (uint32_t)x[q].y, l2 = (uint32_t)y[q].x, l3 = (uint32_t)y[q].y;
-                const uint32_t hi = (uint32_t)(x[q].x >> 32) | (uint32_t)(x[q].y >> 32) | (uint32_t)(y[q].x >> 32) |
-                                    (uint32_t)(y[q].y >> 32);
-                const bool ok = (hi == 0) & (l0 < p) & (l1 < p) & (l2 < p) & (l3 < p);
-                const uint4 val = ok ? make_uint4(l0, l1, l2, l3)
-                                     : make_uint4(mod_u64(x[q].x, m), mod_u64(x[q].y, m), mod_u64(y[q].x, m),
-                                                  mod_u64(y[q].y, m));
-                *reinterpret_cast<uint4*>(tsm + 4 * (g0 + q * kTreeThreads)) = val;
+                for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                    for (int vv = 0; vv < 2; ++vv) {
+                        const int bi = bis[bb], v = vs[vv];
+                        const int o = (bi * W2 + v) * CP + 4 * g;
+                        const long long row = (long long)bi * a.rows + r;
+                        const long long col = (long long)(v / NC) * a.w + c0 + 4 * g + (v % NC) * half;
+                        const uint64_t* src = a.a64 + row * a.ld64 + col;
+                        cp_async16(raw + o, src);
+                        cp_async16(raw + o + 2, src + 2);
+                    }
             }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
     }
 #else
-    uint32_t* buf1 = tsm + 2 * (kSegs << lgCP);
     {
         // every 16-byte chunk of the CTA's 4^D x NC segments of CP columns in flight at once
         const int chunks = (kSegs << lgCP) / 2;
@@ -594,9 +590,8 @@ __global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kerne
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
     }
-#endif
     __syncthreads();
-    const int lgG = lgCP - 2;
+#endif
     tree_level<S, PAIR, D, 0>(a, raw, tsm, D > 1 ? buf1 : nullptr, r, c0, CP, lgG);
     if constexpr (D > 1) {
         __syncthreads();
@@ -612,7 +607,7 @@ size_t prep_tree_smem(int D, bool pair, int cp) {
     const size_t nc = pair ? 2 : 1;
     // buffer 0: the root's uint64 input (4^D blocks; level 2's 9 x 4^(D-2) uint32 blocks fit in
     // it); buffer 1: level 1 = 3 * 4^(D-1) blocks of uint32
-    return ((size_t)1 << (2 * D)) * nc * cp * (FSYRK_TREE_NARROW ? 4 : 8) + 3 * ((size_t)1 << (2 * (D - 1))) * nc * cp * 4;
+    return ((size_t)1 << (2 * D)) * nc * cp * 8 + 3 * ((size_t)1 << (2 * (D - 1))) * nc * cp * 4;
 }
 
 template <int S, bool PAIR, int D>

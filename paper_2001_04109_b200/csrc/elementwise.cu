@@ -55,6 +55,9 @@ namespace fsyrk_b200 {
 #ifndef FSYRK_TREE_MINB
 #define FSYRK_TREE_MINB 5  // fused subtree prep: blocks per SM the registers must allow
 #endif
+#ifndef FSYRK_POST_STAGED
+#define FSYRK_POST_STAGED 1  // post_vec_pair: second-round loads staged by cp.async (one memory round trip per pair)
+#endif
 #ifndef FSYRK_POST_MINB
 #define FSYRK_POST_MINB 6  // measured: cfg2 post 60 -> 55 us, cfg5 2.53 -> 2.13 ms
 #endif
@@ -765,8 +768,15 @@ __global__ void post_kernel(const __grid_constant__ PostArgs args) {
 
 // Vector variant (h, all ld % 4 == 0): block (8 x 32), thread = 4 columns of one row.
 // One 32 x 32 tile pair (I >= J) of a node's post-addition, 8 x 32 threads.
+// STAGED: the loads that do not feed the shared-memory transposes (P4, P3, P2 of tile (I, J) and
+// P3 of tile (J, I)) start as cp.async copies into sP before anything else, each thread copying
+// what it reads back itself, so the pair is one round trip to memory instead of two dependent
+// ones (the root post was latency-bound at ~31% of DRAM throughput, profiles/r02/ncu_post_cfg2.md)
+// without holding registers across the barrier.
+template <bool STAGED>
 __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNode& nd, int I, int J,
-                                              uint32_t (&sU)[TS][TS + 1], uint32_t (&sT)[TS][TS + 1]) {
+                                              uint32_t (&sU)[TS][TS + 1], uint32_t (&sT)[TS][TS + 1],
+                                              uint4 (*sP)[TS][TS / 4]) {
     const uint32_t p = args.m.p;
     const int h = args.h;
     const PostOut out = make_out(args, nd);
@@ -775,6 +785,14 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
     const int i = I * TS + r, j = J * TS + c0;        // tile (I, J)
     const int it = J * TS + r, jt = I * TS + c0;      // tile (J, I)
     const bool ok = i < h && j < h, okt = it < h && jt < h;
+    if constexpr (STAGED) {
+        if (ok) {
+            cp_async16(&sP[0][r][tx], nd.p4 + (long long)i * nd.ld4 + j);
+            cp_async16(&sP[1][r][tx], nd.p3 + (long long)i * nd.ld3 + j);
+            cp_async16(&sP[2][r][tx], nd.p2 + (long long)i * nd.ld2 + j);
+        }
+        if (I != J && okt) cp_async16(&sP[3][r][tx], nd.p3 + (long long)it * nd.ld3 + jt);
+    }
     uint4 p1 = {0, 0, 0, 0}, p5 = p1, p4t = p1;
     if (ok) {
         p1 = *reinterpret_cast<const uint4*>(nd.p1 + (long long)i * nd.ld1 + j);
@@ -784,11 +802,12 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
     const uint4 l15 = add4(p1, p5, p);
     sU[r][c0] = l15.x; sU[r][c0 + 1] = l15.y; sU[r][c0 + 2] = l15.z; sU[r][c0 + 3] = l15.w;
     sT[r][c0] = p4t.x; sT[r][c0 + 1] = p4t.y; sT[r][c0 + 2] = p4t.z; sT[r][c0 + 3] = p4t.w;
+    if constexpr (STAGED) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (ok) {
-        const uint4 p4 = *reinterpret_cast<const uint4*>(nd.p4 + (long long)i * nd.ld4 + j);
-        const uint4 p3 = *reinterpret_cast<const uint4*>(nd.p3 + (long long)i * nd.ld3 + j);
-        const uint4 p2 = *reinterpret_cast<const uint4*>(nd.p2 + (long long)i * nd.ld2 + j);
+        const uint4 p4 = STAGED ? sP[0][r][tx] : *reinterpret_cast<const uint4*>(nd.p4 + (long long)i * nd.ld4 + j);
+        const uint4 p3 = STAGED ? sP[1][r][tx] : *reinterpret_cast<const uint4*>(nd.p3 + (long long)i * nd.ld3 + j);
+        const uint4 p2 = STAGED ? sP[2][r][tx] : *reinterpret_cast<const uint4*>(nd.p2 + (long long)i * nd.ld2 + j);
         uint32_t u1[4], t4[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -815,7 +834,7 @@ __device__ __forceinline__ void post_vec_pair(const PostArgs& args, const PostNo
         }
     }
     if (I != J && okt) {
-        const uint4 p3t = *reinterpret_cast<const uint4*>(nd.p3 + (long long)it * nd.ld3 + jt);
+        const uint4 p3t = STAGED ? sP[3][r][tx] : *reinterpret_cast<const uint4*>(nd.p3 + (long long)it * nd.ld3 + jt);
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = addm(sU[c0 + e][r], sT[r][c0 + e], p);
@@ -830,6 +849,7 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const __
     pdl_trigger();
     __shared__ uint32_t sU[TS][TS + 1];
     __shared__ uint32_t sT[TS][TS + 1];
+    __shared__ __align__(16) uint4 sP[FSYRK_POST_STAGED ? 4 : 1][TS][TS / 4];  // P4, P3, P2 (I, J), P3 (J, I)
     const PostNode nd = post_node(args, INL ? args.inl[blockIdx.z] : args.nodes[blockIdx.z]);
     int I, J;
     if (args.pairs) {
@@ -838,7 +858,7 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const __
     } else {
         tri_decode(blockIdx.x, I, J);
     }
-    post_vec_pair(args, nd, I, J, sU, sT);
+    post_vec_pair<FSYRK_POST_STAGED != 0>(args, nd, I, J, sU, sT, sP);
 }
 
 // ------------------------------------------------------------ post (two levels fused)
@@ -1024,7 +1044,7 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_rounds_kernel(const
             __syncthreads();
             ready_round = r;
         }
-        post_vec_pair(args, nd, I, J, sU, sT);
+        post_vec_pair<false>(args, nd, I, J, sU, sT, nullptr);
         __syncthreads();  // sU / sT are reused by the next pair
     }
 }

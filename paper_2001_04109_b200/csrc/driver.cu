@@ -54,6 +54,8 @@ thread_local std::string g_last_error;
 thread_local int g_launch_counts[5] = {0, 0, 0, 0, 0};
 thread_local std::string g_last_plan_json;
 thread_local bool g_phase_timing = false;
+// FSYRK_B200_ALWAYS_WAIT=1: every call waits on the plan's previous call even on the same stream (A/B switch)
+const bool g_always_wait = getenv("FSYRK_B200_ALWAYS_WAIT") != nullptr;
 thread_local float g_phase_ms[5] = {0, 0, 0, 0, 0};
 thread_local uint64_t g_transfer[2] = {0, 0};  // host<->device bytes of the last host-API call
 constexpr size_t kTriRows = 256;                // row block of the triangular C transfers
@@ -418,6 +420,8 @@ struct Plan {
     // previous call's last kernel (ev_done), whatever stream that call used.
     std::mutex use_mu;
     cudaEvent_t ev_done = nullptr;
+    unsigned long long last_sid = 0;  // id of the stream the previous call ran on
+    bool last_sid_valid = false;
 
     ~Plan() {
         if (ev_done) cudaEventDestroy(ev_done);
@@ -2166,8 +2170,18 @@ void run_dev(uint64_t p, uint32_t alpha, const uint64_t* a_dev, size_t n, size_t
     const std::shared_ptr<Plan> plan_ref = get_plan(p, (int)n, (int)k, kbar, pol, xf != nullptr, rank, nranks);
     Plan* plan = plan_ref.get();
     std::lock_guard<std::mutex> use(plan->use_mu);
+    // Calls that share a plan share its arena: wait for the previous call's last kernel -- unless
+    // that call ran on this very stream (stream order already serialises them; the wait would only
+    // put a semaphore command in front of the first kernel).  Stream ids are unique for the
+    // life of the process, handles are not.
+    unsigned long long sid = 0;
+    const bool have_sid = cudaStreamGetId(s, &sid) == cudaSuccess;
+    if (!have_sid) cudaGetLastError();
     if (!plan->ev_done) ck(cudaEventCreateWithFlags(&plan->ev_done, cudaEventDisableTiming), "event");
-    else ck(cudaStreamWaitEvent(s, plan->ev_done, 0), "wait for the plan's previous call");
+    else if (g_always_wait || !(have_sid && plan->last_sid_valid && plan->last_sid == sid))
+        ck(cudaStreamWaitEvent(s, plan->ev_done, 0), "wait for the plan's previous call");
+    plan->last_sid = sid;
+    plan->last_sid_valid = have_sid;
     if (xf) {
         auto same = [](const std::vector<ColMap>& x, const std::vector<ColMap>& y) {
             return x.size() == y.size() && std::memcmp(x.data(), y.data(), x.size() * sizeof(ColMap)) == 0;

@@ -51,7 +51,6 @@ namespace fsyrk_b200 {
 #ifndef FSYRK_TREE_OWN
 #define FSYRK_TREE_OWN 1
 #endif
-#define FSYRK_TREE_NARROW 0
 #ifndef FSYRK_TREE_MINB
 #define FSYRK_TREE_MINB 5  // fused subtree prep: blocks per SM the registers must allow
 #endif
@@ -476,7 +475,7 @@ __device__ __forceinline__ void tree_level(const PrepTreeArgs& a, const uint64_t
         uint4 a11[NU], a12[NU], a21[NU], a22[NU], s1[NU], ay[NU];
         auto at = [&](int bi, int v) -> uint4 {
             const int o = ((t * B + bi) * W2 + v) * CP + 4 * g;
-            if constexpr (d > 0 || FSYRK_TREE_NARROW) {
+            if constexpr (d > 0) {
                 return *reinterpret_cast<const uint4*>(in + o);
             } else {
                 // the caller's uint64 values: canonical residues are the contract (fields.hpp:32-36);
@@ -545,7 +544,7 @@ __global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kerne
     const int CP = a.cp, lgCP = 31 - __clz(CP);
     const int r = blockIdx.y, c0 = blockIdx.x * CP;
     const int half = a.w / 2;
-    // buffer 0: the root's input (raw uint64, or narrowed to uint32), later level 2; buffer 1: level 1
+    // buffer 0: the root's raw uint64 input, later level 2; buffer 1: level 1
     constexpr int kSegs = B * B * NC;
     uint64_t* raw = reinterpret_cast<uint64_t*>(tsm);
     uint32_t* buf1 = tsm + 2 * (kSegs << lgCP);
@@ -595,7 +594,7 @@ __global__ void __launch_bounds__(kTreeThreads, FSYRK_TREE_MINB) prep_tree_kerne
     }
     __syncthreads();
 #endif
-    tree_level<S, PAIR, D, 0>(a, raw, tsm, D > 1 ? buf1 : nullptr, r, c0, CP, lgG);
+    tree_level<S, PAIR, D, 0>(a, raw, nullptr, D > 1 ? buf1 : nullptr, r, c0, CP, lgG);
     if constexpr (D > 1) {
         __syncthreads();
         tree_level<S, PAIR, D, (D > 1 ? 1 : 0)>(a, nullptr, buf1, tsm, r, c0, CP, lgG);

@@ -870,6 +870,9 @@ __global__ void __launch_bounds__(256, FSYRK_POST_MINB) post_vec_kernel(const __
 // pairs (I_s, J_s) from those tiles and its P3 / P4 in HBM.  The children's X never round-trip
 // through HBM and one launch replaces two; every global load of a phase is issued before its
 // barrier (3 blocks / SM by shared memory, so the registers allow it).
+#ifndef FSYRK_POST2_UNROLL
+#define FSYRK_POST2_UNROLL 1  // the seven steps fully unrolled; rolled (0) measured slower: cfg2 post 45.2 -> 48.2 us (profiles/r02/post2.txt)
+#endif
 #ifndef FSYRK_POST2_TILE
 #define FSYRK_POST2_TILE 32  // measured: 16 -> cfg2 post 61 us, 32 -> 53 us (per-depth: 51 us, but one launch more)
 #endif
@@ -949,7 +952,11 @@ __global__ void __launch_bounds__(PT * PT / 4, 3) post2_kernel(const __grid_cons
     };
     uint4 cur[7], nxt[7];
     load(0, cur);
+#if FSYRK_POST2_UNROLL
 #pragma unroll
+#else
+#pragma unroll 1
+#endif
     for (int st = 0; st < 7; ++st) {
         if (st == 5 && dg) continue;  // parent slot 2 is slot 1 on a diagonal pair
         const int s = st - 3;

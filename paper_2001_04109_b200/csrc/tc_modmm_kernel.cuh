@@ -53,6 +53,9 @@ namespace tc {
 #ifndef FSYRK_STAGGER
 #define FSYRK_STAGGER 1
 #endif
+#ifndef FSYRK_TMA_HINTS
+#define FSYRK_TMA_HINTS 0  // L2 eviction hints on the operand loads of general products (experiment)
+#endif
 #ifndef FSYRK_EPI_WARPS
 #define FSYRK_EPI_WARPS 8
 #endif
@@ -271,6 +274,9 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
             // ------------------------------------------------ TMA producer (both CTAs of a pair)
             int stage = 0;
             uint32_t phase = 0;
+#if FSYRK_TMA_HINTS
+            const uint64_t pol_a = sm100::l2_policy_evict_last(), pol_b = sm100::l2_policy_evict_first();
+#endif
             int t = dyn ? unit : t_beg;
             for (int n = 0;; ++n) {
                 if (dyn) {  // publish the claimed tile (or the end marker)
@@ -309,6 +315,27 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         }
                     } else {
                         sm100::mbar_arrive_expect_tx(&full[stage], C::LOAD_BYTES);
+#if FSYRK_TMA_HINTS
+                        // general products: the A row panels of a 12-row tile group are read again by
+                        // the next wave (column by column inside the group), the B column panels stream
+                        const bool hint = !g.syrk;
+#pragma unroll
+                        for (int l = 0; l < C::PA_LOAD; ++l) {
+                            if (hint)
+                                sm100::tma_load_4d_hint(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA, pol_a);
+                            else
+                                sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
+                        }
+#pragma unroll
+                        for (int l = 0; l < Sc::PB; ++l) {
+                            if (hint && FSYRK_TMA_HINTS == 1)
+                                sm100::tma_load_4d_hint(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
+                                                        kb * BK, brow, l, bB, pol_b);
+                            else
+                                sm100::tma_load_4d(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
+                                                   kb * BK, brow, l, bB);
+                        }
+#else
 #pragma unroll
                         for (int l = 0; l < C::PA_LOAD; ++l)
                             sm100::tma_load_4d(st + l * C::A_TILE, &g.tmA, &full[stage], kb * BK, arow, l, bA);
@@ -316,6 +343,7 @@ __global__ void __launch_bounds__(64 + 32 * EPI, 1)
                         for (int l = 0; l < Sc::PB; ++l)
                             sm100::tma_load_4d(st + Sc::PA * C::A_TILE + l * C::B_TILE, &g.tmB, &full[stage],
                                                kb * BK, brow, l, bB);
+#endif
                     }
                     if (++stage == STAGES) {
                         stage = 0;
